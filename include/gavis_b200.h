@@ -1,0 +1,227 @@
+/*
+ * gavis_b200.h -- C ABI of the B200-native GAVIS hot paths.
+ *
+ * Drop-in boundary for the two data-parallel paths of the GAVIS reference
+ * (R/ = /root/reference/proj/include/gavis/):
+ *   VF CONST   construct_field      vfield.hpp:68-92
+ *              accumulate_view      vfield.hpp:38-63
+ *              single_view_visibility raster.hpp:237-290
+ *   VF QUERY   query_visibility     vfield.hpp:96-112
+ *              query_view           vfield.hpp:121-134
+ *   UA RENDER  render_entropy       uncertainty.hpp:242-260 (+ render_entropy_core :124-238)
+ *              rasterize            raster.hpp:175-231
+ *              image_entropy        uncertainty.hpp:264-278
+ *              select_nbv           planner.hpp:117-137
+ *
+ * The reference has no FFI of its own: its boundary is the header-only C++ API
+ * called by tools/gavis_main.cpp:79-80, :104-105 and planner.hpp:297-301.
+ * include/gavis/gavis_b200.hpp re-exposes those exact C++ signatures on top of
+ * this C ABI.
+ *
+ * Conventions
+ *   - plain pointers and sizes; no CUDA or torch types in any signature;
+ *   - every entry point returns a gavis_status; on failure gavis_last_error()
+ *     holds a thread-local message. Status codes mirror the reference's
+ *     exception taxonomy (common.hpp:22-46, exit codes gavis_main.cpp:358-371);
+ *   - host output buffers are caller-owned; a NULL output pointer skips that
+ *     output; calls are synchronous at the ABI;
+ *   - scene arrays are fp32 (BASELINE.json configs); every decision on the path
+ *     (projection, culling, tile keys, coverage, alpha, transmittance and the
+ *     early-termination test) is computed in fp64 like the reference;
+ *   - outputs are double, the reference's own type.
+ */
+#ifndef GAVIS_B200_H
+#define GAVIS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GAVIS_ABI_VERSION 1
+
+typedef enum {
+  GAVIS_OK = 0,
+  GAVIS_ERR_PARAMETER = 2, /* ParameterError  (common.hpp:25-28) */
+  GAVIS_ERR_INVARIANT = 3, /* InvariantError  (common.hpp:30-33) */
+  GAVIS_ERR_ORACLE = 4,    /* OracleError     (common.hpp:35-38) */
+  GAVIS_ERR_DEVICE = 5     /* CUDA / NCCL failure                 */
+} gavis_status;
+
+/* CameraView (model.hpp:66-105). rotation is row-major camera-to-world with
+ * columns = camera x (image right), y (image down), z (forward). */
+typedef struct {
+  double rotation[9];
+  double position[3];
+  int32_t width, height;
+  double fov_h, fov_v, near_plane;
+} gavis_camera;
+
+/* RasterConfig (raster.hpp:21-35). Defaults 16 / 1e-4 / 0.3 / 0.99. */
+typedef struct {
+  int32_t tile_size;
+  int32_t _pad;
+  double transmittance_cutoff, dilation, alpha_clamp_max;
+} gavis_raster_config;
+
+/* UncertaintyConfig (uncertainty.hpp:24-52), constant variance provider.
+ * variance_provider and correlation must be 0 (kConstant, kNone). */
+typedef struct {
+  double beta, prior_opacity, color_sigma;
+  double prior_cov[9];
+  int32_t variance_provider, correlation;
+  double correlation_lambda;
+} gavis_uncertainty_config;
+
+/* Scene (model.hpp:130-134) as fp32 structure of arrays. */
+typedef struct {
+  int64_t num_particles;
+  int32_t color_degree, _pad;
+  const float* positions;    /* [N*3]                                     */
+  const float* rotations;    /* [N*4] quaternion (w, x, y, z)             */
+  const float* scales;       /* [N*3] per-axis standard deviations        */
+  const float* opacities;    /* [N]                                       */
+  const float* colors;       /* [N*3*(Lc+1)^2] per particle, channel-major */
+  const uint8_t* is_virtual; /* [N] or NULL                               */
+} gavis_scene_desc;
+
+typedef struct gavis_ctx gavis_ctx;
+typedef struct gavis_scene gavis_scene;
+typedef struct gavis_field gavis_field;
+
+/* ---- runtime ---------------------------------------------------------- */
+int gavis_abi_version(void);
+const char* gavis_last_error(void);
+/* One context per device (one process per GPU). stream: a cudaStream_t passed
+ * as void* to run on the caller's stream, or NULL for a private stream. */
+gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out);
+gavis_status gavis_ctx_destroy(gavis_ctx* ctx);
+gavis_status gavis_ctx_synchronize(gavis_ctx* ctx);
+/* Views processed per launch batch (0 = automatic from free memory). */
+gavis_status gavis_ctx_set_batch(gavis_ctx* ctx, int32_t max_views_per_batch);
+/* Per-kernel CUDA-event timing on the context stream (off by default). */
+gavis_status gavis_ctx_set_profiling(gavis_ctx* ctx, int32_t enabled);
+/* Accumulated device milliseconds and launch count of a kernel family:
+ * "preprocess", "emit_keys", "sort", "ranges", "vf_blend", "vf_finalize",
+ * "ua_blend", "score", "query". Resets when reset != 0. */
+gavis_status gavis_ctx_kernel_time(gavis_ctx* ctx, const char* kernel, double* ms,
+                                   int64_t* launches, int32_t reset);
+/* Device-side stopwatch on the context stream (bench timing). */
+gavis_status gavis_ctx_timer_start(gavis_ctx* ctx);
+gavis_status gavis_ctx_timer_stop(gavis_ctx* ctx, double* ms);
+/* Total kernels launched by this context since creation. */
+gavis_status gavis_ctx_launch_count(gavis_ctx* ctx, int64_t* launches);
+
+/* ---- scene ------------------------------------------------------------ */
+gavis_status gavis_scene_upload(gavis_ctx* ctx, const gavis_scene_desc* desc,
+                                gavis_scene** out);
+gavis_status gavis_scene_destroy(gavis_scene* scene);
+gavis_status gavis_scene_num_particles(const gavis_scene* scene, int64_t* n);
+
+/* ---- visibility field (vfield.hpp) ------------------------------------ */
+/* construct_field (vfield.hpp:68-92): zeroed field, every view rendered, SH
+ * accumulated in trajectory order, num_views = n_views. */
+gavis_status gavis_vf_construct(gavis_ctx* ctx, const gavis_scene* scene,
+                                const gavis_camera* views, int32_t n_views, double kappa,
+                                int32_t degree, const gavis_raster_config* rc,
+                                gavis_field** out);
+/* An all-zero field (num_views = 0) to accumulate into. */
+gavis_status gavis_vf_create(gavis_ctx* ctx, const gavis_scene* scene, double kappa,
+                             int32_t degree, gavis_field** out);
+/* Renders and accumulates views into an existing field in order; adds n_views
+ * to num_views (incremental / sharded construction, vfield.hpp:38-63, :88-90). */
+gavis_status gavis_vf_accumulate_views(gavis_ctx* ctx, gavis_field* field,
+                                       const gavis_scene* scene, const gavis_camera* views,
+                                       int32_t n_views, const gavis_raster_config* rc);
+/* accumulate_view with caller-provided per-particle visibility [N]. */
+gavis_status gavis_vf_accumulate_visibility(gavis_ctx* ctx, gavis_field* field,
+                                            const gavis_scene* scene,
+                                            const gavis_camera* view, const double* visibility);
+/* Field from host coefficients (e.g. a field.json written by the reference). */
+gavis_status gavis_vf_upload(gavis_ctx* ctx, const gavis_scene* scene, double kappa,
+                             int32_t degree, int32_t num_views, const double* gamma,
+                             gavis_field** out);
+gavis_status gavis_vf_download(const gavis_field* field, double* gamma, int32_t* num_views,
+                               int32_t* degree);
+gavis_status gavis_vf_set_num_views(gavis_field* field, int32_t num_views);
+/* Device pointer and element count of gamma (float64, N*(L+1)^2 row-major) for
+ * an in-place NCCL all-reduce of per-rank partial fields. */
+gavis_status gavis_vf_device_gamma(gavis_field* field, void** device_ptr, int64_t* count);
+gavis_status gavis_vf_destroy(gavis_field* field);
+
+/* single_view_visibility (raster.hpp:237-290): v [N]; optional touch counts [N]
+ * and per-pixel contributor counts [W*H]. */
+gavis_status gavis_single_view_visibility(gavis_ctx* ctx, const gavis_scene* scene,
+                                          const gavis_camera* cam,
+                                          const gavis_raster_config* rc, double* visibility,
+                                          int64_t* touch, int32_t* contributors);
+
+/* query_visibility (vfield.hpp:96-112) for n (particle, direction) pairs. */
+gavis_status gavis_vf_query(gavis_ctx* ctx, const gavis_field* field,
+                            const int64_t* particle_index, const double* directions,
+                            int64_t n, double* visibility);
+/* query_view (vfield.hpp:121-134): non-culled particles in index order. */
+gavis_status gavis_vf_query_view(gavis_ctx* ctx, const gavis_field* field,
+                                 const gavis_scene* scene, const gavis_camera* cam,
+                                 double dilation, int32_t* particle_index, double* visibility,
+                                 int64_t* n_out);
+
+/* ---- uncertainty-aware render (uncertainty.hpp, raster.hpp) ------------- */
+/* Fused render of n cameras (all outputs nullable, laid out camera-major):
+ *   rgb [n*H*W*3], depth [n*H*W], transmittance [n*H*W]   -- rasterize
+ *   entropy [n*H*W], invisible_mass [n*H*W], entropy_depth [n*H*W]
+ *                                                         -- render_entropy
+ *   scores [n]                                            -- image_entropy
+ * field == NULL with splat_visibility != NULL runs render_entropy_core with
+ * caller-provided per-particle visibility [N] (one vector for all cameras).
+ * If every image pointer is NULL but scores is set, images are not written
+ * back (device-resident), but RGB is still composited when with_rgb != 0. */
+typedef struct {
+  double* rgb;
+  double* depth;
+  double* transmittance;
+  double* entropy;
+  double* invisible_mass;
+  double* entropy_depth;
+  double* scores;
+  int32_t* rgb_contributors;     /* per-pixel covered entries, RGB track  */
+  int32_t* entropy_contributors; /* per-pixel covered entries, entropy track */
+  int32_t with_rgb;              /* composite RGB even if rgb == NULL       */
+  int32_t with_entropy;          /* composite entropy even if entropy == NULL */
+} gavis_render_outputs;
+
+gavis_status gavis_ua_render(gavis_ctx* ctx, const gavis_scene* scene,
+                             const gavis_field* field, const double* splat_visibility,
+                             const gavis_camera* cams, int32_t n_cams,
+                             const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
+                             gavis_render_outputs* out);
+
+/* select_nbv (planner.hpp:117-137): scores [n] and the first maximum. */
+gavis_status gavis_select_nbv(gavis_ctx* ctx, const gavis_scene* scene,
+                              const gavis_field* field, const gavis_camera* cams,
+                              int32_t n_cams, const gavis_raster_config* rc,
+                              const gavis_uncertainty_config* uc, int32_t with_rgb,
+                              double* scores, int32_t* best_index);
+
+/* ---- parity / debug ----------------------------------------------------- */
+/* Projection records of one camera (ImageSpaceSplat, raster.hpp:37-44) for all
+ * N particles: culled[N] (1 = culled), mean[2N], conic[3N] (a, b, c), depth[N],
+ * cover_rect[4N] (x0, x1, y0, y1: pixels whose centre passes splat_covers,
+ * raster.hpp:97-99; empty when x0 > x1) and tile_rect[4N] (tx0, tx1, ty0, ty1
+ * from covered_pixel_range, raster.hpp:138-159; empty when tx0 > tx1). */
+gavis_status gavis_debug_project(gavis_ctx* ctx, const gavis_scene* scene,
+                                 const gavis_camera* cam, double dilation, int32_t tile_size,
+                                 uint8_t* culled, double* mean, double* conic, double* depth,
+                                 int32_t* cover_rect, int32_t* tile_rect);
+/* Sorted (tile, depth) keys of one camera: keys[K], particle ids[K] and the
+ * tile ranges[2*tiles]. Call with keys == NULL to get K in *n_pairs. */
+gavis_status gavis_debug_binning(gavis_ctx* ctx, const gavis_scene* scene,
+                                 const gavis_camera* cam, const gavis_raster_config* rc,
+                                 uint64_t* keys, int32_t* particle_ids, int64_t* ranges,
+                                 int64_t* n_pairs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAVIS_B200_H */

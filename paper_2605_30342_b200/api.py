@@ -1,0 +1,388 @@
+"""Python mirror of the reference's C++ API for the two hot paths, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference:
+  construct_field          R/include/gavis/vfield.hpp:68-92
+  accumulate_view          vfield.hpp:38-63
+  single_view_visibility   raster.hpp:237-290
+  query_visibility         vfield.hpp:96-112
+  query_view               vfield.hpp:121-134
+  rasterize                raster.hpp:175-231
+  render_entropy(_core)    uncertainty.hpp:124-260
+  image_entropy            uncertainty.hpp:264-278
+  select_nbv               planner.hpp:117-137
+ParameterError / InvariantError are raised where the reference throws them.
+Everything runs on the GPU through libgavis_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .model import (CameraView, EntropyMap, NbvResult, ParameterError, RasterConfig, RenderOutput,
+                    Scene, UncertaintyConfig, ViewQuery, VisibilityField, VmfParams, require)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def camera_c(cam: CameraView) -> N.Camera:
+    c = N.Camera()
+    r = np.asarray(cam.rotation, np.float64).reshape(9)
+    for i in range(9):
+        c.rotation[i] = float(r[i])
+    for i in range(3):
+        c.position[i] = float(cam.position[i])
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fov_h, c.fov_v, c.near_plane = float(cam.fov_h), float(cam.fov_v), float(cam.near)
+    return c
+
+
+def cameras_c(cams: Sequence[CameraView]):
+    arr = (N.Camera * max(1, len(cams)))()
+    for i, cam in enumerate(cams):
+        arr[i] = camera_c(cam)
+    return arr
+
+
+def raster_c(rc: RasterConfig) -> N.RasterConfigC:
+    return N.RasterConfigC(int(rc.tile_size), 0, float(rc.transmittance_cutoff), float(rc.dilation),
+                           float(rc.alpha_clamp_max))
+
+
+def unc_c(uc: UncertaintyConfig) -> N.UncertaintyConfigC:
+    u = N.UncertaintyConfigC()
+    u.beta, u.prior_opacity, u.color_sigma = float(uc.beta), float(uc.prior_opacity), float(uc.color_sigma)
+    q = np.asarray(uc.prior_cov, np.float64).reshape(9)
+    for i in range(9):
+        u.prior_cov[i] = float(q[i])
+    u.correlation_lambda = 1.0
+    return u
+
+
+class Context:
+    """One device context (one process per GPU). stream: an int cudaStream_t handle or None."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self.lib = N.load()
+        h = C.c_void_p()
+        N.check(self.lib.gavis_ctx_create(C.c_int32(device), C.c_void_p(stream) if stream else None,
+                                          C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.h:
+            N.check(self.lib.gavis_ctx_destroy(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self) -> None:
+        N.check(self.lib.gavis_ctx_synchronize(self.h))
+
+    def set_batch(self, n: int) -> None:
+        N.check(self.lib.gavis_ctx_set_batch(self.h, C.c_int32(n)))
+
+    def set_profiling(self, on: bool) -> None:
+        N.check(self.lib.gavis_ctx_set_profiling(self.h, C.c_int32(1 if on else 0)))
+
+    def kernel_time(self, name: str, reset: bool = False):
+        ms = C.c_double()
+        n = C.c_int64()
+        N.check(self.lib.gavis_ctx_kernel_time(self.h, name.encode(), C.byref(ms), C.byref(n),
+                                               C.c_int32(1 if reset else 0)))
+        return ms.value, n.value
+
+    def timer_start(self) -> None:
+        N.check(self.lib.gavis_ctx_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double()
+        N.check(self.lib.gavis_ctx_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        N.check(self.lib.gavis_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def upload(self, scene: Scene) -> "DeviceScene":
+        return DeviceScene(self, scene)
+
+
+class DeviceScene:
+    def __init__(self, ctx: Context, scene: Scene):
+        s = scene.contiguous()
+        self.ctx = ctx
+        self.n = s.num_particles
+        self.color_degree = s.color_degree
+        self.bounds = (s.bounds_min, s.bounds_max)
+        d = N.SceneDesc(self.n, s.color_degree, 0, _ptr(s.positions), _ptr(s.rotations),
+                        _ptr(s.scales), _ptr(s.opacities), _ptr(s.colors), _ptr(s.is_virtual))
+        h = C.c_void_p()
+        N.check(ctx.lib.gavis_scene_upload(ctx.h, C.byref(d), C.byref(h)))
+        self.h = h
+
+    def close(self) -> None:
+        if self.h:
+            N.check(self.ctx.lib.gavis_scene_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceField:
+    def __init__(self, ctx: Context, scene: DeviceScene, handle, degree: int, vmf: VmfParams):
+        self.ctx = ctx
+        self.scene = scene
+        self.h = handle
+        self.degree = degree
+        self.vmf = vmf
+
+    @property
+    def num_views(self) -> int:
+        nv = C.c_int32()
+        N.check(self.ctx.lib.gavis_vf_download(self.h, None, C.byref(nv), None))
+        return nv.value
+
+    def set_num_views(self, n: int) -> None:
+        N.check(self.ctx.lib.gavis_vf_set_num_views(self.h, C.c_int32(n)))
+
+    def download(self) -> VisibilityField:
+        nb = (self.degree + 1) ** 2
+        g = np.zeros((max(1, self.scene.n), nb), np.float64)
+        nv = C.c_int32()
+        N.check(self.ctx.lib.gavis_vf_download(self.h, _ptr(g), C.byref(nv), None))
+        return VisibilityField(self.degree, self.vmf, nv.value, g[: self.scene.n], np.zeros(0, np.uint8))
+
+    def device_gamma(self):
+        p = C.c_void_p()
+        n = C.c_int64()
+        N.check(self.ctx.lib.gavis_vf_device_gamma(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def close(self) -> None:
+        if self.h:
+            N.check(self.ctx.lib.gavis_vf_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _as_dev(ctx: Context, scene) -> DeviceScene:
+    return scene if isinstance(scene, DeviceScene) else ctx.upload(scene)
+
+
+# ----------------------------------------------------------------- VF CONST
+def construct_field(ctx: Context, scene, views: Sequence[CameraView], vmf: VmfParams, degree: int,
+                    rc: RasterConfig = RasterConfig()) -> DeviceField:
+    ds = _as_dev(ctx, scene)
+    arr = cameras_c(views)
+    h = C.c_void_p()
+    N.check(ctx.lib.gavis_vf_construct(ctx.h, ds.h, arr, C.c_int32(len(views)), C.c_double(vmf.kappa),
+                                       C.c_int32(degree), C.byref(raster_c(rc)), C.byref(h)))
+    return DeviceField(ctx, ds, h, degree, vmf)
+
+
+def empty_field(ctx: Context, scene, vmf: VmfParams, degree: int) -> DeviceField:
+    ds = _as_dev(ctx, scene)
+    h = C.c_void_p()
+    N.check(ctx.lib.gavis_vf_create(ctx.h, ds.h, C.c_double(vmf.kappa), C.c_int32(degree), C.byref(h)))
+    return DeviceField(ctx, ds, h, degree, vmf)
+
+
+def accumulate_views(ctx: Context, field: DeviceField, scene, views: Sequence[CameraView],
+                     rc: RasterConfig = RasterConfig()) -> None:
+    ds = _as_dev(ctx, scene)
+    arr = cameras_c(views)
+    N.check(ctx.lib.gavis_vf_accumulate_views(ctx.h, field.h, ds.h, arr, C.c_int32(len(views)),
+                                              C.byref(raster_c(rc))))
+
+
+def accumulate_view(ctx: Context, field: DeviceField, scene, view: CameraView, visibility) -> None:
+    ds = _as_dev(ctx, scene)
+    v = np.ascontiguousarray(visibility, np.float64)
+    N.check(ctx.lib.gavis_vf_accumulate_visibility(ctx.h, field.h, ds.h, C.byref(camera_c(view)), _ptr(v)))
+
+
+def upload_field(ctx: Context, scene, field: VisibilityField) -> DeviceField:
+    ds = _as_dev(ctx, scene)
+    g = np.ascontiguousarray(field.gamma, np.float64)
+    h = C.c_void_p()
+    N.check(ctx.lib.gavis_vf_upload(ctx.h, ds.h, C.c_double(field.vmf.kappa), C.c_int32(field.degree),
+                                    C.c_int32(field.num_views), _ptr(g), C.byref(h)))
+    return DeviceField(ctx, ds, h, field.degree, field.vmf)
+
+
+def single_view_visibility(ctx: Context, scene, cam: CameraView, rc: RasterConfig = RasterConfig(),
+                           with_counts: bool = False):
+    ds = _as_dev(ctx, scene)
+    n = max(1, ds.n)
+    v = np.zeros(n)
+    touch = np.zeros(n, np.int64)
+    cc = np.zeros(cam.width * cam.height, np.int32)
+    N.check(ctx.lib.gavis_single_view_visibility(ctx.h, ds.h, C.byref(camera_c(cam)), C.byref(raster_c(rc)),
+                                                 _ptr(v), _ptr(touch), _ptr(cc) if with_counts else None))
+    if with_counts:
+        return v[: ds.n], touch[: ds.n], cc
+    return v[: ds.n]
+
+
+def query_visibility(ctx: Context, field: DeviceField, particle_index, d) -> np.ndarray:
+    idx = np.ascontiguousarray(np.atleast_1d(particle_index), np.int64)
+    dirs = np.ascontiguousarray(np.asarray(d, np.float64).reshape(-1, 3))
+    require(dirs.shape[0] == idx.shape[0], "query: one direction per particle index")
+    out = np.zeros(max(1, idx.size))
+    N.check(ctx.lib.gavis_vf_query(ctx.h, field.h, _ptr(idx), _ptr(dirs), C.c_int64(idx.size), _ptr(out)))
+    return out[: idx.size]
+
+
+def query_view(ctx: Context, field: DeviceField, scene, cam: CameraView, dilation: float = 0.3) -> ViewQuery:
+    ds = _as_dev(ctx, scene)
+    idx = np.zeros(max(1, ds.n), np.int32)
+    vis = np.zeros(max(1, ds.n))
+    n = C.c_int64()
+    N.check(ctx.lib.gavis_vf_query_view(ctx.h, field.h, ds.h, C.byref(camera_c(cam)), C.c_double(dilation),
+                                        _ptr(idx), _ptr(vis), C.byref(n)))
+    return ViewQuery(idx[: n.value], vis[: n.value])
+
+
+# ----------------------------------------------------------------- UA render
+def render(ctx: Context, scene, field: Optional[DeviceField], cams: Sequence[CameraView],
+           rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(), *,
+           rgb: bool = False, depth: bool = False, transmittance: bool = False, entropy: bool = False,
+           invisible_mass: bool = False, entropy_depth: bool = False, scores: bool = False,
+           contributors: bool = False, splat_visibility=None, with_rgb: bool = False) -> Dict[str, np.ndarray]:
+    """Fused RGB + uncertainty render of several cameras (gavis_ua_render)."""
+    ds = _as_dev(ctx, scene)
+    P = sum(c.width * c.height for c in cams)
+    out: Dict[str, np.ndarray] = {}
+
+    def buf(name, flag, shape, dtype=np.float64):
+        if not flag:
+            return None
+        out[name] = np.zeros(shape, dtype)
+        return out[name]
+
+    o = N.RenderOutputs()
+    o.rgb = _ptr(buf("rgb", rgb, P * 3))
+    o.depth = _ptr(buf("depth", depth, P))
+    o.transmittance = _ptr(buf("transmittance", transmittance, P))
+    o.entropy = _ptr(buf("entropy", entropy, P))
+    o.invisible_mass = _ptr(buf("invisible_mass", invisible_mass, P))
+    o.entropy_depth = _ptr(buf("entropy_depth", entropy_depth, P))
+    o.scores = _ptr(buf("scores", scores, max(1, len(cams))))
+    o.rgb_contributors = _ptr(buf("rgb_contributors", contributors and (rgb or with_rgb), P, np.int32))
+    o.entropy_contributors = _ptr(buf("entropy_contributors", contributors and (entropy or scores), P, np.int32))
+    o.with_rgb = 1 if with_rgb else 0
+    o.with_entropy = 0
+    vis = None if splat_visibility is None else np.ascontiguousarray(splat_visibility, np.float64)
+    if vis is not None and vis.size == 0:
+        vis = np.zeros(1)
+    arr = cameras_c(cams)
+    N.check(ctx.lib.gavis_ua_render(ctx.h, ds.h, field.h if field is not None else None, _ptr(vis), arr,
+                                    C.c_int32(len(cams)), C.byref(raster_c(rc)), C.byref(unc_c(uc)),
+                                    C.byref(o)))
+    if "scores" in out:
+        out["scores"] = out["scores"][: len(cams)]
+    return out
+
+
+def rasterize(ctx: Context, scene, cam: CameraView, rc: RasterConfig = RasterConfig()) -> RenderOutput:
+    r = render(ctx, scene, None, [cam], rc, UncertaintyConfig(), rgb=True, depth=True, transmittance=True)
+    return RenderOutput(cam.width, cam.height, r["rgb"], r["depth"], r["transmittance"])
+
+
+def render_entropy(ctx: Context, scene, field: DeviceField, cam: CameraView, rc: RasterConfig = RasterConfig(),
+                   uc: UncertaintyConfig = UncertaintyConfig(), want_depth: bool = False):
+    require(field is not None, "render_entropy needs a field")
+    r = render(ctx, scene, field, [cam], rc, uc, entropy=True, invisible_mass=True, entropy_depth=want_depth)
+    m = EntropyMap(cam.width, cam.height, r["entropy"], r["invisible_mass"])
+    return (m, r["entropy_depth"]) if want_depth else m
+
+
+def render_entropy_core(ctx: Context, scene, cam: CameraView, rc: RasterConfig, uc: UncertaintyConfig,
+                        vis_by_particle, want_depth: bool = False):
+    r = render(ctx, scene, None, [cam], rc, uc, entropy=True, invisible_mass=True, entropy_depth=want_depth,
+               splat_visibility=vis_by_particle)
+    m = EntropyMap(cam.width, cam.height, r["entropy"], r["invisible_mass"])
+    return (m, r["entropy_depth"]) if want_depth else m
+
+
+def image_entropy(m: EntropyMap, depth=None, uc: Optional[UncertaintyConfig] = None) -> float:
+    """uncertainty.hpp:264-272 (correlation none): plain sum in pixel order."""
+    if depth is not None:
+        require(len(depth) == len(m.entropy), "image_entropy: depth map shape differs from the entropy map")
+    s = 0.0
+    for h in m.entropy:
+        s += float(h)
+    return s
+
+
+def select_nbv(ctx: Context, scene, field: DeviceField, candidates: Sequence[CameraView],
+               rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(),
+               with_rgb: bool = False) -> NbvResult:
+    require(len(candidates) > 0, "select_nbv: candidate list must be nonempty")
+    ds = _as_dev(ctx, scene)
+    scores = np.zeros(len(candidates))
+    best = C.c_int32()
+    arr = cameras_c(candidates)
+    N.check(ctx.lib.gavis_select_nbv(ctx.h, ds.h, field.h, arr, C.c_int32(len(candidates)),
+                                     C.byref(raster_c(rc)), C.byref(unc_c(uc)), C.c_int32(1 if with_rgb else 0),
+                                     _ptr(scores), C.byref(best)))
+    return NbvResult(best.value, scores)
+
+
+# ------------------------------------------------------------------ debug
+def debug_project(ctx: Context, scene, cam: CameraView, dilation: float = 0.3, tile_size: int = 16):
+    ds = _as_dev(ctx, scene)
+    n = max(1, ds.n)
+    culled = np.zeros(n, np.uint8)
+    mean = np.zeros((n, 2))
+    conic = np.zeros((n, 3))
+    depth = np.zeros(n)
+    cover = np.zeros((n, 4), np.int32)
+    trect = np.zeros((n, 4), np.int32)
+    N.check(ctx.lib.gavis_debug_project(ctx.h, ds.h, C.byref(camera_c(cam)), C.c_double(dilation),
+                                        C.c_int32(tile_size), _ptr(culled), _ptr(mean), _ptr(conic),
+                                        _ptr(depth), _ptr(cover), _ptr(trect)))
+    k = ds.n
+    return dict(culled=culled[:k], mean=mean[:k], conic=conic[:k], depth=depth[:k], cover=cover[:k],
+                tile_rect=trect[:k])
+
+
+def debug_binning(ctx: Context, scene, cam: CameraView, rc: RasterConfig = RasterConfig()):
+    ds = _as_dev(ctx, scene)
+    npairs = C.c_int64()
+    N.check(ctx.lib.gavis_debug_binning(ctx.h, ds.h, C.byref(camera_c(cam)), C.byref(raster_c(rc)),
+                                        None, None, None, C.byref(npairs)))
+    K = npairs.value
+    tiles = ((cam.width + rc.tile_size - 1) // rc.tile_size) * ((cam.height + rc.tile_size - 1) // rc.tile_size)
+    keys = np.zeros(max(1, K), np.uint64)
+    ids = np.zeros(max(1, K), np.int32)
+    ranges = np.zeros((tiles, 2), np.int64)
+    N.check(ctx.lib.gavis_debug_binning(ctx.h, ds.h, C.byref(camera_c(cam)), C.byref(raster_c(rc)),
+                                        _ptr(keys), _ptr(ids), _ptr(ranges), C.byref(npairs)))
+    return keys[:K], ids[:K], ranges

@@ -1,0 +1,1212 @@
+// gavis_abi.cu -- host C++ behind the C ABI (include/gavis_b200.h).
+//
+// Orchestrates, per batch of views on one device stream:
+//   K1 preprocess -> K2 scan -> K3 emit keys -> K4 radix sort -> K5 ranges
+//   then VF:  K6a vf_blend -> K6b vf_finalize   (construct_field, vfield.hpp:68-92)
+//   or   UA:  K7 ua_blend  -> K8 score          (render_entropy / rasterize /
+//                                                select_nbv, planner.hpp:117-137)
+// Validation follows the reference's validate() methods (raster.hpp:27-34,
+// model.hpp:99-104, uncertainty.hpp:39-51, sh.hpp:126-128) and maps its
+// exception taxonomy onto status codes (common.hpp:22-46).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "gavis_b200.h"
+#include "kernels.h"
+
+using namespace gavis;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ParamErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DevErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void require(bool cond, const std::string& msg) {
+  if (!cond) throw ParamErr(msg);
+}
+void invariant(bool cond, const std::string& msg) {
+  if (!cond) throw InvErr(msg);
+}
+
+#define CK(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw DevErr(std::string(#expr) + " failed: " + cudaGetErrorString(e_));          \
+  } while (0)
+
+template <class F>
+gavis_status guard(F&& f) {
+  try {
+    f();
+    return GAVIS_OK;
+  } catch (const ParamErr& e) {
+    g_last_error = e.what();
+    return GAVIS_ERR_PARAMETER;
+  } catch (const InvErr& e) {
+    g_last_error = e.what();
+    return GAVIS_ERR_INVARIANT;
+  } catch (const DevErr& e) {
+    g_last_error = e.what();
+    return GAVIS_ERR_DEVICE;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return GAVIS_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GAVIS_ERR_INVARIANT;
+  }
+}
+
+constexpr double kPi = 3.14159265358979323846;
+
+// bessel_i (sh.hpp:93-119) and vmf_degree_scales (sh.hpp:140-147), host side.
+double bessel_i(int l, double x) {
+  require(l >= 0 && l <= 20, "bessel_i: order out of range");
+  require(x >= 0.0 && x <= 50.0, "bessel_i: argument out of range [0, 50]");
+  if (x == 0.0) return l == 0 ? 1.0 : 0.0;
+  if (l == 0) return std::sinh(x) / x;
+  if (l == 1) return (x * std::cosh(x) - std::sinh(x)) / (x * x);
+  if (x >= 2.0 * l + 2.0) {
+    double prev = std::sinh(x) / x;
+    double cur = (x * std::cosh(x) - std::sinh(x)) / (x * x);
+    for (int k = 1; k < l; ++k) {
+      double next = prev - (2.0 * k + 1.0) / x * cur;
+      prev = cur;
+      cur = next;
+    }
+    return cur;
+  }
+  double term = std::pow(x, l);
+  for (int k = 3; k <= 2 * l + 1; k += 2) term /= k;
+  double sum = term;
+  const double x2h = 0.5 * x * x;
+  for (int k = 1; k < 400; ++k) {
+    term *= x2h / (k * (2.0 * l + 2.0 * k + 1.0));
+    sum += term;
+    if (term <= sum * 1e-17) break;
+  }
+  return sum;
+}
+
+void vmf_scales(double kappa, int degree, double* out) {
+  const double zeta = std::exp(-kappa);
+  for (int l = 0; l <= degree; ++l) out[l] = 4.0 * kPi * zeta * bessel_i(l, kappa);
+}
+
+void validate_raster(const gavis_raster_config* rc) {
+  require(rc != nullptr, "raster config must not be null");
+  require(rc->tile_size >= 1, "tile_size must be at least 1");
+  require(rc->transmittance_cutoff > 0.0 && rc->transmittance_cutoff < 1.0,
+          "transmittance_cutoff must lie in (0, 1)");
+  require(rc->dilation >= 0.0, "dilation must be non-negative");
+  require(rc->alpha_clamp_max > 0.0 && rc->alpha_clamp_max <= 1.0,
+          "alpha_clamp_max must lie in (0, 1]");
+}
+
+void validate_camera(const gavis_camera& c) {
+  require(c.width >= 1 && c.height >= 1, "camera image size must be at least 1x1");
+  require(c.fov_h > 0.0 && c.fov_h < kPi && c.fov_v > 0.0 && c.fov_v < kPi,
+          "camera fov must lie in (0, pi)");
+  require(c.near_plane > 0.0, "camera near plane must be positive");
+  require(c.width <= 32767 && c.height <= 32767,
+          "camera image size exceeds the device limit of 32767 pixels per side");
+}
+
+// LLT success and log-determinant of a 3x3 (uncertainty.hpp:44-45, :108-113).
+bool llt3(const double* m, double* logdet) {
+  double L[9] = {0};
+  for (int k = 0; k < 3; ++k) {
+    double sq = 0.0;
+    for (int j = 0; j < k; ++j) sq += L[k * 3 + j] * L[k * 3 + j];
+    double x = k > 0 ? m[k * 3 + k] - sq : m[k * 3 + k];
+    if (!(x > 0.0)) return false;
+    L[k * 3 + k] = std::sqrt(x);
+    for (int r = k + 1; r < 3; ++r) {
+      double dot = 0.0;
+      for (int j = 0; j < k; ++j) dot += L[r * 3 + j] * L[k * 3 + j];
+      double y = k > 0 ? m[r * 3 + k] - dot : m[r * 3 + k];
+      L[r * 3 + k] = y / L[k * 3 + k];
+    }
+  }
+  *logdet = 2.0 * (std::log(L[0]) + std::log(L[4]) + std::log(L[8]));
+  return true;
+}
+
+double det3(const double* m) {
+  return m[0] * (m[4] * m[8] - m[5] * m[7]) - m[3] * (m[1] * m[8] - m[2] * m[7]) +
+         m[6] * (m[1] * m[5] - m[2] * m[4]);
+}
+
+void validate_unc(const gavis_uncertainty_config* uc, double* hl_q0) {
+  require(uc != nullptr, "uncertainty config must not be null");
+  require(uc->beta >= 0.0 && uc->beta <= 1.0, "beta must lie in [0, 1]");
+  require(uc->prior_opacity >= 0.0 && uc->prior_opacity <= 1.0,
+          "prior_opacity must lie in [0, 1]");
+  require(uc->color_sigma > 0.0, "color_sigma must be positive");
+  double logdet = 0.0;
+  require(llt3(uc->prior_cov, &logdet), "prior_cov must be symmetric positive-definite");
+  require(uc->variance_provider == 0,
+          "variance_provider sh_propagation is not supported by the device path");
+  require(uc->correlation == 0, "correlation hook is not supported by the device path");
+  const double det_qc = std::pow(uc->color_sigma, 6.0);
+  require(det3(uc->prior_cov) >= det_qc,
+          "prior_cov determinant must dominate the color covariance");
+  *hl_q0 = 0.5 * logdet;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Timing {
+  double ms = 0.0;
+  int64_t launches = 0;
+};
+
+int bits_for(int64_t n) {  // bits needed to hold values in [0, n)
+  int b = 0;
+  while (b < 62 && (int64_t(1) << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct gavis_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::map<std::string, DevBuf> bufs;
+  int max_batch = 0;
+  bool profiling = false;
+  std::map<std::string, Timing> timing;
+  std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> pending;
+  std::vector<cudaEvent_t> spare_events;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  int64_t launches = 0;
+  int32_t* pinned = nullptr;
+  std::recursive_mutex mu;
+
+  void use() { CK(cudaSetDevice(device)); }
+
+  void* buf(const std::string& name, size_t bytes) {
+    DevBuf& b = bufs[name];
+    if (bytes == 0) bytes = 16;
+    if (b.bytes < bytes) {
+      if (b.p) CK(cudaFree(b.p));
+      size_t want = bytes + bytes / 4;
+      cudaError_t e = cudaMalloc(&b.p, want);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        b.p = nullptr;
+        b.bytes = 0;
+        throw DevErr("cudaMalloc(" + std::to_string(want) + ") for '" + name +
+                     "' failed: " + cudaGetErrorString(e));
+      }
+      b.bytes = want;
+    }
+    return b.p;
+  }
+
+  cudaEvent_t event() {
+    if (!spare_events.empty()) {
+      cudaEvent_t e = spare_events.back();
+      spare_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    return e;
+  }
+
+  template <class F>
+  void run(const char* name, F&& launch, int nlaunch = 1) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profiling) {
+      a = event();
+      b = event();
+      CK(cudaEventRecord(a, stream));
+    }
+    launch();
+    CK(cudaGetLastError());
+    if (profiling) {
+      CK(cudaEventRecord(b, stream));
+      pending.emplace_back(name, a, b);
+    }
+    launches += nlaunch;
+  }
+
+  void sync() {
+    CK(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, std::get<1>(p), std::get<2>(p)));
+      Timing& t = timing[std::get<0>(p)];
+      t.ms += ms;
+      t.launches += 1;
+      spare_events.push_back(std::get<1>(p));
+      spare_events.push_back(std::get<2>(p));
+    }
+    pending.clear();
+  }
+};
+
+struct gavis_scene {
+  gavis_ctx* ctx = nullptr;
+  SceneDev dev;
+  float4* pos_op = nullptr;
+  float4* rot = nullptr;
+  float4* scale = nullptr;
+  uint8_t* virt = nullptr;
+  float* colors = nullptr;
+};
+
+struct gavis_field {
+  gavis_ctx* ctx = nullptr;
+  const gavis_scene* scene = nullptr;
+  int64_t n = 0;
+  int degree = 0;
+  double kappa = 1.0;
+  int num_views = 0;
+  double* gamma = nullptr;
+};
+
+namespace {
+
+DevCam make_devcam(const gavis_camera& c, int ts, int64_t tile_base, int64_t pix_base) {
+  DevCam d;
+  std::memcpy(d.R, c.rotation, sizeof(d.R));
+  std::memcpy(d.pos, c.position, sizeof(d.pos));
+  d.fx = 0.5 * c.width / std::tan(0.5 * c.fov_h);
+  d.fy = 0.5 * c.height / std::tan(0.5 * c.fov_v);
+  d.cx = 0.5 * c.width;
+  d.cy = 0.5 * c.height;
+  d.limx = 1.3 * std::tan(0.5 * c.fov_h);
+  d.limy = 1.3 * std::tan(0.5 * c.fov_v);
+  d.near_plane = c.near_plane;
+  d.width = c.width;
+  d.height = c.height;
+  d.tiles_x = (c.width + ts - 1) / ts;
+  d.tiles_y = (c.height + ts - 1) / ts;
+  d.tile_base = tile_base;
+  d.pix_base = pix_base;
+  return d;
+}
+
+int batch_views(gavis_ctx* c, int64_t N, int n_views) {
+  int vmax = c->max_batch > 0 ? c->max_batch : 16;
+  if (N > 0) {
+    // ~112 B of per-(view, particle) state; keep a batch under ~6 GB of it.
+    const int64_t by_mem = (int64_t)(6.0e9 / (112.0 * (double)N));
+    vmax = (int)std::max<int64_t>(1, std::min<int64_t>(vmax, by_mem));
+  }
+  vmax = std::min(vmax, 64);
+  return std::max(1, std::min(vmax, n_views));
+}
+
+struct Binned {
+  int V = 0;
+  int64_t K = 0;
+  int64_t total_tiles = 0;
+  int64_t total_pix = 0;
+  DevCam* dcams = nullptr;
+  std::vector<DevCam> hcams;
+  GeoRec* geo = nullptr;
+  UaRec* ua = nullptr;
+  int32_t* counts = nullptr;
+  int32_t* offsets = nullptr;
+  uint64_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  uint32_t* pair_gid = nullptr;
+  uint2* ranges = nullptr;
+};
+
+struct BinOpts {
+  bool vf_mode = false;
+  bool ua = false;
+  bool write_culled = false;
+  const gavis_field* field = nullptr;
+  const double* vis_given_dev = nullptr;
+  double beta = 0.5, o0b = 0.075;
+};
+
+// K1..K5 for one batch of cameras.
+Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, int V,
+                 const gavis_raster_config* rc, const BinOpts& o) {
+  Binned b;
+  b.V = V;
+  const int64_t N = s->dev.n;
+  const int ts = rc->tile_size;
+  int64_t tile_base = 0, pix_base = 0;
+  for (int v = 0; v < V; ++v) {
+    DevCam d = make_devcam(cams[v], ts, tile_base, pix_base);
+    tile_base += (int64_t)d.tiles_x * d.tiles_y;
+    pix_base += (int64_t)cams[v].width * cams[v].height;
+    b.hcams.push_back(d);
+  }
+  b.total_tiles = tile_base;
+  b.total_pix = pix_base;
+  invariant(b.total_tiles < (int64_t(1) << 31), "too many tiles in one batch");
+  b.dcams = (DevCam*)c->buf("cams", sizeof(DevCam) * V);
+  CK(cudaMemcpyAsync(b.dcams, b.hcams.data(), sizeof(DevCam) * V, cudaMemcpyHostToDevice,
+                     c->stream));
+  const int64_t VN = (int64_t)V * N;
+  b.geo = (GeoRec*)c->buf("geo", sizeof(GeoRec) * VN);
+  if (o.ua) b.ua = (UaRec*)c->buf("ua", sizeof(UaRec) * VN);
+  b.counts = (int32_t*)c->buf("counts", sizeof(int32_t) * (VN + 1));
+  b.offsets = (int32_t*)c->buf("offsets", sizeof(int32_t) * (VN + 1));
+  uint2* trect = (uint2*)c->buf("trect", sizeof(uint2) * VN);
+
+  PreprocessArgs pa;
+  pa.scene = s->dev;
+  pa.cams = b.dcams;
+  pa.V = V;
+  pa.dilation = rc->dilation;
+  pa.tile_size = ts;
+  pa.geo = b.geo;
+  pa.ua = b.ua;
+  pa.counts = b.counts;
+  pa.trect = trect;
+  pa.write_culled = o.write_culled;
+  pa.beta = o.beta;
+  pa.o0b = o.o0b;
+  if (o.ua) {
+    if (o.vis_given_dev) {
+      pa.query_mode = kQueryGiven;
+      pa.vis_in = o.vis_given_dev;
+    } else if (o.field) {
+      pa.query_mode = kQueryField;
+      pa.gamma = o.field->gamma;
+      pa.degree = o.field->degree;
+      pa.num_views = o.field->num_views;
+    }
+  }
+  c->run("preprocess", [&] { launch_preprocess(pa, c->stream); }, N > 0 ? 1 : 0);
+
+  int32_t total = 0;
+  if (VN > 0) {
+    const size_t sb = scan_temp_bytes(VN);
+    void* tmp = c->buf("scan_tmp", sb);
+    c->run("scan", [&] { exclusive_scan(b.counts, b.offsets, VN, tmp, sb, c->stream); });
+    CK(cudaMemcpyAsync(c->pinned, b.offsets + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 1, b.counts + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    const int64_t K64 = (int64_t)c->pinned[0] + (int64_t)c->pinned[1];
+    invariant(K64 >= 0 && K64 < (int64_t(1) << 31), "pair count overflow in one batch");
+    total = (int32_t)K64;
+  }
+  b.K = total;
+  const int64_t K = b.K;
+  uint64_t* ka = (uint64_t*)c->buf("keys_a", sizeof(uint64_t) * K);
+  uint64_t* kb = (uint64_t*)c->buf("keys_b", sizeof(uint64_t) * K);
+  uint32_t* va = (uint32_t*)c->buf("vals_a", sizeof(uint32_t) * K);
+  uint32_t* vb = (uint32_t*)c->buf("vals_b", sizeof(uint32_t) * K);
+  if (o.vf_mode) b.pair_gid = (uint32_t*)c->buf("pair_gid", sizeof(uint32_t) * K);
+  if (K > 0) {
+    EmitArgs ea;
+    ea.cams = b.dcams;
+    ea.V = V;
+    ea.N = N;
+    ea.geo = b.geo;
+    ea.counts = b.counts;
+    ea.offsets = b.offsets;
+    ea.trect = trect;
+    ea.keys = ka;
+    ea.vals = va;
+    ea.pair_gid = b.pair_gid;
+    c->run("emit_keys", [&] { launch_emit_keys(ea, c->stream); });
+    const size_t sb = sort_temp_bytes(K);
+    void* tmp = c->buf("sort_tmp", sb);
+    const int end_bit = 32 + std::max(1, bits_for(b.total_tiles));
+    c->run("sort", [&] {
+      radix_sort_pairs(ka, kb, va, vb, K, end_bit, tmp, sb, c->stream, &b.keys, &b.vals);
+    });
+  } else {
+    b.keys = ka;
+    b.vals = va;
+  }
+  b.ranges = (uint2*)c->buf("ranges", sizeof(uint2) * std::max<int64_t>(1, b.total_tiles));
+  CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.total_tiles, c->stream));
+  if (K > 0) {
+    RangesArgs ra;
+    ra.cams = b.dcams;
+    ra.V = V;
+    ra.N = N;
+    ra.K = K;
+    ra.keys = b.keys;
+    ra.vals = b.vals;
+    ra.pair_gid = b.pair_gid;
+    ra.geo = b.geo;
+    ra.ranges = b.ranges;
+    c->run("ranges", [&] { launch_ranges(ra, c->stream); });
+  }
+  return b;
+}
+
+void check_scene_field(const gavis_scene* s, const gavis_field* f) {
+  require(s != nullptr, "scene must not be null");
+  if (f) require(f->n == s->dev.n, "field was built for a different scene");
+}
+
+// VF accumulation of views [0, n) into field (or only per-view outputs).
+void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_camera* views,
+              int n_views, const gavis_raster_config* rc, double* vis_host, int64_t* touch_host,
+              int32_t* contrib_host) {
+  const int64_t N = s->dev.n;
+  const int bv = batch_views(c, N, n_views);
+  double scales[kMaxFieldDegree + 1] = {0};
+  if (f) vmf_scales(f->kappa, f->degree, scales);
+  for (int v0 = 0; v0 < n_views; v0 += bv) {
+    const int V = std::min(bv, n_views - v0);
+    BinOpts o;
+    o.vf_mode = true;
+    Binned b = bin_batch(c, s, views + v0, V, rc, o);
+    double* psum = (double*)c->buf("pair_sum", sizeof(double) * b.K);
+    int32_t* pcnt = (int32_t*)c->buf("pair_cnt", sizeof(int32_t) * b.K);
+    if (b.K > 0) {
+      CK(cudaMemsetAsync(psum, 0, sizeof(double) * b.K, c->stream));
+      CK(cudaMemsetAsync(pcnt, 0, sizeof(int32_t) * b.K, c->stream));
+    }
+    int32_t* dcontrib = nullptr;
+    if (contrib_host) dcontrib = (int32_t*)c->buf("contrib", sizeof(int32_t) * b.total_pix);
+    VfBlendArgs va;
+    va.cams = b.dcams;
+    va.V = V;
+    va.N = N;
+    va.total_tiles = b.total_tiles;
+    va.tile_size = rc->tile_size;
+    va.cutoff = rc->transmittance_cutoff;
+    va.amax = rc->alpha_clamp_max;
+    va.geo = b.geo;
+    va.ranges = b.ranges;
+    va.vals = b.vals;
+    va.pair_gid = b.pair_gid;
+    va.pair_sum = psum;
+    va.pair_cnt = pcnt;
+    va.contrib = dcontrib;
+    if (b.K > 0 || dcontrib) c->run("vf_blend", [&] { launch_vf_blend(va, c->stream); });
+    VfFinalizeArgs fa;
+    fa.scene = s->dev;
+    fa.cams = b.dcams;
+    fa.V = V;
+    fa.counts = b.counts;
+    fa.offsets = b.offsets;
+    fa.pair_sum = psum;
+    fa.pair_cnt = pcnt;
+    fa.gamma = f ? f->gamma : nullptr;
+    fa.degree = f ? f->degree : 0;
+    std::memcpy(fa.scales, scales, sizeof(scales));
+    if (vis_host) fa.vis_out = (double*)c->buf("vis_out", sizeof(double) * V * std::max<int64_t>(1, N));
+    if (touch_host)
+      fa.touch_out = (int64_t*)c->buf("touch_out", sizeof(int64_t) * V * std::max<int64_t>(1, N));
+    c->run("vf_finalize", [&] { launch_vf_finalize(fa, N, c->stream); }, N > 0 ? 1 : 0);
+    if (vis_host && N > 0)
+      CK(cudaMemcpyAsync(vis_host + (int64_t)v0 * N, fa.vis_out, sizeof(double) * V * N,
+                         cudaMemcpyDeviceToHost, c->stream));
+    if (touch_host && N > 0)
+      CK(cudaMemcpyAsync(touch_host + (int64_t)v0 * N, fa.touch_out, sizeof(int64_t) * V * N,
+                         cudaMemcpyDeviceToHost, c->stream));
+    if (contrib_host)
+      CK(cudaMemcpyAsync(contrib_host, dcontrib, sizeof(int32_t) * b.total_pix,
+                         cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  }
+  if (f) f->num_views += n_views;
+}
+
+void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t count) {
+  if (host && count > 0)
+    CK(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+}
+
+void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const double* vis_host,
+               const gavis_camera* cams, int n, const gavis_raster_config* rc,
+               const gavis_uncertainty_config* uc, gavis_render_outputs* out) {
+  validate_raster(rc);
+  double hl_q0 = 0.0;
+  validate_unc(uc, &hl_q0);
+  require(cams != nullptr || n == 0, "cameras must not be null");
+  require(out != nullptr, "render outputs must not be null");
+  check_scene_field(s, f);
+  for (int i = 0; i < n; ++i) validate_camera(cams[i]);
+  const int64_t N = s->dev.n;
+  const bool do_rgb = out->rgb || out->depth || out->transmittance || out->rgb_contributors ||
+                      out->with_rgb;
+  const bool do_ent = out->entropy || out->invisible_mass || out->entropy_depth || out->scores ||
+                      out->entropy_contributors || out->with_entropy;
+  if (!do_rgb && !do_ent) return;
+  const double* vis_dev = nullptr;
+  if (!f) {
+    require(vis_host != nullptr || N == 0 || !do_ent,
+            "render needs a field or per-particle splat visibility");
+    if (vis_host && N > 0) {
+      double* d = (double*)c->buf("vis_given", sizeof(double) * N);
+      CK(cudaMemcpyAsync(d, vis_host, sizeof(double) * N, cudaMemcpyHostToDevice, c->stream));
+      vis_dev = d;
+    }
+  }
+  const int bv = batch_views(c, N, n);
+  int64_t pix_done = 0;
+  for (int v0 = 0; v0 < n; v0 += bv) {
+    const int V = std::min(bv, n - v0);
+    BinOpts o;
+    o.ua = do_ent;
+    o.field = f;
+    o.vis_given_dev = vis_dev;
+    o.beta = uc->beta;
+    o.o0b = uc->prior_opacity * (1.0 - uc->beta);
+    Binned b = bin_batch(c, s, cams + v0, V, rc, o);
+    const int64_t P = b.total_pix;
+    UaBlendArgs ua;
+    ua.scene = s->dev;
+    ua.cams = b.dcams;
+    ua.V = V;
+    ua.total_tiles = b.total_tiles;
+    ua.tile_size = rc->tile_size;
+    ua.cutoff = rc->transmittance_cutoff;
+    ua.amax = rc->alpha_clamp_max;
+    ua.hl_qc = 3.0 * std::log(uc->color_sigma);
+    ua.hl_q0 = hl_q0;
+    ua.geo = b.geo;
+    ua.ua = b.ua;
+    ua.ranges = b.ranges;
+    ua.vals = b.vals;
+    ua.do_rgb = do_rgb;
+    ua.do_ent = do_ent;
+    // Images always land in device memory; host copies only when requested.
+    if (do_rgb) {
+      ua.rgb = (double*)c->buf("img_rgb", sizeof(double) * 3 * P);
+      ua.depth = (double*)c->buf("img_depth", sizeof(double) * P);
+      ua.trans = (double*)c->buf("img_trans", sizeof(double) * P);
+      if (out->rgb_contributors) ua.rgb_contrib = (int32_t*)c->buf("img_nrgb", sizeof(int32_t) * P);
+    }
+    if (do_ent) {
+      ua.entropy = (double*)c->buf("img_entropy", sizeof(double) * P);
+      ua.w0 = (double*)c->buf("img_w0", sizeof(double) * P);
+      ua.edepth = out->entropy_depth ? (double*)c->buf("img_edepth", sizeof(double) * P) : nullptr;
+      if (out->entropy_contributors)
+        ua.ent_contrib = (int32_t*)c->buf("img_nent", sizeof(int32_t) * P);
+      ua.tile_score = (double*)c->buf("tile_score", sizeof(double) * std::max<int64_t>(1, b.total_tiles));
+    }
+    c->run("ua_blend", [&] { launch_ua_blend(ua, c->stream); }, b.total_tiles > 0 ? 1 : 0);
+    double* dscores = nullptr;
+    if (do_ent) {
+      dscores = (double*)c->buf("scores", sizeof(double) * V);
+      c->run("score", [&] { launch_score(b.dcams, V, ua.tile_score, dscores, c->stream); });
+    }
+    copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P);
+    copy_out(c, out->depth ? out->depth + pix_done : nullptr, ua.depth, P);
+    copy_out(c, out->transmittance ? out->transmittance + pix_done : nullptr, ua.trans, P);
+    copy_out(c, out->entropy ? out->entropy + pix_done : nullptr, ua.entropy, P);
+    copy_out(c, out->invisible_mass ? out->invisible_mass + pix_done : nullptr, ua.w0, P);
+    copy_out(c, out->entropy_depth ? out->entropy_depth + pix_done : nullptr, ua.edepth, P);
+    copy_out(c, out->scores ? out->scores + v0 : nullptr, dscores, V);
+    if (out->rgb_contributors)
+      CK(cudaMemcpyAsync(out->rgb_contributors + pix_done, ua.rgb_contrib, sizeof(int32_t) * P,
+                         cudaMemcpyDeviceToHost, c->stream));
+    if (out->entropy_contributors)
+      CK(cudaMemcpyAsync(out->entropy_contributors + pix_done, ua.ent_contrib,
+                         sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    pix_done += P;
+  }
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int gavis_abi_version(void) { return GAVIS_ABI_VERSION; }
+
+const char* gavis_last_error(void) { return g_last_error.c_str(); }
+
+gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
+  return guard([&] {
+    require(out != nullptr, "out must not be null");
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    require(device >= 0 && device < count, "device index out of range");
+    auto* c = new gavis_ctx();
+    c->device = device;
+    try {
+      c->use();
+      if (stream) {
+        c->stream = (cudaStream_t)stream;
+      } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+      }
+      CK(cudaMallocHost(&c->pinned, 64));
+      CK(cudaEventCreate(&c->t0));
+      CK(cudaEventCreate(&c->t1));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+gavis_status gavis_ctx_destroy(gavis_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    c->use();
+    cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->bufs)
+      if (kv.second.p) cudaFree(kv.second.p);
+    for (auto e : c->spare_events) cudaEventDestroy(e);
+    for (auto& p : c->pending) {
+      cudaEventDestroy(std::get<1>(p));
+      cudaEventDestroy(std::get<2>(p));
+    }
+    if (c->t0) cudaEventDestroy(c->t0);
+    if (c->t1) cudaEventDestroy(c->t1);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+gavis_status gavis_ctx_synchronize(gavis_ctx* c) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    c->sync();
+  });
+}
+
+gavis_status gavis_ctx_set_batch(gavis_ctx* c, int32_t n) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    require(n >= 0 && n <= 64, "batch must lie in [0, 64]");
+    c->max_batch = n;
+  });
+}
+
+gavis_status gavis_ctx_set_profiling(gavis_ctx* c, int32_t enabled) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    c->sync();
+    c->profiling = enabled != 0;
+  });
+}
+
+gavis_status gavis_ctx_kernel_time(gavis_ctx* c, const char* kernel, double* ms,
+                                   int64_t* launches, int32_t reset) {
+  return guard([&] {
+    require(c != nullptr && kernel != nullptr, "context and kernel name must not be null");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    c->sync();
+    Timing t;
+    auto it = c->timing.find(kernel);
+    if (it != c->timing.end()) t = it->second;
+    if (ms) *ms = t.ms;
+    if (launches) *launches = t.launches;
+    if (reset) c->timing.erase(kernel);
+  });
+}
+
+gavis_status gavis_ctx_timer_start(gavis_ctx* c) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    c->use();
+    CK(cudaEventRecord(c->t0, c->stream));
+  });
+}
+
+gavis_status gavis_ctx_timer_stop(gavis_ctx* c, double* ms) {
+  return guard([&] {
+    require(c != nullptr && ms != nullptr, "context and ms must not be null");
+    c->use();
+    CK(cudaEventRecord(c->t1, c->stream));
+    CK(cudaEventSynchronize(c->t1));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, c->t0, c->t1));
+    *ms = f;
+  });
+}
+
+gavis_status gavis_ctx_launch_count(gavis_ctx* c, int64_t* launches) {
+  return guard([&] {
+    require(c != nullptr && launches != nullptr, "context and out must not be null");
+    *launches = c->launches;
+  });
+}
+
+gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_scene** out) {
+  return guard([&] {
+    require(c != nullptr && d != nullptr && out != nullptr, "null argument");
+    require(d->num_particles >= 0, "num_particles must be non-negative");
+    require(d->num_particles < (int64_t(1) << 31), "num_particles exceeds 2^31 - 1");
+    require(d->color_degree >= 0 && d->color_degree <= kMaxColorDegree,
+            "color_degree must lie in [0, 3] for the device path");
+    const int64_t N = d->num_particles;
+    if (N > 0)
+      require(d->positions && d->rotations && d->scales && d->opacities && d->colors,
+              "scene arrays must not be null");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    auto* s = new gavis_scene();
+    s->ctx = c;
+    const int nb = (d->color_degree + 1) * (d->color_degree + 1);
+    const int cstride = ((3 * nb + 3) / 4) * 4;
+    try {
+      const int64_t M = std::max<int64_t>(N, 1);
+      CK(cudaMalloc(&s->pos_op, sizeof(float4) * M));
+      CK(cudaMalloc(&s->rot, sizeof(float4) * M));
+      CK(cudaMalloc(&s->scale, sizeof(float4) * M));
+      CK(cudaMalloc(&s->virt, M));
+      CK(cudaMalloc(&s->colors, sizeof(float) * cstride * M));
+      std::vector<float4> tmp((size_t)M);
+      for (int64_t i = 0; i < N; ++i)
+        tmp[i] = make_float4(d->positions[3 * i], d->positions[3 * i + 1], d->positions[3 * i + 2],
+                             d->opacities[i]);
+      CK(cudaMemcpy(s->pos_op, tmp.data(), sizeof(float4) * M, cudaMemcpyHostToDevice));
+      for (int64_t i = 0; i < N; ++i)
+        tmp[i] = make_float4(d->rotations[4 * i], d->rotations[4 * i + 1], d->rotations[4 * i + 2],
+                             d->rotations[4 * i + 3]);
+      CK(cudaMemcpy(s->rot, tmp.data(), sizeof(float4) * M, cudaMemcpyHostToDevice));
+      for (int64_t i = 0; i < N; ++i)
+        tmp[i] = make_float4(d->scales[3 * i], d->scales[3 * i + 1], d->scales[3 * i + 2], 0.f);
+      CK(cudaMemcpy(s->scale, tmp.data(), sizeof(float4) * M, cudaMemcpyHostToDevice));
+      std::vector<uint8_t> vm((size_t)M, 0);
+      if (d->is_virtual)
+        for (int64_t i = 0; i < N; ++i) vm[i] = d->is_virtual[i] ? 1 : 0;
+      CK(cudaMemcpy(s->virt, vm.data(), M, cudaMemcpyHostToDevice));
+      if (cstride == 3 * nb) {
+        if (N > 0)
+          CK(cudaMemcpy(s->colors, d->colors, sizeof(float) * cstride * N, cudaMemcpyHostToDevice));
+      } else {
+        std::vector<float> col((size_t)(cstride * M), 0.f);
+        for (int64_t i = 0; i < N; ++i)
+          std::memcpy(&col[i * cstride], d->colors + i * 3 * nb, sizeof(float) * 3 * nb);
+        CK(cudaMemcpy(s->colors, col.data(), sizeof(float) * cstride * M, cudaMemcpyHostToDevice));
+      }
+    } catch (...) {
+      cudaFree(s->pos_op);
+      cudaFree(s->rot);
+      cudaFree(s->scale);
+      cudaFree(s->virt);
+      cudaFree(s->colors);
+      delete s;
+      throw;
+    }
+    s->dev.n = N;
+    s->dev.color_degree = d->color_degree;
+    s->dev.nb = nb;
+    s->dev.cstride = cstride;
+    s->dev.pos_op = s->pos_op;
+    s->dev.rot = s->rot;
+    s->dev.scale = s->scale;
+    s->dev.virt = s->virt;
+    s->dev.colors = s->colors;
+    *out = s;
+  });
+}
+
+gavis_status gavis_scene_destroy(gavis_scene* s) {
+  return guard([&] {
+    if (!s) return;
+    s->ctx->use();
+    cudaStreamSynchronize(s->ctx->stream);
+    cudaFree(s->pos_op);
+    cudaFree(s->rot);
+    cudaFree(s->scale);
+    cudaFree(s->virt);
+    cudaFree(s->colors);
+    delete s;
+  });
+}
+
+gavis_status gavis_scene_num_particles(const gavis_scene* s, int64_t* n) {
+  return guard([&] {
+    require(s != nullptr && n != nullptr, "null argument");
+    *n = s->dev.n;
+  });
+}
+
+static gavis_field* new_field(gavis_ctx* c, const gavis_scene* s, double kappa, int degree) {
+  require(degree >= 0 && degree <= 20, "construct_field: degree out of range");
+  require(degree <= kMaxFieldDegree, "field degree above 4 is not supported by the device path");
+  require(kappa >= 0.0 && kappa <= 50.0, "vmf kappa must lie in [0, 50]");
+  auto* f = new gavis_field();
+  f->ctx = c;
+  f->scene = s;
+  f->n = s->dev.n;
+  f->degree = degree;
+  f->kappa = kappa;
+  const int nb = (degree + 1) * (degree + 1);
+  const size_t bytes = sizeof(double) * nb * std::max<int64_t>(1, f->n);
+  cudaError_t e = cudaMalloc(&f->gamma, bytes);
+  if (e != cudaSuccess) {
+    delete f;
+    throw DevErr(std::string("cudaMalloc(field) failed: ") + cudaGetErrorString(e));
+  }
+  CK(cudaMemsetAsync(f->gamma, 0, bytes, c->stream));
+  return f;
+}
+
+gavis_status gavis_vf_create(gavis_ctx* c, const gavis_scene* s, double kappa, int32_t degree,
+                             gavis_field** out) {
+  return guard([&] {
+    require(c && s && out, "null argument");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    *out = new_field(c, s, kappa, degree);
+    c->sync();
+  });
+}
+
+gavis_status gavis_vf_construct(gavis_ctx* c, const gavis_scene* s, const gavis_camera* views,
+                                int32_t n_views, double kappa, int32_t degree,
+                                const gavis_raster_config* rc, gavis_field** out) {
+  return guard([&] {
+    require(c && s && out, "null argument");
+    require(n_views > 0 && views != nullptr, "construct_field: trajectory must be nonempty");
+    require(degree >= 0 && degree <= 20, "construct_field: degree out of range");
+    validate_raster(rc);
+    for (int i = 0; i < n_views; ++i) validate_camera(views[i]);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    gavis_field* f = new_field(c, s, kappa, degree);
+    try {
+      vf_views(c, s, f, views, n_views, rc, nullptr, nullptr, nullptr);
+    } catch (...) {
+      cudaFree(f->gamma);
+      delete f;
+      throw;
+    }
+    f->num_views = n_views;
+    *out = f;
+  });
+}
+
+gavis_status gavis_vf_accumulate_views(gavis_ctx* c, gavis_field* f, const gavis_scene* s,
+                                       const gavis_camera* views, int32_t n_views,
+                                       const gavis_raster_config* rc) {
+  return guard([&] {
+    require(c && f && s, "null argument");
+    invariant(f->n == s->dev.n, "accumulate_view: field/scene particle count mismatch");
+    require(n_views >= 0 && (views != nullptr || n_views == 0), "views must not be null");
+    validate_raster(rc);
+    for (int i = 0; i < n_views; ++i) validate_camera(views[i]);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    vf_views(c, s, f, views, n_views, rc, nullptr, nullptr, nullptr);
+  });
+}
+
+gavis_status gavis_vf_accumulate_visibility(gavis_ctx* c, gavis_field* f, const gavis_scene* s,
+                                            const gavis_camera* view, const double* vis) {
+  return guard([&] {
+    require(c && f && s && view, "null argument");
+    invariant(f->n == s->dev.n, "accumulate_view: field/scene particle count mismatch");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    const int64_t N = s->dev.n;
+    if (N > 0) {
+      require(vis != nullptr, "visibility must not be null");
+      DevCam d = make_devcam(*view, 16, 0, 0);
+      DevCam* dc = (DevCam*)c->buf("cams", sizeof(DevCam));
+      CK(cudaMemcpyAsync(dc, &d, sizeof(DevCam), cudaMemcpyHostToDevice, c->stream));
+      double* dv = (double*)c->buf("vis_given", sizeof(double) * N);
+      CK(cudaMemcpyAsync(dv, vis, sizeof(double) * N, cudaMemcpyHostToDevice, c->stream));
+      VfFinalizeArgs fa;
+      fa.scene = s->dev;
+      fa.cams = dc;
+      fa.V = 1;
+      fa.vis_given = dv;
+      fa.gamma = f->gamma;
+      fa.degree = f->degree;
+      vmf_scales(f->kappa, f->degree, fa.scales);
+      c->run("vf_finalize", [&] { launch_vf_finalize(fa, N, c->stream); });
+      c->sync();
+    }
+    f->num_views += 1;
+  });
+}
+
+gavis_status gavis_vf_upload(gavis_ctx* c, const gavis_scene* s, double kappa, int32_t degree,
+                             int32_t num_views, const double* gamma, gavis_field** out) {
+  return guard([&] {
+    require(c && s && out, "null argument");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    gavis_field* f = new_field(c, s, kappa, degree);
+    const int nb = (degree + 1) * (degree + 1);
+    if (f->n > 0) {
+      require(gamma != nullptr, "gamma must not be null");
+      CK(cudaMemcpyAsync(f->gamma, gamma, sizeof(double) * nb * f->n, cudaMemcpyHostToDevice,
+                         c->stream));
+    }
+    f->num_views = num_views;
+    c->sync();
+    *out = f;
+  });
+}
+
+gavis_status gavis_vf_download(const gavis_field* f, double* gamma, int32_t* num_views,
+                               int32_t* degree) {
+  return guard([&] {
+    require(f != nullptr, "field must not be null");
+    gavis_ctx* c = f->ctx;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    const int nb = (f->degree + 1) * (f->degree + 1);
+    if (gamma && f->n > 0)
+      CK(cudaMemcpyAsync(gamma, f->gamma, sizeof(double) * nb * f->n, cudaMemcpyDeviceToHost,
+                         c->stream));
+    c->sync();
+    if (num_views) *num_views = f->num_views;
+    if (degree) *degree = f->degree;
+  });
+}
+
+gavis_status gavis_vf_set_num_views(gavis_field* f, int32_t num_views) {
+  return guard([&] {
+    require(f != nullptr, "field must not be null");
+    f->num_views = num_views;
+  });
+}
+
+gavis_status gavis_vf_device_gamma(gavis_field* f, void** ptr, int64_t* count) {
+  return guard([&] {
+    require(f != nullptr, "field must not be null");
+    if (ptr) *ptr = f->gamma;
+    if (count) *count = f->n * (int64_t)((f->degree + 1) * (f->degree + 1));
+  });
+}
+
+gavis_status gavis_vf_destroy(gavis_field* f) {
+  return guard([&] {
+    if (!f) return;
+    f->ctx->use();
+    cudaStreamSynchronize(f->ctx->stream);
+    cudaFree(f->gamma);
+    delete f;
+  });
+}
+
+gavis_status gavis_single_view_visibility(gavis_ctx* c, const gavis_scene* s,
+                                          const gavis_camera* cam, const gavis_raster_config* rc,
+                                          double* vis, int64_t* touch, int32_t* contrib) {
+  return guard([&] {
+    require(c && s && cam, "null argument");
+    validate_raster(rc);
+    validate_camera(*cam);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    vf_views(c, s, nullptr, cam, 1, rc, vis, touch, contrib);
+  });
+}
+
+gavis_status gavis_vf_query(gavis_ctx* c, const gavis_field* f, const int64_t* idx,
+                            const double* dirs, int64_t n, double* out) {
+  return guard([&] {
+    require(c && f, "null argument");
+    require(n >= 0 && (n == 0 || (idx && dirs && out)), "null argument");
+    for (int64_t i = 0; i < n; ++i)
+      require(idx[i] >= 0 && idx[i] < f->n, "query: particle index out of range");
+    if (n == 0) return;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    int64_t* di = (int64_t*)c->buf("q_idx", sizeof(int64_t) * n);
+    double* dd = (double*)c->buf("q_dir", sizeof(double) * 3 * n);
+    double* dout = (double*)c->buf("q_out", sizeof(double) * n);
+    CK(cudaMemcpyAsync(di, idx, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dd, dirs, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    QueryArgs qa;
+    qa.gamma = f->gamma;
+    qa.virt = f->scene->dev.virt;
+    qa.degree = f->degree;
+    qa.num_views = f->num_views;
+    qa.idx = di;
+    qa.dirs = dd;
+    qa.n = n;
+    qa.out = dout;
+    c->run("query", [&] { launch_query(qa, c->stream); });
+    CK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  });
+}
+
+gavis_status gavis_vf_query_view(gavis_ctx* c, const gavis_field* f, const gavis_scene* s,
+                                 const gavis_camera* cam, double dilation, int32_t* idx,
+                                 double* vis, int64_t* n_out) {
+  return guard([&] {
+    require(c && f && s && cam && n_out, "null argument");
+    require(f->n == s->dev.n, "query_view: field/scene particle count mismatch");
+    validate_camera(*cam);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    const int64_t N = s->dev.n;
+    *n_out = 0;
+    if (N == 0) return;
+    gavis_raster_config rc = {16, 0, 1e-4, dilation, 0.99};
+    BinOpts o;
+    o.ua = true;
+    o.field = f;
+    o.write_culled = true;
+    Binned b = bin_batch(c, s, cam, 1, &rc, o);
+    std::vector<uint32_t> flags((size_t)N);
+    std::vector<double> v((size_t)N);
+    CK(cudaMemcpy2DAsync(flags.data(), sizeof(uint32_t), &b.geo[0].flags, sizeof(GeoRec),
+                         sizeof(uint32_t), N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpy2DAsync(v.data(), sizeof(double), &b.ua[0].v, sizeof(UaRec), sizeof(double), N,
+                         cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    int64_t k = 0;
+    for (int64_t i = 0; i < N; ++i) {
+      if (!(flags[i] & 1u)) continue;
+      if (idx) idx[k] = (int32_t)i;
+      if (vis) vis[k] = v[i];
+      ++k;
+    }
+    *n_out = k;
+  });
+}
+
+gavis_status gavis_ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
+                             const double* splat_visibility, const gavis_camera* cams,
+                             int32_t n_cams, const gavis_raster_config* rc,
+                             const gavis_uncertainty_config* uc, gavis_render_outputs* out) {
+  return guard([&] {
+    require(c && s, "null argument");
+    require(n_cams >= 0, "camera count must be non-negative");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    ua_render(c, s, f, splat_visibility, cams, n_cams, rc, uc, out);
+  });
+}
+
+gavis_status gavis_select_nbv(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
+                              const gavis_camera* cams, int32_t n_cams,
+                              const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
+                              int32_t with_rgb, double* scores, int32_t* best) {
+  return guard([&] {
+    require(c && s && f, "null argument");
+    require(n_cams > 0 && cams != nullptr, "select_nbv: candidate list must be nonempty");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    std::vector<double> sc((size_t)n_cams);
+    gavis_render_outputs o = {};
+    o.scores = sc.data();
+    o.with_rgb = with_rgb;
+    ua_render(c, s, f, nullptr, cams, n_cams, rc, uc, &o);
+    int b = 0;
+    for (int i = 1; i < n_cams; ++i)
+      if (sc[i] > sc[b]) b = i;
+    if (scores) std::memcpy(scores, sc.data(), sizeof(double) * n_cams);
+    if (best) *best = b;
+  });
+}
+
+gavis_status gavis_debug_project(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cam,
+                                 double dilation, int32_t tile_size, uint8_t* culled,
+                                 double* mean, double* conic, double* depth, int32_t* cover_rect,
+                                 int32_t* tile_rect) {
+  return guard([&] {
+    require(c && s && cam, "null argument");
+    validate_camera(*cam);
+    require(tile_size >= 1, "tile_size must be at least 1");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    const int64_t N = s->dev.n;
+    if (N == 0) return;
+    gavis_raster_config rc = {tile_size, 0, 1e-4, dilation, 0.99};
+    BinOpts o;
+    o.write_culled = true;
+    Binned b = bin_batch(c, s, cam, 1, &rc, o);
+    std::vector<GeoRec> g((size_t)N);
+    std::vector<uint2> tr((size_t)N);
+    CK(cudaMemcpyAsync(g.data(), b.geo, sizeof(GeoRec) * N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(tr.data(), c->bufs["trect"].p, sizeof(uint2) * N, cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    for (int64_t i = 0; i < N; ++i) {
+      const bool ok = g[i].flags & 1u;
+      if (culled) culled[i] = ok ? 0 : 1;
+      if (mean) {
+        mean[2 * i] = g[i].mx;
+        mean[2 * i + 1] = g[i].my;
+      }
+      if (conic) {
+        conic[3 * i] = g[i].ca;
+        conic[3 * i + 1] = g[i].cb2 * 0.5;
+        conic[3 * i + 2] = g[i].cc;
+      }
+      if (depth) depth[i] = g[i].depth;
+      if (cover_rect) {
+        cover_rect[4 * i] = g[i].cov_x & 0xFFFF;
+        cover_rect[4 * i + 1] = (g[i].cov_x >> 16) & 0xFFFF;
+        cover_rect[4 * i + 2] = g[i].cov_y & 0xFFFF;
+        cover_rect[4 * i + 3] = (g[i].cov_y >> 16) & 0xFFFF;
+      }
+      if (tile_rect) {
+        tile_rect[4 * i] = tr[i].x & 0xFFFF;
+        tile_rect[4 * i + 1] = tr[i].x >> 16;
+        tile_rect[4 * i + 2] = tr[i].y & 0xFFFF;
+        tile_rect[4 * i + 3] = tr[i].y >> 16;
+      }
+    }
+  });
+}
+
+gavis_status gavis_debug_binning(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cam,
+                                 const gavis_raster_config* rc, uint64_t* keys,
+                                 int32_t* particle_ids, int64_t* ranges, int64_t* n_pairs) {
+  return guard([&] {
+    require(c && s && cam && n_pairs, "null argument");
+    validate_raster(rc);
+    validate_camera(*cam);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    BinOpts o;
+    Binned b = bin_batch(c, s, cam, 1, rc, o);
+    *n_pairs = b.K;
+    if (keys && b.K > 0)
+      CK(cudaMemcpyAsync(keys, b.keys, sizeof(uint64_t) * b.K, cudaMemcpyDeviceToHost, c->stream));
+    if (particle_ids && b.K > 0)
+      CK(cudaMemcpyAsync(particle_ids, b.vals, sizeof(uint32_t) * b.K, cudaMemcpyDeviceToHost,
+                         c->stream));
+    std::vector<uint2> rg((size_t)std::max<int64_t>(1, b.total_tiles));
+    if (ranges && b.total_tiles > 0)
+      CK(cudaMemcpyAsync(rg.data(), b.ranges, sizeof(uint2) * b.total_tiles,
+                         cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (ranges)
+      for (int64_t t = 0; t < b.total_tiles; ++t) {
+        ranges[2 * t] = rg[t].x;
+        ranges[2 * t + 1] = rg[t].y;
+      }
+  });
+}
+
+}  // extern "C"

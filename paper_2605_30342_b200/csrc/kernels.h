@@ -1,0 +1,159 @@
+// kernels.h -- host-callable launchers of the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device_common.cuh"
+
+namespace gavis {
+
+// Device-resident scene (fp32 SoA, 16-byte vectors).
+struct SceneDev {
+  int64_t n = 0;
+  int color_degree = 0;
+  int nb = 1;       // (Lc+1)^2
+  int cstride = 4;  // floats per particle in `colors` (3*nb rounded up to 4)
+  const float4* pos_op = nullptr;  // x, y, z, opacity
+  const float4* rot = nullptr;     // w, x, y, z
+  const float4* scale = nullptr;   // sx, sy, sz, 0
+  const uint8_t* virt = nullptr;
+  const float* colors = nullptr;
+};
+
+enum QueryMode : int { kQueryNone = 0, kQueryField = 1, kQueryGiven = 2 };
+
+struct PreprocessArgs {
+  SceneDev scene;
+  const DevCam* cams = nullptr;
+  int V = 0;
+  double dilation = 0.3;
+  int tile_size = 16;
+  GeoRec* geo = nullptr;     // [V*N]
+  UaRec* ua = nullptr;       // [V*N] (null for VF)
+  int32_t* counts = nullptr; // [V*N] tiles touched
+  uint2* trect = nullptr;    // [V*N] tx0|tx1<<16, ty0|ty1<<16
+  int query_mode = kQueryNone;
+  const double* gamma = nullptr;  // [N*(L+1)^2]
+  int degree = 0;
+  int num_views = 0;
+  const double* vis_in = nullptr;  // [N] for kQueryGiven
+  double beta = 0.5, o0b = 0.075;  // o0b = o0 * (1 - beta)
+  bool write_culled = false;
+};
+
+struct EmitArgs {
+  const DevCam* cams = nullptr;
+  int V = 0;
+  int64_t N = 0;
+  const GeoRec* geo = nullptr;
+  const int32_t* counts = nullptr;
+  const int32_t* offsets = nullptr;
+  const uint2* trect = nullptr;
+  uint64_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  uint32_t* pair_gid = nullptr;  // VF mode: vals = pair index, pair_gid[pair] = particle
+};
+
+struct RangesArgs {
+  const DevCam* cams = nullptr;
+  int V = 0;
+  int64_t N = 0;
+  int64_t K = 0;
+  const uint64_t* keys = nullptr;
+  uint32_t* vals = nullptr;
+  const uint32_t* pair_gid = nullptr;
+  const GeoRec* geo = nullptr;
+  uint2* ranges = nullptr;
+};
+
+struct VfBlendArgs {
+  const DevCam* cams = nullptr;
+  int V = 0;
+  int64_t N = 0;
+  int64_t total_tiles = 0;
+  int tile_size = 16;
+  double cutoff = 1e-4, amax = 0.99;
+  const GeoRec* geo = nullptr;
+  const uint2* ranges = nullptr;
+  const uint32_t* vals = nullptr;      // sorted pair indices
+  const uint32_t* pair_gid = nullptr;
+  double* pair_sum = nullptr;          // [K] sum of T (original pair order)
+  int32_t* pair_cnt = nullptr;         // [K]
+  int32_t* contrib = nullptr;          // [V*W*H] or null
+};
+
+struct VfFinalizeArgs {
+  SceneDev scene;
+  const DevCam* cams = nullptr;
+  int V = 0;
+  const int32_t* counts = nullptr;
+  const int32_t* offsets = nullptr;
+  const double* pair_sum = nullptr;
+  const int32_t* pair_cnt = nullptr;
+  const double* vis_given = nullptr;  // [N] accumulate caller-provided v (V == 1)
+  double* gamma = nullptr;            // null: do not accumulate
+  int degree = 0;
+  double scales[kMaxFieldDegree + 1] = {0};
+  double* vis_out = nullptr;          // [V*N]
+  int64_t* touch_out = nullptr;       // [V*N]
+};
+
+struct UaBlendArgs {
+  SceneDev scene;
+  const DevCam* cams = nullptr;
+  int V = 0;
+  int64_t total_tiles = 0;
+  int tile_size = 16;
+  double cutoff = 1e-4, amax = 0.99;
+  double hl_qc = 0.0, hl_q0 = 0.0;
+  const GeoRec* geo = nullptr;
+  const UaRec* ua = nullptr;
+  const uint2* ranges = nullptr;
+  const uint32_t* vals = nullptr;  // sorted particle ids
+  // outputs (device, camera-major); null = not written
+  double* rgb = nullptr;
+  double* depth = nullptr;
+  double* trans = nullptr;
+  double* entropy = nullptr;
+  double* w0 = nullptr;
+  double* edepth = nullptr;
+  int32_t* rgb_contrib = nullptr;
+  int32_t* ent_contrib = nullptr;
+  double* tile_score = nullptr;  // [total_tiles] per-tile entropy sum
+  bool do_rgb = true, do_ent = true;
+};
+
+struct QueryArgs {
+  const double* gamma = nullptr;
+  const uint8_t* virt = nullptr;
+  int degree = 0;
+  int num_views = 0;
+  const int64_t* idx = nullptr;
+  const double* dirs = nullptr;
+  int64_t n = 0;
+  double* out = nullptr;
+};
+
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
+void launch_emit_keys(const EmitArgs& a, cudaStream_t s);
+void launch_ranges(const RangesArgs& a, cudaStream_t s);
+void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s);
+void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s);
+void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s);
+void launch_score(const DevCam* cams, int V, const double* tile_score, double* scores,
+                  cudaStream_t s);
+void launch_query(const QueryArgs& a, cudaStream_t s);
+
+// CUB-backed device primitives (sort.cu)
+size_t scan_temp_bytes(int64_t n);
+void exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes,
+                    cudaStream_t s);
+size_t sort_temp_bytes(int64_t n);
+// Sorts (keys, vals) ascending by bits [0, end_bit); results land in the
+// buffers returned through *keys_out / *vals_out (one of the two pairs).
+void radix_sort_pairs(uint64_t* keys_a, uint64_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                      int64_t n, int end_bit, void* temp, size_t temp_bytes, cudaStream_t s,
+                      uint64_t** keys_out, uint32_t** vals_out);
+
+}  // namespace gavis

@@ -1,0 +1,347 @@
+// kernels_preprocess.cu -- projection (K1), key emission (K3), tile ranges with
+// depth-tie fix-up (K5) and the batch field query.
+//
+// K1 replaces project_particle / project_scene (R/include/gavis/raster.hpp:51-130)
+// and, for the uncertainty render, query_visibility at the camera-to-centre
+// direction (vfield.hpp:96-112 via uncertainty.hpp:251-257). One thread per
+// Gaussian projects it into all V views of the batch, so the particle record
+// and its SH field row are read from HBM once per batch, not once per view.
+#include "kernels.h"
+
+#include <cstdio>
+
+namespace gavis {
+
+namespace {
+
+constexpr int kMaxBatchViews = 64;
+
+struct Sigma {
+  double s00, s01, s02, s11, s12, s22;
+};
+
+// GaussianParticle::covariance (model.hpp:42-45), Eigen toRotationMatrix order.
+__device__ __forceinline__ Sigma covariance(float4 q, float4 sc) {
+  const double w = q.x, x = q.y, y = q.z, z = q.w;
+  const double tx = 2.0 * x, ty = 2.0 * y, tz = 2.0 * z;
+  const double twx = tx * w, twy = ty * w, twz = tz * w;
+  const double txx = tx * x, txy = ty * x, txz = tz * x;
+  const double tyy = ty * y, tyz = tz * y, tzz = tz * z;
+  const double R00 = 1.0 - (tyy + tzz), R01 = txy - twz, R02 = txz + twy;
+  const double R10 = txy + twz, R11 = 1.0 - (txx + tzz), R12 = tyz - twx;
+  const double R20 = txz - twy, R21 = tyz + twx, R22 = 1.0 - (txx + tyy);
+  const double sx = sc.x, sy = sc.y, sz = sc.z;
+  const double m00 = R00 * sx, m01 = R01 * sy, m02 = R02 * sz;
+  const double m10 = R10 * sx, m11 = R11 * sy, m12 = R12 * sz;
+  const double m20 = R20 * sx, m21 = R21 * sy, m22 = R22 * sz;
+  Sigma s;
+  s.s00 = m00 * m00 + m01 * m01 + m02 * m02;
+  s.s01 = m00 * m10 + m01 * m11 + m02 * m12;
+  s.s02 = m00 * m20 + m01 * m21 + m02 * m22;
+  s.s11 = m10 * m10 + m11 * m11 + m12 * m12;
+  s.s12 = m10 * m20 + m11 * m21 + m12 * m22;
+  s.s22 = m20 * m20 + m21 * m21 + m22 * m22;
+  return s;
+}
+
+struct Projected {
+  double mx, my, c00, c01, c10, c11, depth, radius, det;
+};
+
+// project_particle (raster.hpp:51-93): returns false when culled.
+__device__ __forceinline__ bool project(const DevCam& c, double px, double py, double pz,
+                                        const Sigma& S, double dilation, Projected& o) {
+  const double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
+  const double t0 = c.R[0] * d0 + c.R[3] * d1 + c.R[6] * d2;
+  const double t1 = c.R[1] * d0 + c.R[4] * d1 + c.R[7] * d2;
+  const double t2 = c.R[2] * d0 + c.R[5] * d1 + c.R[8] * d2;
+  if (t2 < c.near_plane) return false;
+  const double fx = c.fx, fy = c.fy;
+  const double inv_z = 1.0 / t2;
+  const double mx = c.cx + fx * t0 * inv_z;
+  const double my = c.cy + fy * t1 * inv_z;
+  double ux = t0 * inv_z, uy = t1 * inv_z;
+  ux = ux < -c.limx ? -c.limx : (c.limx < ux ? c.limx : ux);
+  uy = uy < -c.limy ? -c.limy : (c.limy < uy ? c.limy : uy);
+  const double jx = ux * t2;
+  const double jy = uy * t2;
+  // W = R^T, cov_cam = (W Sigma) W^T ; W(r,k) = R(k,r) = c.R[k*3+r]
+  const double Sg[9] = {S.s00, S.s01, S.s02, S.s01, S.s11, S.s12, S.s02, S.s12, S.s22};
+  double A[9], C[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      A[r * 3 + k] = c.R[0 * 3 + r] * Sg[0 * 3 + k] + c.R[1 * 3 + r] * Sg[1 * 3 + k] +
+                     c.R[2 * 3 + r] * Sg[2 * 3 + k];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      C[r * 3 + k] = A[r * 3 + 0] * c.R[0 * 3 + k] + A[r * 3 + 1] * c.R[1 * 3 + k] +
+                     A[r * 3 + 2] * c.R[2 * 3 + k];
+  const double J[6] = {fx * inv_z, 0.0, -fx * jx * inv_z * inv_z,
+                       0.0, fy * inv_z, -fy * jy * inv_z * inv_z};
+  double B[6];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      B[r * 3 + k] = J[r * 3 + 0] * C[0 * 3 + k] + J[r * 3 + 1] * C[1 * 3 + k] +
+                     J[r * 3 + 2] * C[2 * 3 + k];
+  double c00 = B[0] * J[0] + B[1] * J[1] + B[2] * J[2];
+  const double c01 = B[0] * J[3] + B[1] * J[4] + B[2] * J[5];
+  const double c10 = B[3] * J[0] + B[4] * J[1] + B[5] * J[2];
+  double c11 = B[3] * J[3] + B[4] * J[4] + B[5] * J[5];
+  c00 += dilation * dilation;
+  c11 += dilation * dilation;
+  const double det = c00 * c11 - c01 * c10;
+  if (det <= 0.0) return false;
+  const double mid = 0.5 * (c00 + c11);
+  const double disc = mid * mid - det;
+  const double lam_max = mid + sqrt(disc > 0.0 ? disc : 0.0);
+  const double radius = 3.0 * sqrt(lam_max);
+  if (mx < -radius || mx > c.width + radius || my < -radius || my > c.height + radius)
+    return false;
+  o.mx = mx;
+  o.my = my;
+  o.c00 = c00;
+  o.c01 = c01;
+  o.c10 = c10;
+  o.c11 = c11;
+  o.depth = t2;
+  o.radius = radius;
+  o.det = det;
+  return true;
+}
+
+// query_visibility (vfield.hpp:96-112) on a register-resident row.
+template <int DEG>
+__device__ __forceinline__ double query_row(const double* row, int num_views, double x, double y,
+                                            double z) {
+  constexpr int NB = (DEG + 1) * (DEG + 1);
+  double basis[NB];
+  eval_sh<DEG>(x, y, z, basis);
+  double vt = 0.0;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) vt += row[i] * basis[i];
+  const double p = (double)num_views;
+  if (vt < 0.0) vt = 0.0;
+  if (vt > p) vt = p;
+  double v = 1.0 - pow(1.0 - vt / p, p);
+  return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+}
+
+template <int QDEG>
+__global__ void __launch_bounds__(128) preprocess_kernel(PreprocessArgs a) {
+  __shared__ DevCam s_cam[kMaxBatchViews];
+  for (int i = threadIdx.x; i < a.V * (int)(sizeof(DevCam) / 8); i += blockDim.x)
+    reinterpret_cast<double*>(s_cam)[i] = reinterpret_cast<const double*>(a.cams)[i];
+  __syncthreads();
+  const int64_t N = a.scene.n;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= N) return;
+  const float4 po = a.scene.pos_op[g];
+  const float4 q = a.scene.rot[g];
+  const float4 sc = a.scene.scale[g];
+  const uint8_t virt = a.scene.virt ? a.scene.virt[g] : 0;
+  const Sigma S = covariance(q, sc);
+  const double px = po.x, py = po.y, pz = po.z;
+  constexpr int NBQ = QDEG >= 0 ? (QDEG + 1) * (QDEG + 1) : 1;
+  double row[NBQ];
+  bool have_row = false;
+  if (QDEG >= 0 && a.query_mode == kQueryField && !virt && a.num_views > 0) {
+    const double* gr = a.gamma + g * NBQ;
+#pragma unroll
+    for (int i = 0; i < NBQ; ++i) row[i] = gr[i];
+    have_row = true;
+  }
+  for (int v = 0; v < a.V; ++v) {
+    const DevCam& c = s_cam[v];
+    const int64_t slot = (int64_t)v * N + g;
+    Projected p;
+    int tx0 = 1, tx1 = 0, ty0 = 1, ty1 = 0;
+    bool ok = project(c, px, py, pz, S, a.dilation, p);
+    int32_t count = 0;
+    if (ok) {
+      int x0, x1, y0, y1;
+      covered_pixel_range(p.mx, p.radius, c.width, x0, x1);
+      covered_pixel_range(p.my, p.radius, c.height, y0, y1);
+      if (!(x0 > x1 || y0 > y1)) {
+        tx0 = x0 / a.tile_size;
+        tx1 = x1 / a.tile_size;
+        ty0 = y0 / a.tile_size;
+        ty1 = y1 / a.tile_size;
+        count = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+      }
+      GeoRec r;
+      const double inv_det = 1.0 / p.det;
+      r.mx = p.mx;
+      r.my = p.my;
+      r.ca = p.c11 * inv_det;
+      r.cb2 = 2.0 * (-p.c01 * inv_det);
+      r.cc = p.c00 * inv_det;
+      r.depth = p.depth;
+      r.cov_x = exact_cover(x0, x1, c.width, p.mx, p.radius);
+      r.cov_y = exact_cover(y0, y1, c.height, p.my, p.radius);
+      r.opacity = po.w;
+      r.flags = 1u;
+      a.geo[slot] = r;
+      if (a.ua) {
+        double vis = 0.0;
+        if (a.query_mode == kQueryGiven) {
+          vis = a.vis_in[g];
+        } else if (QDEG >= 0 && have_row) {
+          const double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
+          const double norm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+          if (!(norm < 1e-12))
+            vis = query_row<(QDEG >= 0 ? QDEG : 0)>(row, a.num_views, d0 / norm, d1 / norm,
+                                                     d2 / norm);
+        }
+        UaRec u;
+        u.v = vis;
+        u.omv = 1.0 - vis;
+        u.A = vis + a.beta * (1.0 - vis);
+        u.B = a.o0b * (1.0 - vis);
+        a.ua[slot] = u;
+      }
+    } else if (a.write_culled) {
+      GeoRec r = {};
+      r.cov_x = 1;
+      r.cov_y = 1;
+      a.geo[slot] = r;
+    }
+    a.counts[slot] = count;
+    a.trect[slot] = make_uint2((uint32_t)(tx0 & 0xFFFF) | ((uint32_t)(tx1 & 0xFFFF) << 16),
+                               (uint32_t)(ty0 & 0xFFFF) | ((uint32_t)(ty1 & 0xFFFF) << 16));
+  }
+}
+
+__global__ void emit_keys_kernel(EmitArgs a) {
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= (int64_t)a.V * a.N) return;
+  const int32_t cnt = a.counts[slot];
+  if (cnt == 0) return;
+  const int v = (int)(slot / a.N);
+  const uint32_t g = (uint32_t)(slot - (int64_t)v * a.N);
+  const DevCam& c = a.cams[v];
+  const uint2 tr = a.trect[slot];
+  const int tx0 = tr.x & 0xFFFF, tx1 = tr.x >> 16, ty0 = tr.y & 0xFFFF, ty1 = tr.y >> 16;
+  // fp32 depth rounded toward zero is monotone in the fp64 depth; runs of equal
+  // fp32 keys are re-ordered by (fp64 depth, index) in ranges_kernel.
+  const float df = __double2float_rz(a.geo[slot].depth);
+  const uint64_t dk = (uint64_t)__float_as_uint(df);
+  int64_t o = a.offsets[slot];
+  for (int ty = ty0; ty <= ty1; ++ty) {
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const uint64_t tile = (uint64_t)(c.tile_base + (int64_t)ty * c.tiles_x + tx);
+      a.keys[o] = (tile << 32) | dk;
+      if (a.pair_gid) {
+        a.vals[o] = (uint32_t)o;
+        a.pair_gid[o] = g;
+      } else {
+        a.vals[o] = g;
+      }
+      ++o;
+    }
+  }
+}
+
+__device__ __forceinline__ int view_of_tile(const DevCam* cams, int V, int64_t tile) {
+  int v = 0;
+  while (v + 1 < V && cams[v + 1].tile_base <= tile) ++v;
+  return v;
+}
+
+__global__ void ranges_kernel(RangesArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.K) return;
+  const uint64_t key = a.keys[i];
+  const uint64_t tile = key >> 32;
+  if (i == 0 || (a.keys[i - 1] >> 32) != tile) a.ranges[tile].x = (uint32_t)i;
+  if (i == a.K - 1 || (a.keys[i + 1] >> 32) != tile) a.ranges[tile].y = (uint32_t)(i + 1);
+  // Depth-tie fix-up: the stable radix sort orders equal fp32 keys by particle
+  // index; the reference orders by (fp64 depth, index) (raster.hpp:124-128).
+  if (i + 1 < a.K && a.keys[i + 1] == key && (i == 0 || a.keys[i - 1] != key)) {
+    int64_t j = i;
+    while (j + 1 < a.K && a.keys[j + 1] == key) ++j;
+    const int v = view_of_tile(a.cams, a.V, (int64_t)tile);
+    const GeoRec* geo = a.geo + (int64_t)v * a.N;
+    for (int64_t x = i + 1; x <= j; ++x) {
+      const uint32_t val = a.vals[x];
+      const uint32_t gx = a.pair_gid ? a.pair_gid[val] : val;
+      const double dx = geo[gx].depth;
+      int64_t y = x - 1;
+      while (y >= i) {
+        const uint32_t vy = a.vals[y];
+        const uint32_t gy = a.pair_gid ? a.pair_gid[vy] : vy;
+        const double dy = geo[gy].depth;
+        if (dy < dx || (dy == dx && gy < gx)) break;
+        a.vals[y + 1] = vy;
+        --y;
+      }
+      a.vals[y + 1] = val;
+    }
+  }
+}
+
+template <int DEG>
+__global__ void query_kernel(QueryArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  constexpr int NB = (DEG + 1) * (DEG + 1);
+  const int64_t g = a.idx[i];
+  double out = 0.0;
+  if (!(a.virt && a.virt[g]) && a.num_views > 0) {
+    double row[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) row[k] = a.gamma[g * NB + k];
+    out = query_row<DEG>(row, a.num_views, a.dirs[3 * i], a.dirs[3 * i + 1], a.dirs[3 * i + 2]);
+  }
+  a.out[i] = out;
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
+  if (a.scene.n == 0 || a.V == 0) return;
+  const unsigned grid = blocks_for(a.scene.n, 128);
+  const int qd = a.query_mode == kQueryField ? a.degree : -1;
+  switch (qd) {
+    case -1: preprocess_kernel<-1><<<grid, 128, 0, s>>>(a); break;
+    case 0: preprocess_kernel<0><<<grid, 128, 0, s>>>(a); break;
+    case 1: preprocess_kernel<1><<<grid, 128, 0, s>>>(a); break;
+    case 2: preprocess_kernel<2><<<grid, 128, 0, s>>>(a); break;
+    case 3: preprocess_kernel<3><<<grid, 128, 0, s>>>(a); break;
+    case 4: preprocess_kernel<4><<<grid, 128, 0, s>>>(a); break;
+    default: break;
+  }
+}
+
+void launch_emit_keys(const EmitArgs& a, cudaStream_t s) {
+  const int64_t n = (int64_t)a.V * a.N;
+  if (n == 0) return;
+  emit_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(a);
+}
+
+void launch_ranges(const RangesArgs& a, cudaStream_t s) {
+  if (a.K == 0) return;
+  ranges_kernel<<<blocks_for(a.K, 256), 256, 0, s>>>(a);
+}
+
+void launch_query(const QueryArgs& a, cudaStream_t s) {
+  if (a.n == 0) return;
+  const unsigned grid = blocks_for(a.n, 128);
+  switch (a.degree) {
+    case 0: query_kernel<0><<<grid, 128, 0, s>>>(a); break;
+    case 1: query_kernel<1><<<grid, 128, 0, s>>>(a); break;
+    case 2: query_kernel<2><<<grid, 128, 0, s>>>(a); break;
+    case 3: query_kernel<3><<<grid, 128, 0, s>>>(a); break;
+    case 4: query_kernel<4><<<grid, 128, 0, s>>>(a); break;
+    default: break;
+  }
+}
+
+}  // namespace gavis

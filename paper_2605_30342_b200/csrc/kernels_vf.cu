@@ -1,0 +1,216 @@
+// kernels_vf.cu -- VF CONST blend (K6a) and SH finalize (K6b).
+//
+// K6a replaces the per-tile loop of single_view_visibility
+// (R/include/gavis/raster.hpp:249-274): per pixel, front to back over the
+// covered entries, v_k += T, c_k += 1, T *= 1 - alpha, stop once T < cutoff.
+// One CTA per 16x16 tile, one thread per pixel, warps on 8x4 pixel patches.
+// Entries are staged in shared memory in batches; per entry the covered lanes
+// of a warp are found with a ballot and their T values summed with a
+// fixed-order shuffle tree, so the per-(tile, entry) partial is deterministic.
+// Partials land in the entry's ORIGINAL pair slot: pairs of one particle are
+// emitted in ascending tile order, so K6b can fold them in the reference's
+// tile-merge order (raster.hpp:276-285).
+//
+// K6b replaces the merge/average (raster.hpp:276-289) and accumulate_view
+// (vfield.hpp:38-63): one thread per particle folds its pairs, divides by the
+// touch count and adds v * a_l * Y_lm(d) to its SH row, views in trajectory
+// order.
+#include "kernels.h"
+
+namespace gavis {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBatch = 128;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ int find_view(const DevCam* cams, int V, int64_t tile) {
+  int v = 0;
+  while (v + 1 < V && cams[v + 1].tile_base <= tile) ++v;
+  return v;
+}
+
+// Pixel of thread `tid` in round `round` of a ts x ts tile. For 16x16 tiles each
+// warp owns an 8x4 patch (squarer footprint -> fewer divergent lanes per splat).
+__device__ __forceinline__ void tile_pixel(int ts, int tid, int round, int& lx, int& ly) {
+  if (ts == 16) {
+    const int w = tid >> 5, lane = tid & 31;
+    lx = (w & 1) * 8 + (lane & 7);
+    ly = (w >> 1) * 4 + (lane >> 3);
+  } else {
+    const int li = round * kThreads + tid;
+    lx = li % ts;
+    ly = li / ts;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
+  __shared__ GeoRec s_geo[kBatch];
+  __shared__ uint32_t s_pair[kBatch];
+  __shared__ double s_sum[kWarps][kBatch];
+  __shared__ int32_t s_cnt[kWarps][kBatch];
+
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int ts = a.tile_size;
+  const int rounds = (ts * ts + kThreads - 1) / kThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const GeoRec* geo = a.geo + (int64_t)v * a.N;
+
+  for (int round = 0; round < rounds; ++round) {
+    int lx, ly;
+    tile_pixel(ts, tid, round, lx, ly);
+    const int px = tx * ts + lx, py = ty * ts + ly;
+    const bool inside = lx < ts && ly < ts && px < c.width && py < c.height &&
+                        (ts == 16 || round * kThreads + tid < ts * ts);
+    const double cxp = px + 0.5, cyp = py + 0.5;
+    double T = 1.0;
+    bool done = !inside;
+    int32_t ncontrib = 0;
+
+    for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
+      if (__syncthreads_count(!done) == 0) break;
+      const int n = min((uint32_t)kBatch, rg.y - base);
+      for (int j = tid; j < n; j += kThreads) {
+        const uint32_t p = a.vals[base + j];
+        s_pair[j] = p;
+        s_geo[j] = geo[a.pair_gid[p]];
+      }
+      for (int k = tid; k < kWarps * kBatch; k += kThreads) {
+        (&s_sum[0][0])[k] = 0.0;
+        (&s_cnt[0][0])[k] = 0;
+      }
+      __syncthreads();
+      for (int j = 0; j < n; ++j) {
+        const GeoRec& e = s_geo[j];
+        const bool cov = !done && px >= cov_lo(e.cov_x) && px <= cov_hi(e.cov_x) &&
+                         py >= cov_lo(e.cov_y) && py <= cov_hi(e.cov_y);
+        const unsigned mask = __ballot_sync(0xffffffffu, cov);
+        if (mask == 0u) continue;
+        double contrib = 0.0;
+        if (cov) {
+          contrib = T;  // v_k += T before the splat (raster.hpp:266)
+          ++ncontrib;
+          const double dx = cxp - e.mx;
+          const double dy = cyp - e.my;
+          const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
+          double al = (double)e.opacity * exp(-0.5 * q);
+          al = al > a.amax ? a.amax : al;
+          T *= 1.0 - al;
+          if (T < a.cutoff) done = true;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
+        if (lane == 0) {
+          s_sum[warp][j] = contrib;
+          s_cnt[warp][j] = __popc(mask);
+        }
+      }
+      __syncthreads();
+      for (int j = tid; j < n; j += kThreads) {
+        double sum = 0.0;
+        int32_t cnt = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          sum += s_sum[w][j];
+          cnt += s_cnt[w][j];
+        }
+        if (cnt > 0) {
+          const uint32_t p = s_pair[j];
+          a.pair_sum[p] += sum;
+          a.pair_cnt[p] += cnt;
+        }
+      }
+    }
+    if (a.contrib && inside) a.contrib[c.pix_base + (int64_t)py * c.width + px] = ncontrib;
+    __syncthreads();
+  }
+}
+
+template <int DEG>
+__global__ void vf_finalize_kernel(VfFinalizeArgs a, int64_t N) {
+  constexpr int NB = (DEG + 1) * (DEG + 1);
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= N) return;
+  const bool virt = a.scene.virt ? a.scene.virt[g] != 0 : false;
+  const float4 po = a.scene.pos_op[g];
+  double row[NB];
+  const bool acc = a.gamma != nullptr && !virt;
+  if (acc) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) row[k] = a.gamma[g * NB + k];
+  }
+  bool touched_row = false;
+  for (int v = 0; v < a.V; ++v) {
+    const int64_t slot = (int64_t)v * N + g;
+    double vis;
+    if (a.vis_given) {
+      vis = a.vis_given[g];
+    } else {
+      const int32_t cnt = a.counts[slot];
+      double sum = 0.0;
+      int64_t touch = 0;
+      if (cnt > 0) {
+        const int64_t o = a.offsets[slot];
+        for (int k = 0; k < cnt; ++k) {
+          sum += a.pair_sum[o + k];
+          touch += a.pair_cnt[o + k];
+        }
+      }
+      vis = touch > 0 ? sum / (double)touch : 0.0;
+      if (a.vis_out) a.vis_out[slot] = vis;
+      if (a.touch_out) a.touch_out[slot] = touch;
+    }
+    if (!acc || vis <= 0.0) continue;
+    const DevCam& c = a.cams[v];
+    double d0 = (double)po.x - c.pos[0], d1 = (double)po.y - c.pos[1], d2 = (double)po.z - c.pos[2];
+    const double norm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (norm < 1e-12) continue;
+    d0 /= norm;
+    d1 /= norm;
+    d2 /= norm;
+    double basis[NB];
+    eval_sh<DEG>(d0, d1, d2, basis);
+#pragma unroll
+    for (int l = 0; l <= DEG; ++l) {
+      const double scale = vis * a.scales[l];
+#pragma unroll
+      for (int m = -l; m <= l; ++m) {
+        const int idx = l * l + l + m;
+        row[idx] += scale * basis[idx];
+      }
+    }
+    touched_row = true;
+  }
+  if (acc && touched_row) {
+#pragma unroll
+    for (int k = 0; k < NB; ++k) a.gamma[g * NB + k] = row[k];
+  }
+}
+
+}  // namespace
+
+void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s) {
+  if (a.total_tiles == 0) return;
+  vf_blend_kernel<<<(unsigned)a.total_tiles, kThreads, 0, s>>>(a);
+}
+
+void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s) {
+  if (N == 0) return;
+  const unsigned grid = (unsigned)((N + 127) / 128);
+  switch (a.degree) {
+    case 0: vf_finalize_kernel<0><<<grid, 128, 0, s>>>(a, N); break;
+    case 1: vf_finalize_kernel<1><<<grid, 128, 0, s>>>(a, N); break;
+    case 2: vf_finalize_kernel<2><<<grid, 128, 0, s>>>(a, N); break;
+    case 3: vf_finalize_kernel<3><<<grid, 128, 0, s>>>(a, N); break;
+    case 4: vf_finalize_kernel<4><<<grid, 128, 0, s>>>(a, N); break;
+    default: break;
+  }
+}
+
+}  // namespace gavis

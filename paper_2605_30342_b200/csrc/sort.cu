@@ -1,0 +1,42 @@
+// sort.cu -- device scan and radix sort (CUB, header-only part of the CUDA 12.9
+// toolkit) for the tile-key pipeline: K2 exclusive scan of per-(view, particle)
+// tile counts and K4 stable LSD radix sort of (tile << 32 | fp32 depth) keys.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "kernels.h"
+
+namespace gavis {
+
+size_t scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                (int)n);
+  return bytes;
+}
+
+void exclusive_scan(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes,
+                    cudaStream_t s) {
+  if (n == 0) return;
+  cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)n, s);
+}
+
+size_t sort_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v, (int)n, 0, 64);
+  return bytes;
+}
+
+void radix_sort_pairs(uint64_t* keys_a, uint64_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                      int64_t n, int end_bit, void* temp, size_t temp_bytes, cudaStream_t s,
+                      uint64_t** keys_out, uint32_t** vals_out) {
+  cub::DoubleBuffer<uint64_t> k(keys_a, keys_b);
+  cub::DoubleBuffer<uint32_t> v(vals_a, vals_b);
+  if (n > 0) cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, s);
+  *keys_out = k.Current();
+  *vals_out = v.Current();
+}
+
+}  // namespace gavis

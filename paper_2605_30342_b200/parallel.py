@@ -1,0 +1,93 @@
+"""Multi-GPU decomposition of the two hot paths.
+
+One process per GPU (torch.distributed for the plumbing):
+  * UA render + argmax: candidates are independent (planner.hpp:125-131), so each
+    rank scores a contiguous block with no data-path communication; the V fp64
+    scores are gathered once and reduced with the reference's first-maximum rule
+    (planner.hpp:132-136). Per-candidate scores do not depend on the rank count.
+  * VF CONST: gamma is a linear sum over views (vfield.hpp:53-60; test_vfield.cpp:
+    104-131), so each rank accumulates a contiguous block of training views into a
+    partial field and one all-reduce(sum, fp64) over NCCL/NVLink completes it;
+    num_views is then the trajectory length.
+
+The compute callables are injected so the same host logic runs over the CUDA
+library in production and over gloo on CPU in the tests.
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Sequence, Tuple
+
+import numpy as np
+
+
+def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Static block partition [n*r/w, n*(r+1)/w) -- parallel.hpp:50-51's rule."""
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def first_max(scores: Sequence[float]) -> int:
+    """planner.hpp:132-136: strict '>' keeps the lowest index among ties."""
+    best = 0
+    for i in range(1, len(scores)):
+        if scores[i] > scores[best]:
+            best = i
+    return best
+
+
+def gather_scores(local: np.ndarray, n_total: int, rank: int, world: int, dist=None) -> np.ndarray:
+    """All-gather variable-sized contiguous score blocks into rank order."""
+    if world == 1 or dist is None:
+        return np.asarray(local, np.float64)
+    import torch
+    lo, hi = shard_range(n_total, rank, world)
+    width = max(shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0] for r in range(world))
+    backend = dist.get_backend()
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    buf = torch.zeros(width, dtype=torch.float64, device=dev)
+    buf[: hi - lo] = torch.as_tensor(np.asarray(local, np.float64), device=dev)
+    parts = [torch.zeros(width, dtype=torch.float64, device=dev) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    out = []
+    for r in range(world):
+        a, b = shard_range(n_total, r, world)
+        out.append(parts[r][: b - a].cpu().numpy())
+    return np.concatenate(out) if out else np.zeros(0)
+
+
+def select_nbv_sharded(score_block: Callable[[int, int], np.ndarray], n_candidates: int, rank: int,
+                       world: int, dist=None) -> Tuple[int, np.ndarray]:
+    """score_block(lo, hi) scores candidates [lo, hi) on this rank."""
+    lo, hi = shard_range(n_candidates, rank, world)
+    local = score_block(lo, hi) if hi > lo else np.zeros(0)
+    scores = gather_scores(local, n_candidates, rank, world, dist)
+    return first_max(scores), scores
+
+
+def construct_field_sharded(partial_field: Callable[[int, int], object], n_views: int, rank: int,
+                            world: int, allreduce_sum: Callable[[object], None]) -> object:
+    """partial_field(lo, hi) accumulates views [lo, hi) into a fresh field and returns
+    it; allreduce_sum(field) sums the partial coefficient arrays across ranks in place."""
+    lo, hi = shard_range(n_views, rank, world)
+    field = partial_field(lo, hi)
+    if world > 1:
+        allreduce_sum(field)
+    return field
+
+
+class DeviceArray:
+    """Exposes a raw device pointer of the native library through
+    __cuda_array_interface__ so torch can alias it (zero copy) for NCCL."""
+
+    def __init__(self, ptr: int, count: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def allreduce_device_field(field, dist) -> None:
+    """In-place NCCL all-reduce(sum) of a DeviceField's fp64 coefficients."""
+    import torch
+    ptr, count = field.device_gamma()
+    field.ctx.synchronize()
+    t = torch.as_tensor(DeviceArray(ptr, count), device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    torch.cuda.synchronize()

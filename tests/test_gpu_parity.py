@@ -1,0 +1,385 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded fp32 inputs. Discrete results (culling, tile keys, sorted order, coverage,
+per-pixel contributor counts, argmax) must be bit-exact; fp64 results agree to
+rounding (<= 1e-12 relative); the fp32 colour dot product stays within 1e-6.
+The north_star tolerances (gamma 1e-5 relative, images 1e-4 max-abs) are
+asserted as well, explicitly.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_30342_b200 import api, synth
+from paper_2605_30342_b200.model import (K_GAUSS_ENTROPY, ParameterError, InvariantError, RasterConfig,
+                                         Scene, UncertaintyConfig, VmfParams, make_lookat)
+
+pytestmark = pytest.mark.gpu
+
+RC = RasterConfig()
+UC = UncertaintyConfig()
+NS_GAMMA_REL = 1e-5   # north_star: SH coefficients within 1e-5 relative
+NS_IMAGE_ABS = 1e-4   # north_star: RGB / uncertainty images within 1e-4 max-abs
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = api.Context(0)
+    yield c
+    c.close()
+
+
+def f32_round_toward_zero(d: np.ndarray) -> np.ndarray:
+    f = d.astype(np.float32)
+    over = np.abs(f.astype(np.float64)) > np.abs(d)
+    f[over] = np.nextafter(f[over], np.float32(0))
+    return f
+
+
+def oracle_cover(mx, my, r, W, H):
+    """Pixel interval of splat_covers (raster.hpp:97-99) restricted to the image."""
+    def axis(m, n):
+        xs = np.arange(n)
+        ok = np.abs((xs + 0.5) - m) <= r
+        if not ok.any():
+            return None
+        return int(xs[ok].min()), int(xs[ok].max())
+    return axis(mx, W), axis(my, H)
+
+
+def gamma_rel_err(a, b):
+    scale = np.maximum(np.abs(b).max(axis=1, keepdims=True), 1e-300)
+    return float((np.abs(a - b) / scale).max()) if a.size else 0.0
+
+
+def test_symbols_and_version(ctx):
+    assert ctx.lib.gavis_abi_version() == 1
+
+
+# ------------------------------------------------------------------ K1 / K3-K5
+@pytest.mark.parametrize("seed", [0, 1])
+def test_projection_bit_exact(ctx, seed):
+    c = synth.config1(seed)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    for cam in (c["train"][0], c["candidates"][3]):
+        d = api.debug_project(ctx, scene, cam, 0.3, 16)
+        splats = {s.particle_index: s for s in O.project_scene(osc, cam, 0.3)}
+        culled = np.ones(scene.num_particles, bool)
+        culled[list(splats)] = False
+        assert np.array_equal(d["culled"].astype(bool), culled)
+        for i, s in list(splats.items())[:4000]:
+            assert d["mean"][i, 0] == s.mean_x and d["mean"][i, 1] == s.mean_y
+            assert d["conic"][i, 0] == s.conic_a and d["conic"][i, 1] == s.conic_b and d["conic"][i, 2] == s.conic_c
+            assert d["depth"][i] == s.depth
+            x0, x1 = O.covered_pixel_range(s.mean_x, s.radius, cam.width)
+            y0, y1 = O.covered_pixel_range(s.mean_y, s.radius, cam.height)
+            if x0 <= x1 and y0 <= y1:
+                assert list(d["tile_rect"][i]) == [x0 // 16, x1 // 16, y0 // 16, y1 // 16]
+                cx, cy = oracle_cover(s.mean_x, s.mean_y, s.radius, cam.width, cam.height)
+                cx = cx or (1, 0)
+                cy = cy or (1, 0)
+                assert list(d["cover"][i]) == [cx[0], cx[1], cy[0], cy[1]]
+
+
+@pytest.mark.parametrize("tile", [16, 5, 13])
+def test_tile_keys_and_sorted_order_bit_exact(ctx, tile):
+    c = synth.config1(0)
+    scene, cam = c["scene"], c["train"][2]
+    rc = RasterConfig(tile_size=tile)
+    keys, ids, ranges = api.debug_binning(ctx, scene, cam, rc)
+    osc = O.OracleScene(scene)
+    splats = O.project_scene(osc, cam, rc.dilation)
+    off, ent = O.splat_binning(splats, cam.width, cam.height, tile)
+    pid = np.array([s.particle_index for s in splats], np.int64)
+    depth = np.array([s.depth for s in splats])
+    assert len(keys) == off[-1]
+    tiles = len(off) - 1
+    dk = f32_round_toward_zero(depth).view(np.uint32).astype(np.uint64)
+    for t in range(tiles):
+        lo, hi = ranges[t]
+        if off[t] == off[t + 1]:
+            assert lo == hi
+            continue
+        ref_ids = pid[ent[off[t]:off[t + 1]]]
+        assert np.array_equal(ids[lo:hi], ref_ids), f"tile {t} order differs"
+        ref_keys = (np.uint64(t) << np.uint64(32)) | dk[ent[off[t]:off[t + 1]]]
+        assert np.array_equal(keys[lo:hi], ref_keys)
+
+
+def test_depth_ties_follow_index_order(ctx):
+    """test_raster.cpp:125-141 at the key level: equal depths keep index order."""
+    cam = make_lookat((0, 0, 0), (0, 0, 1), (0, 1, 0), 129, 129)
+    parts = [synth.make_particle((0, 0, 1), 1.0, 0.5, (1, 0, 0)), synth.make_particle((0, 0, 1), 1.0, 0.5, (0, 0, 1)),
+             synth.make_particle((0, 0, 1.0000001), 1.0, 0.5, (0, 1, 0))]
+    sc = Scene.from_particles(parts, 0)
+    keys, ids, ranges = api.debug_binning(ctx, sc, cam, RC)
+    lo, hi = ranges[(64 // 16) * 9 + 64 // 16]
+    assert list(ids[lo:hi]) == [0, 1, 2]
+
+
+# ------------------------------------------------------------------ VF CONST
+@pytest.mark.parametrize("tile", [16, 5, 32])
+def test_single_view_visibility_parity(ctx, tile):
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    rc = RasterConfig(tile_size=tile)
+    for cam in c["train"][:3]:
+        v, touch, cc = api.single_view_visibility(ctx, scene, cam, rc, with_counts=True)
+        ov, otouch, occ = O.single_view_visibility(osc, cam, rc, with_counts=True)
+        assert np.array_equal(touch, otouch)
+        assert np.array_equal(cc, occ)
+        assert np.max(np.abs(v - ov)) <= 1e-12
+
+
+def test_construct_field_config1(ctx):
+    c = synth.config1(0)
+    scene = c["scene"]
+    f = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC)
+    g = f.download()
+    og = O.construct_field(O.OracleScene(scene), c["train"], 1.0, 2, RC, threads=8)
+    assert g.num_views == 16
+    err = gamma_rel_err(g.gamma, og)
+    assert err <= 1e-12
+    assert err <= NS_GAMMA_REL
+    # determinism: a second build is bit-identical
+    g2 = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC).download()
+    assert np.array_equal(g.gamma, g2.gamma)
+
+
+def test_field_linearity_and_batches(ctx):
+    """test_vfield.cpp:91-131 on the device; batching must not change the result."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    ds = ctx.upload(scene)
+    views = c["train"][:6]
+    whole = api.construct_field(ctx, ds, views, VmfParams(1.0), 2, RC).download().gamma
+    ctx.set_batch(1)
+    one = api.construct_field(ctx, ds, views, VmfParams(1.0), 2, RC).download().gamma
+    ctx.set_batch(0)
+    assert np.array_equal(whole, one)
+    f = api.empty_field(ctx, ds, VmfParams(1.0), 2)
+    api.accumulate_views(ctx, f, ds, views[:4], RC)
+    api.accumulate_views(ctx, f, ds, views[4:], RC)
+    assert f.num_views == 6
+    assert np.array_equal(f.download().gamma, whole)
+    twice = api.construct_field(ctx, ds, [views[0], views[0]], VmfParams(1.0), 2, RC).download().gamma
+    once = api.construct_field(ctx, ds, [views[0]], VmfParams(1.0), 2, RC).download().gamma
+    assert np.array_equal(twice, 2.0 * once)
+
+
+def test_field_kats_on_device(ctx):
+    """test_vfield.cpp:56-89 through the C ABI."""
+    parts = [dict(pos=(-5, 0, 0), scale=0.05, opacity=0.8, color_sh=[[2.0]] * 3),
+             dict(pos=(1, 0, 0), scale=0.05, opacity=0.0, color_sh=[[2.0]] * 3, virtual=True)]
+    sc = Scene.from_particles(parts, 0)
+    view = make_lookat((0, 0, 0), (1, 0, 0))
+    f = api.construct_field(ctx, sc, [view], VmfParams(1.0), 2, RC)
+    g = f.download()
+    assert g.num_views == 1 and g.gamma.shape == (2, 9) and np.all(g.gamma == 0)
+    q = api.query_visibility(ctx, f, [0, 1], [[1, 0, 0], [1, 0, 0]])
+    assert np.all(q == 0.0)
+    sc1 = Scene.from_particles([dict(pos=(1, 0, 0), scale=0.05, opacity=0.8, color_sh=[[2.0]] * 3)], 0)
+    f0 = api.construct_field(ctx, sc1, [view], VmfParams(0.0), 2, RC)
+    g0 = f0.download().gamma
+    assert abs(g0[0, 0] - 4.0 * math.pi * 0.28209479177387814) <= 1e-12 * g0[0, 0]
+    assert np.all(g0[0, 1:] == 0.0)
+    q = api.query_visibility(ctx, f0, [0, 0], [[1, 0, 0], [0, 0, 1]])
+    assert np.all(np.abs(q - 1.0) <= 1e-12)
+
+
+def test_accumulate_visibility_closed_form(ctx):
+    """test_vfield.cpp:167-180: kappa=0, four views of v=0.3 -> 0.7599."""
+    sc = Scene.from_particles([dict(pos=(1, 0, 0), scale=0.05, opacity=0.8, color_sh=[[2.0]] * 3)], 0)
+    view = make_lookat((0, 0, 0), (1, 0, 0))
+    f = api.empty_field(ctx, sc, VmfParams(0.0), 2)
+    for _ in range(4):
+        api.accumulate_view(ctx, f, sc, view, [0.3])
+    v = api.query_visibility(ctx, f, [0], [[0, 1, 0]])[0]
+    assert f.num_views == 4
+    assert abs(v - 0.7599) <= 1e-9
+
+
+def test_query_view_parity(ctx):
+    c = synth.config1(0)
+    scene = c["scene"]
+    f = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    for cam in c["candidates"][:3]:
+        q = api.query_view(ctx, f, scene, cam)
+        idx, vis = O.query_view(g, 2, 16, O.OracleScene(scene), cam)
+        assert np.array_equal(q.particle_indices, idx)
+        assert np.max(np.abs(q.visibilities - vis)) <= 1e-12
+
+
+# ------------------------------------------------------------------ UA render
+@pytest.mark.parametrize("tile", [16, 13])
+def test_rasterize_parity(ctx, tile):
+    c = synth.config1(0)
+    scene = c["scene"]
+    rc = RasterConfig(tile_size=tile)
+    osc = O.OracleScene(scene)
+    for cam in c["candidates"][:2]:
+        r = api.render(ctx, scene, None, [cam], rc, UC, rgb=True, depth=True, transmittance=True, contributors=True)
+        rgb, depth, T, cc = O.rasterize(osc, cam, rc, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], cc)
+        assert np.max(np.abs(r["transmittance"] - T)) <= 1e-12
+        assert np.max(np.abs(r["depth"] - depth)) <= 1e-10
+        assert np.max(np.abs(r["rgb"] - rgb)) <= 1e-5
+        assert np.max(np.abs(r["rgb"] - rgb)) <= NS_IMAGE_ABS
+
+
+def test_render_entropy_parity_and_scores(ctx):
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    f = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    cams = c["candidates"][:4]
+    r = api.render(ctx, scene, f, cams, RC, UC, entropy=True, invisible_mass=True, entropy_depth=True,
+                   scores=True, contributors=True)
+    P = cams[0].width * cams[0].height
+    for k, cam in enumerate(cams):
+        H, w0, depth, cc = O.render_entropy(osc, g, 2, 16, cam, RC, UC, contrib=True)
+        sl = slice(k * P, (k + 1) * P)
+        assert np.array_equal(r["entropy_contributors"][sl], cc)
+        assert np.max(np.abs(r["entropy"][sl] - H)) <= 1e-10
+        assert np.max(np.abs(r["invisible_mass"][sl] - w0)) <= 1e-12
+        assert np.max(np.abs(r["entropy_depth"][sl] - depth)) <= 1e-10
+        ref = O.image_entropy(H)
+        assert abs(r["scores"][k] - ref) <= 1e-12 * max(1.0, abs(ref))
+
+
+def test_render_entropy_core_stagewise(ctx):
+    """Entropy track fed the same per-particle visibility (uncertainty.hpp:124-238)."""
+    sc = synth.random_scene(0xBEAD, 60)
+    cam = synth.z_camera()
+    vis = np.array([synth.SplitMix64(23 + i).next_double() for i in range(60)])
+    m = api.render_entropy_core(ctx, sc, cam, RC, UC, vis)
+    H, w0, _ = O.render_entropy_core(O.OracleScene(sc), cam, RC, UC, vis)
+    assert np.max(np.abs(m.entropy - H)) <= 1e-10 and np.max(np.abs(m.invisible_mass - w0)) <= 1e-12
+
+
+def test_select_nbv_config1(ctx):
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    f = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    res = api.select_nbv(ctx, scene, f, c["candidates"], RC, UC)
+    best, scores = O.select_nbv(osc, g, 2, 16, c["candidates"], RC, UC, threads=8)
+    assert res.best_index == best
+    assert np.max(np.abs(res.scores - scores) / np.maximum(1.0, np.abs(scores))) <= 1e-12
+    res2 = api.select_nbv(ctx, scene, f, c["candidates"], RC, UC, with_rgb=True)
+    assert np.array_equal(res.scores, res2.scores)
+
+
+def test_select_nbv_kats(ctx):
+    """test_planner.cpp:143-180: unexplored side wins; identical candidates tie to 0."""
+    sc = synth.wall_scene()
+    front = make_lookat((0.3, 0.5, 0.5), (1, 0.5, 0.5), (0, 0, 1), 64, 64)
+    back = make_lookat((1.7, 0.5, 0.5), (1, 0.5, 0.5), (0, 0, 1), 64, 64)
+    f = api.construct_field(ctx, sc, [front], VmfParams(1.0), 2, RC)
+    r = api.select_nbv(ctx, sc, f, [front, back], RC, UC)
+    assert r.scores[1] > r.scores[0] and r.best_index == 1
+    r = api.select_nbv(ctx, sc, f, [front, front, front], RC, UC)
+    assert r.best_index == 0 and r.scores[1] == r.scores[0] == r.scores[2]
+    with pytest.raises(ParameterError):
+        api.select_nbv(ctx, sc, f, [], RC, UC)
+
+
+def test_exact_fixture_on_device(ctx):
+    """test_uncertainty.cpp:125-171 with the fp32 scene (all fixture values are exact in fp32)."""
+    cam = make_lookat((0, 0, 0), (0, 0, 1), (0, 1, 0), 129, 129)
+    rc = RasterConfig(alpha_clamp_max=1.0)
+    sc = Scene.from_particles([dict(pos=(0, 0, 1), scale=0.01, opacity=1.0, color_sh=[[1.0]] * 3)], 0)
+    f = api.construct_field(ctx, sc, [cam], VmfParams(0.0), 2, rc)
+    m, depth = api.render_entropy(ctx, sc, f, cam, rc, UncertaintyConfig(color_sigma=1.0), want_depth=True)
+    ctr = 64 * 129 + 64
+    assert abs(m.entropy[ctr] - K_GAUSS_ENTROPY) <= 1e-12 and abs(m.invisible_mass[ctr]) <= 1e-12
+    assert abs(depth[ctr] - 1.0) <= 1e-12 and m.entropy[0] == 0.0 and depth[0] == 0.0
+    m0 = api.render_entropy_core(ctx, sc, cam, rc, UncertaintyConfig(color_sigma=0.1), [0.0])
+    w0 = m0.invisible_mass[ctr]
+    assert abs(w0 - 0.575) <= 1e-12
+    assert abs(m0.entropy[ctr] - w0 * (-math.log(w0) + K_GAUSS_ENTROPY)) <= 1e-12
+
+
+def test_raster_kats_on_device(ctx):
+    """test_raster.cpp:104-141 and 234-263 through the C ABI."""
+    r = api.rasterize(ctx, Scene.empty(), synth.z_camera(), RC)
+    assert np.all(r.color == 0) and np.all(r.depth == 0) and np.all(r.transmittance == 1)
+    cam = make_lookat((0, 0, 0), (0, 0, 1), (0, 1, 0), 129, 129)
+    # gray chosen exactly representable after /Y00 rounding: compare to the oracle on the same fp32 scene
+    sc = Scene.from_particles([synth.make_particle((0, 0, 1), 1.0, 1.0, (0.5, 0.5, 0.5))], 0)
+    r = api.rasterize(ctx, sc, cam, RC)
+    pix = 64 * 129 + 64
+    assert abs(r.transmittance[pix] - 0.01) <= 1e-12 and abs(r.depth[pix] - 0.99) <= 1e-12
+    assert abs(r.color[pix * 3] - 0.495) <= 1e-6
+    a = synth.make_particle((0, 0, 1), 1.0, 0.5, (1, 0, 0))
+    b = synth.make_particle((0, 0, 1), 1.0, 0.5, (0, 0, 1))
+    r = api.rasterize(ctx, Scene.from_particles([a, b], 0), cam, RC)
+    assert abs(r.color[pix * 3] - 0.5) <= 1e-6 and abs(r.color[pix * 3 + 2] - 0.25) <= 1e-6
+    r = api.rasterize(ctx, Scene.from_particles([b, a], 0), cam, RC)
+    assert abs(r.color[pix * 3 + 2] - 0.5) <= 1e-6 and abs(r.color[pix * 3] - 0.25) <= 1e-6
+    sc = Scene.from_particles([synth.make_particle((0, 0, 2), 0.05, 0.7, (1, 1, 1))], 0)
+    assert api.single_view_visibility(ctx, sc, synth.z_camera(), RC)[0] == 1.0
+    sc = Scene.from_particles([synth.make_particle((0, 0, -2), 0.05, 0.7, (1, 1, 1)),
+                               synth.make_particle((40, 0, 2), 0.05, 0.7, (1, 1, 1))], 0)
+    assert np.all(api.single_view_visibility(ctx, sc, synth.z_camera(), RC) == 0.0)
+    cam = make_lookat((0, 0, 0), (1, 0, 0), (0, 0, 1), 129, 129)
+    sc = Scene.from_particles([synth.make_particle((1, 0, 0), 0.75, 1.0, (1, 1, 1)),
+                               synth.make_particle((2, 0, 0), 0.02, 0.5, (1, 1, 1))], 0)
+    v = api.single_view_visibility(ctx, sc, cam, RC)
+    assert v[0] == 1.0 and abs(v[1] - 0.01) <= 1e-3
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_weight_conservation_on_device(ctx, seed):
+    sc = synth.random_scene(seed, 100, white=True)
+    r = api.rasterize(ctx, sc, synth.z_camera(), RC)
+    assert np.max(np.abs(r.color[0::3] + r.transmittance - 1.0)) < 1e-5
+
+
+# ------------------------------------------------------------------ edges / errors
+def test_edge_cases(ctx):
+    # 1x1 camera, camera inside the cloud, all particles culled
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    tiny = make_lookat((0, 0, 3), (0, 0, 0), (0, 1, 0), 1, 1)
+    inside = make_lookat((0.1, 0.05, 0.0), (1, 0, 0), (0, 0, 1), 64, 48)
+    away = make_lookat((0, 0, 10), (0, 0, 20), (0, 1, 0), 32, 32)
+    for cam in (tiny, inside, away):
+        r = api.render(ctx, scene, None, [cam], RC, UC, rgb=True, transmittance=True, contributors=True)
+        rgb, _, T, cc = O.rasterize(osc, cam, RC, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], cc)
+        assert np.max(np.abs(r["transmittance"] - T)) <= 1e-12
+    # mixed resolutions in one batch
+    f = api.construct_field(ctx, scene, [tiny, inside, c["train"][0]], VmfParams(1.0), 2, RC)
+    og = O.construct_field(osc, [tiny, inside, c["train"][0]], 1.0, 2, RC)
+    assert gamma_rel_err(f.download().gamma, og) <= 1e-12
+
+
+def test_parameter_errors(ctx):
+    sc = synth.random_scene(1, 5)
+    cam = synth.z_camera()
+    with pytest.raises(ParameterError):
+        api.rasterize(ctx, sc, cam, RasterConfig(tile_size=0))
+    with pytest.raises(ParameterError):
+        api.rasterize(ctx, sc, cam, RasterConfig(alpha_clamp_max=1.5))
+    with pytest.raises(ParameterError):
+        api.construct_field(ctx, sc, [], VmfParams(1.0), 2, RC)
+    with pytest.raises(ParameterError):
+        api.construct_field(ctx, sc, [cam], VmfParams(1.0), 21, RC)
+    f = api.construct_field(ctx, sc, [cam], VmfParams(1.0), 2, RC)
+    with pytest.raises(ParameterError):
+        api.query_visibility(ctx, f, [5], [[1, 0, 0]])
+    with pytest.raises(ParameterError):
+        api.render_entropy(ctx, sc, f, cam, RC, UncertaintyConfig(beta=1.5))
+    bigger = synth.random_scene(1, 6)
+    with pytest.raises(ParameterError):
+        api.render_entropy(ctx, bigger, f, cam, RC, UC)
+    with pytest.raises(InvariantError):
+        api.accumulate_views(ctx, f, bigger, [cam], RC)
