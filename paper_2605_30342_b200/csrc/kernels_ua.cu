@@ -12,6 +12,7 @@
 // leaves the loop when both are done, a CTA when all its pixels are.
 // Per-tile entropy partials feed K8, which folds them in tile order into the
 // image score (image_entropy, uncertainty.hpp:264-272).
+#include "fast_math.cuh"
 #include "kernels.h"
 
 namespace gavis {
@@ -54,6 +55,8 @@ __global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
   __shared__ UaRec s_ua[ENT ? kBatch : 1];
   __shared__ __align__(16) float s_col[RGB ? kBatch * CS : 4];
   __shared__ double s_red[kWarps];
+  __shared__ MathSmem s_math;
+  load_math_tables(&s_math);
 
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
@@ -125,8 +128,11 @@ __global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
           const double dx = cxp - e.mx;
           const double dy = cyp - e.my;
           const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-          double al = (double)e.opacity * exp(-0.5 * q);
-          al = al > a.amax ? a.amax : al;
+          double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
+          if (q <= kQSkip) {
+            al = (double)e.opacity * exp_neg(-0.5 * q, &s_math);
+            al = al > a.amax ? a.amax : al;
+          }
           if (RGB && !rgb_done) {
             ++n_rgb;
             const double w = al * T;
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
             as = as < 0.0 ? 0.0 : (a.amax < as ? a.amax : as);
             const double w = as * Te;
             const double s = w * u.v;
-            if (s > 0.0) H += s * (-log(s) + a.hl_qc + kGaussEntropy);
+            if (s > 0.0) H += s * (-log_pos(s, &s_math) + a.hl_qc + kGaussEntropy);
             w0 += w * u.omv;
             edep += w * e.depth;
             Te *= 1.0 - as;
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
         }
       }
     }
-    if (ENT && w0 > 0.0) H += w0 * (-log(w0) + a.hl_q0 + kGaussEntropy);
+    if (ENT && w0 > 0.0) H += w0 * (-log_pos(w0, &s_math) + a.hl_q0 + kGaussEntropy);
     if (inside) {
       const int64_t pix = c.pix_base + (int64_t)py * c.width + px;
       if (RGB) {

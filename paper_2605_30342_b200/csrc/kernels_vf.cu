@@ -15,6 +15,7 @@
 // (vfield.hpp:38-63): one thread per particle folds its pairs, divides by the
 // touch count and adds v * a_l * Y_lm(d) to its SH row, views in trajectory
 // order.
+#include "fast_math.cuh"
 #include "kernels.h"
 
 namespace gavis {
@@ -50,6 +51,8 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
   __shared__ uint32_t s_pair[kBatch];
   __shared__ double s_sum[kWarps][kBatch];
   __shared__ int32_t s_cnt[kWarps][kBatch];
+  __shared__ MathSmem s_math;
+  load_math_tables(&s_math);
 
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
@@ -99,8 +102,11 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
           const double dx = cxp - e.mx;
           const double dy = cyp - e.my;
           const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-          double al = (double)e.opacity * exp(-0.5 * q);
-          al = al > a.amax ? a.amax : al;
+          double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
+          if (q <= kQSkip) {
+            al = (double)e.opacity * exp_neg(-0.5 * q, &s_math);
+            al = al > a.amax ? a.amax : al;
+          }
           T *= 1.0 - al;
           if (T < a.cutoff) done = true;
         }
