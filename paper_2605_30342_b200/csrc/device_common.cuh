@@ -49,6 +49,22 @@ struct __align__(16) UaRec {
 __device__ __forceinline__ int cov_lo(int32_t packed) { return packed & 0xFFFF; }
 __device__ __forceinline__ int cov_hi(int32_t packed) { return (packed >> 16) & 0xFFFF; }
 
+// Coverage rectangle as (x0, x1-x0, y0, y1-y0) for a two-compare unsigned test
+// (unsigned)(px - x0) <= x1 - x0; an empty axis becomes (2^30, 0), never hit.
+__device__ __forceinline__ int4 cover_rect4(int32_t cov_x, int32_t cov_y) {
+  const int x0 = cov_lo(cov_x), x1 = cov_hi(cov_x), y0 = cov_lo(cov_y), y1 = cov_hi(cov_y);
+  int4 r;
+  r.x = x0 <= x1 ? x0 : (1 << 30);
+  r.y = x0 <= x1 ? x1 - x0 : 0;
+  r.z = y0 <= y1 ? y0 : (1 << 30);
+  r.w = y0 <= y1 ? y1 - y0 : 0;
+  return r;
+}
+
+__device__ __forceinline__ bool in_rect4(int4 r, int px, int py) {
+  return (unsigned)(px - r.x) <= (unsigned)r.y && (unsigned)(py - r.z) <= (unsigned)r.w;
+}
+
 // eval_real_sh_block (sh.hpp:38-79), fixed maximum degree, same recurrence and
 // operation order.
 template <int DEG>

@@ -22,45 +22,55 @@ namespace gavis {
 
 constexpr double kQSkip = 75.0;
 
-struct MathSmem {
-  double exp2_tab[32];
-  double log_inv[128];
-  double log_neg[128];
-};
+// Polynomial coefficients live in constant memory so each DFMA reads its
+// operand straight from the constant bank (no per-use 64-bit immediate moves).
+__constant__ double kExpPoly[6] = {1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0};
+__constant__ double kLogPoly[7] = {1.0 / 7.0, -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5, 1.0};
+__constant__ double kMathConst[8] = {
+    46.16624130844683,        // 0: 32 / ln2
+    0.02166084939249829,      // 1: ln2/32 hi
+    7.247021293269686e-19,    // 2: ln2/32 lo
+    6755399441055744.0,       // 3: 1.5 * 2^52
+    0.6931471805599453,       // 4: ln2 hi
+    2.3190468138462996e-17,   // 5: ln2 lo
+    18014398509481984.0,      // 6: 2^54
+    0.0};
+
+// Shared-memory copies of the lookup tables (namespace scope: direct shared
+// addressing in the inner loops).
+__shared__ double g_exp2_tab[32];
+__shared__ double g_log_inv[128];
+__shared__ double g_log_neg[128];
 
 // Cooperative copy of the constant tables into shared memory (indices diverge
-// per lane, which constant memory would serialise).
-__device__ __forceinline__ void load_math_tables(MathSmem* m) {
+// per lane, which constant memory would serialise). Callers synchronise before use.
+__device__ __forceinline__ void load_math_tables() {
   for (int i = threadIdx.x; i < 32 + 128 + 128; i += blockDim.x) {
     if (i < 32)
-      m->exp2_tab[i] = kExp2Tab[i];
+      g_exp2_tab[i] = kExp2Tab[i];
     else if (i < 160)
-      m->log_inv[i - 32] = kLogInv[i - 32];
+      g_log_inv[i - 32] = kLogInv[i - 32];
     else
-      m->log_neg[i - 160] = kLogNeg[i - 160];
+      g_log_neg[i - 160] = kLogNeg[i - 160];
   }
 }
 
 // exp(x) for x in [-40, 0]: k = round(32 x / ln2), r = x - k ln2/32 (Cody-Waite
 // with FMA), 2^(k/32) = 2^(k>>5) * T[k&31], e^r by a degree-6 Taylor polynomial
 // (|r| <= ln2/64, remainder < 4e-18).
-__device__ __forceinline__ double exp_neg(double x, const MathSmem* m) {
-  const double kInvL = 46.16624130844683;          // 32 / ln2
-  const double kLhi = 0.02166084939249829;         // ln2 / 32
-  const double kLlo = 7.247021293269686e-19;
-  const double kShift = 6755399441055744.0;        // 1.5 * 2^52
-  const double t = fma(x, kInvL, kShift);
+__device__ __forceinline__ double exp_neg(double x) {
+  const double t = fma(x, kMathConst[0], kMathConst[3]);
   const int k = __double2loint(t);
-  const double kd = t - kShift;
-  double r = fma(kd, -kLhi, x);
-  r = fma(kd, -kLlo, r);
-  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
+  const double kd = t - kMathConst[3];
+  double r = fma(kd, -kMathConst[1], x);
+  r = fma(kd, -kMathConst[2], r);
+  double p = fma(r, kExpPoly[0], kExpPoly[1]);
+  p = fma(p, r, kExpPoly[2]);
+  p = fma(p, r, kExpPoly[3]);
+  p = fma(p, r, kExpPoly[4]);
+  p = fma(p, r, kExpPoly[5]);
   p = p * r;  // e^r - 1
-  const double tj = m->exp2_tab[k & 31];
+  const double tj = g_exp2_tab[k & 31];
   const double res = fma(tj, p, tj);
   return __hiloint2double(__double2hiint(res) + ((k >> 5) << 20), __double2loint(res));
 }
@@ -68,42 +78,26 @@ __device__ __forceinline__ double exp_neg(double x, const MathSmem* m) {
 // ln(s) for finite s > 0: s = 2^e * mant, mant in [1,2); mant * inv_j = 1 + r with
 // |r| < 1/256 (inv_j ~ 1/c_j from the top 7 mantissa bits), ln(1+r) by a degree-7
 // Taylor polynomial, ln(s) = e ln2 - ln(inv_j) + ln(1+r).
-__device__ __forceinline__ double log_pos(double s, const MathSmem* m) {
-  int hi = __double2hiint(s);
-  const int lo = __double2loint(s);
+__device__ __forceinline__ double log_pos(double s) {
   int e = 0;
-  if (hi < 0x00100000) {  // subnormal: scale by 2^54
-    const double s2 = s * 18014398509481984.0;
-    hi = __double2hiint(s2);
+  if (__double2hiint(s) < 0x00100000) {  // subnormal: scale by 2^54
+    s *= kMathConst[6];
     e = -54;
-    const int lo2 = __double2loint(s2);
-    const int j = (hi >> 13) & 127;
-    e += (hi >> 20) - 1023;
-    const double mant = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo2);
-    const double r = fma(mant, m->log_inv[j], -1.0);
-    double p = fma(r, 1.0 / 7.0, -1.0 / 6.0);
-    p = fma(p, r, 1.0 / 5.0);
-    p = fma(p, r, -0.25);
-    p = fma(p, r, 1.0 / 3.0);
-    p = fma(p, r, -0.5);
-    p = fma(p, r, 1.0);
-    p = p * r;
-    const double ed = (double)e;
-    return fma(ed, 0.6931471805599453, fma(ed, 2.3190468138462996e-17, m->log_neg[j] + p));
   }
-  e = (hi >> 20) - 1023;
+  const int hi = __double2hiint(s);
+  e += (hi >> 20) - 1023;
   const int j = (hi >> 13) & 127;
-  const double mant = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
-  const double r = fma(mant, m->log_inv[j], -1.0);
-  double p = fma(r, 1.0 / 7.0, -1.0 / 6.0);
-  p = fma(p, r, 1.0 / 5.0);
-  p = fma(p, r, -0.25);
-  p = fma(p, r, 1.0 / 3.0);
-  p = fma(p, r, -0.5);
-  p = fma(p, r, 1.0);
+  const double mant = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(s));
+  const double r = fma(mant, g_log_inv[j], -1.0);
+  double p = fma(r, kLogPoly[0], kLogPoly[1]);
+  p = fma(p, r, kLogPoly[2]);
+  p = fma(p, r, kLogPoly[3]);
+  p = fma(p, r, kLogPoly[4]);
+  p = fma(p, r, kLogPoly[5]);
+  p = fma(p, r, kLogPoly[6]);
   p = p * r;  // ln(1 + r)
   const double ed = (double)e;
-  return fma(ed, 0.6931471805599453, fma(ed, 2.3190468138462996e-17, m->log_neg[j] + p));
+  return fma(ed, kMathConst[4], fma(ed, kMathConst[5], g_log_neg[j] + p));
 }
 
 }  // namespace gavis

@@ -606,13 +606,16 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       ua.edepth = out->entropy_depth ? (double*)c->buf("img_edepth", sizeof(double) * P) : nullptr;
       if (out->entropy_contributors)
         ua.ent_contrib = (int32_t*)c->buf("img_nent", sizeof(int32_t) * P);
-      ua.tile_score = (double*)c->buf("tile_score", sizeof(double) * std::max<int64_t>(1, b.total_tiles));
+      ua.tile_score = (double*)c->buf(
+          "tile_score", sizeof(double) * ua_score_parts(rc->tile_size) * std::max<int64_t>(1, b.total_tiles));
     }
     c->run("ua_blend", [&] { launch_ua_blend(ua, c->stream); }, b.total_tiles > 0 ? 1 : 0);
     double* dscores = nullptr;
     if (do_ent) {
       dscores = (double*)c->buf("scores", sizeof(double) * V);
-      c->run("score", [&] { launch_score(b.dcams, V, ua.tile_score, dscores, c->stream); });
+      c->run("score", [&] {
+        launch_score(b.dcams, V, ua_score_parts(rc->tile_size), ua.tile_score, dscores, c->stream);
+      });
     }
     copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P);
     copy_out(c, out->depth ? out->depth + pix_done : nullptr, ua.depth, P);
@@ -776,7 +779,8 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
     auto* s = new gavis_scene();
     s->ctx = c;
     const int nb = (d->color_degree + 1) * (d->color_degree + 1);
-    const int cstride = ((3 * nb + 3) / 4) * 4;
+    const int nbp = nb + (nb & 1);
+    const int cstride = ((3 * nbp + 3) / 4) * 4;
     try {
       const int64_t M = std::max<int64_t>(N, 1);
       CK(cudaMalloc(&s->pos_op, sizeof(float4) * M));
@@ -800,13 +804,17 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
       if (d->is_virtual)
         for (int64_t i = 0; i < N; ++i) vm[i] = d->is_virtual[i] ? 1 : 0;
       CK(cudaMemcpy(s->virt, vm.data(), M, cudaMemcpyHostToDevice));
-      if (cstride == 3 * nb) {
+      // device layout: per particle [3][nbp] (channel rows padded to an even count so
+      // coefficient pairs feed packed fp32x2 FMAs), particle stride cstride floats.
+      if (cstride == 3 * nb && nbp == nb) {
         if (N > 0)
           CK(cudaMemcpy(s->colors, d->colors, sizeof(float) * cstride * N, cudaMemcpyHostToDevice));
       } else {
         std::vector<float> col((size_t)(cstride * M), 0.f);
         for (int64_t i = 0; i < N; ++i)
-          std::memcpy(&col[i * cstride], d->colors + i * 3 * nb, sizeof(float) * 3 * nb);
+          for (int k = 0; k < 3; ++k)
+            std::memcpy(&col[i * cstride + k * nbp], d->colors + i * 3 * nb + k * nb,
+                        sizeof(float) * nb);
         CK(cudaMemcpy(s->colors, col.data(), sizeof(float) * cstride * M, cudaMemcpyHostToDevice));
       }
     } catch (...) {

@@ -141,7 +141,9 @@ void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s);
 void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s);
 void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s);
-void launch_score(const DevCam* cams, int V, const double* tile_score, double* scores,
+// Entropy partials per tile written by the UA blend (8 patches per 16x16 tile).
+int ua_score_parts(int tile_size);
+void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,
                   cudaStream_t s);
 void launch_query(const QueryArgs& a, cudaStream_t s);
 

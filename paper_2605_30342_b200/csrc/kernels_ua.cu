@@ -9,19 +9,28 @@
 //     H += s(-ln s + 1/2 ln|Qc| + C_H), w0 += w(1-v), T* *= 1-alpha*, stop once
 //     T* < cutoff; afterwards H += w0(-ln w0 + 1/2 ln|Q0| + C_H) (:224-225).
 // The two tracks share the splat's alpha but terminate independently; a pixel
-// leaves the loop when both are done, a CTA when all its pixels are.
+// leaves the loop when both are done.
+//
+// Schedules:
+//   * ua_blend_tile2_kernel (16x16 tiles, default): 128 threads per tile, each
+//     thread owns two pixels 4 rows apart (a warp owns an 8x8 block), so every
+//     shared-memory read of a splat record / SH colour row feeds two pixels and
+//     the two pixels' fp64 dependency chains interleave.
+//   * ua_blend_kernel (any tile size): 256 threads, one pixel each, in rounds.
+// The SH colour dot products run as packed fp32x2 FMAs (FFMA2, sm_100) over
+// coefficient pairs; colour rows are padded to an even length on upload.
 // Per-tile entropy partials feed K8, which folds them in tile order into the
 // image score (image_entropy, uncertainty.hpp:264-272).
 #include "fast_math.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace gavis {
 
 namespace {
 
-constexpr int kThreads = 256;
 constexpr int kBatch = 128;
-constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ int find_view(const DevCam* cams, int V, int64_t tile) {
   int v = 0;
@@ -29,34 +38,268 @@ __device__ __forceinline__ int find_view(const DevCam* cams, int V, int64_t tile
   return v;
 }
 
-__device__ __forceinline__ void tile_pixel(int ts, int tid, int round, int& lx, int& ly) {
-  if (ts == 16) {
-    const int w = tid >> 5, lane = tid & 31;
-    lx = (w & 1) * 8 + (lane & 7);
-    ly = (w >> 1) * 4 + (lane >> 3);
-  } else {
-    const int li = round * kThreads + tid;
-    lx = li % ts;
-    ly = li / ts;
-  }
+template <int LC>
+struct Col {
+  static constexpr int NB = (LC + 1) * (LC + 1);
+  static constexpr int NBP = NB + (NB & 1);      // even-padded channel row
+  static constexpr int NP = NBP / 2;              // coefficient pairs per channel
+  static constexpr int STRIDE = ((3 * NBP + 3) / 4) * 4;
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra, rb, rc, rd;
+  ra = *reinterpret_cast<unsigned long long*>(&a);
+  rb = *reinterpret_cast<unsigned long long*>(&b);
+  rc = *reinterpret_cast<unsigned long long*>(&c);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2*>(&rd);
 }
 
 template <int LC>
-struct ColorSmem {
-  static constexpr int NB = (LC + 1) * (LC + 1);
-  static constexpr int STRIDE = ((3 * NB + 3) / 4) * 4;
+struct Pixel {
+  double cxp, cyp;
+  double T, rgb0, rgb1, rgb2, dep;
+  double Te, H, w0, edep;
+  bool rgb_done, ent_done;
+  int32_t n_rgb, n_ent;
+  float2 bp[Col<LC>::NP];  // SH basis at the pixel ray, as pairs
 };
 
 template <int LC, bool RGB, bool ENT>
-__global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
-  constexpr int NB = ColorSmem<LC>::NB;
-  constexpr int CS = ColorSmem<LC>::STRIDE;
-  __shared__ GeoRec s_geo[kBatch];
-  __shared__ UaRec s_ua[ENT ? kBatch : 1];
-  __shared__ __align__(16) float s_col[RGB ? kBatch * CS : 4];
+__device__ __forceinline__ void pixel_init(Pixel<LC>& P, const DevCam& c, int px, int py,
+                                           bool inside) {
+  constexpr int NB = Col<LC>::NB;
+  P.cxp = px + 0.5;
+  P.cyp = py + 0.5;
+  if (RGB) {
+    // CameraView::pixel_ray (model.hpp:83-86) + eval_real_sh_block at the ray.
+    const double dc0 = (P.cxp - c.cx) / c.fx, dc1 = (P.cyp - c.cy) / c.fy, dc2 = 1.0;
+    const double r0 = c.R[0] * dc0 + c.R[1] * dc1 + c.R[2] * dc2;
+    const double r1 = c.R[3] * dc0 + c.R[4] * dc1 + c.R[5] * dc2;
+    const double r2 = c.R[6] * dc0 + c.R[7] * dc1 + c.R[8] * dc2;
+    const double n2 = r0 * r0 + r1 * r1 + r2 * r2;
+    const double nn = n2 > 0.0 ? sqrt(n2) : 1.0;
+    double bd[Col<LC>::NBP];
+    eval_sh<LC>(r0 / nn, r1 / nn, r2 / nn, bd);
+    if (Col<LC>::NBP != NB) bd[Col<LC>::NBP - 1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < Col<LC>::NP; ++i) P.bp[i] = make_float2((float)bd[2 * i], (float)bd[2 * i + 1]);
+  }
+  P.T = 1.0;
+  P.rgb0 = P.rgb1 = P.rgb2 = P.dep = 0.0;
+  P.Te = 1.0;
+  P.H = P.w0 = P.edep = 0.0;
+  P.rgb_done = !(RGB && inside);
+  P.ent_done = !(ENT && inside);
+  P.n_rgb = P.n_ent = 0;
+}
+
+// SH colour of one splat at one pixel ray, clamped to [0,1] (model.hpp:49-62):
+// packed pairs of coefficients, even/odd partial sums folded at the end.
+template <int LC>
+__device__ __forceinline__ void sh_color(const float2* col2, const float2* bp, float& c0, float& c1,
+                                         float& c2) {
+  constexpr int NP = Col<LC>::NP;
+  float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0;
+#pragma unroll
+  for (int m = 0; m < NP; ++m) {
+    a0 = ffma2(col2[m], bp[m], a0);
+    a1 = ffma2(col2[NP + m], bp[m], a1);
+    a2 = ffma2(col2[2 * NP + m], bp[m], a2);
+  }
+  c0 = __saturatef(a0.x + a0.y);
+  c1 = __saturatef(a1.x + a1.y);
+  c2 = __saturatef(a2.x + a2.y);
+}
+
+// alpha of splat e at the pixel (splat_alpha, raster.hpp:101-108).
+__device__ __forceinline__ double splat_alpha(const GeoRec& e, double cxp, double cyp, double amax) {
+  const double dx = cxp - e.mx;
+  const double dy = cyp - e.my;
+  const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
+  double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
+  if (q <= kQSkip) {
+    al = (double)e.opacity * exp_neg(-0.5 * q);
+    al = al > amax ? amax : al;
+  }
+  return al;
+}
+
+// RGB track update given alpha and (if w > 0) the colour (raster.hpp:209-221).
+template <int LC>
+__device__ __forceinline__ void rgb_step(Pixel<LC>& P, double al, double depth, const float2* col2,
+                                         double cutoff) {
+  ++P.n_rgb;
+  const double w = al * P.T;
+  if (w > 0.0) {
+    float c0, c1, c2;
+    sh_color<LC>(col2, P.bp, c0, c1, c2);
+    P.rgb0 += w * (double)c0;
+    P.rgb1 += w * (double)c1;
+    P.rgb2 += w * (double)c2;
+    P.dep += w * depth;
+  }
+  P.T *= 1.0 - al;
+  if (P.T < cutoff) P.rgb_done = true;
+}
+
+// Entropy track update (uncertainty.hpp:198-222).
+template <int LC>
+__device__ __forceinline__ void ent_step(Pixel<LC>& P, double al, double depth, const UaRec& u,
+                                         double amax, double cutoff, double hl_qc) {
+  ++P.n_ent;
+  double as = u.A * al + u.B;
+  as = as < 0.0 ? 0.0 : (amax < as ? amax : as);
+  const double w = as * P.Te;
+  const double s = w * u.v;
+  if (s > 0.0) P.H += s * (-log_pos(s) + hl_qc + kGaussEntropy);
+  P.w0 += w * u.omv;
+  P.edep += w * depth;
+  P.Te *= 1.0 - as;
+  if (P.Te < cutoff) P.ent_done = true;
+}
+
+template <int LC, bool RGB, bool ENT>
+__device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a, const DevCam& c,
+                                             int px, int py, bool inside) {
+  if (ENT && P.w0 > 0.0) P.H += P.w0 * (-log_pos(P.w0) + a.hl_q0 + kGaussEntropy);
+  if (!inside) return;
+  const int64_t pix = c.pix_base + (int64_t)py * c.width + px;
+  if (RGB) {
+    if (a.rgb) {
+      a.rgb[pix * 3 + 0] = P.rgb0;
+      a.rgb[pix * 3 + 1] = P.rgb1;
+      a.rgb[pix * 3 + 2] = P.rgb2;
+    }
+    if (a.depth) a.depth[pix] = P.dep;
+    if (a.trans) a.trans[pix] = P.T;
+    if (a.rgb_contrib) a.rgb_contrib[pix] = P.n_rgb;
+  }
+  if (ENT) {
+    if (a.entropy) a.entropy[pix] = P.H;
+    if (a.w0) a.w0[pix] = P.w0;
+    if (a.edepth) a.edepth[pix] = P.edep;
+    if (a.ent_contrib) a.ent_contrib[pix] = P.n_ent;
+  }
+}
+
+template <int LC, bool RGB, bool ENT>
+struct Stage {
+  static constexpr size_t bytes(int batch) {
+    return (size_t)batch * (sizeof(GeoRec) + sizeof(int4) + (ENT ? sizeof(UaRec) : 0) +
+                            (RGB ? sizeof(float) * Col<LC>::STRIDE : 0));
+  }
+};
+
+// Stage entries [base, base+n) of the tile list into shared memory.
+template <int LC, bool RGB, bool ENT>
+__device__ __forceinline__ void stage_batch(const UaBlendArgs& a, const GeoRec* geo, const UaRec* uar,
+                                            uint32_t base, int n, GeoRec* s_geo, int4* s_rect,
+                                            UaRec* s_ua, float* s_col) {
+  constexpr int V4 = Col<LC>::STRIDE / 4;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const uint32_t g = a.vals[base + j];
+    const GeoRec r = geo[g];
+    s_geo[j] = r;
+    s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
+    if (ENT) s_ua[j] = uar[g];
+  }
+  if (RGB) {
+    const float4* colors4 = reinterpret_cast<const float4*>(a.scene.colors);
+    for (int k = threadIdx.x; k < n * V4; k += blockDim.x) {
+      const int j = k / V4, qd = k - j * V4;
+      const uint32_t g = a.vals[base + j];
+      reinterpret_cast<float4*>(s_col)[k] = __ldg(colors4 + (int64_t)g * V4 + qd);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 16x16 tiles, 128 threads, two pixels per thread.
+template <int LC, bool RGB, bool ENT>
+__global__ void __launch_bounds__(128) ua_blend_tile2_kernel(UaBlendArgs a) {
+  constexpr int CS = Col<LC>::STRIDE;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
+  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
+                                                            (ENT ? sizeof(UaRec) : 0)));
+  __shared__ double s_red[4];
+  load_math_tables();
+
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = a.scene.n;
+  const GeoRec* geo = a.geo + (int64_t)v * N;
+  const UaRec* uar = a.ua + (int64_t)v * N;
+
+  const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
+  const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3);
+  const int py1 = py0 + 4;
+  const bool in0 = px < c.width && py0 < c.height;
+  const bool in1 = px < c.width && py1 < c.height;
+  Pixel<LC> P0, P1;
+  pixel_init<LC, RGB, ENT>(P0, c, px, py0, in0);
+  pixel_init<LC, RGB, ENT>(P1, c, px, py1, in1);
+
+  for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
+    const bool live = !(P0.rgb_done && P0.ent_done && P1.rgb_done && P1.ent_done);
+    if (__syncthreads_count(live) == 0) break;
+    const int n = min((uint32_t)kBatch, rg.y - base);
+    stage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
+    __syncthreads();
+    if (!live) continue;
+    for (int j = 0; j < n; ++j) {
+      const int4 rr = s_rect[j];
+      const bool c0 = !(P0.rgb_done && P0.ent_done) && in_rect4(rr, px, py0);
+      const bool c1 = !(P1.rgb_done && P1.ent_done) && in_rect4(rr, px, py1);
+      if (!(c0 || c1)) continue;
+      const GeoRec& e = s_geo[j];
+      const float2* col2 = reinterpret_cast<const float2*>(s_col + j * CS);
+      if (c0) {
+        const double al = splat_alpha(e, P0.cxp, P0.cyp, a.amax);
+        if (RGB && !P0.rgb_done) rgb_step<LC>(P0, al, e.depth, col2, a.cutoff);
+        if (ENT && !P0.ent_done) ent_step<LC>(P0, al, e.depth, s_ua[j], a.amax, a.cutoff, a.hl_qc);
+      }
+      if (c1) {
+        const double al = splat_alpha(e, P1.cxp, P1.cyp, a.amax);
+        if (RGB && !P1.rgb_done) rgb_step<LC>(P1, al, e.depth, col2, a.cutoff);
+        if (ENT && !P1.ent_done) ent_step<LC>(P1, al, e.depth, s_ua[j], a.amax, a.cutoff, a.hl_qc);
+      }
+    }
+  }
+  pixel_finish<LC, RGB, ENT>(P0, a, c, px, py0, in0);
+  pixel_finish<LC, RGB, ENT>(P1, a, c, px, py1, in1);
+  if (ENT && a.tile_score) {
+    double h = (in0 ? P0.H : 0.0) + (in1 ? P1.H : 0.0);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
+    if (lane == 0) s_red[warp] = h;
+    __syncthreads();
+    if (tid == 0) a.tile_score[gt] = ((s_red[0] + s_red[1]) + s_red[2]) + s_red[3];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Any tile size: 256 threads, one pixel each, pixels in rounds of 256.
+template <int LC, bool RGB, bool ENT>
+__global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
+  constexpr int CS = Col<LC>::STRIDE;
+  constexpr int kThreads = 256, kWarps = 8;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
+  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
+                                                            (ENT ? sizeof(UaRec) : 0)));
   __shared__ double s_red[kWarps];
-  __shared__ MathSmem s_math;
-  load_math_tables(&s_math);
+  load_math_tables();
 
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
@@ -70,131 +313,35 @@ __global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
   const int64_t N = a.scene.n;
   const GeoRec* geo = a.geo + (int64_t)v * N;
   const UaRec* uar = a.ua + (int64_t)v * N;
-  const float4* colors4 = reinterpret_cast<const float4*>(a.scene.colors);
   double tile_h = 0.0;
 
   for (int round = 0; round < rounds; ++round) {
-    int lx, ly;
-    tile_pixel(ts, tid, round, lx, ly);
+    const int li = round * kThreads + tid;
+    const int lx = li % ts, ly = li / ts;
     const int px = tx * ts + lx, py = ty * ts + ly;
-    const bool inside = lx < ts && ly < ts && px < c.width && py < c.height &&
-                        (ts == 16 || round * kThreads + tid < ts * ts);
-    const double cxp = px + 0.5, cyp = py + 0.5;
-
-    float basis[NB];
-    if (RGB) {
-      // CameraView::pixel_ray (model.hpp:83-86) + eval_real_sh_block at the ray.
-      const double dc0 = (cxp - c.cx) / c.fx, dc1 = (cyp - c.cy) / c.fy, dc2 = 1.0;
-      const double r0 = c.R[0] * dc0 + c.R[1] * dc1 + c.R[2] * dc2;
-      const double r1 = c.R[3] * dc0 + c.R[4] * dc1 + c.R[5] * dc2;
-      const double r2 = c.R[6] * dc0 + c.R[7] * dc1 + c.R[8] * dc2;
-      const double n2 = r0 * r0 + r1 * r1 + r2 * r2;
-      const double nn = n2 > 0.0 ? sqrt(n2) : 1.0;
-      double bd[NB];
-      eval_sh<LC>(r0 / nn, r1 / nn, r2 / nn, bd);
-#pragma unroll
-      for (int i = 0; i < NB; ++i) basis[i] = (float)bd[i];
-    }
-
-    double T = 1.0, rgb0 = 0.0, rgb1 = 0.0, rgb2 = 0.0, dep = 0.0;
-    double Te = 1.0, H = 0.0, w0 = 0.0, edep = 0.0;
-    bool rgb_done = !(RGB && inside);
-    bool ent_done = !(ENT && inside);
-    int32_t n_rgb = 0, n_ent = 0;
-
+    const bool inside = li < ts * ts && px < c.width && py < c.height;
+    Pixel<LC> P;
+    pixel_init<LC, RGB, ENT>(P, c, px, py, inside);
     for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-      if (__syncthreads_count(!(rgb_done && ent_done)) == 0) break;
+      const bool live = !(P.rgb_done && P.ent_done);
+      if (__syncthreads_count(live) == 0) break;
       const int n = min((uint32_t)kBatch, rg.y - base);
-      for (int j = tid; j < n; j += kThreads) {
-        const uint32_t g = a.vals[base + j];
-        s_geo[j] = geo[g];
-        if (ENT) s_ua[j] = uar[g];
-      }
-      if (RGB) {
-        constexpr int V4 = CS / 4;
-        for (int k = tid; k < n * V4; k += kThreads) {
-          const int j = k / V4, q = k - j * V4;
-          const uint32_t g = a.vals[base + j];
-          reinterpret_cast<float4*>(s_col)[k] = colors4[(int64_t)g * V4 + q];
-        }
-      }
+      stage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
       __syncthreads();
-      if (!(rgb_done && ent_done)) {
-        for (int j = 0; j < n; ++j) {
-          const GeoRec& e = s_geo[j];
-          if (px < cov_lo(e.cov_x) || px > cov_hi(e.cov_x) || py < cov_lo(e.cov_y) ||
-              py > cov_hi(e.cov_y))
-            continue;
-          const double dx = cxp - e.mx;
-          const double dy = cyp - e.my;
-          const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-          double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
-          if (q <= kQSkip) {
-            al = (double)e.opacity * exp_neg(-0.5 * q, &s_math);
-            al = al > a.amax ? a.amax : al;
-          }
-          if (RGB && !rgb_done) {
-            ++n_rgb;
-            const double w = al * T;
-            if (w > 0.0) {
-              const float* col = s_col + j * CS;
-              float c0 = 0.f, c1 = 0.f, c2 = 0.f;
-#pragma unroll
-              for (int i = 0; i < NB; ++i) {
-                c0 = __fmaf_rn(col[i], basis[i], c0);
-                c1 = __fmaf_rn(col[NB + i], basis[i], c1);
-                c2 = __fmaf_rn(col[2 * NB + i], basis[i], c2);
-              }
-              c0 = fminf(fmaxf(c0, 0.f), 1.f);
-              c1 = fminf(fmaxf(c1, 0.f), 1.f);
-              c2 = fminf(fmaxf(c2, 0.f), 1.f);
-              rgb0 += w * (double)c0;
-              rgb1 += w * (double)c1;
-              rgb2 += w * (double)c2;
-              dep += w * e.depth;
-            }
-            T *= 1.0 - al;
-            if (T < a.cutoff) rgb_done = true;
-          }
-          if (ENT && !ent_done) {
-            ++n_ent;
-            const UaRec& u = s_ua[j];
-            double as = u.A * al + u.B;
-            as = as < 0.0 ? 0.0 : (a.amax < as ? a.amax : as);
-            const double w = as * Te;
-            const double s = w * u.v;
-            if (s > 0.0) H += s * (-log_pos(s, &s_math) + a.hl_qc + kGaussEntropy);
-            w0 += w * u.omv;
-            edep += w * e.depth;
-            Te *= 1.0 - as;
-            if (Te < a.cutoff) ent_done = true;
-          }
-          if (rgb_done && ent_done) break;
-        }
+      if (!live) continue;
+      for (int j = 0; j < n; ++j) {
+        if (!in_rect4(s_rect[j], px, py)) continue;
+        const GeoRec& e = s_geo[j];
+        const double al = splat_alpha(e, P.cxp, P.cyp, a.amax);
+        if (RGB && !P.rgb_done)
+          rgb_step<LC>(P, al, e.depth, reinterpret_cast<const float2*>(s_col + j * CS), a.cutoff);
+        if (ENT && !P.ent_done) ent_step<LC>(P, al, e.depth, s_ua[j], a.amax, a.cutoff, a.hl_qc);
+        if (P.rgb_done && P.ent_done) break;
       }
     }
-    if (ENT && w0 > 0.0) H += w0 * (-log_pos(w0, &s_math) + a.hl_q0 + kGaussEntropy);
-    if (inside) {
-      const int64_t pix = c.pix_base + (int64_t)py * c.width + px;
-      if (RGB) {
-        if (a.rgb) {
-          a.rgb[pix * 3 + 0] = rgb0;
-          a.rgb[pix * 3 + 1] = rgb1;
-          a.rgb[pix * 3 + 2] = rgb2;
-        }
-        if (a.depth) a.depth[pix] = dep;
-        if (a.trans) a.trans[pix] = T;
-        if (a.rgb_contrib) a.rgb_contrib[pix] = n_rgb;
-      }
-      if (ENT) {
-        if (a.entropy) a.entropy[pix] = H;
-        if (a.w0) a.w0[pix] = w0;
-        if (a.edepth) a.edepth[pix] = edep;
-        if (a.ent_contrib) a.ent_contrib[pix] = n_ent;
-      }
-    }
+    pixel_finish<LC, RGB, ENT>(P, a, c, px, py, inside);
     if (ENT && a.tile_score) {
-      double h = inside ? H : 0.0;
+      double h = inside ? P.H : 0.0;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
       if (lane == 0) s_red[warp] = h;
@@ -211,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) ua_blend_kernel(UaBlendArgs a) {
   if (ENT && a.tile_score && tid == 0) a.tile_score[gt] = tile_h;
 }
 
-// K8: image score per view = fold of its tile partials in tile order, one warp
+// K8: image score per view = fold of its per-tile partials in tile order, one warp
 // per view (lane-contiguous chunks, then a fixed shuffle tree).
 __global__ void score_kernel(const DevCam* cams, int V, const double* tile_score, double* scores) {
   const int v = blockIdx.x;
@@ -226,18 +373,45 @@ __global__ void score_kernel(const DevCam* cams, int V, const double* tile_score
   if (lane == 0) scores[v] = sum;
 }
 
+template <class K>
+void set_smem(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int LC, bool RGB, bool ENT>
+void launch_one(const UaBlendArgs& a, cudaStream_t s) {
+  const size_t smem = Stage<LC, RGB, ENT>::bytes(kBatch);
+  static const bool generic = getenv("GAVIS_UA_GENERIC") != nullptr;
+  if (a.tile_size == 16 && !generic) {
+    static bool configured = false;
+    if (!configured) {
+      set_smem(ua_blend_tile2_kernel<LC, RGB, ENT>, smem);
+      configured = true;
+    }
+    ua_blend_tile2_kernel<LC, RGB, ENT><<<(unsigned)a.total_tiles, 128, smem, s>>>(a);
+    return;
+  }
+  static bool configured = false;
+  if (!configured) {
+    set_smem(ua_blend_kernel<LC, RGB, ENT>, smem);
+    configured = true;
+  }
+  ua_blend_kernel<LC, RGB, ENT><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
+}
+
 template <int LC>
 void launch_lc(const UaBlendArgs& a, cudaStream_t s) {
-  const unsigned grid = (unsigned)a.total_tiles;
   if (a.do_rgb && a.do_ent)
-    ua_blend_kernel<LC, true, true><<<grid, kThreads, 0, s>>>(a);
+    launch_one<LC, true, true>(a, s);
   else if (a.do_rgb)
-    ua_blend_kernel<LC, true, false><<<grid, kThreads, 0, s>>>(a);
+    launch_one<LC, true, false>(a, s);
   else if (a.do_ent)
-    ua_blend_kernel<LC, false, true><<<grid, kThreads, 0, s>>>(a);
+    launch_one<LC, false, true>(a, s);
 }
 
 }  // namespace
+
+int ua_score_parts(int /*tile_size*/) { return 1; }
 
 void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s) {
   if (a.total_tiles == 0) return;
@@ -250,8 +424,9 @@ void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s) {
   }
 }
 
-void launch_score(const DevCam* cams, int V, const double* tile_score, double* scores,
+void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,
                   cudaStream_t s) {
+  (void)parts;
   if (V == 0) return;
   score_kernel<<<V, 32, 0, s>>>(cams, V, tile_score, scores);
 }

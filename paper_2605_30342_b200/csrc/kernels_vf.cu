@@ -48,11 +48,11 @@ __device__ __forceinline__ void tile_pixel(int ts, int tid, int round, int& lx, 
 
 __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
   __shared__ GeoRec s_geo[kBatch];
+  __shared__ int4 s_rect[kBatch];
   __shared__ uint32_t s_pair[kBatch];
   __shared__ double s_sum[kWarps][kBatch];
   __shared__ int32_t s_cnt[kWarps][kBatch];
-  __shared__ MathSmem s_math;
-  load_math_tables(&s_math);
+  load_math_tables();
 
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
       for (int j = tid; j < n; j += kThreads) {
         const uint32_t p = a.vals[base + j];
         s_pair[j] = p;
-        s_geo[j] = geo[a.pair_gid[p]];
+        const GeoRec r = geo[a.pair_gid[p]];
+        s_geo[j] = r;
+        s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
       }
       for (int k = tid; k < kWarps * kBatch; k += kThreads) {
         (&s_sum[0][0])[k] = 0.0;
@@ -90,13 +92,12 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
       }
       __syncthreads();
       for (int j = 0; j < n; ++j) {
-        const GeoRec& e = s_geo[j];
-        const bool cov = !done && px >= cov_lo(e.cov_x) && px <= cov_hi(e.cov_x) &&
-                         py >= cov_lo(e.cov_y) && py <= cov_hi(e.cov_y);
+        const bool cov = !done && in_rect4(s_rect[j], px, py);
         const unsigned mask = __ballot_sync(0xffffffffu, cov);
         if (mask == 0u) continue;
         double contrib = 0.0;
         if (cov) {
+          const GeoRec& e = s_geo[j];
           contrib = T;  // v_k += T before the splat (raster.hpp:266)
           ++ncontrib;
           const double dx = cxp - e.mx;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
           const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
           double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
           if (q <= kQSkip) {
-            al = (double)e.opacity * exp_neg(-0.5 * q, &s_math);
+            al = (double)e.opacity * exp_neg(-0.5 * q);
             al = al > a.amax ? a.amax : al;
           }
           T *= 1.0 - al;
