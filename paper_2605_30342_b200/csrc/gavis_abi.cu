@@ -593,11 +593,12 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     ua.vals = b.vals;
     ua.do_rgb = do_rgb;
     ua.do_ent = do_ent;
-    // Images always land in device memory; host copies only when requested.
+    // The RGB and entropy images always land in device memory (host copies only
+    // when requested); depth and residual-transmittance maps only on request.
     if (do_rgb) {
       ua.rgb = (double*)c->buf("img_rgb", sizeof(double) * 3 * P);
-      ua.depth = (double*)c->buf("img_depth", sizeof(double) * P);
-      ua.trans = (double*)c->buf("img_trans", sizeof(double) * P);
+      ua.depth = out->depth ? (double*)c->buf("img_depth", sizeof(double) * P) : nullptr;
+      ua.trans = out->transmittance ? (double*)c->buf("img_trans", sizeof(double) * P) : nullptr;
       if (out->rgb_contributors) ua.rgb_contrib = (int32_t*)c->buf("img_nrgb", sizeof(int32_t) * P);
     }
     if (do_ent) {

@@ -57,7 +57,6 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 
 template <int LC>
 struct Pixel {
-  double cxp, cyp;
   double T, rgb0, rgb1, rgb2, dep;
   double Te, H, w0, edep;
   bool rgb_done, ent_done;
@@ -69,11 +68,10 @@ template <int LC, bool RGB, bool ENT>
 __device__ __forceinline__ void pixel_init(Pixel<LC>& P, const DevCam& c, int px, int py,
                                            bool inside) {
   constexpr int NB = Col<LC>::NB;
-  P.cxp = px + 0.5;
-  P.cyp = py + 0.5;
   if (RGB) {
     // CameraView::pixel_ray (model.hpp:83-86) + eval_real_sh_block at the ray.
-    const double dc0 = (P.cxp - c.cx) / c.fx, dc1 = (P.cyp - c.cy) / c.fy, dc2 = 1.0;
+    const double cxp = px + 0.5, cyp = py + 0.5;
+    const double dc0 = (cxp - c.cx) / c.fx, dc1 = (cyp - c.cy) / c.fy, dc2 = 1.0;
     const double r0 = c.R[0] * dc0 + c.R[1] * dc1 + c.R[2] * dc2;
     const double r1 = c.R[3] * dc0 + c.R[4] * dc1 + c.R[5] * dc2;
     const double r2 = c.R[6] * dc0 + c.R[7] * dc1 + c.R[8] * dc2;
@@ -126,10 +124,11 @@ __device__ __forceinline__ double splat_alpha(const GeoRec& e, double cxp, doubl
 }
 
 // RGB track update given alpha and (if w > 0) the colour (raster.hpp:209-221).
-template <int LC>
+// EXTRA: depth and contributor counts (only when an output asks for them).
+template <int LC, bool EXTRA>
 __device__ __forceinline__ void rgb_step(Pixel<LC>& P, double al, double depth, const float2* col2,
                                          double cutoff) {
-  ++P.n_rgb;
+  if (EXTRA) ++P.n_rgb;
   const double w = al * P.T;
   if (w > 0.0) {
     float c0, c1, c2;
@@ -137,29 +136,29 @@ __device__ __forceinline__ void rgb_step(Pixel<LC>& P, double al, double depth, 
     P.rgb0 += w * (double)c0;
     P.rgb1 += w * (double)c1;
     P.rgb2 += w * (double)c2;
-    P.dep += w * depth;
+    if (EXTRA) P.dep += w * depth;
   }
   P.T *= 1.0 - al;
   if (P.T < cutoff) P.rgb_done = true;
 }
 
 // Entropy track update (uncertainty.hpp:198-222).
-template <int LC>
+template <int LC, bool EXTRA>
 __device__ __forceinline__ void ent_step(Pixel<LC>& P, double al, double depth, const UaRec& u,
                                          double amax, double cutoff, double hl_qc) {
-  ++P.n_ent;
+  if (EXTRA) ++P.n_ent;
   double as = u.A * al + u.B;
   as = as < 0.0 ? 0.0 : (amax < as ? amax : as);
   const double w = as * P.Te;
   const double s = w * u.v;
   if (s > 0.0) P.H += s * (-log_pos(s) + hl_qc + kGaussEntropy);
   P.w0 += w * u.omv;
-  P.edep += w * depth;
+  if (EXTRA) P.edep += w * depth;
   P.Te *= 1.0 - as;
   if (P.Te < cutoff) P.ent_done = true;
 }
 
-template <int LC, bool RGB, bool ENT>
+template <int LC, bool RGB, bool ENT, bool EXTRA>
 __device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a, const DevCam& c,
                                              int px, int py, bool inside) {
   if (ENT && P.w0 > 0.0) P.H += P.w0 * (-log_pos(P.w0) + a.hl_q0 + kGaussEntropy);
@@ -171,15 +170,15 @@ __device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a,
       a.rgb[pix * 3 + 1] = P.rgb1;
       a.rgb[pix * 3 + 2] = P.rgb2;
     }
-    if (a.depth) a.depth[pix] = P.dep;
+    if (EXTRA && a.depth) a.depth[pix] = P.dep;
     if (a.trans) a.trans[pix] = P.T;
-    if (a.rgb_contrib) a.rgb_contrib[pix] = P.n_rgb;
+    if (EXTRA && a.rgb_contrib) a.rgb_contrib[pix] = P.n_rgb;
   }
   if (ENT) {
     if (a.entropy) a.entropy[pix] = P.H;
     if (a.w0) a.w0[pix] = P.w0;
-    if (a.edepth) a.edepth[pix] = P.edep;
-    if (a.ent_contrib) a.ent_contrib[pix] = P.n_ent;
+    if (EXTRA && a.edepth) a.edepth[pix] = P.edep;
+    if (EXTRA && a.ent_contrib) a.ent_contrib[pix] = P.n_ent;
   }
 }
 
@@ -216,8 +215,8 @@ __device__ __forceinline__ void stage_batch(const UaBlendArgs& a, const GeoRec* 
 
 // ---------------------------------------------------------------------------
 // 16x16 tiles, 128 threads, two pixels per thread.
-template <int LC, bool RGB, bool ENT>
-__global__ void __launch_bounds__(128) ua_blend_tile2_kernel(UaBlendArgs a) {
+template <int LC, bool RGB, bool ENT, bool EXTRA>
+__global__ void __launch_bounds__(128, 5) ua_blend_tile2_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
@@ -228,6 +227,7 @@ __global__ void __launch_bounds__(128) ua_blend_tile2_kernel(UaBlendArgs a) {
   __shared__ double s_red[4];
   load_math_tables();
 
+  const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
   const DevCam& c = a.cams[v];
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(128) ua_blend_tile2_kernel(UaBlendArgs a) {
   const int py1 = py0 + 4;
   const bool in0 = px < c.width && py0 < c.height;
   const bool in1 = px < c.width && py1 < c.height;
+  const double cxp = px + 0.5, cyp0 = py0 + 0.5, cyp1 = py1 + 0.5;
   Pixel<LC> P0, P1;
   pixel_init<LC, RGB, ENT>(P0, c, px, py0, in0);
   pixel_init<LC, RGB, ENT>(P1, c, px, py1, in1);
@@ -263,19 +264,19 @@ __global__ void __launch_bounds__(128) ua_blend_tile2_kernel(UaBlendArgs a) {
       const GeoRec& e = s_geo[j];
       const float2* col2 = reinterpret_cast<const float2*>(s_col + j * CS);
       if (c0) {
-        const double al = splat_alpha(e, P0.cxp, P0.cyp, a.amax);
-        if (RGB && !P0.rgb_done) rgb_step<LC>(P0, al, e.depth, col2, a.cutoff);
-        if (ENT && !P0.ent_done) ent_step<LC>(P0, al, e.depth, s_ua[j], a.amax, a.cutoff, a.hl_qc);
+        const double al = splat_alpha(e, cxp, cyp0, amax);
+        if (RGB && !P0.rgb_done) rgb_step<LC, EXTRA>(P0, al, e.depth, col2, cutoff);
+        if (ENT && !P0.ent_done) ent_step<LC, EXTRA>(P0, al, e.depth, s_ua[j], amax, cutoff, hl_qc);
       }
       if (c1) {
-        const double al = splat_alpha(e, P1.cxp, P1.cyp, a.amax);
-        if (RGB && !P1.rgb_done) rgb_step<LC>(P1, al, e.depth, col2, a.cutoff);
-        if (ENT && !P1.ent_done) ent_step<LC>(P1, al, e.depth, s_ua[j], a.amax, a.cutoff, a.hl_qc);
+        const double al = splat_alpha(e, cxp, cyp1, amax);
+        if (RGB && !P1.rgb_done) rgb_step<LC, EXTRA>(P1, al, e.depth, col2, cutoff);
+        if (ENT && !P1.ent_done) ent_step<LC, EXTRA>(P1, al, e.depth, s_ua[j], amax, cutoff, hl_qc);
       }
     }
   }
-  pixel_finish<LC, RGB, ENT>(P0, a, c, px, py0, in0);
-  pixel_finish<LC, RGB, ENT>(P1, a, c, px, py1, in1);
+  pixel_finish<LC, RGB, ENT, EXTRA>(P0, a, c, px, py0, in0);
+  pixel_finish<LC, RGB, ENT, EXTRA>(P1, a, c, px, py1, in1);
   if (ENT && a.tile_score) {
     double h = (in0 ? P0.H : 0.0) + (in1 ? P1.H : 0.0);
 #pragma unroll
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(128) ua_blend_tile2_kernel(UaBlendArgs a) {
 
 // ---------------------------------------------------------------------------
 // Any tile size: 256 threads, one pixel each, pixels in rounds of 256.
-template <int LC, bool RGB, bool ENT>
+template <int LC, bool RGB, bool ENT, bool EXTRA>
 __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
   constexpr int kThreads = 256, kWarps = 8;
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   __shared__ double s_red[kWarps];
   load_math_tables();
 
+  const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
   const DevCam& c = a.cams[v];
@@ -320,6 +322,7 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
     const int lx = li % ts, ly = li / ts;
     const int px = tx * ts + lx, py = ty * ts + ly;
     const bool inside = li < ts * ts && px < c.width && py < c.height;
+    const double cxp = px + 0.5, cyp = py + 0.5;
     Pixel<LC> P;
     pixel_init<LC, RGB, ENT>(P, c, px, py, inside);
     for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
@@ -332,14 +335,14 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
       for (int j = 0; j < n; ++j) {
         if (!in_rect4(s_rect[j], px, py)) continue;
         const GeoRec& e = s_geo[j];
-        const double al = splat_alpha(e, P.cxp, P.cyp, a.amax);
+        const double al = splat_alpha(e, cxp, cyp, amax);
         if (RGB && !P.rgb_done)
-          rgb_step<LC>(P, al, e.depth, reinterpret_cast<const float2*>(s_col + j * CS), a.cutoff);
-        if (ENT && !P.ent_done) ent_step<LC>(P, al, e.depth, s_ua[j], a.amax, a.cutoff, a.hl_qc);
+          rgb_step<LC, EXTRA>(P, al, e.depth, reinterpret_cast<const float2*>(s_col + j * CS), cutoff);
+        if (ENT && !P.ent_done) ent_step<LC, EXTRA>(P, al, e.depth, s_ua[j], amax, cutoff, hl_qc);
         if (P.rgb_done && P.ent_done) break;
       }
     }
-    pixel_finish<LC, RGB, ENT>(P, a, c, px, py, inside);
+    pixel_finish<LC, RGB, ENT, EXTRA>(P, a, c, px, py, inside);
     if (ENT && a.tile_score) {
       double h = inside ? P.H : 0.0;
 #pragma unroll
@@ -378,35 +381,44 @@ void set_smem(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int LC, bool RGB, bool ENT>
+template <int LC, bool RGB, bool ENT, bool EXTRA>
 void launch_one(const UaBlendArgs& a, cudaStream_t s) {
   const size_t smem = Stage<LC, RGB, ENT>::bytes(kBatch);
   static const bool generic = getenv("GAVIS_UA_GENERIC") != nullptr;
   if (a.tile_size == 16 && !generic) {
     static bool configured = false;
     if (!configured) {
-      set_smem(ua_blend_tile2_kernel<LC, RGB, ENT>, smem);
+      set_smem(ua_blend_tile2_kernel<LC, RGB, ENT, EXTRA>, smem);
       configured = true;
     }
-    ua_blend_tile2_kernel<LC, RGB, ENT><<<(unsigned)a.total_tiles, 128, smem, s>>>(a);
+    ua_blend_tile2_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 128, smem, s>>>(a);
     return;
   }
   static bool configured = false;
   if (!configured) {
-    set_smem(ua_blend_kernel<LC, RGB, ENT>, smem);
+    set_smem(ua_blend_kernel<LC, RGB, ENT, EXTRA>, smem);
     configured = true;
   }
-  ua_blend_kernel<LC, RGB, ENT><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
+  ua_blend_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
+}
+
+template <int LC, bool EXTRA>
+void launch_lc_x(const UaBlendArgs& a, cudaStream_t s) {
+  if (a.do_rgb && a.do_ent)
+    launch_one<LC, true, true, EXTRA>(a, s);
+  else if (a.do_rgb)
+    launch_one<LC, true, false, EXTRA>(a, s);
+  else if (a.do_ent)
+    launch_one<LC, false, true, EXTRA>(a, s);
 }
 
 template <int LC>
 void launch_lc(const UaBlendArgs& a, cudaStream_t s) {
-  if (a.do_rgb && a.do_ent)
-    launch_one<LC, true, true>(a, s);
-  else if (a.do_rgb)
-    launch_one<LC, true, false>(a, s);
-  else if (a.do_ent)
-    launch_one<LC, false, true>(a, s);
+  const bool extra = a.depth || a.edepth || a.rgb_contrib || a.ent_contrib;
+  if (extra)
+    launch_lc_x<LC, true>(a, s);
+  else
+    launch_lc_x<LC, false>(a, s);
 }
 
 }  // namespace
