@@ -293,6 +293,13 @@ def run_ours(args):
     total_cands = sum_over_ranks(float(len(cands) * args.steps), dist)
     value = total_cands / (ms_max / 1000.0)
 
+    # secondary: the reference planner's own select_nbv work (entropy + score, no RGB)
+    barrier(ctx, dist)
+    ctx.timer_start()
+    api.select_nbv(ctx, ds, field, cands, rc, uc, with_rgb=False)
+    ms_sel = max_over_ranks(ctx.timer_stop(), dist)
+    select_only = sum_over_ranks(float(len(cands)), dist) / (ms_sel / 1000.0)
+
     # algorithmic bytes of the dominant kernel (ua_blend): per view 24 B per tile pair
     # (8 B key + 4 B id written once, read once) + 16 B per pixel (RGB + entropy, fp32)
     keys_per_view = []
@@ -385,6 +392,7 @@ def run_ours(args):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
             "pipeline": {"bytes_per_step": pipe_bytes, "achieved_gbs": pipe_bytes / (step_ms / 1000.0) / 1e9,
                          "pairs_per_view": K_avg, "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()}},
+            "select_nbv_entropy_only_views_per_s": select_only,
             "vf_build_ms": vf_ms, "vf_build_views": len(train), "vf_build_200_views_ms": vf200_ms,
             "best_index_last_step": int(res.best_index) + lo,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
