@@ -204,6 +204,28 @@ gavis_status gavis_select_nbv(gavis_ctx* ctx, const gavis_scene* scene,
                               const gavis_uncertainty_config* uc, int32_t with_rgb,
                               double* scores, int32_t* best_index);
 
+/* ---- density control (vfield.hpp:136-199) ------------------------------ */
+/* DensityControlConfig (vfield.hpp:136-147). Defaults rho 100, eta 0.5,
+ * eps_v 0.95, seed 0. */
+typedef struct {
+  double rho, eta, eps_v;
+  uint64_t seed;
+} gavis_density_config;
+
+/* density_control: floor(rho * volume(bounds)) transparent virtual probes
+ * (SplitMix64(derive_seed(seed, k)) positions, scale cbrt(3(1+eta)/(4 pi rho)),
+ * stored in fp32 like every scene array), isotropic multi-view visibility
+ * 1 - prod_views(1 - b) computed on the device with the VF kernels, probes with
+ * visibility <= eps_v appended after the real particles in a new device scene
+ * (*out, caller destroys). kept_ids (nullable, capacity kept_capacity) receives
+ * the probe indices k in sampling order. */
+gavis_status gavis_density_control(gavis_ctx* ctx, const gavis_scene* scene,
+                                   const double* bounds_min, const double* bounds_max,
+                                   const gavis_camera* views, int32_t n_views,
+                                   const gavis_density_config* cfg,
+                                   const gavis_raster_config* rc, gavis_scene** out,
+                                   int64_t* n_kept, int64_t* kept_ids, int64_t kept_capacity);
+
 /* ---- parity / debug ----------------------------------------------------- */
 /* Projection records of one camera (ImageSpaceSplat, raster.hpp:37-44) for all
  * N particles: culled[N] (1 = culled), mean[2N], conic[3N] (a, b, c), depth[N],

@@ -773,6 +773,98 @@ int gor_select_nbv(const gor_scene* s, const double* gamma, int degree, int num_
 
 /* ------------------------------------------------------------- oracle.hpp */
 
+/* ------------------------------------------------ rng.hpp + density control */
+
+static uint64_t mix64_(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+/* derive_seed rng.hpp:26-28 */
+uint64_t gor_derive_seed(uint64_t seed, uint64_t stream) {
+  return mix64_(seed ^ mix64_(stream + 0x632be59bd9b4e019ull));
+}
+
+/* SplitMix64::next_double rng.hpp:35-45 */
+static double sm_next_double(uint64_t* state) {
+  *state += 0x9e3779b97f4a7c15ull;
+  uint64_t z = *state;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z = z ^ (z >> 31);
+  return (double)(z >> 11) * 0x1.0p-53;
+}
+
+/* density_control vfield.hpp:149-199 */
+int64_t gor_density_control(const gor_scene* s, const double* bmin, const double* bmax,
+                            const gor_camera* views, int n_views, double rho, double eta,
+                            double eps_v, uint64_t seed, const gor_raster* rc, int threads,
+                            int round_f32, int64_t* kept_ids, double* unseen_out) {
+  const double ext[3] = {bmax[0] - bmin[0], bmax[1] - bmin[1], bmax[2] - bmin[2]};
+  const double volume = ext[0] * ext[1] * ext[2];
+  const int64_t n_virtual = (int64_t)floor(rho * volume);
+  const int64_t n_real = s->num_particles;
+  const int64_t n = n_real + n_virtual;
+  const int nb = (s->color_degree + 1) * (s->color_degree + 1);
+  double sc = cbrt(3.0 * (1.0 + eta) / (4.0 * K_PI * rho));
+  if (round_f32) sc = (double)(float)sc;
+  double* pos = (double*)malloc(sizeof(double) * 3 * (size_t)(n + 1));
+  double* rot = (double*)malloc(sizeof(double) * 4 * (size_t)(n + 1));
+  double* scl = (double*)malloc(sizeof(double) * 3 * (size_t)(n + 1));
+  double* op = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+  double* col = (double*)calloc((size_t)(3 * nb * (n + 1)), sizeof(double));
+  uint8_t* virt = (uint8_t*)calloc((size_t)(n + 1), 1);
+  memcpy(pos, s->positions, sizeof(double) * 3 * (size_t)n_real);
+  memcpy(rot, s->rotations, sizeof(double) * 4 * (size_t)n_real);
+  memcpy(scl, s->scales, sizeof(double) * 3 * (size_t)n_real);
+  memcpy(op, s->opacities, sizeof(double) * (size_t)n_real);
+  memcpy(col, s->colors, sizeof(double) * 3 * nb * (size_t)n_real);
+  if (s->is_virtual) memcpy(virt, s->is_virtual, (size_t)n_real);
+  for (int64_t k = 0; k < n_virtual; ++k) {
+    uint64_t st = gor_derive_seed(seed, (uint64_t)k);
+    const double ux = sm_next_double(&st), uy = sm_next_double(&st), uz = sm_next_double(&st);
+    const double u[3] = {ux, uy, uz};
+    const int64_t i = n_real + k;
+    for (int d = 0; d < 3; ++d) {
+      double p = bmin[d] + ext[d] * u[d];
+      pos[3 * i + d] = round_f32 ? (double)(float)p : p;
+      scl[3 * i + d] = sc;
+    }
+    rot[4 * i] = 1.0;
+    rot[4 * i + 1] = rot[4 * i + 2] = rot[4 * i + 3] = 0.0;
+    op[i] = 0.0;
+    virt[i] = 1;
+  }
+  gor_scene probe = {n, s->color_degree, 0, pos, rot, scl, op, col, virt};
+  double* unseen = (double*)malloc(sizeof(double) * (size_t)(n_virtual + 1));
+  for (int64_t k = 0; k < n_virtual; ++k) unseen[k] = 1.0;
+  double* b = (double*)malloc(sizeof(double) * (size_t)(n + 1));
+  (void)threads;
+  for (int v = 0; v < n_views; ++v) {
+    gor_single_view_visibility(&probe, &views[v], rc, b, NULL, NULL);
+    for (int64_t k = 0; k < n_virtual; ++k) unseen[k] *= 1.0 - b[n_real + k];
+  }
+  int64_t kept = 0;
+  for (int64_t k = 0; k < n_virtual; ++k) {
+    if (unseen_out) unseen_out[k] = unseen[k];
+    double vtilde = 1.0 - unseen[k];
+    if (vtilde > eps_v) continue;
+    if (kept_ids) kept_ids[kept] = k;
+    ++kept;
+  }
+  free(pos);
+  free(rot);
+  free(scl);
+  free(op);
+  free(col);
+  free(virt);
+  free(unseen);
+  free(b);
+  return kept;
+}
+
 /* raymarch_transmittance oracle.hpp:70-103 */
 double gor_raymarch_transmittance(const gor_scene* s, const double* origin,
                                   const double* target, double step, int64_t exclude,

@@ -110,6 +110,16 @@ int gor_select_nbv(const gor_scene* s, const double* gamma, int degree, int num_
                    const gor_camera* cams, int n_cams, const gor_raster* rc,
                    const gor_unc* uc, int threads, int with_rgb, double* scores);
 
+/* density_control vfield.hpp:157-199: appends the retained virtual probes to a
+ * copy of the scene arrays. Writes kept probe ids (k) into kept_ids (capacity
+ * n_virtual = floor(rho * volume)) and returns their count. round_f32 != 0 rounds
+ * the probe position/scale to fp32 first (what the device stores). */
+int64_t gor_density_control(const gor_scene* s, const double* bounds_min, const double* bounds_max,
+                            const gor_camera* views, int n_views, double rho, double eta,
+                            double eps_v, uint64_t seed, const gor_raster* rc, int threads,
+                            int round_f32, int64_t* kept_ids, double* unseen_out);
+uint64_t gor_derive_seed(uint64_t seed, uint64_t stream);
+
 /* oracle.hpp:70-103 */
 double gor_raymarch_transmittance(const gor_scene* s, const double* origin,
                                   const double* target, double step, int64_t exclude,

@@ -306,3 +306,28 @@ def raymarch_transmittance(scene, origin, target, step: float, exclude: int = -1
     t = np.ascontiguousarray(target, np.float64)
     return lib().gor_raymarch_transmittance(C.byref(s.c), _p(o), _p(t), C.c_double(step),
                                             C.c_int64(exclude), C.c_double(alpha_clamp_max))
+
+
+def derive_seed(seed: int, stream: int) -> int:
+    lib().gor_derive_seed.restype = C.c_uint64
+    return lib().gor_derive_seed(C.c_uint64(seed), C.c_uint64(stream))
+
+
+def density_control(scene, bounds_min, bounds_max, views, rho=100.0, eta=0.5, eps_v=0.95, seed=0,
+                    rc=None, round_f32: bool = True):
+    """density_control (vfield.hpp:157-199); returns (kept probe ids, unseen products)."""
+    from paper_2605_30342_b200.model import RasterConfig
+    rc = rc or RasterConfig()
+    s = _scene(scene)
+    bmin = np.ascontiguousarray(bounds_min, np.float64)
+    bmax = np.ascontiguousarray(bounds_max, np.float64)
+    ext = bmax - bmin
+    n_virtual = int(np.floor(rho * (ext[0] * ext[1] * ext[2])))
+    kept = np.zeros(max(1, n_virtual), np.int64)
+    unseen = np.zeros(max(1, n_virtual))
+    arr = cameras_array(views)
+    lib().gor_density_control.restype = C.c_int64
+    n = lib().gor_density_control(C.byref(s.c), _p(bmin), _p(bmax), arr, len(views), C.c_double(rho),
+                                  C.c_double(eta), C.c_double(eps_v), C.c_uint64(seed),
+                                  C.byref(raster_struct(rc)), 1, int(round_f32), _p(kept), _p(unseen))
+    return kept[:n], unseen[:n_virtual]

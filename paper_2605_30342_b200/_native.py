@@ -45,6 +45,10 @@ class RenderOutputs(C.Structure):
                 ("with_rgb", C.c_int32), ("with_entropy", C.c_int32)]
 
 
+class DensityConfigC(C.Structure):
+    _fields_ = [("rho", C.c_double), ("eta", C.c_double), ("eps_v", C.c_double), ("seed", C.c_uint64)]
+
+
 # Every symbol include/gavis_b200.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = [
     "gavis_abi_version", "gavis_last_error", "gavis_ctx_create", "gavis_ctx_destroy",
@@ -55,7 +59,7 @@ EXPORTS = [
     "gavis_vf_accumulate_views", "gavis_vf_accumulate_visibility", "gavis_vf_upload",
     "gavis_vf_download", "gavis_vf_set_num_views", "gavis_vf_device_gamma", "gavis_vf_destroy",
     "gavis_single_view_visibility", "gavis_vf_query", "gavis_vf_query_view", "gavis_ua_render",
-    "gavis_select_nbv", "gavis_debug_project", "gavis_debug_binning",
+    "gavis_select_nbv", "gavis_density_control", "gavis_debug_project", "gavis_debug_binning",
 ]
 
 _lib = None

@@ -137,6 +137,12 @@ class DeviceScene:
         N.check(ctx.lib.gavis_scene_upload(ctx.h, C.byref(d), C.byref(h)))
         self.h = h
 
+    @classmethod
+    def _adopt(cls, ctx: Context, handle, n: int, color_degree: int, bounds) -> "DeviceScene":
+        obj = cls.__new__(cls)
+        obj.ctx, obj.h, obj.n, obj.color_degree, obj.bounds = ctx, handle, n, color_degree, bounds
+        return obj
+
     def close(self) -> None:
         if self.h:
             N.check(self.ctx.lib.gavis_scene_destroy(self.h))
@@ -147,6 +153,13 @@ class DeviceScene:
             self.close()
         except Exception:
             pass
+
+
+class DensityControlConfig:
+    """vfield.hpp:136-147"""
+
+    def __init__(self, rho: float = 100.0, eta: float = 0.5, eps_v: float = 0.95, seed: int = 0):
+        self.rho, self.eta, self.eps_v, self.seed = rho, eta, eps_v, seed
 
 
 class DeviceField:
@@ -267,6 +280,28 @@ def query_view(ctx: Context, field: DeviceField, scene, cam: CameraView, dilatio
     N.check(ctx.lib.gavis_vf_query_view(ctx.h, field.h, ds.h, C.byref(camera_c(cam)), C.c_double(dilation),
                                         _ptr(idx), _ptr(vis), C.byref(n)))
     return ViewQuery(idx[: n.value], vis[: n.value])
+
+
+def density_control(ctx: Context, scene, views: Sequence[CameraView], cfg: "DensityControlConfig",
+                    rc: RasterConfig = RasterConfig(), bounds=None):
+    """density_control (vfield.hpp:157-199) on the device. Returns the augmented device
+    scene (real particles, then retained probes) and the retained probe ids."""
+    ds = _as_dev(ctx, scene)
+    bmin, bmax = bounds if bounds is not None else ds.bounds
+    bmin = np.ascontiguousarray(bmin, np.float64)
+    bmax = np.ascontiguousarray(bmax, np.float64)
+    ext = bmax - bmin
+    cap = max(1, int(np.floor(cfg.rho * max(0.0, ext[0] * ext[1] * ext[2]))))
+    kept = np.zeros(cap, np.int64)
+    n_kept = C.c_int64()
+    h = C.c_void_p()
+    dc = N.DensityConfigC(float(cfg.rho), float(cfg.eta), float(cfg.eps_v), int(cfg.seed))
+    arr = cameras_c(views)
+    N.check(ctx.lib.gavis_density_control(ctx.h, ds.h, _ptr(bmin), _ptr(bmax), arr, C.c_int32(len(views)),
+                                          C.byref(dc), C.byref(raster_c(rc)), C.byref(h), C.byref(n_kept),
+                                          _ptr(kept), C.c_int64(cap)))
+    out = DeviceScene._adopt(ctx, h, ds.n + n_kept.value, ds.color_degree, (bmin, bmax))
+    return out, kept[: n_kept.value]
 
 
 # ----------------------------------------------------------------- UA render

@@ -469,9 +469,16 @@ void check_scene_field(const gavis_scene* s, const gavis_field* f) {
 }
 
 // VF accumulation of views [0, n) into field (or only per-view outputs).
+// Optional per-batch consumer of the device visibilities: density control's
+// unseen[k] *= 1 - b[n_real + k], views in trajectory order (vfield.hpp:187-190).
+struct DensityHook {
+  double* unseen = nullptr;  // device [n_virtual]
+  int64_t n_real = 0, n_virtual = 0;
+};
+
 void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_camera* views,
               int n_views, const gavis_raster_config* rc, double* vis_host, int64_t* touch_host,
-              int32_t* contrib_host) {
+              int32_t* contrib_host, const DensityHook* dh = nullptr) {
   const int64_t N = s->dev.n;
   const int bv = batch_views(c, N, n_views);
   double scales[kMaxFieldDegree + 1] = {0};
@@ -516,10 +523,14 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
     fa.gamma = f ? f->gamma : nullptr;
     fa.degree = f ? f->degree : 0;
     std::memcpy(fa.scales, scales, sizeof(scales));
-    if (vis_host) fa.vis_out = (double*)c->buf("vis_out", sizeof(double) * V * std::max<int64_t>(1, N));
+    if (vis_host || dh) fa.vis_out = (double*)c->buf("vis_out", sizeof(double) * V * std::max<int64_t>(1, N));
     if (touch_host)
       fa.touch_out = (int64_t*)c->buf("touch_out", sizeof(int64_t) * V * std::max<int64_t>(1, N));
     c->run("vf_finalize", [&] { launch_vf_finalize(fa, N, c->stream); }, N > 0 ? 1 : 0);
+    if (dh && dh->n_virtual > 0)
+      c->run("density", [&] {
+        launch_density_update(dh->unseen, fa.vis_out, V, N, dh->n_real, dh->n_virtual, c->stream);
+      });
     if (vis_host && N > 0)
       CK(cudaMemcpyAsync(vis_host + (int64_t)v0 * N, fa.vis_out, sizeof(double) * V * N,
                          cudaMemcpyDeviceToHost, c->stream));
@@ -761,6 +772,178 @@ gavis_status gavis_ctx_launch_count(gavis_ctx* c, int64_t* launches) {
   return guard([&] {
     require(c != nullptr && launches != nullptr, "context and out must not be null");
     *launches = c->launches;
+  });
+}
+
+// Device scene with room for n particles (arrays uninitialised).
+static gavis_scene* alloc_scene(gavis_ctx* c, int64_t n, int color_degree) {
+  auto* s = new gavis_scene();
+  s->ctx = c;
+  const int nb = (color_degree + 1) * (color_degree + 1);
+  const int nbp = nb + (nb & 1);
+  const int cstride = ((3 * nbp + 3) / 4) * 4;
+  const int64_t M = std::max<int64_t>(n, 1);
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = cudaMalloc(&s->pos_op, sizeof(float4) * M);
+  if (e == cudaSuccess) e = cudaMalloc(&s->rot, sizeof(float4) * M);
+  if (e == cudaSuccess) e = cudaMalloc(&s->scale, sizeof(float4) * M);
+  if (e == cudaSuccess) e = cudaMalloc(&s->virt, M);
+  if (e == cudaSuccess) e = cudaMalloc(&s->colors, sizeof(float) * cstride * M);
+  if (e != cudaSuccess) {
+    cudaFree(s->pos_op);
+    cudaFree(s->rot);
+    cudaFree(s->scale);
+    cudaFree(s->virt);
+    cudaFree(s->colors);
+    delete s;
+    throw DevErr(std::string("cudaMalloc(scene) failed: ") + cudaGetErrorString(e));
+  }
+  s->dev.n = n;
+  s->dev.color_degree = color_degree;
+  s->dev.nb = nb;
+  s->dev.cstride = cstride;
+  s->dev.pos_op = s->pos_op;
+  s->dev.rot = s->rot;
+  s->dev.scale = s->scale;
+  s->dev.virt = s->virt;
+  s->dev.colors = s->colors;
+  return s;
+}
+
+// Copies particles [0, n) of src into dst at offset `at` (device to device).
+static void copy_particles(gavis_ctx* c, gavis_scene* dst, int64_t at, const gavis_scene* src,
+                           int64_t n) {
+  if (n == 0) return;
+  const int cs = src->dev.cstride;
+  CK(cudaMemcpyAsync(dst->pos_op + at, src->pos_op, sizeof(float4) * n, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->rot + at, src->rot, sizeof(float4) * n, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->scale + at, src->scale, sizeof(float4) * n, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->virt + at, src->virt, n, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->colors + at * cs, src->colors, sizeof(float) * cs * n,
+                     cudaMemcpyDeviceToDevice, c->stream));
+}
+
+struct ProbeSet {
+  std::vector<float4> pos_op, rot, scale;
+  std::vector<uint8_t> virt;
+};
+
+// Writes probes [first, first + n) of `p` after the particles already in dst.
+static void upload_probes(gavis_ctx* c, gavis_scene* dst, int64_t at, const ProbeSet& p,
+                          const std::vector<int64_t>& pick) {
+  const int64_t n = (int64_t)pick.size();
+  if (n == 0) return;
+  std::vector<float4> a(n), b(n), d(n);
+  std::vector<uint8_t> v(n, 1);
+  for (int64_t i = 0; i < n; ++i) {
+    a[i] = p.pos_op[pick[i]];
+    b[i] = p.rot[pick[i]];
+    d[i] = p.scale[pick[i]];
+  }
+  const int cs = dst->dev.cstride;
+  CK(cudaMemcpyAsync(dst->pos_op + at, a.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->rot + at, b.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->scale + at, d.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(dst->virt + at, v.data(), n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(dst->colors + at * cs, 0, sizeof(float) * cs * n, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
+}
+
+static uint64_t mix64_host(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// density_control (vfield.hpp:149-199): probes uniform in the bounds
+// (SplitMix64(derive_seed(seed, k)), rng.hpp:26-45), isotropic multi-view
+// visibility 1 - prod(1 - b_p) over the trajectory on the device, probes with
+// visibility <= eps_v appended (flagged virtual, opacity 0, identity rotation).
+gavis_status gavis_density_control(gavis_ctx* c, const gavis_scene* scene, const double* bmin,
+                                   const double* bmax, const gavis_camera* views, int32_t n_views,
+                                   const gavis_density_config* cfg, const gavis_raster_config* rc,
+                                   gavis_scene** out, int64_t* n_kept, int64_t* kept_ids,
+                                   int64_t kept_capacity) {
+  return guard([&] {
+    require(c && scene && bmin && bmax && cfg && out, "null argument");
+    require(cfg->rho > 0.0, "density rho must be positive");
+    require(cfg->eta > -1.0, "density eta must exceed -1");
+    require(cfg->eps_v > 0.0 && cfg->eps_v <= 1.0, "density eps_v must lie in (0, 1]");
+    validate_raster(rc);
+    require(n_views >= 0 && (views || n_views == 0), "views must not be null");
+    for (int i = 0; i < n_views; ++i) validate_camera(views[i]);
+    const double ext[3] = {bmax[0] - bmin[0], bmax[1] - bmin[1], bmax[2] - bmin[2]};
+    const double volume = ext[0] * ext[1] * ext[2];
+    require(volume > 0.0, "density_control: scene bounds volume must be positive");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    const int64_t n_virtual = (int64_t)std::floor(cfg->rho * volume);
+    const int64_t n_real = scene->dev.n;
+    require(n_real + n_virtual < (int64_t(1) << 31), "density_control: too many probes");
+    const double sc = std::cbrt(3.0 * (1.0 + cfg->eta) / (4.0 * kPi * cfg->rho));
+    ProbeSet p;
+    p.pos_op.resize(n_virtual);
+    p.rot.resize(n_virtual, make_float4(1.f, 0.f, 0.f, 0.f));
+    p.scale.resize(n_virtual, make_float4((float)sc, (float)sc, (float)sc, 0.f));
+    for (int64_t k = 0; k < n_virtual; ++k) {
+      uint64_t st = mix64_host(cfg->seed ^ mix64_host((uint64_t)k + 0x632be59bd9b4e019ull));
+      double u[3];
+      for (int d = 0; d < 3; ++d) {
+        st += 0x9e3779b97f4a7c15ull;
+        uint64_t z = st;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z = z ^ (z >> 31);
+        u[d] = (double)(z >> 11) * 0x1.0p-53;
+      }
+      p.pos_op[k] = make_float4((float)(bmin[0] + ext[0] * u[0]), (float)(bmin[1] + ext[1] * u[1]),
+                                (float)(bmin[2] + ext[2] * u[2]), 0.f);
+    }
+    std::vector<int64_t> all(n_virtual);
+    for (int64_t k = 0; k < n_virtual; ++k) all[k] = k;
+    gavis_scene* probe = alloc_scene(c, n_real + n_virtual, scene->dev.color_degree);
+    std::vector<double> unseen((size_t)std::max<int64_t>(1, n_virtual), 1.0);
+    try {
+      copy_particles(c, probe, 0, scene, n_real);
+      upload_probes(c, probe, n_real, p, all);
+      if (n_virtual > 0 && n_views > 0) {
+        double* du = (double*)c->buf("unseen", sizeof(double) * n_virtual);
+        CK(cudaMemcpyAsync(du, unseen.data(), sizeof(double) * n_virtual, cudaMemcpyHostToDevice,
+                           c->stream));
+        DensityHook dh;
+        dh.unseen = du;
+        dh.n_real = n_real;
+        dh.n_virtual = n_virtual;
+        vf_views(c, probe, nullptr, views, n_views, rc, nullptr, nullptr, nullptr, &dh);
+        CK(cudaMemcpyAsync(unseen.data(), du, sizeof(double) * n_virtual, cudaMemcpyDeviceToHost,
+                           c->stream));
+        c->sync();
+      }
+    } catch (...) {
+      gavis_scene_destroy(probe);
+      throw;
+    }
+    gavis_scene_destroy(probe);
+    std::vector<int64_t> keep;
+    for (int64_t k = 0; k < n_virtual; ++k) {
+      const double vtilde = 1.0 - unseen[k];
+      if (vtilde > cfg->eps_v) continue;  // free space
+      keep.push_back(k);
+    }
+    gavis_scene* o = alloc_scene(c, n_real + (int64_t)keep.size(), scene->dev.color_degree);
+    try {
+      copy_particles(c, o, 0, scene, n_real);
+      upload_probes(c, o, n_real, p, keep);
+      c->sync();
+    } catch (...) {
+      gavis_scene_destroy(o);
+      throw;
+    }
+    if (n_kept) *n_kept = (int64_t)keep.size();
+    if (kept_ids)
+      for (int64_t i = 0; i < (int64_t)keep.size() && i < kept_capacity; ++i) kept_ids[i] = keep[i];
+    *out = o;
   });
 }
 

@@ -146,6 +146,9 @@ int ua_score_parts(int tile_size);
 void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,
                   cudaStream_t s);
 void launch_query(const QueryArgs& a, cudaStream_t s);
+// unseen[k] *= 1 - vis[v*N + n_real + k] for v = 0..V-1 in order.
+void launch_density_update(double* unseen, const double* vis, int V, int64_t N, int64_t n_real,
+                           int64_t n_virtual, cudaStream_t s);
 
 // CUB-backed device primitives (sort.cu)
 size_t scan_temp_bytes(int64_t n);

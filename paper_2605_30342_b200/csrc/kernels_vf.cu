@@ -200,7 +200,24 @@ __global__ void vf_finalize_kernel(VfFinalizeArgs a, int64_t N) {
   }
 }
 
+// density_control's probe product (vfield.hpp:186-190), views in order.
+__global__ void density_update_kernel(double* unseen, const double* vis, int V, int64_t N,
+                                      int64_t n_real, int64_t n_virtual) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_virtual) return;
+  double u = unseen[k];
+  for (int v = 0; v < V; ++v) u *= 1.0 - vis[(int64_t)v * N + n_real + k];
+  unseen[k] = u;
+}
+
 }  // namespace
+
+void launch_density_update(double* unseen, const double* vis, int V, int64_t N, int64_t n_real,
+                           int64_t n_virtual, cudaStream_t s) {
+  if (n_virtual == 0) return;
+  density_update_kernel<<<(unsigned)((n_virtual + 255) / 256), 256, 0, s>>>(unseen, vis, V, N, n_real,
+                                                                            n_virtual);
+}
 
 void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s) {
   if (a.total_tiles == 0) return;
