@@ -204,6 +204,18 @@ gavis_status gavis_select_nbv(gavis_ctx* ctx, const gavis_scene* scene,
                               const gavis_uncertainty_config* uc, int32_t with_rgb,
                               double* scores, int32_t* best_index);
 
+/* Greedy NBV loop with incremental field updates (run_active_mapping,
+ * planner.hpp:284-316, with density control off): for each of `steps` rounds,
+ * select_nbv over the candidate pool, append the chosen camera to the field by
+ * accumulating its view (gamma is linear in the views, vfield.hpp:53-60), and
+ * record chosen index and score. chosen[steps], scores[steps] (nullable),
+ * all_scores[steps * n_cams] (nullable). */
+gavis_status gavis_nbv_loop(gavis_ctx* ctx, const gavis_scene* scene, gavis_field* field,
+                            const gavis_camera* cams, int32_t n_cams, int32_t steps,
+                            const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
+                            int32_t with_rgb, int32_t* chosen, double* scores,
+                            double* all_scores);
+
 /* ---- density control (vfield.hpp:136-199) ------------------------------ */
 /* DensityControlConfig (vfield.hpp:136-147). Defaults rho 100, eta 0.5,
  * eps_v 0.95, seed 0. */

@@ -390,6 +390,24 @@ def select_nbv(ctx: Context, scene, field: DeviceField, candidates: Sequence[Cam
     return NbvResult(best.value, scores)
 
 
+def nbv_loop(ctx: Context, scene, field: DeviceField, candidates: Sequence[CameraView], steps: int,
+             rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(),
+             with_rgb: bool = False):
+    """run_active_mapping (planner.hpp:284-316) over a fixed candidate pool with the
+    field updated incrementally (density control off): returns (chosen, scores,
+    all_scores[steps, n])."""
+    ds = _as_dev(ctx, scene)
+    n = len(candidates)
+    chosen = np.zeros(max(1, steps), np.int32)
+    best = np.zeros(max(1, steps))
+    allsc = np.zeros((max(1, steps), n))
+    arr = cameras_c(candidates)
+    N.check(ctx.lib.gavis_nbv_loop(ctx.h, ds.h, field.h, arr, C.c_int32(n), C.c_int32(steps),
+                                   C.byref(raster_c(rc)), C.byref(unc_c(uc)), C.c_int32(1 if with_rgb else 0),
+                                   _ptr(chosen), _ptr(best), _ptr(allsc)))
+    return chosen[:steps], best[:steps], allsc[:steps]
+
+
 # ------------------------------------------------------------------ debug
 def debug_project(ctx: Context, scene, cam: CameraView, dilation: float = 0.3, tile_size: int = 16):
     ds = _as_dev(ctx, scene)

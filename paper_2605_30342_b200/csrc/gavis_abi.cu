@@ -775,6 +775,35 @@ gavis_status gavis_ctx_launch_count(gavis_ctx* c, int64_t* launches) {
   });
 }
 
+gavis_status gavis_nbv_loop(gavis_ctx* c, const gavis_scene* s, gavis_field* f,
+                            const gavis_camera* cams, int32_t n_cams, int32_t steps,
+                            const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
+                            int32_t with_rgb, int32_t* chosen, double* scores,
+                            double* all_scores) {
+  return guard([&] {
+    require(c && s && f, "null argument");
+    require(n_cams > 0 && cams != nullptr, "select_nbv: candidate list must be nonempty");
+    require(steps >= 0, "steps must be non-negative");
+    invariant(f->n == s->dev.n, "accumulate_view: field/scene particle count mismatch");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    std::vector<double> sc((size_t)n_cams);
+    for (int step = 0; step < steps; ++step) {
+      gavis_render_outputs o = {};
+      o.scores = sc.data();
+      o.with_rgb = with_rgb;
+      ua_render(c, s, f, nullptr, cams, n_cams, rc, uc, &o);
+      int b = 0;
+      for (int i = 1; i < n_cams; ++i)
+        if (sc[i] > sc[b]) b = i;  // planner.hpp:132-136
+      vf_views(c, s, f, cams + b, 1, rc, nullptr, nullptr, nullptr);
+      if (chosen) chosen[step] = b;
+      if (scores) scores[step] = sc[b];
+      if (all_scores) std::memcpy(all_scores + (int64_t)step * n_cams, sc.data(), sizeof(double) * n_cams);
+    }
+  });
+}
+
 // Device scene with room for n particles (arrays uninitialised).
 static gavis_scene* alloc_scene(gavis_ctx* c, int64_t n, int color_degree) {
   auto* s = new gavis_scene();

@@ -342,6 +342,26 @@ def test_weight_conservation_on_device(ctx, seed):
     assert np.max(np.abs(r.color[0::3] + r.transmittance - 1.0)) < 1e-5
 
 
+def test_nbv_loop_incremental_matches_oracle(ctx):
+    """planner.hpp:284-316 with density control off: greedy rounds, field updated by
+    appending the chosen view; the oracle rebuilds the field from scratch each round."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    init = c["train"][:4]
+    pool = c["candidates"][:12]
+    f = api.construct_field(ctx, scene, init, VmfParams(1.0), 2, RC)
+    chosen, best, allsc = api.nbv_loop(ctx, scene, f, pool, 3, RC, UC)
+    traj = list(init)
+    for step in range(3):
+        og = O.construct_field(osc, traj, 1.0, 2, RC, threads=8)
+        ob, osc_scores = O.select_nbv(osc, og, 2, len(traj), pool, RC, UC, threads=8)
+        assert chosen[step] == ob
+        assert np.max(np.abs(allsc[step] - osc_scores) / np.maximum(1.0, np.abs(osc_scores))) <= 1e-9
+        traj.append(pool[ob])
+    assert f.num_views == 4 + 3
+
+
 # ------------------------------------------------------------------ edges / errors
 def test_edge_cases(ctx):
     # 1x1 camera, camera inside the cloud, all particles culled
