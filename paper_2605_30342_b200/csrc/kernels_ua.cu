@@ -374,117 +374,6 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   if (ENT && a.tile_score && tid == 0) a.tile_score[gt] = tile_h;
 }
 
-// ---------------------------------------------------------------------------
-// 16x16 tiles, 256 threads, one pixel each, software-pipelined over chunks of M
-// list entries: phase A computes alpha (exp) and the compensated alpha* of all
-// M entries -- independent of the transmittances, so the M fp64 exp chains
-// overlap; phase B runs the serial T / T* updates, colour and log in list order.
-// Alphas computed past a pixel's termination point are simply never used.
-template <int LC, bool RGB, bool ENT, bool EXTRA, int M>
-__global__ void __launch_bounds__(256, 2) ua_blend_pipe_kernel(UaBlendArgs a) {
-  constexpr int CS = Col<LC>::STRIDE;
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
-  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
-  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
-  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
-                                                            (ENT ? sizeof(UaRec) : 0)));
-  __shared__ double s_red[8];
-  load_math_tables();
-
-  const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
-  const int64_t gt = blockIdx.x;
-  const int v = find_view(a.cams, a.V, gt);
-  const DevCam& c = a.cams[v];
-  const int64_t t = gt - c.tile_base;
-  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
-  const uint2 rg = a.ranges[gt];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t N = a.scene.n;
-  const GeoRec* geo = a.geo + (int64_t)v * N;
-  const UaRec* uar = a.ua + (int64_t)v * N;
-
-  const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
-  const int py = ty * 16 + (warp >> 1) * 4 + (lane >> 3);
-  const bool inside = px < c.width && py < c.height;
-  const double cxp = px + 0.5, cyp = py + 0.5;
-  Pixel<LC> P;
-  pixel_init<LC, RGB, ENT>(P, c, px, py, inside);
-
-  for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-    const bool live = !(P.rgb_done && P.ent_done);
-    if (__syncthreads_count(live) == 0) break;
-    const int n = min((uint32_t)kBatch, rg.y - base);
-    stage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
-    __syncthreads();
-    if (!live) continue;
-    for (int j0 = 0; j0 < n; j0 += M) {
-      double al[M], as[M];
-      unsigned cov = 0u;
-#pragma unroll
-      for (int k = 0; k < M; ++k) {  // phase A
-        const int j = j0 + k;
-        al[k] = 0.0;
-        as[k] = 0.0;
-        if (j < n && in_rect4(s_rect[j], px, py)) {
-          cov |= 1u << k;
-          al[k] = splat_alpha(s_geo[j], cxp, cyp, amax);
-          if (ENT) {
-            const UaRec& u = s_ua[j];
-            const double x = u.A * al[k] + u.B;
-            as[k] = x < 0.0 ? 0.0 : (amax < x ? amax : x);
-          }
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < M; ++k) {  // phase B
-        if (!((cov >> k) & 1u)) continue;
-        const int j = j0 + k;
-        if (RGB && !P.rgb_done) {
-          if (EXTRA) ++P.n_rgb;
-          const double w = al[k] * P.T;
-          if (w > 0.0) {
-            float c0, c1, c2;
-            sh_color<LC>(reinterpret_cast<const float2*>(s_col + j * CS), P.bp, c0, c1, c2);
-            P.rgb0 += w * (double)c0;
-            P.rgb1 += w * (double)c1;
-            P.rgb2 += w * (double)c2;
-            if (EXTRA) P.dep += w * s_geo[j].depth;
-          }
-          P.T *= 1.0 - al[k];
-          if (P.T < cutoff) P.rgb_done = true;
-        }
-        if (ENT && !P.ent_done) {
-          if (EXTRA) ++P.n_ent;
-          const UaRec& u = s_ua[j];
-          const double w = as[k] * P.Te;
-          const double s = w * u.v;
-          if (s > 0.0) P.H += s * (-log_pos(s) + hl_qc + kGaussEntropy);
-          P.w0 += w * u.omv;
-          if (EXTRA) P.edep += w * s_geo[j].depth;
-          P.Te *= 1.0 - as[k];
-          if (P.Te < cutoff) P.ent_done = true;
-        }
-      }
-      if (P.rgb_done && P.ent_done) break;
-    }
-  }
-  pixel_finish<LC, RGB, ENT, EXTRA>(P, a, c, px, py, inside);
-  if (ENT && a.tile_score) {
-    double h = inside ? P.H : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
-    if (lane == 0) s_red[warp] = h;
-    __syncthreads();
-    if (tid == 0) {
-      double sum = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) sum += s_red[w];
-      a.tile_score[gt] = sum;
-    }
-  }
-}
-
 // K8: image score per view = fold of its per-tile partials in tile order, one warp
 // per view (lane-contiguous chunks, then a fixed shuffle tree).
 __global__ void score_kernel(const DevCam* cams, int V, const double* tile_score, double* scores) {
@@ -512,19 +401,6 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
     const char* e = getenv("GAVIS_UA_KERNEL");
     return e ? atoi(e) : 0;
   }();
-  if (a.tile_size == 16 && (choice == 3 || choice == 4)) {
-    static bool configured = false;
-    if (choice == 3) {
-      if (!configured) set_smem(ua_blend_pipe_kernel<LC, RGB, ENT, EXTRA, 4>, smem);
-      configured = true;
-      ua_blend_pipe_kernel<LC, RGB, ENT, EXTRA, 4><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
-    } else {
-      if (!configured) set_smem(ua_blend_pipe_kernel<LC, RGB, ENT, EXTRA, 8>, smem);
-      configured = true;
-      ua_blend_pipe_kernel<LC, RGB, ENT, EXTRA, 8><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
-    }
-    return;
-  }
   if (a.tile_size == 16 && choice != 1) {
     static bool configured = false;
     if (!configured) {
