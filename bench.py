@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="candidates in the CPU sample")
+    p.add_argument("--no-extra-vf", action="store_true", help="skip the config-2/4 VF-build timings")
     return p.parse_args()
 
 
@@ -232,11 +233,14 @@ def run_ours(args):
     train = c["train"]
 
     # ---------------- VF CONST: sharded views + NCCL all-reduce --------------
-    def build_field(views):
+    def build_field(views, dscene=None, deg=None):
+        dscene = dscene or ds
+        deg = degree if deg is None else deg
+
         def partial(lo, hi):
-            f = api.empty_field(ctx, ds, vmf, degree)
+            f = api.empty_field(ctx, dscene, vmf, deg)
             if hi > lo:
-                api.accumulate_views(ctx, f, ds, views[lo:hi], rc)
+                api.accumulate_views(ctx, f, dscene, views[lo:hi], rc)
             return f
         f = parallel.construct_field_sharded(partial, len(views), rank, world,
                                              lambda fld: parallel.allreduce_device_field(fld, dist))
@@ -364,6 +368,31 @@ def run_ours(args):
                "d2h_bytes_per_step": int(d2h),
                "timing": "host wall clock around upload(scene)+upload(field)+select_nbv, synchronised"}
 
+    # ---------------- VF-build ms on configs 2 and 4 (BASELINE metric) ------
+    vf_other = {}
+    if not args.no_extra_vf:
+        from paper_2605_30342_b200 import synth
+        for cid, gen in ((2, lambda: synth.config2(0, n_candidates=0)),
+                         (4, lambda: synth.config4(0, n_candidates=0))):
+            cc = gen()
+            dsc = ctx.upload(cc["scene"])
+            fld = build_field(cc["train"], dsc, cc["degree"])  # warm-up
+            fld.close()
+            times = []
+            for _ in range(2):
+                barrier(ctx, dist)
+                t0 = time.perf_counter()
+                fld = build_field(cc["train"], dsc, cc["degree"])
+                barrier(ctx, dist)
+                times.append((time.perf_counter() - t0) * 1000.0)
+                fld.close()
+            cam = cc["train"][0]
+            vf_other[f"config{cid}"] = {"vf_build_ms": max_over_ranks(min(times), dist),
+                                        "views": len(cc["train"]), "particles": cc["scene"].num_particles,
+                                        "resolution": [cam.width, cam.height], "field_degree": cc["degree"]}
+            dsc.close()
+            del cc
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         model, cores = cpu_info()
@@ -394,6 +423,7 @@ def run_ours(args):
                          "pairs_per_view": K_avg, "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()}},
             "select_nbv_entropy_only_views_per_s": select_only,
             "vf_build_ms": vf_ms, "vf_build_views": len(train), "vf_build_200_views_ms": vf200_ms,
+            "vf_build_other_configs": vf_other,
             "best_index_last_step": int(res.best_index) + lo,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
         }

@@ -18,6 +18,8 @@
 #include "fast_math.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace gavis {
 
 namespace {
@@ -139,6 +141,123 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
   }
 }
 
+// 16x16 tiles: 128 threads, two pixels per thread (rows y and y+4 of the warp's
+// 8x8 block). A warp pre-filter (one lane per entry, ballot) skips entries that
+// miss the block; per hit the thread folds its two pixels' T before the
+// fixed-order shuffle tree, so the per-(tile, entry) partial stays deterministic.
+__global__ void __launch_bounds__(128) vf_blend_tile2_kernel(VfBlendArgs a) {
+  constexpr int W = 4;
+  __shared__ GeoRec s_geo[kBatch];
+  __shared__ int4 s_rect[kBatch];
+  __shared__ uint32_t s_pair[kBatch];
+  __shared__ double s_sum[W][kBatch];
+  __shared__ int32_t s_cnt[W][kBatch];
+  load_math_tables();
+
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const GeoRec* geo = a.geo + (int64_t)v * a.N;
+  const double amax = a.amax, cutoff = a.cutoff;
+
+  const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
+  const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3), py1 = py0 + 4;
+  const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 8;
+  const bool in0 = px < c.width && py0 < c.height, in1 = px < c.width && py1 < c.height;
+  const double cxp = px + 0.5, cy0 = py0 + 0.5, cy1 = py1 + 0.5;
+  double T0 = 1.0, T1 = 1.0;
+  bool d0 = !in0, d1 = !in1;
+  int32_t n0 = 0, n1 = 0;
+
+  for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
+    if (__syncthreads_count(!(d0 && d1)) == 0) break;
+    const int n = min((uint32_t)kBatch, rg.y - base);
+    for (int j = tid; j < n; j += 128) {
+      const uint32_t p = a.vals[base + j];
+      s_pair[j] = p;
+      const GeoRec r = geo[a.pair_gid[p]];
+      s_geo[j] = r;
+      s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
+    }
+    for (int k = tid; k < W * kBatch; k += 128) {
+      (&s_sum[0][0])[k] = 0.0;
+      (&s_cnt[0][0])[k] = 0;
+    }
+    __syncthreads();
+    if (!__all_sync(0xffffffffu, d0 && d1)) {
+      for (int j0 = 0; j0 < n; j0 += 32) {
+        bool hit = false;
+        if (j0 + lane < n) {
+          const int4 r = s_rect[j0 + lane];
+          hit = r.x <= bx0 + 7 && r.x + r.y >= bx0 && r.z <= by0 + 7 && r.z + r.w >= by0;
+        }
+        unsigned hits = __ballot_sync(0xffffffffu, hit);
+        while (hits != 0u) {
+          const int j = j0 + __ffs(hits) - 1;
+          hits &= hits - 1u;
+          const int4 rr = s_rect[j];
+          const bool c0 = !d0 && in_rect4(rr, px, py0);
+          const bool c1 = !d1 && in_rect4(rr, px, py1);
+          const unsigned m0 = __ballot_sync(0xffffffffu, c0), m1 = __ballot_sync(0xffffffffu, c1);
+          if ((m0 | m1) == 0u) continue;
+          const GeoRec& e = s_geo[j];
+          double contrib = 0.0;
+          if (c0) {
+            contrib = T0;  // v_k += T before the splat (raster.hpp:266)
+            ++n0;
+            const double dx = cxp - e.mx, dy = cy0 - e.my;
+            const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
+            double al = 0.0;
+            if (q <= kQSkip) {
+              al = (double)e.opacity * exp_neg(-0.5 * q);
+              al = al > amax ? amax : al;
+            }
+            T0 *= 1.0 - al;
+            d0 = T0 < cutoff;
+          }
+          if (c1) {
+            contrib += T1;
+            ++n1;
+            const double dx = cxp - e.mx, dy = cy1 - e.my;
+            const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
+            double al = 0.0;
+            if (q <= kQSkip) {
+              al = (double)e.opacity * exp_neg(-0.5 * q);
+              al = al > amax ? amax : al;
+            }
+            T1 *= 1.0 - al;
+            d1 = T1 < cutoff;
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
+          if (lane == 0) {
+            s_sum[warp][j] = contrib;
+            s_cnt[warp][j] = __popc(m0) + __popc(m1);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < n; j += 128) {
+      const double sum = ((s_sum[0][j] + s_sum[1][j]) + s_sum[2][j]) + s_sum[3][j];
+      const int32_t cnt = s_cnt[0][j] + s_cnt[1][j] + s_cnt[2][j] + s_cnt[3][j];
+      if (cnt > 0) {
+        const uint32_t p = s_pair[j];
+        a.pair_sum[p] += sum;
+        a.pair_cnt[p] += cnt;
+      }
+    }
+  }
+  if (a.contrib) {
+    if (in0) a.contrib[c.pix_base + (int64_t)py0 * c.width + px] = n0;
+    if (in1) a.contrib[c.pix_base + (int64_t)py1 * c.width + px] = n1;
+  }
+}
+
 template <int DEG>
 __global__ void vf_finalize_kernel(VfFinalizeArgs a, int64_t N) {
   constexpr int NB = (DEG + 1) * (DEG + 1);
@@ -221,7 +340,11 @@ void launch_density_update(double* unseen, const double* vis, int V, int64_t N, 
 
 void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s) {
   if (a.total_tiles == 0) return;
-  vf_blend_kernel<<<(unsigned)a.total_tiles, kThreads, 0, s>>>(a);
+  static const bool generic = getenv("GAVIS_VF_GENERIC") != nullptr;
+  if (a.tile_size == 16 && !generic)
+    vf_blend_tile2_kernel<<<(unsigned)a.total_tiles, 128, 0, s>>>(a);
+  else
+    vf_blend_kernel<<<(unsigned)a.total_tiles, kThreads, 0, s>>>(a);
 }
 
 void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s) {
