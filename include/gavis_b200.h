@@ -65,8 +65,10 @@ typedef struct {
   double transmittance_cutoff, dilation, alpha_clamp_max;
 } gavis_raster_config;
 
-/* UncertaintyConfig (uncertainty.hpp:24-52), constant variance provider.
- * variance_provider and correlation must be 0 (kConstant, kNone). */
+/* UncertaintyConfig (uncertainty.hpp:24-52). variance_provider: 0 kConstant,
+ * 1 kShPropagation (needs gavis_scene_set_coeff_variances); correlation: 0 kNone,
+ * 1 kHook (image score sum of H - H exp(-d / correlation_lambda), d the entropy
+ * depth; lambda must be positive). */
 typedef struct {
   double beta, prior_opacity, color_sigma;
   double prior_cov[9];
@@ -117,6 +119,11 @@ gavis_status gavis_ctx_launch_count(gavis_ctx* ctx, int64_t* launches);
 gavis_status gavis_scene_upload(gavis_ctx* ctx, const gavis_scene_desc* desc,
                                 gavis_scene** out);
 gavis_status gavis_scene_destroy(gavis_scene* scene);
+/* Per-particle per-channel SH coefficient variances [N][3][(Lv+1)^2] for the
+ * sh_propagation variance provider (UncertaintyConfig::coeff_variances,
+ * uncertainty.hpp:38, :63-83). Lv <= 4; negative entries -> PARAMETER. */
+gavis_status gavis_scene_set_coeff_variances(gavis_ctx* ctx, gavis_scene* scene,
+                                             const float* variances, int32_t degree);
 gavis_status gavis_scene_num_particles(const gavis_scene* scene, int64_t* n);
 
 /* ---- visibility field (vfield.hpp) ------------------------------------ */

@@ -651,13 +651,57 @@ static double logdet_spd3(const double* m) {
   return 2.0 * (log(L[0]) + log(L[4]) + log(L[8]));
 }
 
-/* render_entropy_core uncertainty.hpp:124-238 (kConstant provider) */
+/* UncertaintyConfig::coeff_variances (uncertainty.hpp:38): [N][3][(Lv+1)^2] */
+static const double* g_coeff_var = NULL;
+static int g_coeff_var_degree = -1;
+
+void gor_set_coeff_variances(const double* var, int degree) {
+  g_coeff_var = var;
+  g_coeff_var_degree = degree;
+}
+
+/* sh_variance_propagation uncertainty.hpp:63-83; returns 0 if a q <= 0 */
+static int propagated_half_logdet(const double* var, int degree, const double* d, double* hl) {
+  double basis[MAX_SH];
+  gor_eval_sh(degree, d, basis);
+  const int n = (degree + 1) * (degree + 1);
+  double q[3] = {0.0, 0.0, 0.0};
+  for (int i = 0; i < n; ++i) {
+    double y2 = basis[i] * basis[i];
+    for (int k = 0; k < 3; ++k) q[k] += y2 * var[k * n + i];
+  }
+  if (!(q[0] > 0.0 && q[1] > 0.0 && q[2] > 0.0)) return 0;
+  *hl = 0.5 * (log(q[0]) + log(q[1]) + log(q[2]));
+  return 1;
+}
+
+/* render_entropy_core uncertainty.hpp:124-238; variance_provider 1 uses the
+ * coefficient variances set by gor_set_coeff_variances (:149-163). */
 void gor_render_entropy_core(const gor_scene* s, const gor_camera* cam, const gor_raster* rc,
                              const gor_unc* uc, const double* vis_by_particle, double* entropy,
                              double* w0_out, double* depth_out, int32_t* contrib) {
   binned_view b = bin_view(s, cam, rc);
-  const double hl_qc = 3.0 * log(uc->color_sigma);
+  const double hl_const = 3.0 * log(uc->color_sigma);
   const double hl_q0 = 0.5 * logdet_spd3(uc->prior_cov);
+  double* hl_of = NULL; /* per sorted splat */
+  if (uc->variance_provider == 1) {
+    hl_of = (double*)malloc(sizeof(double) * (size_t)(b.n + 1));
+    const int nbv = (g_coeff_var_degree + 1) * (g_coeff_var_degree + 1);
+    for (int64_t k = 0; k < b.n; ++k) {
+      const int64_t i = b.splats[k].particle_index;
+      double d[3] = {s->positions[3 * i] - cam->position[0], s->positions[3 * i + 1] - cam->position[1],
+                     s->positions[3 * i + 2] - cam->position[2]};
+      double n2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+      if (n2 > 0.0) {
+        double nn = sqrt(n2);
+        d[0] /= nn;
+        d[1] /= nn;
+        d[2] /= nn;
+      }
+      if (!propagated_half_logdet(g_coeff_var + i * 3 * nbv, g_coeff_var_degree, d, &hl_of[k]))
+        hl_of[k] = NAN;
+    }
+  }
   const int W = cam->width, H = cam->height, ts = rc->tile_size;
   for (int tile = 0; tile < b.tx_n * b.ty_n; ++tile) {
     int tx = tile % b.tx_n, ty = tile / b.tx_n;
@@ -678,6 +722,7 @@ void gor_render_entropy_core(const gor_scene* s, const gor_camera* cam, const go
           double astar = compensated_alpha(a, v, uc, rc->alpha_clamp_max);
           double w = astar * t_cur;
           double seen = w * v;
+          const double hl_qc = hl_of ? hl_of[b.ent[e]] : hl_const;
           if (seen > 0.0) h += seen * (-log(seen) + hl_qc + K_GAUSS_ENTROPY);
           w0 += w * (1.0 - v);
           depth_acc += w * sp->depth;
@@ -692,6 +737,7 @@ void gor_render_entropy_core(const gor_scene* s, const gor_camera* cam, const go
       }
     }
   }
+  free(hl_of);
   free_view(&b);
 }
 
@@ -731,6 +777,16 @@ double gor_image_entropy(const double* entropy, int64_t n) {
   return sum;
 }
 
+/* image_entropy with the correlation hook uncertainty.hpp:273-277 */
+double gor_image_entropy_hook(const double* entropy, const double* depth, int64_t n, double lambda) {
+  double sum = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double h = entropy[i];
+    sum += h - h * exp(-depth[i] / lambda);
+  }
+  return sum;
+}
+
 /* ------------------------------------------------------------ planner.hpp */
 
 typedef struct {
@@ -753,9 +809,17 @@ static void nbv_body(int c, void* p) {
     gor_rasterize(x->s, &x->cams[c], x->rc, rgb, NULL, NULL, NULL);
     free(rgb);
   }
-  gor_render_entropy(x->s, x->gamma, x->degree, x->num_views, &x->cams[c], x->rc, x->uc, ent,
-                     NULL, NULL, NULL);
-  x->scores[c] = gor_image_entropy(ent, P);
+  if (x->uc->correlation == 1) { /* planner.hpp:124-130: depth for the hook */
+    double* dep = (double*)malloc(sizeof(double) * (size_t)P);
+    gor_render_entropy(x->s, x->gamma, x->degree, x->num_views, &x->cams[c], x->rc, x->uc, ent,
+                       NULL, dep, NULL);
+    x->scores[c] = gor_image_entropy_hook(ent, dep, P, x->uc->correlation_lambda);
+    free(dep);
+  } else {
+    gor_render_entropy(x->s, x->gamma, x->degree, x->num_views, &x->cams[c], x->rc, x->uc, ent,
+                       NULL, NULL, NULL);
+    x->scores[c] = gor_image_entropy(ent, P);
+  }
   free(ent);
 }
 

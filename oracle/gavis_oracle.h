@@ -103,6 +103,9 @@ void gor_render_entropy(const gor_scene* s, const double* gamma, int degree, int
                         const gor_camera* cam, const gor_raster* rc, const gor_unc* uc,
                         double* entropy, double* w0, double* depth, int32_t* contrib);
 double gor_image_entropy(const double* entropy, int64_t n);
+double gor_image_entropy_hook(const double* entropy, const double* depth, int64_t n, double lambda);
+/* coefficient variances [N][3][(Lv+1)^2] for variance_provider 1 (NULL to clear) */
+void gor_set_coeff_variances(const double* var, int degree);
 
 /* planner.hpp: returns best index; with_rgb additionally runs rasterize per
  * candidate (the fused GPU render's RGB work) and discards it. */

@@ -111,8 +111,27 @@ def unc_struct(uc) -> Unc:
     q = np.asarray(uc.prior_cov, np.float64).reshape(9)
     for i in range(9):
         u.prior_cov[i] = float(q[i])
-    u.correlation_lambda = 1.0
+    u.variance_provider = int(getattr(uc, "variance_provider", 0))
+    u.correlation = int(getattr(uc, "correlation", 0))
+    u.correlation_lambda = float(getattr(uc, "correlation_lambda", 1.0))
     return u
+
+
+_var_keepalive = None
+
+
+def set_coeff_variances(variances, degree: int) -> None:
+    """Coefficient variances [N][3][(degree+1)^2] used when variance_provider == 1."""
+    global _var_keepalive
+    _var_keepalive = None if variances is None else np.ascontiguousarray(variances, np.float64).reshape(-1)
+    lib().gor_set_coeff_variances(_p(_var_keepalive), degree)
+
+
+def image_entropy_hook(H, depth, lam: float) -> float:
+    lib().gor_image_entropy_hook.restype = C.c_double
+    h = np.ascontiguousarray(H, np.float64)
+    d = np.ascontiguousarray(depth, np.float64)
+    return lib().gor_image_entropy_hook(_p(h), _p(d), h.size, C.c_double(lam))
 
 
 class OracleScene:

@@ -55,6 +55,7 @@ EXPORTS = [
     "gavis_ctx_synchronize", "gavis_ctx_set_batch", "gavis_ctx_set_profiling",
     "gavis_ctx_kernel_time", "gavis_ctx_timer_start", "gavis_ctx_timer_stop",
     "gavis_ctx_launch_count", "gavis_scene_upload", "gavis_scene_destroy",
+    "gavis_scene_set_coeff_variances",
     "gavis_scene_num_particles", "gavis_vf_construct", "gavis_vf_create",
     "gavis_vf_accumulate_views", "gavis_vf_accumulate_visibility", "gavis_vf_upload",
     "gavis_vf_download", "gavis_vf_set_num_views", "gavis_vf_device_gamma", "gavis_vf_destroy",

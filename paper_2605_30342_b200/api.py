@@ -59,7 +59,9 @@ def unc_c(uc: UncertaintyConfig) -> N.UncertaintyConfigC:
     q = np.asarray(uc.prior_cov, np.float64).reshape(9)
     for i in range(9):
         u.prior_cov[i] = float(q[i])
-    u.correlation_lambda = 1.0
+    u.variance_provider = int(uc.variance_provider)
+    u.correlation = int(uc.correlation)
+    u.correlation_lambda = float(uc.correlation_lambda)
     return u
 
 
@@ -136,6 +138,13 @@ class DeviceScene:
         h = C.c_void_p()
         N.check(ctx.lib.gavis_scene_upload(ctx.h, C.byref(d), C.byref(h)))
         self.h = h
+
+    def set_coeff_variances(self, variances, degree: int) -> None:
+        """UncertaintyConfig::coeff_variances for the sh_propagation provider:
+        [N][3][(degree+1)^2] per-particle per-channel SH coefficient variances."""
+        var = np.ascontiguousarray(variances, np.float32).reshape(-1)
+        N.check(self.ctx.lib.gavis_scene_set_coeff_variances(self.ctx.h, self.h, _ptr(var) if var.size else None,
+                                                             C.c_int32(degree)))
 
     @classmethod
     def _adopt(cls, ctx: Context, handle, n: int, color_degree: int, bounds) -> "DeviceScene":

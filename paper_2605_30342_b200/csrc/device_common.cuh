@@ -41,9 +41,11 @@ struct __align__(16) GeoRec {
 };
 
 // Entropy-track constants of one splat (compensated_alpha, uncertainty.hpp:55-59):
-// alpha* = A*alpha + B with A = v + beta(1-v), B = o0(1-beta)(1-v).
+// alpha* = A*alpha + B with A = v + beta(1-v), B = o0(1-beta)(1-v); hl is the
+// splat's 1/2 log|Q_c| (constant provider: 3 ln sigma_c; sh_propagation:
+// 1/2 sum_c ln q_c(d), uncertainty.hpp:143-163).
 struct __align__(16) UaRec {
-  double A, B, v, omv;  // omv = 1 - v
+  double A, B, v, hl;
 };
 
 __device__ __forceinline__ int cov_lo(int32_t packed) { return packed & 0xFFFF; }
@@ -86,6 +88,47 @@ __device__ __forceinline__ void eval_sh(double x, double y, double z, double* ou
     double plm = pmm, plm_prev = 0.0;
 #pragma unroll
     for (int l = m; l <= DEG; ++l) {
+      if (l > m) {
+        double next;
+        if (l == m + 1) {
+          next = z * sqrt(2.0 * m + 3.0) * pmm;
+        } else {
+          double a = sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m));
+          double b = sqrt(((double)(l - 1) * (l - 1) - (double)m * m) /
+                          (4.0 * (double)(l - 1) * (l - 1) - 1.0));
+          next = a * (z * plm - b * plm_prev);
+        }
+        plm_prev = plm;
+        plm = next;
+      }
+      if (m == 0) {
+        out[l * l + l] = plm;
+      } else {
+        out[l * l + l + m] = kSqrt2 * plm * cm;
+        out[l * l + l - m] = kSqrt2 * plm * sm;
+      }
+    }
+  }
+}
+
+// Runtime-degree variant (degree <= kMaxFieldDegree) for the non-default
+// variance-propagation provider.
+__device__ __forceinline__ void eval_sh_rt(int degree, double x, double y, double z, double* out) {
+  const double s = sqrt(x * x + y * y);
+  const double cphi = s > 1e-14 ? x / s : 1.0;
+  const double sphi = s > 1e-14 ? y / s : 0.0;
+  const double kSqrt2 = 1.4142135623730951;
+  double pmm = kY00;
+  double cm = 1.0, sm = 0.0;
+  for (int m = 0; m <= degree; ++m) {
+    if (m > 0) {
+      pmm *= s * sqrt((2.0 * m + 1.0) / (2.0 * m));
+      double cnext = cm * cphi - sm * sphi;
+      sm = sm * cphi + cm * sphi;
+      cm = cnext;
+    }
+    double plm = pmm, plm_prev = 0.0;
+    for (int l = m; l <= degree; ++l) {
       if (l > m) {
         double next;
         if (l == m + 1) {

@@ -163,12 +163,16 @@ void validate_unc(const gavis_uncertainty_config* uc, double* hl_q0) {
   require(uc->color_sigma > 0.0, "color_sigma must be positive");
   double logdet = 0.0;
   require(llt3(uc->prior_cov, &logdet), "prior_cov must be symmetric positive-definite");
-  require(uc->variance_provider == 0,
-          "variance_provider sh_propagation is not supported by the device path");
-  require(uc->correlation == 0, "correlation hook is not supported by the device path");
-  const double det_qc = std::pow(uc->color_sigma, 6.0);
-  require(det3(uc->prior_cov) >= det_qc,
-          "prior_cov determinant must dominate the color covariance");
+  require(uc->variance_provider == 0 || uc->variance_provider == 1,
+          "variance_provider must be constant (0) or sh_propagation (1)");
+  require(uc->correlation == 0 || uc->correlation == 1, "correlation must be none (0) or hook (1)");
+  if (uc->correlation == 1)
+    require(uc->correlation_lambda > 0.0, "correlation_lambda must be positive");
+  if (uc->variance_provider == 0) {
+    const double det_qc = std::pow(uc->color_sigma, 6.0);
+    require(det3(uc->prior_cov) >= det_qc,
+            "prior_cov determinant must dominate the color covariance");
+  }
   *hl_q0 = 0.5 * logdet;
 }
 
@@ -277,6 +281,8 @@ struct gavis_scene {
   float4* scale = nullptr;
   uint8_t* virt = nullptr;
   float* colors = nullptr;
+  float* var = nullptr;  // coefficient variances for the sh_propagation provider
+  int var_degree = -1;
 };
 
 struct gavis_field {
@@ -346,6 +352,10 @@ struct BinOpts {
   const gavis_field* field = nullptr;
   const double* vis_given_dev = nullptr;
   double beta = 0.5, o0b = 0.075;
+  double hl_const = 0.0;
+  const float* var = nullptr;
+  int var_degree = -1;
+  int* err_flag = nullptr;
 };
 
 // K1..K5 for one batch of cameras.
@@ -388,6 +398,10 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
   pa.write_culled = o.write_culled;
   pa.beta = o.beta;
   pa.o0b = o.o0b;
+  pa.hl_const = o.hl_const;
+  pa.var = o.var;
+  pa.var_degree = o.var_degree;
+  pa.err_flag = o.err_flag;
   if (o.ua) {
     if (o.vis_given_dev) {
       pa.query_mode = kQueryGiven;
@@ -586,7 +600,23 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     o.vis_given_dev = vis_dev;
     o.beta = uc->beta;
     o.o0b = uc->prior_opacity * (1.0 - uc->beta);
+    o.hl_const = 3.0 * std::log(uc->color_sigma);  // 0.5 log(sigma^6), uncertainty.hpp:145
+    int* err = nullptr;
+    if (do_ent && uc->variance_provider == 1) {
+      require(s->var != nullptr || s->dev.n == 0,
+              "variance_provider sh_propagation requires coeff_variances");
+      o.var = s->var;
+      o.var_degree = s->var_degree;
+      err = (int*)c->buf("err_flag", sizeof(int));
+      CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+      o.err_flag = err;
+    }
     Binned b = bin_batch(c, s, cams + v0, V, rc, o);
+    if (err) {
+      CK(cudaMemcpyAsync(c->pinned + 2, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      require(c->pinned[2] == 0, "propagated color variance must be positive");
+    }
     const int64_t P = b.total_pix;
     UaBlendArgs ua;
     ua.scene = s->dev;
@@ -598,6 +628,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     ua.amax = rc->alpha_clamp_max;
     ua.hl_qc = 3.0 * std::log(uc->color_sigma);
     ua.hl_q0 = hl_q0;
+    ua.corr_lambda = uc->correlation == 1 ? uc->correlation_lambda : 0.0;
     ua.geo = b.geo;
     ua.ua = b.ua;
     ua.ranges = b.ranges;
@@ -1062,7 +1093,30 @@ gavis_status gavis_scene_destroy(gavis_scene* s) {
     cudaFree(s->scale);
     cudaFree(s->virt);
     cudaFree(s->colors);
+    cudaFree(s->var);
     delete s;
+  });
+}
+
+gavis_status gavis_scene_set_coeff_variances(gavis_ctx* c, gavis_scene* s, const float* var,
+                                             int32_t degree) {
+  return guard([&] {
+    require(c && s, "null argument");
+    require(degree >= 0 && degree <= kMaxFieldDegree,
+            "sh_variance_propagation: variance degree must lie in [0, 4] on the device");
+    const int64_t N = s->dev.n;
+    const int nbv = (degree + 1) * (degree + 1);
+    require(var != nullptr || N == 0, "coeff_variances must not be null");
+    for (int64_t i = 0; i < N * 3 * nbv; ++i)
+      require(var[i] >= 0.0f, "sh_variance_propagation: negative variance entry");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    if (s->var) CK(cudaFree(s->var));
+    s->var = nullptr;
+    CK(cudaMalloc(&s->var, sizeof(float) * 3 * nbv * std::max<int64_t>(1, N)));
+    if (N > 0)
+      CK(cudaMemcpy(s->var, var, sizeof(float) * 3 * nbv * N, cudaMemcpyHostToDevice));
+    s->var_degree = degree;
   });
 }
 

@@ -39,6 +39,10 @@ struct PreprocessArgs {
   int num_views = 0;
   const double* vis_in = nullptr;  // [N] for kQueryGiven
   double beta = 0.5, o0b = 0.075;  // o0b = o0 * (1 - beta)
+  double hl_const = 0.0;           // 3 ln sigma_c (constant provider)
+  const float* var = nullptr;      // [N][3][(Lv+1)^2] coefficient variances (sh_propagation)
+  int var_degree = -1;
+  int* err_flag = nullptr;         // set to 1 when a propagated variance is not positive
   bool write_culled = false;
 };
 
@@ -121,6 +125,7 @@ struct UaBlendArgs {
   int32_t* rgb_contrib = nullptr;
   int32_t* ent_contrib = nullptr;
   double* tile_score = nullptr;  // [total_tiles] per-tile entropy sum
+  double corr_lambda = 0.0;      // > 0: correlation hook in the image score
   bool do_rgb = true, do_ent = true;
 };
 

@@ -200,9 +200,34 @@ __global__ void __launch_bounds__(128) preprocess_kernel(PreprocessArgs a) {
         }
         UaRec u;
         u.v = vis;
-        u.omv = 1.0 - vis;
         u.A = vis + a.beta * (1.0 - vis);
         u.B = a.o0b * (1.0 - vis);
+        u.hl = a.hl_const;
+        if (a.var) {
+          // sh_variance_propagation (uncertainty.hpp:63-83) at the camera-to-centre
+          // direction, half log-determinant of the diagonal Q_c (:149-163).
+          double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
+          const double n2 = d0 * d0 + d1 * d1 + d2 * d2;
+          if (n2 > 0.0) {
+            const double nn = sqrt(n2);
+            d0 /= nn;
+            d1 /= nn;
+            d2 /= nn;
+          }
+          double basis[(kMaxFieldDegree + 1) * (kMaxFieldDegree + 1)];
+          eval_sh_rt(a.var_degree, d0, d1, d2, basis);
+          const int nbv = (a.var_degree + 1) * (a.var_degree + 1);
+          const float* vr = a.var + g * 3 * nbv;
+          double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+          for (int i = 0; i < nbv; ++i) {
+            const double y2 = basis[i] * basis[i];
+            q0 += y2 * (double)vr[i];
+            q1 += y2 * (double)vr[nbv + i];
+            q2 += y2 * (double)vr[2 * nbv + i];
+          }
+          if (!(q0 > 0.0 && q1 > 0.0 && q2 > 0.0)) atomicOr(a.err_flag, 1);
+          u.hl = 0.5 * (log(q0) + log(q1) + log(q2));
+        }
         a.ua[slot] = u;
       }
     } else if (a.write_culled) {

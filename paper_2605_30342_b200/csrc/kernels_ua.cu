@@ -151,8 +151,8 @@ __device__ __forceinline__ void ent_step(Pixel<LC>& P, double al, double depth, 
   as = as < 0.0 ? 0.0 : (amax < as ? amax : as);
   const double w = as * P.Te;
   const double s = w * u.v;
-  if (s > 0.0) P.H += s * (-log_pos(s) + hl_qc + kGaussEntropy);
-  P.w0 += w * u.omv;
+  if (s > 0.0) P.H += s * (-log_pos(s) + u.hl + kGaussEntropy);
+  P.w0 += w * (1.0 - u.v);
   if (EXTRA) P.edep += w * depth;
   P.Te *= 1.0 - as;
   if (P.Te < cutoff) P.ent_done = true;
@@ -180,6 +180,14 @@ __device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a,
     if (EXTRA && a.edepth) a.edepth[pix] = P.edep;
     if (EXTRA && a.ent_contrib) a.ent_contrib[pix] = P.n_ent;
   }
+}
+
+// Per-pixel contribution to image_entropy (uncertainty.hpp:264-278): H, or with
+// the correlation hook H - H exp(-d / lambda), d the entropy-track depth.
+template <int LC>
+__device__ __forceinline__ double score_term(const Pixel<LC>& P, const UaBlendArgs& a) {
+  if (a.corr_lambda > 0.0) return P.H - P.H * exp(-P.edep / a.corr_lambda);
+  return P.H;
 }
 
 template <int LC, bool RGB, bool ENT>
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(128, 5) ua_blend_tile2_kernel(UaBlendArgs a) {
   pixel_finish<LC, RGB, ENT, EXTRA>(P0, a, c, px, py0, in0);
   pixel_finish<LC, RGB, ENT, EXTRA>(P1, a, c, px, py1, in1);
   if (ENT && a.tile_score) {
-    double h = (in0 ? P0.H : 0.0) + (in1 ? P1.H : 0.0);
+    double h = (in0 ? score_term(P0, a) : 0.0) + (in1 ? score_term(P1, a) : 0.0);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
     if (lane == 0) s_red[warp] = h;
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
     }
     pixel_finish<LC, RGB, ENT, EXTRA>(P, a, c, px, py, inside);
     if (ENT && a.tile_score) {
-      double h = inside ? P.H : 0.0;
+      double h = inside ? score_term(P, a) : 0.0;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
       if (lane == 0) s_red[warp] = h;
@@ -430,7 +438,7 @@ void launch_lc_x(const UaBlendArgs& a, cudaStream_t s) {
 
 template <int LC>
 void launch_lc(const UaBlendArgs& a, cudaStream_t s) {
-  const bool extra = a.depth || a.edepth || a.rgb_contrib || a.ent_contrib;
+  const bool extra = a.depth || a.edepth || a.rgb_contrib || a.ent_contrib || a.corr_lambda > 0.0;
   if (extra)
     launch_lc_x<LC, true>(a, s);
   else

@@ -74,11 +74,15 @@ class VmfParams:
 
 @dataclass
 class UncertaintyConfig:
-    """uncertainty.hpp:24-52 (constant variance provider, no correlation hook)."""
+    """uncertainty.hpp:24-52. variance_provider 0 = kConstant, 1 = kShPropagation
+    (coefficient variances attached to the scene); correlation 0 = kNone, 1 = kHook."""
     beta: float = 0.5
     prior_opacity: float = 0.15
     color_sigma: float = 0.1
     prior_cov: np.ndarray = field(default_factory=lambda: np.eye(3))
+    variance_provider: int = 0
+    correlation: int = 0
+    correlation_lambda: float = 1.0
 
 
 @dataclass
