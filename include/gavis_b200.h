@@ -245,6 +245,26 @@ gavis_status gavis_density_control(gavis_ctx* ctx, const gavis_scene* scene,
                                    const gavis_raster_config* rc, gavis_scene** out,
                                    int64_t* n_kept, int64_t* kept_ids, int64_t kept_capacity);
 
+/* ---- on-disk formats (host only; io.hpp) -------------------------------- */
+/* load_splat_ply (io.hpp:493-637), two-phase: gavis_ply_info gives the vertex
+ * count and the colour degree implied by f_rest_*; gavis_read_splat_ply fills
+ * caller arrays laid out like gavis_scene_desc (activations applied: sigmoid
+ * opacity, exp scale, normalised quaternion, DC + 0.5/Y00) and the particle
+ * AABB as bounds. Malformed files -> PARAMETER. */
+gavis_status gavis_ply_info(const char* path, int64_t* n, int32_t* color_degree);
+gavis_status gavis_read_splat_ply(const char* path, int64_t capacity, float* positions,
+                                  float* rotations, float* scales, float* opacities,
+                                  float* colors, double* bounds_min, double* bounds_max);
+/* save_field / load_field (io.hpp:255-295): {"L", "kappa", "num_views",
+ * "gamma" (one row of (L+1)^2 per particle), "virtual"}. Read is two-phase
+ * (gamma == NULL first to get the row count). */
+gavis_status gavis_field_json_write(const char* path, int32_t degree, double kappa,
+                                    int32_t num_views, int64_t n, const double* gamma,
+                                    const uint8_t* is_virtual);
+gavis_status gavis_field_json_read(const char* path, int64_t capacity, int32_t* degree,
+                                   double* kappa, int32_t* num_views, int64_t* n,
+                                   double* gamma, uint8_t* is_virtual);
+
 /* ---- parity / debug ----------------------------------------------------- */
 /* Projection records of one camera (ImageSpaceSplat, raster.hpp:37-44) for all
  * N particles: culled[N] (1 = culled), mean[2N], conic[3N] (a, b, c), depth[N],

@@ -417,6 +417,48 @@ def nbv_loop(ctx: Context, scene, field: DeviceField, candidates: Sequence[Camer
     return chosen[:steps], best[:steps], allsc[:steps]
 
 
+# ------------------------------------------------------------------ formats
+def load_splat_ply(path: str) -> Scene:
+    """load_splat_ply (io.hpp:493-637) -> fp32 SoA scene (host)."""
+    lib = N.load()
+    n = C.c_int64()
+    deg = C.c_int32()
+    N.check(lib.gavis_ply_info(path.encode(), C.byref(n), C.byref(deg)))
+    nb = (deg.value + 1) ** 2
+    k = max(1, n.value)
+    pos, rot = np.zeros((k, 3), np.float32), np.zeros((k, 4), np.float32)
+    scl, op = np.zeros((k, 3), np.float32), np.zeros(k, np.float32)
+    col = np.zeros((k, 3, nb), np.float32)
+    bmin, bmax = np.zeros(3), np.zeros(3)
+    N.check(lib.gavis_read_splat_ply(path.encode(), C.c_int64(k), _ptr(pos), _ptr(rot), _ptr(scl), _ptr(op),
+                                     _ptr(col), _ptr(bmin), _ptr(bmax)))
+    m = n.value
+    return Scene(pos[:m], rot[:m], scl[:m], op[:m], col[:m], np.zeros(m, np.uint8), deg.value, bmin, bmax)
+
+
+def save_field_json(path: str, field: VisibilityField, is_virtual=None) -> None:
+    """save_field (io.hpp:255-269)."""
+    g = np.ascontiguousarray(field.gamma, np.float64)
+    v = None if is_virtual is None else np.ascontiguousarray(is_virtual, np.uint8)
+    N.check(N.load().gavis_field_json_write(path.encode(), C.c_int32(field.degree), C.c_double(field.vmf.kappa),
+                                            C.c_int32(field.num_views), C.c_int64(g.shape[0]), _ptr(g), _ptr(v)))
+
+
+def load_field_json(path: str) -> VisibilityField:
+    """load_field (io.hpp:271-295)."""
+    lib = N.load()
+    deg, nv, n = C.c_int32(), C.c_int32(), C.c_int64()
+    kappa = C.c_double()
+    N.check(lib.gavis_field_json_read(path.encode(), C.c_int64(0), C.byref(deg), C.byref(kappa), C.byref(nv),
+                                      C.byref(n), None, None))
+    nb = (deg.value + 1) ** 2
+    g = np.zeros((max(1, n.value), nb))
+    v = np.zeros(max(1, n.value), np.uint8)
+    N.check(lib.gavis_field_json_read(path.encode(), C.c_int64(max(1, n.value)), C.byref(deg), C.byref(kappa),
+                                      C.byref(nv), C.byref(n), _ptr(g), _ptr(v)))
+    return VisibilityField(deg.value, VmfParams(kappa.value), nv.value, g[: n.value], v[: n.value])
+
+
 # ------------------------------------------------------------------ debug
 def debug_project(ctx: Context, scene, cam: CameraView, dilation: float = 0.3, tile_size: int = 16):
     ds = _as_dev(ctx, scene)

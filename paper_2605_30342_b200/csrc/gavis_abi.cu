@@ -689,6 +689,14 @@ int gavis_abi_version(void) { return GAVIS_ABI_VERSION; }
 
 const char* gavis_last_error(void) { return g_last_error.c_str(); }
 
+}  // extern "C"
+
+namespace gavis {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace gavis
+
+extern "C" {
+
 gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
   return guard([&] {
     require(out != nullptr, "out must not be null");
