@@ -12,10 +12,10 @@
 // leaves the loop when both are done.
 //
 // Schedules:
-//   * ua_blend_tile2_kernel (16x16 tiles, default): 128 threads per tile, each
-//     thread owns two pixels 4 rows apart (a warp owns an 8x8 block), so every
-//     shared-memory read of a splat record / SH colour row feeds two pixels and
-//     the two pixels' fp64 dependency chains interleave.
+//   * ua_blend_ilp_kernel (16x16 tiles, default): 256 threads, one pixel each,
+//     warp pre-filter of the tile list, list entries walked two at a time in
+//     straight-line code (fp64 instruction-level parallelism).
+//   * ua_blend_tile2_kernel (16x16 tiles): 128 threads, two pixels per thread.
 //   * ua_blend_kernel (any tile size): 256 threads, one pixel each, in rounds.
 // The SH colour dot products run as packed fp32x2 FMAs (FFMA2, sm_100) over
 // coefficient pairs; colour rows are padded to an even length on upload.
@@ -382,6 +382,154 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   if (ENT && a.tile_score && tid == 0) a.tile_score[gt] = tile_h;
 }
 
+// ---------------------------------------------------------------------------
+// 16x16 tiles, 256 threads, one pixel each (warp = 8x4 patch), list entries
+// walked TWO AT A TIME in straight-line code. fp64 ops have an 8-cycle
+// dependent latency on B200 (tools/micro/lat.cu): the alphas (exp), colours and
+// logs of the two entries are independent, so the pair doubles the fp64
+// instruction-level parallelism; only T, T*, rgb, H and w0 chain. Masks replace
+// branches: an entry a pixel does not cover, or one past its termination, gets
+// alpha = alpha* = 0, which leaves every accumulator bit-identical.
+template <int LC, bool RGB, bool ENT, bool EXTRA>
+__global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
+  constexpr int CS = Col<LC>::STRIDE;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
+  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
+                                                            (ENT ? sizeof(UaRec) : 0)));
+  __shared__ double s_red[8];
+  load_math_tables();
+
+  const double amax = a.amax, cutoff = a.cutoff;
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = a.scene.n;
+  const GeoRec* geo = a.geo + (int64_t)v * N;
+  const UaRec* uar = a.ua + (int64_t)v * N;
+
+  const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 4;
+  const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+  const bool inside = px < c.width && py < c.height;
+  const double cxp = px + 0.5, cyp = py + 0.5;
+  Pixel<LC> P;
+  pixel_init<LC, RGB, ENT>(P, c, px, py, inside);
+
+  for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
+    const bool live = !(P.rgb_done && P.ent_done);
+    if (__syncthreads_count(live) == 0) break;
+    const int n = min((uint32_t)kBatch, rg.y - base);
+    stage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
+    __syncthreads();
+    if (__all_sync(0xffffffffu, !live)) continue;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      bool hit = false;
+      if (j0 + lane < n) {
+        const int4 r = s_rect[j0 + lane];
+        hit = r.x <= bx0 + 7 && r.x + r.y >= bx0 && r.z <= by0 + 3 && r.z + r.w >= by0;
+      }
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      while (hits != 0u) {
+        const int ja = j0 + __ffs(hits) - 1;
+        hits &= hits - 1u;
+        const bool has_b = hits != 0u;
+        const int jb = has_b ? j0 + __ffs(hits) - 1 : ja;
+        if (has_b) hits &= hits - 1u;
+        const bool ca = in_rect4(s_rect[ja], px, py);
+        const bool cb = has_b && in_rect4(s_rect[jb], px, py);
+        const GeoRec& ea = s_geo[ja];
+        const GeoRec& eb = s_geo[jb];
+        // alphas of both entries (splat_alpha, raster.hpp:101-108), independent chains
+        const double dxa = cxp - ea.mx, dya = cyp - ea.my;
+        const double dxb = cxp - eb.mx, dyb = cyp - eb.my;
+        const double qa = ea.ca * dxa * dxa + ea.cb2 * dxa * dya + ea.cc * dya * dya;
+        const double qb = eb.ca * dxb * dxb + eb.cb2 * dxb * dyb + eb.cc * dyb * dyb;
+        const double exa = exp_neg(fmax(-0.5 * qa, -40.0));
+        const double exb = exp_neg(fmax(-0.5 * qb, -40.0));
+        double ala = (double)ea.opacity * exa, alb = (double)eb.opacity * exb;
+        ala = qa <= kQSkip ? (ala > amax ? amax : ala) : 0.0;
+        alb = qb <= kQSkip ? (alb > amax ? amax : alb) : 0.0;
+        if (RGB) {
+          const bool ra = ca && !P.rgb_done;
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
+          sh_color<LC>(reinterpret_cast<const float2*>(s_col + ja * CS), P.bp, a0, a1, a2);
+          sh_color<LC>(reinterpret_cast<const float2*>(s_col + jb * CS), P.bp, b0, b1, b2);
+          const double aa = ra ? ala : 0.0;
+          const double wa = aa * P.T;
+          P.rgb0 += wa * (double)a0;
+          P.rgb1 += wa * (double)a1;
+          P.rgb2 += wa * (double)a2;
+          if (EXTRA) P.dep += wa * ea.depth;
+          P.T *= 1.0 - aa;
+          const bool rd = P.rgb_done || (ra && P.T < cutoff);
+          const bool rb = cb && !rd;
+          const double ab = rb ? alb : 0.0;
+          const double wb = ab * P.T;
+          P.rgb0 += wb * (double)b0;
+          P.rgb1 += wb * (double)b1;
+          P.rgb2 += wb * (double)b2;
+          if (EXTRA) {
+            P.dep += wb * eb.depth;
+            P.n_rgb += (int)ra + (int)rb;
+          }
+          P.T *= 1.0 - ab;
+          P.rgb_done = rd || (rb && P.T < cutoff);
+        }
+        if (ENT) {
+          const bool ea_on = ca && !P.ent_done;
+          const UaRec& ua = s_ua[ja];
+          const UaRec& ub = s_ua[jb];
+          double xa = ua.A * ala + ua.B, xb = ub.A * alb + ub.B;
+          xa = xa < 0.0 ? 0.0 : (amax < xa ? amax : xa);
+          xb = xb < 0.0 ? 0.0 : (amax < xb ? amax : xb);
+          const double asa = ea_on ? xa : 0.0;
+          const double wa = asa * P.Te;
+          const double sa = wa * ua.v;
+          P.w0 += wa * (1.0 - ua.v);
+          if (EXTRA) P.edep += wa * ea.depth;
+          P.Te *= 1.0 - asa;
+          const bool ed = P.ent_done || (ea_on && P.Te < cutoff);
+          const bool eb_on = cb && !ed;
+          const double asb = eb_on ? xb : 0.0;
+          const double wb = asb * P.Te;
+          const double sb = wb * ub.v;
+          const double la = log_pos(sa > 0.0 ? sa : 1.0);
+          const double lb = log_pos(sb > 0.0 ? sb : 1.0);
+          if (sa > 0.0) P.H += sa * (-la + ua.hl + kGaussEntropy);
+          if (sb > 0.0) P.H += sb * (-lb + ub.hl + kGaussEntropy);
+          P.w0 += wb * (1.0 - ub.v);
+          if (EXTRA) {
+            P.edep += wb * eb.depth;
+            P.n_ent += (int)ea_on + (int)eb_on;
+          }
+          P.Te *= 1.0 - asb;
+          P.ent_done = ed || (eb_on && P.Te < cutoff);
+        }
+      }
+    }
+  }
+  pixel_finish<LC, RGB, ENT, EXTRA>(P, a, c, px, py, inside);
+  if (ENT && a.tile_score) {
+    double h = inside ? score_term(P, a) : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
+    if (lane == 0) s_red[warp] = h;
+    __syncthreads();
+    if (tid == 0) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sum += s_red[w];
+      a.tile_score[gt] = sum;
+    }
+  }
+}
+
 // K8: image score per view = fold of its per-tile partials in tile order, one warp
 // per view (lane-contiguous chunks, then a fixed shuffle tree).
 __global__ void score_kernel(const DevCam* cams, int V, const double* tile_score, double* scores) {
@@ -409,7 +557,16 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
     const char* e = getenv("GAVIS_UA_KERNEL");
     return e ? atoi(e) : 0;
   }();
-  if (a.tile_size == 16 && choice != 1) {
+  // default for 16x16 tiles: the entry-pair (ILP) kernel; GAVIS_UA_KERNEL=3 selects
+  // the two-pixel kernel, =1 the generic per-pixel kernel (A/B measurements).
+  if (a.tile_size == 16 && (choice == 0 || choice == 2)) {
+    static bool configured = false;
+    if (!configured) set_smem(ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA>, smem);
+    configured = true;
+    ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
+    return;
+  }
+  if (a.tile_size == 16 && choice == 3) {
     static bool configured = false;
     if (!configured) {
       set_smem(ua_blend_tile2_kernel<LC, RGB, ENT, EXTRA>, smem);
