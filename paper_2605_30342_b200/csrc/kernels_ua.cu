@@ -390,15 +390,15 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
 // instruction-level parallelism; only T, T*, rgb, H and w0 chain. Masks replace
 // branches: an entry a pixel does not cover, or one past its termination, gets
 // alpha = alpha* = 0, which leaves every accumulator bit-identical.
-template <int LC, bool RGB, bool ENT, bool EXTRA>
+template <int LC, bool RGB, bool ENT, bool EXTRA, int BATCH = kBatch>
 __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
-  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
-  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
-  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
-                                                            (ENT ? sizeof(UaRec) : 0)));
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + BATCH * sizeof(GeoRec));
+  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + BATCH * (sizeof(GeoRec) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + BATCH * (sizeof(GeoRec) + sizeof(int4) +
+                                                           (ENT ? sizeof(UaRec) : 0)));
   __shared__ double s_red[8];
   load_math_tables();
 
@@ -421,10 +421,10 @@ __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
   Pixel<LC> P;
   pixel_init<LC, RGB, ENT>(P, c, px, py, inside);
 
-  for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
+  for (uint32_t base = rg.x; base < rg.y; base += BATCH) {
     const bool live = !(P.rgb_done && P.ent_done);
     if (__syncthreads_count(live) == 0) break;
-    const int n = min((uint32_t)kBatch, rg.y - base);
+    const int n = min((uint32_t)BATCH, rg.y - base);
     stage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
     __syncthreads();
     if (__all_sync(0xffffffffu, !live)) continue;
@@ -559,11 +559,14 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
   }();
   // default for 16x16 tiles: the entry-pair (ILP) kernel; GAVIS_UA_KERNEL=3 selects
   // the two-pixel kernel, =1 the generic per-pixel kernel (A/B measurements).
+  // (batch 192: fewer block barriers per tile list than 128; 3 CTAs of 58 KB fit)
   if (a.tile_size == 16 && (choice == 0 || choice == 2)) {
+    constexpr int kIlpBatch = 192;
+    const size_t sm = Stage<LC, RGB, ENT>::bytes(kIlpBatch);
     static bool configured = false;
-    if (!configured) set_smem(ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA>, smem);
+    if (!configured) set_smem(ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, kIlpBatch>, sm);
     configured = true;
-    ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
+    ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, kIlpBatch><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
     return;
   }
   if (a.tile_size == 16 && choice == 3) {
