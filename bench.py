@@ -403,6 +403,18 @@ def run_ours(args):
                "sample": f"{n} of the config-{args.config} candidates (800x800, full scene), oracle "
                          f"select_nbv + rasterize on {cores} threads, {dt:.1f} s ({model})"}
 
+    # dram bytes per ua_blend launch from the committed ncu --set full capture
+    # (profiles/ncu_ua_blend.json, same launch shape: 16 config-3 views, RGB+entropy)
+    traffic, traffic_src, compute = None, None, None
+    prof = os.path.join(ROOT, "profiles", "ncu_ua_blend.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        traffic = pj["traffic_bytes_per_launch"] * views_per_launch / pj["views_per_launch"]
+        traffic_src = f"{pj['command']} ({pj['views_per_launch']} views/launch)"
+        compute = {"bound": "fp64 issue/latency", "fp64_pipe_active_pct": pj["fp64_pipe_active_pct"],
+                   "issue_slots_busy_pct": pj["issue_slots_busy_pct"], "source": "same ncu capture"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -415,7 +427,8 @@ def run_ours(args):
                        "parallelism": f"candidates sharded over {world} GPU(s), VF views sharded + NCCL all-reduce",
                        "l2": "inputs (scene+field) exceed the 126 MB L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src, "compute": compute,
                          "kernel": "ua_blend", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": blend_ms / max(1, blend_n), "launches": blend_n,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
