@@ -494,4 +494,231 @@ inline CameraView make_lookat(const Vec3& position, const Vec3& target, const Ve
   return v;
 }
 
+// ---- density control (vfield.hpp:136-199) ---------------------------------
+struct DensityControlConfig {
+  double rho = 100.0, eta = 0.5, eps_v = 0.95;
+  uint64_t seed = 0;
+};
+
+inline double virtual_particle_scale(const DensityControlConfig& cfg) {
+  return std::cbrt(3.0 * (1.0 + cfg.eta) / (4.0 * kPi * cfg.rho));
+}
+
+namespace detail {
+inline uint64_t mix64(uint64_t x) {  // rng.hpp:18-28
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+inline gavis_density_config dc_c(const DensityControlConfig& d) {
+  return gavis_density_config{d.rho, d.eta, d.eps_v, d.seed};
+}
+inline CameraView cam_from_c(const gavis_camera& g) {
+  CameraView c;
+  for (int i = 0; i < 9; ++i) c.rotation.m[i] = g.rotation[i];
+  c.position = Vec3(g.position[0], g.position[1], g.position[2]);
+  c.width = g.width;
+  c.height = g.height;
+  c.fov_h = g.fov_h;
+  c.fov_v = g.fov_v;
+  c.near = g.near_plane;
+  return c;
+}
+}  // namespace detail
+
+inline uint64_t derive_seed(uint64_t seed, uint64_t stream) {
+  return detail::mix64(seed ^ detail::mix64(stream + 0x632be59bd9b4e019ull));
+}
+
+// The device decides which probes survive (isotropic multi-view visibility on
+// the VF kernels); the returned host scene appends them exactly as the
+// reference does (double positions bounds.min + extent * u, scale s, o = 0).
+inline Scene density_control(const Scene& scene, const Trajectory& trajectory,
+                             const DensityControlConfig& cfg, const RasterConfig& rc = {},
+                             int /*threads*/ = 1) {
+  auto ds = detail::upload(scene);
+  std::vector<gavis_camera> views;
+  for (const auto& v : trajectory.views) views.push_back(detail::cam_c(v));
+  const double bmin[3] = {scene.bounds.min[0], scene.bounds.min[1], scene.bounds.min[2]};
+  const double bmax[3] = {scene.bounds.max[0], scene.bounds.max[1], scene.bounds.max[2]};
+  const double ext[3] = {bmax[0] - bmin[0], bmax[1] - bmin[1], bmax[2] - bmin[2]};
+  const double vol = ext[0] * ext[1] * ext[2];
+  const std::size_t cap = vol > 0.0 && cfg.rho > 0.0 ? (std::size_t)std::floor(cfg.rho * vol) : 0;
+  std::vector<int64_t> kept(std::max<std::size_t>(1, cap));
+  int64_t n_kept = 0;
+  gavis_scene* aug = nullptr;
+  const gavis_density_config d = detail::dc_c(cfg);
+  const gavis_raster_config r = detail::rc_c(rc);
+  check(gavis_density_control(detail::holder().get(), ds->h, bmin, bmax, views.data(),
+                              (int32_t)views.size(), &d, &r, &aug, &n_kept, kept.data(),
+                              (int64_t)kept.size()));
+  gavis_scene_destroy(aug);
+  Scene out = scene;
+  const double s = virtual_particle_scale(cfg);
+  const int nb = (scene.color_degree + 1) * (scene.color_degree + 1);
+  for (int64_t i = 0; i < n_kept; ++i) {
+    uint64_t st = derive_seed(cfg.seed, (uint64_t)kept[i]);
+    double u[3];
+    for (int k = 0; k < 3; ++k) {
+      st += 0x9e3779b97f4a7c15ull;
+      u[k] = (double)(detail::mix64(st - 0x9e3779b97f4a7c15ull) >> 11) * 0x1.0p-53;
+    }
+    GaussianParticle vp;
+    vp.position = Vec3(bmin[0] + ext[0] * u[0], bmin[1] + ext[1] * u[1], bmin[2] + ext[2] * u[2]);
+    vp.scale = Vec3(s, s, s);
+    vp.opacity = 0.0;
+    vp.is_virtual = true;
+    for (int c = 0; c < 3; ++c) vp.color_sh[c].assign(nb, 0.0);
+    out.particles.push_back(vp);
+  }
+  return out;
+}
+
+// ---- planner (planner.hpp) --------------------------------------------------
+enum class PoseMode { kSe3, kSe2 };
+
+struct PlannerConfig {  // planner.hpp:24-42
+  PoseMode mode = PoseMode::kSe3;
+  int num_candidates = 128;
+  double se2_height = 1.5;
+  int steps = 10;
+  uint64_t seed = 0;
+  bool look_inward = true;
+  double clearance = 0.1;
+  int cam_width = 128, cam_height = 128;
+  double fov_h = kPi / 2.0, fov_v = kPi / 2.0;
+  double cam_near = 0.05;
+};
+
+struct OccluderRect {  // model.hpp:141-150
+  Vec3 corner = Vec3(0, 0, 0), edge_u = Vec3(1, 0, 0), edge_v = Vec3(0, 1, 0);
+  bool opaque = true;
+};
+
+struct OccluderSet {  // model.hpp:152-155
+  std::vector<OccluderRect> rectangles;
+  double sample_density = 64.0;
+};
+
+struct MappingContext {  // planner.hpp:255-262
+  VmfParams vmf;
+  int field_degree = 2;
+  RasterConfig raster;
+  UncertaintyConfig uncertainty;
+  DensityControlConfig density;
+  bool density_enabled = true;
+};
+
+struct MappingStep {  // planner.hpp:264-270
+  std::vector<double> scores;
+  int chosen_index = -1;
+  double score = 0.0, vis_coverage = 0.0, mean_entropy = 0.0;
+};
+
+struct MappingLog {  // planner.hpp:272-275
+  Trajectory chosen_views;
+  std::vector<MappingStep> steps;
+};
+
+namespace detail {
+inline std::vector<gavis_occluder_rect> rects_c(const OccluderSet& o) {
+  std::vector<gavis_occluder_rect> out;
+  for (const auto& r : o.rectangles) {
+    gavis_occluder_rect g{};
+    for (int k = 0; k < 3; ++k) {
+      g.corner[k] = r.corner[k];
+      g.edge_u[k] = r.edge_u[k];
+      g.edge_v[k] = r.edge_v[k];
+    }
+    g.opaque = r.opaque ? 1 : 0;
+    out.push_back(g);
+  }
+  return out;
+}
+inline gavis_planner_config pc_c(const PlannerConfig& p) {
+  gavis_planner_config g{};
+  g.mode = p.mode == PoseMode::kSe2 ? 1 : 0;
+  g.num_candidates = p.num_candidates;
+  g.se2_height = p.se2_height;
+  g.steps = p.steps;
+  g.look_inward = p.look_inward ? 1 : 0;
+  g.seed = p.seed;
+  g.clearance = p.clearance;
+  g.cam_width = p.cam_width;
+  g.cam_height = p.cam_height;
+  g.fov_h = p.fov_h;
+  g.fov_v = p.fov_v;
+  g.cam_near = p.cam_near;
+  return g;
+}
+}  // namespace detail
+
+// planner.hpp:56-107 (host code in the library; no device needed)
+inline std::vector<CameraView> sample_candidates(const Bounds& bounds, const OccluderSet& occluders,
+                                                 const PlannerConfig& pc, uint64_t step_seed) {
+  const auto rects = detail::rects_c(occluders);
+  const gavis_planner_config g = detail::pc_c(pc);
+  std::vector<gavis_camera> out(std::max(1, pc.num_candidates));
+  const double bmin[3] = {bounds.min[0], bounds.min[1], bounds.min[2]};
+  const double bmax[3] = {bounds.max[0], bounds.max[1], bounds.max[2]};
+  check(gavis_sample_candidates(bmin, bmax, rects.data(), (int32_t)rects.size(), &g, step_seed,
+                                out.data()));
+  std::vector<CameraView> views;
+  for (int i = 0; i < pc.num_candidates; ++i) views.push_back(detail::cam_from_c(out[i]));
+  return views;
+}
+
+// planner.hpp:155-184
+inline double vis_coverage(const OccluderSet& occluders, const Trajectory& trajectory) {
+  const auto rects = detail::rects_c(occluders);
+  std::vector<gavis_camera> views;
+  for (const auto& v : trajectory.views) views.push_back(detail::cam_c(v));
+  double cov = 0.0;
+  check(gavis_vis_coverage(rects.data(), (int32_t)rects.size(), occluders.sample_density,
+                           views.data(), (int32_t)views.size(), &cov));
+  return cov;
+}
+
+// planner.hpp:284-316
+inline MappingLog run_active_mapping(const Scene& scene, const OccluderSet& occluders,
+                                     const Trajectory& init, const PlannerConfig& pc,
+                                     const MappingContext& ctx, int /*threads*/ = 1) {
+  auto ds = detail::upload(scene);
+  const auto rects = detail::rects_c(occluders);
+  const gavis_planner_config g = detail::pc_c(pc);
+  gavis_mapping_config mc{};
+  mc.kappa = ctx.vmf.kappa;
+  mc.field_degree = ctx.field_degree;
+  mc.density_enabled = ctx.density_enabled ? 1 : 0;
+  mc.raster = detail::rc_c(ctx.raster);
+  mc.uncertainty = detail::uc_c(ctx.uncertainty);
+  mc.density = detail::dc_c(ctx.density);
+  std::vector<gavis_camera> init_c;
+  for (const auto& v : init.views) init_c.push_back(detail::cam_c(v));
+  const int steps = std::max(0, pc.steps), nc = std::max(1, pc.num_candidates);
+  std::vector<gavis_camera> chosen(std::max(1, steps));
+  std::vector<int32_t> idx(std::max(1, steps));
+  std::vector<double> score(std::max(1, steps)), all((size_t)std::max(1, steps) * nc),
+      cov(std::max(1, steps)), ment(std::max(1, steps));
+  const double bmin[3] = {scene.bounds.min[0], scene.bounds.min[1], scene.bounds.min[2]};
+  const double bmax[3] = {scene.bounds.max[0], scene.bounds.max[1], scene.bounds.max[2]};
+  check(gavis_active_mapping(detail::holder().get(), ds->h, bmin, bmax, rects.data(),
+                             (int32_t)rects.size(), occluders.sample_density, init_c.data(),
+                             (int32_t)init_c.size(), &g, &mc, chosen.data(), idx.data(),
+                             score.data(), all.data(), cov.data(), ment.data()));
+  MappingLog log;
+  for (int s = 0; s < steps; ++s) {
+    log.chosen_views.views.push_back(detail::cam_from_c(chosen[s]));
+    MappingStep st;
+    st.scores.assign(all.begin() + (size_t)s * nc, all.begin() + (size_t)(s + 1) * nc);
+    st.chosen_index = idx[s];
+    st.score = score[s];
+    st.vis_coverage = cov[s];
+    st.mean_entropy = ment[s];
+    log.steps.push_back(std::move(st));
+  }
+  return log;
+}
+
 }  // namespace gavis_b200

@@ -245,6 +245,70 @@ gavis_status gavis_density_control(gavis_ctx* ctx, const gavis_scene* scene,
                                    const gavis_raster_config* rc, gavis_scene** out,
                                    int64_t* n_kept, int64_t* kept_ids, int64_t kept_capacity);
 
+/* ---- planner (planner.hpp; host C++ around the device entry points) ------ */
+/* OccluderRect (model.hpp:141-150): corner + u edge_u + v edge_v, u, v in [0,1]. */
+typedef struct {
+  double corner[3], edge_u[3], edge_v[3];
+  int32_t opaque;
+  int32_t _pad;
+} gavis_occluder_rect;
+
+/* PlannerConfig (planner.hpp:24-42). mode: 0 kSe3, 1 kSe2. Defaults 0, 128,
+ * 1.5, 10, 0, look_inward 1, clearance 0.1, 128x128, fov pi/2 x pi/2, near 0.05. */
+typedef struct {
+  int32_t mode, num_candidates;
+  double se2_height;
+  int32_t steps, look_inward;
+  uint64_t seed;
+  double clearance;
+  int32_t cam_width, cam_height;
+  double fov_h, fov_v, cam_near;
+} gavis_planner_config;
+
+/* MappingContext (planner.hpp:255-262): vmf kappa (default 1), field degree
+ * (default 2), raster / uncertainty / density configs, density_enabled
+ * (default 1). */
+typedef struct {
+  double kappa;
+  int32_t field_degree, density_enabled;
+  gavis_raster_config raster;
+  gavis_uncertainty_config uncertainty;
+  gavis_density_config density;
+} gavis_mapping_config;
+
+/* sample_candidates (planner.hpp:56-107), host only: rejection-sampled poses
+ * from SplitMix64(derive_seed(step_seed, 0xca4d1d)), discarded within
+ * `clearance` of an opaque rectangle; out[num_candidates]. Budget exhaustion
+ * (100 draws per candidate) -> PARAMETER. */
+gavis_status gavis_sample_candidates(const double* bounds_min, const double* bounds_max,
+                                     const gavis_occluder_rect* rects, int32_t n_rects,
+                                     const gavis_planner_config* pc, uint64_t step_seed,
+                                     gavis_camera* out);
+
+/* vis_coverage (planner.hpp:155-184), host only: area-weighted fraction of
+ * occluder surface (sample_density samples per unit area) seen by a view. */
+gavis_status gavis_vis_coverage(const gavis_occluder_rect* rects, int32_t n_rects,
+                                double sample_density, const gavis_camera* views,
+                                int32_t n_views, double* coverage);
+
+/* run_active_mapping (planner.hpp:284-316): per step, density control
+ * reseeded with derive_seed(density.seed, step) over the current trajectory
+ * (if enabled), a field rebuilt on the augmented scene, candidates from
+ * gavis_sample_candidates(bounds, ..., derive_seed(pc.seed, step)), select_nbv
+ * (entropy only), the chosen view appended. Per step outputs (nullable):
+ * chosen_views[steps], chosen_index[steps], chosen_score[steps],
+ * all_scores[steps * num_candidates], vis_coverage[steps] (needs occluders),
+ * mean_entropy[steps] = score / (width * height). */
+gavis_status gavis_active_mapping(gavis_ctx* ctx, const gavis_scene* scene,
+                                  const double* bounds_min, const double* bounds_max,
+                                  const gavis_occluder_rect* rects, int32_t n_rects,
+                                  double sample_density, const gavis_camera* init_views,
+                                  int32_t n_init, const gavis_planner_config* pc,
+                                  const gavis_mapping_config* mc, gavis_camera* chosen_views,
+                                  int32_t* chosen_index, double* chosen_score,
+                                  double* all_scores, double* vis_coverage,
+                                  double* mean_entropy);
+
 /* ---- on-disk formats (host only; io.hpp) -------------------------------- */
 /* load_splat_ply (io.hpp:493-637), two-phase: gavis_ply_info gives the vertex
  * count and the colour degree implied by f_rest_*; gavis_read_splat_ply fills

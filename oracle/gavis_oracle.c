@@ -979,3 +979,204 @@ double gor_raymarch_transmittance(const gor_scene* s, const double* origin,
   }
   return tr;
 }
+
+/* ------------------------------------------------------------------------- */
+/* planner.hpp:45-107 (sample_candidates) and :141-184 (vis_coverage).       */
+/* Eigen fixed-size kernels written out: 3x3 determinant / cofactor inverse   */
+/* (Eigen LU module), Quaternion::normalized + toRotationMatrix.              */
+
+typedef struct {
+  uint64_t state;
+} gor_sm64;
+
+static uint64_t sm64_next(gor_sm64* g) { /* rng.hpp:34-40 */
+  g->state += 0x9e3779b97f4a7c15ull;
+  return mix64_(g->state - 0x9e3779b97f4a7c15ull);
+}
+static double sm64_double(gor_sm64* g) { return (double)(sm64_next(g) >> 11) * 0x1.0p-53; }
+static double sm64_uniform(gor_sm64* g, double lo, double hi) { return lo + (hi - lo) * sm64_double(g); }
+
+static double v3_norm(const double* a) { return sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+static void v3_cross(const double* a, const double* b, double* o) {
+  o[0] = a[1] * b[2] - a[2] * b[1];
+  o[1] = a[2] * b[0] - a[0] * b[2];
+  o[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* make_lookat, model.hpp:107-128, up = (0,0,1). Returns 0 on coincident points. */
+static int lookat_(const double* pos, const double* target, gor_camera* cam) {
+  double f[3] = {target[0] - pos[0], target[1] - pos[1], target[2] - pos[2]};
+  if (!(v3_norm(f) > 1e-12)) return 0;
+  double n = v3_norm(f);
+  for (int i = 0; i < 3; ++i) f[i] /= n;
+  const double up[3] = {0.0, 0.0, 1.0}, ex[3] = {1.0, 0.0, 0.0};
+  double r[3], d[3];
+  v3_cross(f, up, r);
+  if (v3_norm(r) < 1e-9) v3_cross(f, ex, r);
+  n = v3_norm(r);
+  for (int i = 0; i < 3; ++i) r[i] /= n;
+  v3_cross(f, r, d);
+  for (int i = 0; i < 3; ++i) {
+    cam->rotation[i * 3 + 0] = r[i];
+    cam->rotation[i * 3 + 1] = d[i];
+    cam->rotation[i * 3 + 2] = f[i];
+  }
+  return 1;
+}
+
+/* rect: corner[3], edge_u[3], edge_v[3], opaque flag (layout of gor_rect). */
+static double rect_dist_(const gor_rect* rc, const double* p) { /* planner.hpp:45-52 */
+  double w[3], uu = 0, vv = 0, wu, wv;
+  for (int i = 0; i < 3; ++i) w[i] = p[i] - rc->corner[i];
+  uu = rc->edge_u[0] * rc->edge_u[0] + rc->edge_u[1] * rc->edge_u[1] + rc->edge_u[2] * rc->edge_u[2];
+  vv = rc->edge_v[0] * rc->edge_v[0] + rc->edge_v[1] * rc->edge_v[1] + rc->edge_v[2] * rc->edge_v[2];
+  wu = w[0] * rc->edge_u[0] + w[1] * rc->edge_u[1] + w[2] * rc->edge_u[2];
+  wv = w[0] * rc->edge_v[0] + w[1] * rc->edge_v[1] + w[2] * rc->edge_v[2];
+  double u = 0.0, v = 0.0;
+  if (uu > 0.0) { u = wu / uu; u = u < 0.0 ? 0.0 : (u > 1.0 ? 1.0 : u); }
+  if (vv > 0.0) { v = wv / vv; v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+  double q[3];
+  for (int i = 0; i < 3; ++i) q[i] = (rc->corner[i] + u * rc->edge_u[i]) + v * rc->edge_v[i] - p[i];
+  return v3_norm(q);
+}
+
+int gor_sample_candidates(const double* bmin, const double* bmax, const gor_rect* rects,
+                          int n_rects, const gor_planner* pc, uint64_t step_seed, gor_camera* out) {
+  const double ext[3] = {bmax[0] - bmin[0], bmax[1] - bmin[1], bmax[2] - bmin[2]};
+  if (!(ext[0] * ext[1] * ext[2] > 0.0) || pc->num_candidates < 1) return -1;
+  gor_sm64 g = {gor_derive_seed(step_seed, 0xca4d1d)};
+  long long budget = 100LL * pc->num_candidates, attempts = 0;
+  int n = 0;
+  while (n < pc->num_candidates) {
+    if (attempts++ >= budget) return -2;
+    double p[3];
+    for (int i = 0; i < 3; ++i) p[i] = sm64_uniform(&g, bmin[i], bmax[i]);
+    const double yaw = sm64_uniform(&g, 0.0, 2.0 * K_PI);
+    const double u1 = sm64_double(&g), u2 = sm64_double(&g), u3 = sm64_double(&g);
+    const double qa = sqrt(1.0 - u1), qb = sqrt(u1);
+    /* Quat(w, x, y, z) = (a sin 2pi u2, a cos 2pi u2, b sin 2pi u3, b cos 2pi u3) */
+    const double qw = qa * sin(2.0 * K_PI * u2), qx = qa * cos(2.0 * K_PI * u2);
+    const double qy = qb * sin(2.0 * K_PI * u3), qz = qb * cos(2.0 * K_PI * u3);
+    if (pc->mode == 1) p[2] = pc->se2_height;
+    int hit = 0;
+    for (int r = 0; r < n_rects && !hit; ++r)
+      if (rects[r].opaque && rect_dist_(&rects[r], p) < pc->clearance) hit = 1;
+    if (hit) continue;
+    gor_camera cam;
+    memset(&cam, 0, sizeof(cam));
+    if (pc->mode == 1) {
+      const double t[3] = {p[0] + cos(yaw), p[1] + sin(yaw), p[2] + 0.0};
+      if (!lookat_(p, t, &cam)) return -3;
+    } else if (pc->look_inward) {
+      double t[3] = {0.5 * (bmin[0] + bmax[0]), 0.5 * (bmin[1] + bmax[1]), 0.5 * (bmin[2] + bmax[2])};
+      const double dd[3] = {t[0] - p[0], t[1] - p[1], t[2] - p[2]};
+      if (v3_norm(dd) < 1e-9) t[0] += 1e-3;
+      if (!lookat_(p, t, &cam)) return -3;
+    } else {
+      /* Eigen stores (x, y, z, w); SSE2 squaredNorm = (x^2 + z^2) + (y^2 + w^2) */
+      const double nq = sqrt((qx * qx + qz * qz) + (qy * qy + qw * qw));
+      const double w = qw / nq, x = qx / nq, y = qy / nq, z = qz / nq;
+      const double tx = 2 * x, ty = 2 * y, tz = 2 * z;
+      double* R = cam.rotation;
+      R[0] = 1 - (ty * y + tz * z);
+      R[1] = ty * x - tz * w;
+      R[2] = tz * x + ty * w;
+      R[3] = ty * x + tz * w;
+      R[4] = 1 - (tx * x + tz * z);
+      R[5] = tz * y - tx * w;
+      R[6] = tz * x - ty * w;
+      R[7] = tz * y + tx * w;
+      R[8] = 1 - (tx * x + ty * y);
+    }
+    for (int i = 0; i < 3; ++i) cam.position[i] = p[i];
+    cam.width = pc->cam_width;
+    cam.height = pc->cam_height;
+    cam.fov_h = pc->fov_h;
+    cam.fov_v = pc->fov_v;
+    cam.near_plane = pc->cam_near;
+    out[n++] = cam;
+  }
+  return n;
+}
+
+/* intersect_rect, model.hpp:157-175 */
+static int isect_(const gor_rect* rc, const double* o, const double* dir, double* t_out) {
+  double m[9] = {rc->edge_u[0], rc->edge_v[0], -dir[0], rc->edge_u[1], rc->edge_v[1], -dir[1],
+                 rc->edge_u[2], rc->edge_v[2], -dir[2]};
+#define M_(r, c) m[(r) * 3 + (c)]
+  const double det = M_(0, 0) * (M_(1, 1) * M_(2, 2) - M_(1, 2) * M_(2, 1)) -
+                     M_(0, 1) * (M_(1, 0) * M_(2, 2) - M_(1, 2) * M_(2, 0)) +
+                     M_(0, 2) * (M_(1, 0) * M_(2, 1) - M_(1, 1) * M_(2, 0));
+  if (fabs(det) < 1e-14) return 0;
+  /* cofactor C(i,j) = M(i1,j1) M(i2,j2) - M(i1,j2) M(i2,j1), i1 = i+1, i2 = i+2 mod 3 */
+  double C[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+      C[i * 3 + j] = M_(i1, j1) * M_(i2, j2) - M_(i1, j2) * M_(i2, j1);
+    }
+  const double d2 = (C[0] * M_(0, 0) + C[3] * M_(1, 0)) + C[6] * M_(2, 0);
+#undef M_
+  const double inv_det = 1.0 / d2;
+  /* inverse = adjugate / det: inv(i, j) = C(j, i) * inv_det */
+  const double w[3] = {o[0] - rc->corner[0], o[1] - rc->corner[1], o[2] - rc->corner[2]};
+  double sol[3];
+  for (int i = 0; i < 3; ++i)
+    sol[i] = (C[0 * 3 + i] * inv_det) * w[0] + (C[1 * 3 + i] * inv_det) * w[1] + (C[2 * 3 + i] * inv_det) * w[2];
+  if (sol[0] < 0.0 || sol[0] > 1.0 || sol[1] < 0.0 || sol[1] > 1.0) return 0;
+  *t_out = sol[2];
+  return 1;
+}
+
+/* CameraView::project, model.hpp:90-97 */
+static int project_(const gor_camera* c, const double* p) {
+  const double d[3] = {p[0] - c->position[0], p[1] - c->position[1], p[2] - c->position[2]};
+  double cc[3];
+  for (int i = 0; i < 3; ++i)
+    cc[i] = c->rotation[0 * 3 + i] * d[0] + c->rotation[1 * 3 + i] * d[1] + c->rotation[2 * 3 + i] * d[2];
+  if (cc[2] < c->near_plane) return 0;
+  const double fx = 0.5 * c->width / tan(0.5 * c->fov_h), fy = 0.5 * c->height / tan(0.5 * c->fov_v);
+  const double px = 0.5 * c->width + fx * cc[0] / cc[2], py = 0.5 * c->height + fy * cc[1] / cc[2];
+  return px >= 0.0 && px <= c->width && py >= 0.0 && py <= c->height;
+}
+
+double gor_vis_coverage(const gor_rect* rects, int n_rects, double density, const gor_camera* views,
+                        int n_views) {
+  double total = 0.0, vis = 0.0;
+  for (int r = 0; r < n_rects; ++r) {
+    const gor_rect* rc = &rects[r];
+    double cr[3];
+    v3_cross(rc->edge_u, rc->edge_v, cr);
+    const double area = v3_norm(cr);
+    total += area;
+    if (n_views == 0) continue;
+    const double ps = sqrt(density);
+    int nu = (int)lround(v3_norm(rc->edge_u) * ps), nv = (int)lround(v3_norm(rc->edge_v) * ps);
+    if (nu < 1) nu = 1;
+    if (nv < 1) nv = 1;
+    long long seen = 0;
+    for (int i = 0; i < nu; ++i)
+      for (int j = 0; j < nv; ++j) {
+        const double u = (i + 0.5) / nu, v = (j + 0.5) / nv;
+        double p[3];
+        for (int k = 0; k < 3; ++k) p[k] = (rc->corner[k] + u * rc->edge_u[k]) + v * rc->edge_v[k];
+        for (int k = 0; k < n_views; ++k) {
+          const gor_camera* c = &views[k];
+          if (!project_(c, p)) continue;
+          const double seg[3] = {p[0] - c->position[0], p[1] - c->position[1], p[2] - c->position[2]};
+          int blocked = 0;
+          for (int q = 0; q < n_rects && !blocked; ++q) {
+            double t;
+            if (!rects[q].opaque || q == r) continue;
+            if (isect_(&rects[q], c->position, seg, &t) && t > 1e-9 && t < 1.0 - 1e-9) blocked = 1;
+          }
+          if (!blocked) {
+            ++seen;
+            break;
+          }
+        }
+      }
+    vis += area * (double)seen / ((double)nu * nv);
+  }
+  return total > 0.0 ? vis / total : 0.0;
+}

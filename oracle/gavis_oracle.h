@@ -123,6 +123,31 @@ int64_t gor_density_control(const gor_scene* s, const double* bounds_min, const 
                             int round_f32, int64_t* kept_ids, double* unseen_out);
 uint64_t gor_derive_seed(uint64_t seed, uint64_t stream);
 
+/* planner.hpp:24-42 PlannerConfig / model.hpp:141-150 OccluderRect (layouts of
+ * gavis_planner_config / gavis_occluder_rect). */
+typedef struct {
+  int32_t mode, num_candidates;
+  double se2_height;
+  int32_t steps, look_inward;
+  uint64_t seed;
+  double clearance;
+  int32_t cam_width, cam_height;
+  double fov_h, fov_v, cam_near;
+} gor_planner;
+
+typedef struct {
+  double corner[3], edge_u[3], edge_v[3];
+  int32_t opaque, _pad;
+} gor_rect;
+
+/* sample_candidates planner.hpp:56-107: returns the count, < 0 on error
+ * (-1 bad bounds/config, -2 budget exhausted, -3 degenerate look-at). */
+int gor_sample_candidates(const double* bmin, const double* bmax, const gor_rect* rects,
+                          int n_rects, const gor_planner* pc, uint64_t step_seed, gor_camera* out);
+/* vis_coverage planner.hpp:155-184 */
+double gor_vis_coverage(const gor_rect* rects, int n_rects, double density, const gor_camera* views,
+                        int n_views);
+
 /* oracle.hpp:70-103 */
 double gor_raymarch_transmittance(const gor_scene* s, const double* origin,
                                   const double* target, double step, int64_t exclude,

@@ -350,3 +350,53 @@ def density_control(scene, bounds_min, bounds_max, views, rho=100.0, eta=0.5, ep
                                   C.c_double(eta), C.c_double(eps_v), C.c_uint64(seed),
                                   C.byref(raster_struct(rc)), 1, int(round_f32), _p(kept), _p(unseen))
     return kept[:n], unseen[:n_virtual]
+
+
+class Planner(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("num_candidates", C.c_int32), ("se2_height", C.c_double),
+                ("steps", C.c_int32), ("look_inward", C.c_int32), ("seed", C.c_uint64),
+                ("clearance", C.c_double), ("cam_width", C.c_int32), ("cam_height", C.c_int32),
+                ("fov_h", C.c_double), ("fov_v", C.c_double), ("cam_near", C.c_double)]
+
+
+class Rect(C.Structure):
+    _fields_ = [("corner", C.c_double * 3), ("edge_u", C.c_double * 3), ("edge_v", C.c_double * 3),
+                ("opaque", C.c_int32), ("_pad", C.c_int32)]
+
+
+def _rects(occ):
+    rs = occ.rectangles if occ is not None else []
+    arr = (Rect * max(1, len(rs)))()
+    for i, r in enumerate(rs):
+        for k in range(3):
+            arr[i].corner[k], arr[i].edge_u[k], arr[i].edge_v[k] = r.corner[k], r.edge_u[k], r.edge_v[k]
+        arr[i].opaque = 1 if r.opaque else 0
+    return arr, len(rs)
+
+
+def _camera_from(c):
+    from paper_2605_30342_b200.model import CameraView
+    return CameraView(rotation=np.array(list(c.rotation)).reshape(3, 3), position=np.array(list(c.position)),
+                      width=c.width, height=c.height, fov_h=c.fov_h, fov_v=c.fov_v, near=c.near_plane)
+
+
+def sample_candidates(bounds, occ, pc, step_seed: int):
+    """sample_candidates (planner.hpp:56-107); raises ValueError where the reference throws."""
+    p = Planner(int(pc.mode), int(pc.num_candidates), float(pc.se2_height), int(pc.steps),
+                1 if pc.look_inward else 0, int(pc.seed), float(pc.clearance), int(pc.cam_width),
+                int(pc.cam_height), float(pc.fov_h), float(pc.fov_v), float(pc.cam_near))
+    bmin = np.ascontiguousarray(bounds[0], np.float64)
+    bmax = np.ascontiguousarray(bounds[1], np.float64)
+    rects, nr = _rects(occ)
+    out = (Camera * max(1, int(pc.num_candidates)))()
+    n = lib().gor_sample_candidates(_p(bmin), _p(bmax), rects, nr, C.byref(p), C.c_uint64(step_seed), out)
+    if n < 0:
+        raise ValueError(f"sample_candidates failed ({n})")
+    return [_camera_from(out[i]) for i in range(n)]
+
+
+def vis_coverage(occ, views) -> float:
+    """vis_coverage (planner.hpp:155-184)"""
+    lib().gor_vis_coverage.restype = C.c_double
+    rects, nr = _rects(occ)
+    return lib().gor_vis_coverage(rects, nr, C.c_double(occ.sample_density), cameras_array(views), len(views))

@@ -49,6 +49,24 @@ class DensityConfigC(C.Structure):
     _fields_ = [("rho", C.c_double), ("eta", C.c_double), ("eps_v", C.c_double), ("seed", C.c_uint64)]
 
 
+class OccluderRectC(C.Structure):
+    _fields_ = [("corner", C.c_double * 3), ("edge_u", C.c_double * 3), ("edge_v", C.c_double * 3),
+                ("opaque", C.c_int32), ("_pad", C.c_int32)]
+
+
+class PlannerConfigC(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("num_candidates", C.c_int32), ("se2_height", C.c_double),
+                ("steps", C.c_int32), ("look_inward", C.c_int32), ("seed", C.c_uint64),
+                ("clearance", C.c_double), ("cam_width", C.c_int32), ("cam_height", C.c_int32),
+                ("fov_h", C.c_double), ("fov_v", C.c_double), ("cam_near", C.c_double)]
+
+
+class MappingConfigC(C.Structure):
+    _fields_ = [("kappa", C.c_double), ("field_degree", C.c_int32), ("density_enabled", C.c_int32),
+                ("raster", RasterConfigC), ("uncertainty", UncertaintyConfigC),
+                ("density", DensityConfigC)]
+
+
 # Every symbol include/gavis_b200.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = [
     "gavis_abi_version", "gavis_last_error", "gavis_ctx_create", "gavis_ctx_destroy",
@@ -60,7 +78,8 @@ EXPORTS = [
     "gavis_vf_accumulate_views", "gavis_vf_accumulate_visibility", "gavis_vf_upload",
     "gavis_vf_download", "gavis_vf_set_num_views", "gavis_vf_device_gamma", "gavis_vf_destroy",
     "gavis_single_view_visibility", "gavis_vf_query", "gavis_vf_query_view", "gavis_ua_render",
-    "gavis_select_nbv", "gavis_nbv_loop", "gavis_density_control", "gavis_ply_info",
+    "gavis_select_nbv", "gavis_nbv_loop", "gavis_density_control", "gavis_sample_candidates",
+    "gavis_vis_coverage", "gavis_active_mapping", "gavis_ply_info",
     "gavis_read_splat_ply", "gavis_field_json_write", "gavis_field_json_read", "gavis_debug_project", "gavis_debug_binning",
 ]
 

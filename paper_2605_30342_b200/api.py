@@ -10,6 +10,9 @@ Names, argument meaning and error behaviour follow the reference:
   render_entropy(_core)    uncertainty.hpp:124-260
   image_entropy            uncertainty.hpp:264-278
   select_nbv               planner.hpp:117-137
+  sample_candidates        planner.hpp:56-107
+  vis_coverage             planner.hpp:155-184
+  active_mapping           planner.hpp:284-316 (run_active_mapping)
 ParameterError / InvariantError are raised where the reference throws them.
 Everything runs on the GPU through libgavis_b200.so; there is no CPU path.
 """
@@ -21,8 +24,9 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import _native as N
-from .model import (CameraView, EntropyMap, NbvResult, ParameterError, RasterConfig, RenderOutput,
-                    Scene, UncertaintyConfig, ViewQuery, VisibilityField, VmfParams, require)
+from .model import (CameraView, EntropyMap, MappingLog, MappingStep, NbvResult, OccluderSet, ParameterError,
+                    PlannerConfig, RasterConfig, RenderOutput, Scene, UncertaintyConfig, ViewQuery,
+                    VisibilityField, VmfParams, require)
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -415,6 +419,92 @@ def nbv_loop(ctx: Context, scene, field: DeviceField, candidates: Sequence[Camer
                                    C.byref(raster_c(rc)), C.byref(unc_c(uc)), C.c_int32(1 if with_rgb else 0),
                                    _ptr(chosen), _ptr(best), _ptr(allsc)))
     return chosen[:steps], best[:steps], allsc[:steps]
+
+
+# ------------------------------------------------------------------ planner
+def camera_from_c(c: N.Camera) -> CameraView:
+    return CameraView(rotation=np.array(list(c.rotation), np.float64).reshape(3, 3),
+                      position=np.array(list(c.position), np.float64), width=int(c.width),
+                      height=int(c.height), fov_h=float(c.fov_h), fov_v=float(c.fov_v),
+                      near=float(c.near_plane))
+
+
+def _rects_c(occluders: Optional[OccluderSet]):
+    rects = occluders.rectangles if occluders is not None else []
+    arr = (N.OccluderRectC * max(1, len(rects)))()
+    for i, r in enumerate(rects):
+        for k in range(3):
+            arr[i].corner[k] = float(r.corner[k])
+            arr[i].edge_u[k] = float(r.edge_u[k])
+            arr[i].edge_v[k] = float(r.edge_v[k])
+        arr[i].opaque = 1 if r.opaque else 0
+    return arr, len(rects)
+
+
+def _planner_c(pc: PlannerConfig) -> N.PlannerConfigC:
+    return N.PlannerConfigC(int(pc.mode), int(pc.num_candidates), float(pc.se2_height), int(pc.steps),
+                            1 if pc.look_inward else 0, int(pc.seed), float(pc.clearance), int(pc.cam_width),
+                            int(pc.cam_height), float(pc.fov_h), float(pc.fov_v), float(pc.cam_near))
+
+
+def sample_candidates(bounds, occluders: Optional[OccluderSet], pc: PlannerConfig, step_seed: int) -> List[CameraView]:
+    """sample_candidates (planner.hpp:56-107): host-side rejection sampling in the
+    native library (no device needed). bounds = (min[3], max[3])."""
+    lib = N.load()
+    bmin = np.ascontiguousarray(bounds[0], np.float64)
+    bmax = np.ascontiguousarray(bounds[1], np.float64)
+    rects, nr = _rects_c(occluders)
+    out = (N.Camera * max(1, int(pc.num_candidates)))()
+    N.check(lib.gavis_sample_candidates(_ptr(bmin), _ptr(bmax), rects, C.c_int32(nr), C.byref(_planner_c(pc)),
+                                        C.c_uint64(int(step_seed) & (2 ** 64 - 1)), out))
+    return [camera_from_c(out[i]) for i in range(int(pc.num_candidates))]
+
+
+def vis_coverage(occluders: OccluderSet, views: Sequence[CameraView]) -> float:
+    """vis_coverage (planner.hpp:155-184), host-side in the native library."""
+    lib = N.load()
+    rects, nr = _rects_c(occluders)
+    arr = cameras_c(views)
+    cov = C.c_double()
+    N.check(lib.gavis_vis_coverage(rects, C.c_int32(nr), C.c_double(float(occluders.sample_density)), arr,
+                                   C.c_int32(len(views)), C.byref(cov)))
+    return cov.value
+
+
+def active_mapping(ctx: Context, scene, occluders: Optional[OccluderSet], init: Sequence[CameraView],
+                   pc: PlannerConfig, vmf: VmfParams = VmfParams(1.0), field_degree: int = 2,
+                   rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(),
+                   density: Optional["DensityControlConfig"] = None, density_enabled: bool = True,
+                   bounds=None) -> MappingLog:
+    """run_active_mapping (planner.hpp:284-316): per step density control (reseeded
+    with derive_seed(density.seed, step)), field rebuild over the trajectory,
+    sample_candidates(derive_seed(pc.seed, step)), select_nbv, append. Device work
+    through the C ABI; the loop itself is native (gavis_active_mapping)."""
+    ds = _as_dev(ctx, scene)
+    density = density or DensityControlConfig()
+    bmin, bmax = bounds if bounds is not None else ds.bounds
+    bmin = np.ascontiguousarray(bmin, np.float64)
+    bmax = np.ascontiguousarray(bmax, np.float64)
+    rects, nr = _rects_c(occluders)
+    steps, nc = int(pc.steps), int(pc.num_candidates)
+    mc = N.MappingConfigC(float(vmf.kappa), int(field_degree), 1 if density_enabled else 0, raster_c(rc), unc_c(uc),
+                          N.DensityConfigC(float(density.rho), float(density.eta), float(density.eps_v),
+                                           int(density.seed)))
+    views = (N.Camera * max(1, steps))()
+    idx = np.zeros(max(1, steps), np.int32)
+    best = np.zeros(max(1, steps))
+    allsc = np.zeros((max(1, steps), nc))
+    cov = np.zeros(max(1, steps))
+    ment = np.zeros(max(1, steps))
+    init_arr = cameras_c(init)
+    sd = occluders.sample_density if occluders is not None else 64.0
+    N.check(ctx.lib.gavis_active_mapping(ctx.h, ds.h, _ptr(bmin), _ptr(bmax), rects, C.c_int32(nr), C.c_double(sd),
+                                         init_arr, C.c_int32(len(init)), C.byref(_planner_c(pc)), C.byref(mc), views,
+                                         _ptr(idx), _ptr(best), _ptr(allsc), _ptr(cov), _ptr(ment)))
+    log = MappingLog([camera_from_c(views[i]) for i in range(steps)], [])
+    for i in range(steps):
+        log.steps.append(MappingStep(allsc[i].copy(), int(idx[i]), float(best[i]), float(cov[i]), float(ment[i])))
+    return log
 
 
 # ------------------------------------------------------------------ formats

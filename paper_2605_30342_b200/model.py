@@ -270,3 +270,57 @@ class NbvResult:
     """planner.hpp:109-112"""
     best_index: int
     scores: np.ndarray
+
+
+@dataclass
+class OccluderRect:
+    """model.hpp:141-150: corner + u edge_u + v edge_v, u, v in [0, 1]."""
+    corner: Sequence[float] = (0.0, 0.0, 0.0)
+    edge_u: Sequence[float] = (1.0, 0.0, 0.0)
+    edge_v: Sequence[float] = (0.0, 1.0, 0.0)
+    opaque: bool = True
+
+
+@dataclass
+class OccluderSet:
+    """model.hpp:152-155"""
+    rectangles: List[OccluderRect] = field(default_factory=list)
+    sample_density: float = 64.0  # surface samples per unit area
+
+
+@dataclass
+class PlannerConfig:
+    """planner.hpp:24-42; mode 0 = kSe3, 1 = kSe2."""
+    mode: int = 0
+    num_candidates: int = 128
+    se2_height: float = 1.5
+    steps: int = 10
+    seed: int = 0
+    look_inward: bool = True
+    clearance: float = 0.1
+    cam_width: int = 128
+    cam_height: int = 128
+    fov_h: float = K_PI / 2.0
+    fov_v: float = K_PI / 2.0
+    cam_near: float = 0.05
+
+    def validate(self) -> None:
+        require(self.num_candidates >= 1, "num_candidates must be at least 1")
+        require(self.steps >= 0, "steps must be non-negative")
+
+
+@dataclass
+class MappingStep:
+    """planner.hpp:264-270"""
+    scores: np.ndarray
+    chosen_index: int
+    score: float
+    vis_coverage: float
+    mean_entropy: float
+
+
+@dataclass
+class MappingLog:
+    """planner.hpp:272-275"""
+    chosen_views: List[CameraView]
+    steps: List[MappingStep]

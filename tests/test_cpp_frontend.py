@@ -29,3 +29,37 @@ def test_cpp_frontend_select_nbv_kat(tmp_path):
     r = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "best 1" in r.stdout
+
+
+def _build_planner(tmp_path):
+    from paper_2605_30342_b200 import build
+    build.build()
+    exe = str(tmp_path / "cpp_planner")
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "cpp_planner.cpp"), "-L", os.path.join(ROOT, "paper_2605_30342_b200"),
+           "-lgavis_b200", "-Wl,-rpath," + os.path.join(ROOT, "paper_2605_30342_b200"), "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_cpp_planner_host_parts_match_python(tmp_path):
+    """sample_candidates / vis_coverage from C++ equal the Python mirror (same library)."""
+    from paper_2605_30342_b200 import api
+    from paper_2605_30342_b200.model import OccluderRect, OccluderSet, PlannerConfig
+    r = subprocess.run([_build_planner(tmp_path)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = r.stdout.split("\n")
+    occ = OccluderSet([OccluderRect((1, -1, 0), (0, 3, 0), (0, 0, 2.5))], sample_density=16.0)
+    pc = PlannerConfig(num_candidates=4, steps=2, cam_width=32, cam_height=32)
+    cands = api.sample_candidates(((-1, -1, 0), (3, 2, 2.5)), occ, pc, 7)
+    for cam, line in zip(cands, lines[:4]):
+        vals = [float(x) for x in line.split()[1:]]
+        assert vals == [cam.position[0], cam.position[1], cam.position[2], cam.rotation[0, 0]]
+    assert float(lines[4].split()[1]) == api.vis_coverage(occ, cands)
+
+
+@pytest.mark.gpu
+def test_cpp_planner_active_mapping_runs(tmp_path):
+    r = subprocess.run([_build_planner(tmp_path), "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("step chosen") == 2
