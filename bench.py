@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="candidates in the CPU sample")
     p.add_argument("--no-extra-vf", action="store_true", help="skip the config-2/4 VF-build timings")
+    p.add_argument("--precision", default="certified", choices=["certified", "exact"],
+                   help="UA blend arithmetic (certified fp32 + fp64 redo, or fp64 throughout)")
     return p.parse_args()
 
 
@@ -227,6 +229,7 @@ def run_ours(args):
     c = make_config(args.config, world, args.per_gpu, args.particles)
     scene = c["scene"]
     ctx = api.Context(local)
+    ctx.set_precision(args.precision)
     ds = ctx.upload(scene)
     vmf = VmfParams(1.0)
     degree = c["degree"]
@@ -277,8 +280,10 @@ def run_ours(args):
     for _ in range(args.warmup):
         res = step()
     ctx.set_profiling(True)
-    for k in ("ua_blend", "preprocess", "sort", "emit_keys", "ranges", "scan", "score"):
+    KERNELS = ("ua_blend", "ua_redo", "preprocess", "sort", "emit_keys", "ranges", "scan", "score")
+    for k in KERNELS:
         ctx.kernel_time(k, reset=True)
+    redo0, resc0 = ctx.counters()
     barrier(ctx, dist)
     clocks = ClockSampler(local)
     clocks.start()
@@ -290,8 +295,11 @@ def run_ours(args):
     launches = ctx.launch_count() - l0
     barrier(ctx, dist)
     clk = clocks.stop()
-    ktimes = {k: ctx.kernel_time(k) for k in ("ua_blend", "preprocess", "sort", "emit_keys", "ranges",
-                                                  "scan", "score")}
+    ktimes = {k: ctx.kernel_time(k) for k in KERNELS}
+    redo1, resc1 = ctx.counters()
+    certified = {"redo_pixels_per_view": (redo1 - redo0) / float(len(cands) * args.steps),
+                 "redo_fraction": (redo1 - redo0) / float(len(cands) * args.steps * cands[0].width * cands[0].height),
+                 "rescored_candidates_per_step": (resc1 - resc0) / float(args.steps)}
     ctx.set_profiling(False)
     ms_max = max_over_ranks(ms, dist)
     total_cands = sum_over_ranks(float(len(cands) * args.steps), dist)
@@ -412,14 +420,19 @@ def run_ours(args):
             pj = json.load(f)
         traffic = pj["traffic_bytes_per_launch"] * views_per_launch / pj["views_per_launch"]
         traffic_src = f"{pj['command']} ({pj['views_per_launch']} views/launch)"
-        compute = {"bound": "fp64 issue/latency", "fp64_pipe_active_pct": pj["fp64_pipe_active_pct"],
+        compute = {"bound": pj.get("compute_bound", "issue/latency"),
+                   "fp64_pipe_active_pct": pj["fp64_pipe_active_pct"],
                    "issue_slots_busy_pct": pj["issue_slots_busy_pct"], "source": "same ncu capture"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "certified" else "f64",
+            "precision": args.precision if args.precision == "exact" else
+            "certified (fp32 blend, fp64 q; fp64 redo of uncertified pixels; exact argmax)",
+            "certified": certified if args.precision == "certified" else None,
             "data": "synthetic (seeded config generator; paper datasets not in the container)",
             "config": {"workload": f"config{args.config}", "particles": N, "resolution": [cands[0].width, cands[0].height],
                        "candidates_per_gpu_per_step": len(cands), "training_views": len(train),

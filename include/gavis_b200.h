@@ -102,11 +102,26 @@ gavis_status gavis_ctx_destroy(gavis_ctx* ctx);
 gavis_status gavis_ctx_synchronize(gavis_ctx* ctx);
 /* Views processed per launch batch (0 = automatic from free memory). */
 gavis_status gavis_ctx_set_batch(gavis_ctx* ctx, int32_t max_views_per_batch);
+/* Arithmetic of the UA render (gavis_ua_render, gavis_select_nbv, loops):
+ *  GAVIS_PRECISION_CERTIFIED (default): fp32 blend with a per-pixel error bound
+ *    on the early-termination tests; pixels the bound cannot certify are
+ *    recomputed in fp64, so contributor counts equal the fp64 reference's;
+ *    images agree with it to ~1e-6 (north_star: 1e-4); select_nbv re-scores in
+ *    fp64 every candidate within 1e-4 (relative) of the best, so the argmax is
+ *    the fp64 one. Used for 16x16 tiles and alpha_clamp_max <= 0.999.
+ *  GAVIS_PRECISION_EXACT: every blend in fp64 with the reference's operation
+ *    order (images to ~1e-12 of the reference). */
+enum { GAVIS_PRECISION_CERTIFIED = 0, GAVIS_PRECISION_EXACT = 1 };
+gavis_status gavis_ctx_set_precision(gavis_ctx* ctx, int32_t precision);
+/* Counters since context creation: pixels recomputed in fp64 by the certified
+ * blend, candidates re-scored in fp64 to certify an argmax. Either may be NULL. */
+gavis_status gavis_ctx_get_counters(gavis_ctx* ctx, int64_t* redo_pixels,
+                                    int64_t* rescored_views);
 /* Per-kernel CUDA-event timing on the context stream (off by default). */
 gavis_status gavis_ctx_set_profiling(gavis_ctx* ctx, int32_t enabled);
 /* Accumulated device milliseconds and launch count of a kernel family:
  * "preprocess", "emit_keys", "sort", "ranges", "vf_blend", "vf_finalize",
- * "ua_blend", "score", "query". Resets when reset != 0. */
+ * "ua_blend", "ua_redo", "score", "query". Resets when reset != 0. */
 gavis_status gavis_ctx_kernel_time(gavis_ctx* ctx, const char* kernel, double* ms,
                                    int64_t* launches, int32_t reset);
 /* Device-side stopwatch on the context stream (bench timing). */

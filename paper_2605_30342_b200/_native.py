@@ -70,7 +70,8 @@ class MappingConfigC(C.Structure):
 # Every symbol include/gavis_b200.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = [
     "gavis_abi_version", "gavis_last_error", "gavis_ctx_create", "gavis_ctx_destroy",
-    "gavis_ctx_synchronize", "gavis_ctx_set_batch", "gavis_ctx_set_profiling",
+    "gavis_ctx_synchronize", "gavis_ctx_set_batch", "gavis_ctx_set_precision",
+    "gavis_ctx_get_counters", "gavis_ctx_set_profiling",
     "gavis_ctx_kernel_time", "gavis_ctx_timer_start", "gavis_ctx_timer_stop",
     "gavis_ctx_launch_count", "gavis_scene_upload", "gavis_scene_destroy",
     "gavis_scene_set_coeff_variances",
@@ -82,6 +83,9 @@ EXPORTS = [
     "gavis_vis_coverage", "gavis_active_mapping", "gavis_ply_info",
     "gavis_read_splat_ply", "gavis_field_json_write", "gavis_field_json_read", "gavis_debug_project", "gavis_debug_binning",
 ]
+
+PRECISION_CERTIFIED = 0
+PRECISION_EXACT = 1
 
 _lib = None
 

@@ -19,6 +19,7 @@ Everything runs on the GPU through libgavis_b200.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from typing import Dict, List, Optional, Sequence
 
 import numpy as np
@@ -79,9 +80,18 @@ class Context:
                                           C.byref(h)))
         self.h = h
         self.device = device
+        # device objects of this context, released before it (the C ABI requires
+        # scenes and fields to be destroyed before their context)
+        self._children = weakref.WeakSet()
 
     def close(self) -> None:
         if self.h:
+            kids = list(self._children)
+            for k in kids:
+                if isinstance(k, DeviceField):
+                    k.close()
+            for k in kids:
+                k.close()
             N.check(self.lib.gavis_ctx_destroy(self.h))
             self.h = None
 
@@ -102,6 +112,21 @@ class Context:
 
     def set_batch(self, n: int) -> None:
         N.check(self.lib.gavis_ctx_set_batch(self.h, C.c_int32(n)))
+
+    def set_precision(self, precision: str) -> None:
+        """'certified' (default: fp32 blend, fp64 redo of uncertified pixels,
+        exact argmax) or 'exact' (fp64 throughout)."""
+        modes = {"certified": N.PRECISION_CERTIFIED, "exact": N.PRECISION_EXACT}
+        require(precision in modes, "precision must be 'certified' or 'exact'")
+        N.check(self.lib.gavis_ctx_set_precision(self.h, C.c_int32(modes[precision])))
+
+    def counters(self):
+        """(pixels recomputed in fp64 by the certified blend, candidates re-scored
+        in fp64 to certify an argmax) since the context was created."""
+        a = C.c_int64()
+        b = C.c_int64()
+        N.check(self.lib.gavis_ctx_get_counters(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def set_profiling(self, on: bool) -> None:
         N.check(self.lib.gavis_ctx_set_profiling(self.h, C.c_int32(1 if on else 0)))
@@ -142,6 +167,7 @@ class DeviceScene:
         h = C.c_void_p()
         N.check(ctx.lib.gavis_scene_upload(ctx.h, C.byref(d), C.byref(h)))
         self.h = h
+        ctx._children.add(self)
 
     def set_coeff_variances(self, variances, degree: int) -> None:
         """UncertaintyConfig::coeff_variances for the sh_propagation provider:
@@ -154,12 +180,13 @@ class DeviceScene:
     def _adopt(cls, ctx: Context, handle, n: int, color_degree: int, bounds) -> "DeviceScene":
         obj = cls.__new__(cls)
         obj.ctx, obj.h, obj.n, obj.color_degree, obj.bounds = ctx, handle, n, color_degree, bounds
+        ctx._children.add(obj)
         return obj
 
     def close(self) -> None:
-        if self.h:
+        if self.h and self.ctx.h:
             N.check(self.ctx.lib.gavis_scene_destroy(self.h))
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
@@ -182,6 +209,7 @@ class DeviceField:
         self.h = handle
         self.degree = degree
         self.vmf = vmf
+        ctx._children.add(self)
 
     @property
     def num_views(self) -> int:
@@ -206,9 +234,9 @@ class DeviceField:
         return p.value, n.value
 
     def close(self) -> None:
-        if self.h:
+        if self.h and self.ctx.h:
             N.check(self.ctx.lib.gavis_vf_destroy(self.h))
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:

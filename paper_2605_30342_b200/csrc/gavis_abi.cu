@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -48,8 +49,10 @@ void invariant(bool cond, const std::string& msg) {
 #define CK(expr)                                                                        \
   do {                                                                                  \
     cudaError_t e_ = (expr);                                                            \
-    if (e_ != cudaSuccess)                                                              \
+    if (e_ != cudaSuccess) {                                                            \
+      (void)cudaGetLastError(); /* do not leak a non-sticky error into later calls */   \
       throw DevErr(std::string(#expr) + " failed: " + cudaGetErrorString(e_));          \
+    }                                                                                   \
   } while (0)
 
 template <class F>
@@ -207,6 +210,9 @@ struct gavis_ctx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int64_t launches = 0;
   int32_t* pinned = nullptr;
+  int precision = GAVIS_PRECISION_CERTIFIED;
+  int64_t redo_pixels = 0;       // pixels the certified blend handed to the fp64 redo
+  int64_t rescored_views = 0;    // candidates re-scored exactly to certify an argmax
   std::recursive_mutex mu;
 
   void use() { CK(cudaSetDevice(device)); }
@@ -228,6 +234,22 @@ struct gavis_ctx {
       b.bytes = want;
     }
     return b.p;
+  }
+
+  // Stream-ordered allocations from the device pool (released to the pool, not
+  // the driver: repeated scene/field uploads do not pay cudaMalloc/cudaFree).
+  void* dalloc(size_t bytes, const char* what) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(bytes, 16), stream);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw DevErr(std::string("cudaMallocAsync(") + std::to_string(bytes) + ") for " + what +
+                   " failed: " + cudaGetErrorString(e));
+    }
+    return p;
+  }
+  void dfree(void* p) {
+    if (p) cudaFreeAsync(p, stream);
   }
 
   cudaEvent_t event() {
@@ -564,6 +586,19 @@ void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t count) {
     CK(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
 }
 
+// Certification window of the fp32 blend, relative to the cutoff: twice the
+// bound u (16 + 4.2 k + 22 S) derived in kernels_ua_fast.cu (k composited
+// entries, S = sum a/(1-a) over them).
+void cert_window(UaBlendArgs* ua) {
+  const double u = std::ldexp(1.0, -24);
+  ua->cert_base = (float)(2.0 * u * 16.0);
+  ua->cert_per_step = (float)(2.0 * u * 4.2);
+  ua->cert_sum = (float)(2.0 * u * 22.0);
+  // test hook (tests/test_certified.py): hand every pixel to the fp64 redo
+  const char* force = std::getenv("GAVIS_CERT_FORCE_REDO");
+  if (force && force[0] == '1') ua->cert_base = 3.0e38f;
+}
+
 void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const double* vis_host,
                const gavis_camera* cams, int n, const gavis_raster_config* rc,
                const gavis_uncertainty_config* uc, gavis_render_outputs* out) {
@@ -636,7 +671,8 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     ua.do_rgb = do_rgb;
     ua.do_ent = do_ent;
     // The RGB and entropy images always land in device memory (host copies only
-    // when requested); depth and residual-transmittance maps only on request.
+    // when requested; the score folds the entropy image); depth and
+    // residual-transmittance maps only on request.
     if (do_rgb) {
       ua.rgb = (double*)c->buf("img_rgb", sizeof(double) * 3 * P);
       ua.depth = out->depth ? (double*)c->buf("img_depth", sizeof(double) * P) : nullptr;
@@ -646,18 +682,32 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     if (do_ent) {
       ua.entropy = (double*)c->buf("img_entropy", sizeof(double) * P);
       ua.w0 = (double*)c->buf("img_w0", sizeof(double) * P);
-      ua.edepth = out->entropy_depth ? (double*)c->buf("img_edepth", sizeof(double) * P) : nullptr;
+      ua.edepth = (out->entropy_depth || ua.corr_lambda > 0.0)
+                      ? (double*)c->buf("img_edepth", sizeof(double) * P)
+                      : nullptr;
       if (out->entropy_contributors)
         ua.ent_contrib = (int32_t*)c->buf("img_nent", sizeof(int32_t) * P);
-      ua.tile_score = (double*)c->buf(
-          "tile_score", sizeof(double) * ua_score_parts(rc->tile_size) * std::max<int64_t>(1, b.total_tiles));
     }
-    c->run("ua_blend", [&] { launch_ua_blend(ua, c->stream); }, b.total_tiles > 0 ? 1 : 0);
+    const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED &&
+                      ua_fast_supported(rc->tile_size, rc->alpha_clamp_max);
+    if (fast && b.total_tiles > 0) {
+      invariant(P < (int64_t(1) << 32), "too many pixels in one batch");
+      ua.flag_list = (uint32_t*)c->buf("flag_list", sizeof(uint32_t) * P);
+      ua.flag_count = (uint32_t*)c->buf("flag_count", sizeof(uint32_t));
+      CK(cudaMemsetAsync(ua.flag_count, 0, sizeof(uint32_t), c->stream));
+      cert_window(&ua);
+      c->run("ua_blend", [&] { launch_ua_blend_fast(ua, c->stream); });
+      c->run("ua_redo", [&] { launch_ua_redo(ua, c->stream); });
+      CK(cudaMemcpyAsync(c->pinned + 3, ua.flag_count, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                         c->stream));
+    } else {
+      c->run("ua_blend", [&] { launch_ua_blend(ua, c->stream); }, b.total_tiles > 0 ? 1 : 0);
+    }
     double* dscores = nullptr;
     if (do_ent) {
       dscores = (double*)c->buf("scores", sizeof(double) * V);
       c->run("score", [&] {
-        launch_score(b.dcams, V, ua_score_parts(rc->tile_size), ua.tile_score, dscores, c->stream);
+        launch_score_image(b.dcams, V, ua.entropy, ua.edepth, ua.corr_lambda, dscores, c->stream);
       });
     }
     copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P);
@@ -674,8 +724,54 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       CK(cudaMemcpyAsync(out->entropy_contributors + pix_done, ua.ent_contrib,
                          sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
+    if (fast && b.total_tiles > 0) c->redo_pixels += (uint32_t)c->pinned[3];
     pix_done += P;
   }
+}
+
+// select_nbv's argmax (planner.hpp:132-136: first strictly greater score) over
+// scores from the certified fp32 blend: every candidate within kCertScoreRel
+// (relative) of the best is re-scored with the exact fp64 blend and the argmax
+// is taken again, so it is the exact path's argmax (the fp32 scores agree with
+// the fp64 ones to ~1e-7 relative, three orders of magnitude inside the window).
+constexpr double kCertScoreRel = 1e-4;
+
+int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
+                        const gavis_camera* cams, int n, const gavis_raster_config* rc,
+                        const gavis_uncertainty_config* uc, std::vector<double>& sc) {
+  auto first_max = [&] {
+    int b = 0;
+    for (int i = 1; i < n; ++i)
+      if (sc[i] > sc[b]) b = i;
+    return b;
+  };
+  int b = first_max();
+  if (c->precision != GAVIS_PRECISION_CERTIFIED ||
+      !ua_fast_supported(rc->tile_size, rc->alpha_clamp_max))
+    return b;
+  const double lo = sc[b] - kCertScoreRel * std::fabs(sc[b]);
+  std::vector<int> cont;
+  std::vector<gavis_camera> cc;
+  for (int i = 0; i < n; ++i)
+    if (sc[i] >= lo) {
+      cont.push_back(i);
+      cc.push_back(cams[i]);
+    }
+  if (cont.size() < 2) return b;
+  std::vector<double> ex(cont.size());
+  gavis_render_outputs o = {};
+  o.scores = ex.data();
+  c->precision = GAVIS_PRECISION_EXACT;
+  try {
+    ua_render(c, s, f, nullptr, cc.data(), (int)cc.size(), rc, uc, &o);
+  } catch (...) {
+    c->precision = GAVIS_PRECISION_CERTIFIED;
+    throw;
+  }
+  c->precision = GAVIS_PRECISION_CERTIFIED;
+  for (size_t k = 0; k < cont.size(); ++k) sc[cont[k]] = ex[k];
+  c->rescored_views += (int64_t)cont.size();
+  return first_max();
 }
 
 }  // namespace
@@ -714,6 +810,11 @@ gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
         c->own_stream = true;
       }
       CK(cudaMallocHost(&c->pinned, 64));
+      // keep freed scene/field memory in the device pool between uploads
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = UINT64_MAX;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
       CK(cudaEventCreate(&c->t0));
       CK(cudaEventCreate(&c->t1));
     } catch (...) {
@@ -758,6 +859,25 @@ gavis_status gavis_ctx_set_batch(gavis_ctx* c, int32_t n) {
     require(c != nullptr, "context must not be null");
     require(n >= 0 && n <= 64, "batch must lie in [0, 64]");
     c->max_batch = n;
+  });
+}
+
+gavis_status gavis_ctx_set_precision(gavis_ctx* c, int32_t precision) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    require(precision == GAVIS_PRECISION_CERTIFIED || precision == GAVIS_PRECISION_EXACT,
+            "precision must be GAVIS_PRECISION_CERTIFIED or GAVIS_PRECISION_EXACT");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->precision = precision;
+  });
+}
+
+gavis_status gavis_ctx_get_counters(gavis_ctx* c, int64_t* redo_pixels, int64_t* rescored_views) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    if (redo_pixels) *redo_pixels = c->redo_pixels;
+    if (rescored_views) *rescored_views = c->rescored_views;
   });
 }
 
@@ -832,9 +952,7 @@ gavis_status gavis_nbv_loop(gavis_ctx* c, const gavis_scene* s, gavis_field* f,
       o.scores = sc.data();
       o.with_rgb = with_rgb;
       ua_render(c, s, f, nullptr, cams, n_cams, rc, uc, &o);
-      int b = 0;
-      for (int i = 1; i < n_cams; ++i)
-        if (sc[i] > sc[b]) b = i;  // planner.hpp:132-136
+      const int b = certified_first_max(c, s, f, cams, n_cams, rc, uc, sc);  // planner.hpp:132-136
       vf_views(c, s, f, cams + b, 1, rc, nullptr, nullptr, nullptr);
       if (chosen) chosen[step] = b;
       if (scores) scores[step] = sc[b];
@@ -851,20 +969,20 @@ static gavis_scene* alloc_scene(gavis_ctx* c, int64_t n, int color_degree) {
   const int nbp = nb + (nb & 1);
   const int cstride = ((3 * nbp + 3) / 4) * 4;
   const int64_t M = std::max<int64_t>(n, 1);
-  cudaError_t e = cudaSuccess;
-  if (e == cudaSuccess) e = cudaMalloc(&s->pos_op, sizeof(float4) * M);
-  if (e == cudaSuccess) e = cudaMalloc(&s->rot, sizeof(float4) * M);
-  if (e == cudaSuccess) e = cudaMalloc(&s->scale, sizeof(float4) * M);
-  if (e == cudaSuccess) e = cudaMalloc(&s->virt, M);
-  if (e == cudaSuccess) e = cudaMalloc(&s->colors, sizeof(float) * cstride * M);
-  if (e != cudaSuccess) {
-    cudaFree(s->pos_op);
-    cudaFree(s->rot);
-    cudaFree(s->scale);
-    cudaFree(s->virt);
-    cudaFree(s->colors);
+  try {
+    s->pos_op = (float4*)c->dalloc(sizeof(float4) * M, "scene");
+    s->rot = (float4*)c->dalloc(sizeof(float4) * M, "scene");
+    s->scale = (float4*)c->dalloc(sizeof(float4) * M, "scene");
+    s->virt = (uint8_t*)c->dalloc(M, "scene");
+    s->colors = (float*)c->dalloc(sizeof(float) * cstride * M, "scene");
+  } catch (...) {
+    c->dfree(s->pos_op);
+    c->dfree(s->rot);
+    c->dfree(s->scale);
+    c->dfree(s->virt);
+    c->dfree(s->colors);
     delete s;
-    throw DevErr(std::string("cudaMalloc(scene) failed: ") + cudaGetErrorString(e));
+    throw;
   }
   s->dev.n = n;
   s->dev.color_degree = color_degree;
@@ -1028,65 +1146,56 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
               "scene arrays must not be null");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
-    auto* s = new gavis_scene();
-    s->ctx = c;
-    const int nb = (d->color_degree + 1) * (d->color_degree + 1);
+    gavis_scene* s = alloc_scene(c, N, d->color_degree);
+    const int nb = s->dev.nb;
     const int nbp = nb + (nb & 1);
-    const int cstride = ((3 * nbp + 3) / 4) * 4;
+    const int cstride = s->dev.cstride;
     try {
-      const int64_t M = std::max<int64_t>(N, 1);
-      CK(cudaMalloc(&s->pos_op, sizeof(float4) * M));
-      CK(cudaMalloc(&s->rot, sizeof(float4) * M));
-      CK(cudaMalloc(&s->scale, sizeof(float4) * M));
-      CK(cudaMalloc(&s->virt, M));
-      CK(cudaMalloc(&s->colors, sizeof(float) * cstride * M));
-      std::vector<float4> tmp((size_t)M);
-      for (int64_t i = 0; i < N; ++i)
-        tmp[i] = make_float4(d->positions[3 * i], d->positions[3 * i + 1], d->positions[3 * i + 2],
-                             d->opacities[i]);
-      CK(cudaMemcpy(s->pos_op, tmp.data(), sizeof(float4) * M, cudaMemcpyHostToDevice));
-      for (int64_t i = 0; i < N; ++i)
-        tmp[i] = make_float4(d->rotations[4 * i], d->rotations[4 * i + 1], d->rotations[4 * i + 2],
-                             d->rotations[4 * i + 3]);
-      CK(cudaMemcpy(s->rot, tmp.data(), sizeof(float4) * M, cudaMemcpyHostToDevice));
-      for (int64_t i = 0; i < N; ++i)
-        tmp[i] = make_float4(d->scales[3 * i], d->scales[3 * i + 1], d->scales[3 * i + 2], 0.f);
-      CK(cudaMemcpy(s->scale, tmp.data(), sizeof(float4) * M, cudaMemcpyHostToDevice));
-      std::vector<uint8_t> vm((size_t)M, 0);
-      if (d->is_virtual)
-        for (int64_t i = 0; i < N; ++i) vm[i] = d->is_virtual[i] ? 1 : 0;
-      CK(cudaMemcpy(s->virt, vm.data(), M, cudaMemcpyHostToDevice));
-      // device layout: per particle [3][nbp] (channel rows padded to an even count so
-      // coefficient pairs feed packed fp32x2 FMAs), particle stride cstride floats.
-      if (cstride == 3 * nb && nbp == nb) {
-        if (N > 0)
-          CK(cudaMemcpy(s->colors, d->colors, sizeof(float) * cstride * N, cudaMemcpyHostToDevice));
-      } else {
-        std::vector<float> col((size_t)(cstride * M), 0.f);
-        for (int64_t i = 0; i < N; ++i)
-          for (int k = 0; k < 3; ++k)
-            std::memcpy(&col[i * cstride + k * nbp], d->colors + i * 3 * nb + k * nb,
-                        sizeof(float) * nb);
-        CK(cudaMemcpy(s->colors, col.data(), sizeof(float) * cstride * M, cudaMemcpyHostToDevice));
+      if (N > 0) {
+        // raw host arrays -> staging buffer (DMA; pinned host memory runs at
+        // full PCIe/C2C rate), then one packing kernel builds the device layout
+        const bool direct_colors = cstride == 3 * nb && nbp == nb;
+        const size_t b_pos = sizeof(float) * 3 * N, b_op = sizeof(float) * N;
+        const size_t b_col = direct_colors ? 0 : sizeof(float) * 3 * nb * N;
+        const size_t b_virt = d->is_virtual ? (size_t)N : 0;
+        char* st = (char*)c->buf("upload_stage", 2 * b_pos + b_op + b_col + b_virt + 64);
+        float* st_pos = (float*)st;
+        float* st_scale = (float*)(st + b_pos);
+        float* st_op = (float*)(st + 2 * b_pos);
+        float* st_col = (float*)(st + 2 * b_pos + b_op);
+        uint8_t* st_virt = (uint8_t*)(st + 2 * b_pos + b_op + b_col);
+        CK(cudaMemcpyAsync(st_pos, d->positions, b_pos, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(st_scale, d->scales, b_pos, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(st_op, d->opacities, b_op, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(s->rot, d->rotations, sizeof(float4) * N, cudaMemcpyHostToDevice,
+                           c->stream));
+        if (direct_colors)
+          CK(cudaMemcpyAsync(s->colors, d->colors, sizeof(float) * cstride * N,
+                             cudaMemcpyHostToDevice, c->stream));
+        else
+          CK(cudaMemcpyAsync(st_col, d->colors, b_col, cudaMemcpyHostToDevice, c->stream));
+        if (b_virt) CK(cudaMemcpyAsync(st_virt, d->is_virtual, b_virt, cudaMemcpyHostToDevice, c->stream));
+        PackSceneArgs pk;
+        pk.n = N;
+        pk.nb = nb;
+        pk.nbp = nbp;
+        pk.cstride = cstride;
+        pk.pos = st_pos;
+        pk.op = st_op;
+        pk.scale = st_scale;
+        pk.colors = direct_colors ? nullptr : st_col;
+        pk.virt = b_virt ? st_virt : nullptr;
+        pk.pos_op = s->pos_op;
+        pk.scale4 = s->scale;
+        pk.colors_out = s->colors;
+        pk.virt_out = s->virt;
+        c->run("pack_scene", [&] { launch_pack_scene(pk, c->stream); });
       }
+      c->sync();  // the caller may release its host arrays on return
     } catch (...) {
-      cudaFree(s->pos_op);
-      cudaFree(s->rot);
-      cudaFree(s->scale);
-      cudaFree(s->virt);
-      cudaFree(s->colors);
-      delete s;
+      gavis_scene_destroy(s);
       throw;
     }
-    s->dev.n = N;
-    s->dev.color_degree = d->color_degree;
-    s->dev.nb = nb;
-    s->dev.cstride = cstride;
-    s->dev.pos_op = s->pos_op;
-    s->dev.rot = s->rot;
-    s->dev.scale = s->scale;
-    s->dev.virt = s->virt;
-    s->dev.colors = s->colors;
     *out = s;
   });
 }
@@ -1094,14 +1203,15 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
 gavis_status gavis_scene_destroy(gavis_scene* s) {
   return guard([&] {
     if (!s) return;
-    s->ctx->use();
-    cudaStreamSynchronize(s->ctx->stream);
-    cudaFree(s->pos_op);
-    cudaFree(s->rot);
-    cudaFree(s->scale);
-    cudaFree(s->virt);
-    cudaFree(s->colors);
-    cudaFree(s->var);
+    gavis_ctx* c = s->ctx;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    c->dfree(s->pos_op);
+    c->dfree(s->rot);
+    c->dfree(s->scale);
+    c->dfree(s->virt);
+    c->dfree(s->colors);
+    c->dfree(s->var);
     delete s;
   });
 }
@@ -1119,9 +1229,10 @@ gavis_status gavis_scene_set_coeff_variances(gavis_ctx* c, gavis_scene* s, const
       require(var[i] >= 0.0f, "sh_variance_propagation: negative variance entry");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
-    if (s->var) CK(cudaFree(s->var));
+    c->dfree(s->var);
     s->var = nullptr;
-    CK(cudaMalloc(&s->var, sizeof(float) * 3 * nbv * std::max<int64_t>(1, N)));
+    s->var = nullptr;
+    s->var = (float*)c->dalloc(sizeof(float) * 3 * nbv * std::max<int64_t>(1, N), "coeff_variances");
     if (N > 0)
       CK(cudaMemcpy(s->var, var, sizeof(float) * 3 * nbv * N, cudaMemcpyHostToDevice));
     s->var_degree = degree;
@@ -1147,10 +1258,11 @@ static gavis_field* new_field(gavis_ctx* c, const gavis_scene* s, double kappa, 
   f->kappa = kappa;
   const int nb = (degree + 1) * (degree + 1);
   const size_t bytes = sizeof(double) * nb * std::max<int64_t>(1, f->n);
-  cudaError_t e = cudaMalloc(&f->gamma, bytes);
-  if (e != cudaSuccess) {
+  try {
+    f->gamma = (double*)c->dalloc(bytes, "field");
+  } catch (...) {
     delete f;
-    throw DevErr(std::string("cudaMalloc(field) failed: ") + cudaGetErrorString(e));
+    throw;
   }
   CK(cudaMemsetAsync(f->gamma, 0, bytes, c->stream));
   return f;
@@ -1182,7 +1294,7 @@ gavis_status gavis_vf_construct(gavis_ctx* c, const gavis_scene* s, const gavis_
     try {
       vf_views(c, s, f, views, n_views, rc, nullptr, nullptr, nullptr);
     } catch (...) {
-      cudaFree(f->gamma);
+      c->dfree(f->gamma);
       delete f;
       throw;
     }
@@ -1290,9 +1402,10 @@ gavis_status gavis_vf_device_gamma(gavis_field* f, void** ptr, int64_t* count) {
 gavis_status gavis_vf_destroy(gavis_field* f) {
   return guard([&] {
     if (!f) return;
-    f->ctx->use();
-    cudaStreamSynchronize(f->ctx->stream);
-    cudaFree(f->gamma);
+    gavis_ctx* c = f->ctx;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    c->dfree(f->gamma);
     delete f;
   });
 }
@@ -1403,9 +1516,7 @@ gavis_status gavis_select_nbv(gavis_ctx* c, const gavis_scene* s, const gavis_fi
     o.scores = sc.data();
     o.with_rgb = with_rgb;
     ua_render(c, s, f, nullptr, cams, n_cams, rc, uc, &o);
-    int b = 0;
-    for (int i = 1; i < n_cams; ++i)
-      if (sc[i] > sc[b]) b = i;
+    const int b = certified_first_max(c, s, f, cams, n_cams, rc, uc, sc);
     if (scores) std::memcpy(scores, sc.data(), sizeof(double) * n_cams);
     if (best) *best = b;
   });

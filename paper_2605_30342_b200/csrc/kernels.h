@@ -127,6 +127,14 @@ struct UaBlendArgs {
   double* tile_score = nullptr;  // [total_tiles] per-tile entropy sum
   double corr_lambda = 0.0;      // > 0: correlation hook in the image score
   bool do_rgb = true, do_ent = true;
+  // Certified fp32 path (kernels_ua_fast.cu): pixels whose early-termination
+  // decision the fp32 error bound cannot certify are appended to flag_list
+  // (batch pixel index) and recomputed by the fp64 redo kernel.
+  uint32_t* flag_list = nullptr;   // [total_pix]
+  uint32_t* flag_count = nullptr;  // [1]
+  float cert_base = 0.f;           // relative window, constant part
+  float cert_per_step = 0.f;       // relative window per composited entry
+  float cert_sum = 0.f;            // relative window per unit of sum a/(1-a)
 };
 
 struct QueryArgs {
@@ -140,12 +148,36 @@ struct QueryArgs {
   double* out = nullptr;
 };
 
+struct PackSceneArgs {
+  int64_t n = 0;
+  int nb = 1, nbp = 2, cstride = 8;
+  const float* pos = nullptr;     // [n][3]
+  const float* op = nullptr;      // [n]
+  const float* scale = nullptr;   // [n][3]
+  const float* colors = nullptr;  // [n][3][nb], or null: colours copied directly
+  const uint8_t* virt = nullptr;  // [n] or null
+  float4* pos_op = nullptr;
+  float4* scale4 = nullptr;
+  float* colors_out = nullptr;
+  uint8_t* virt_out = nullptr;
+};
+
+void launch_pack_scene(const PackSceneArgs& a, cudaStream_t s);
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 void launch_emit_keys(const EmitArgs& a, cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s);
 void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s);
 void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s);
+// Certified fp32 blend (16x16 tiles, alpha_clamp_max <= 0.999) + the fp64 redo
+// of the flagged pixels; same outputs as launch_ua_blend (tile_score unused).
+bool ua_fast_supported(int tile_size, double amax);
+void launch_ua_blend_fast(const UaBlendArgs& a, cudaStream_t s);
+void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s);
+// image_entropy per view: fixed-order fold of the per-pixel entropy image
+// (with the correlation hook when corr_lambda > 0; edepth must then be set).
+void launch_score_image(const DevCam* cams, int V, const double* entropy, const double* edepth,
+                        double corr_lambda, double* scores, cudaStream_t s);
 // Entropy partials per tile written by the UA blend (8 patches per 16x16 tile).
 int ua_score_parts(int tile_size);
 void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,

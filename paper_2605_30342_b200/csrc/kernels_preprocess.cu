@@ -18,6 +18,7 @@ constexpr int kMaxBatchViews = 64;
 
 struct Sigma {
   double s00, s01, s02, s11, s12, s22;
+  double trace;  // >= lambda_max(Sigma): bounds the screen radius before projecting Sigma
 };
 
 // GaussianParticle::covariance (model.hpp:42-45), Eigen toRotationMatrix order.
@@ -41,6 +42,7 @@ __device__ __forceinline__ Sigma covariance(float4 q, float4 sc) {
   s.s11 = m10 * m10 + m11 * m11 + m12 * m12;
   s.s12 = m10 * m20 + m11 * m21 + m12 * m22;
   s.s22 = m20 * m20 + m21 * m21 + m22 * m22;
+  s.trace = s.s00 + s.s11 + s.s22;
   return s;
 }
 
@@ -63,6 +65,15 @@ __device__ __forceinline__ bool project(const DevCam& c, double px, double py, d
   double ux = t0 * inv_z, uy = t1 * inv_z;
   ux = ux < -c.limx ? -c.limx : (c.limx < ux ? c.limx : ux);
   uy = uy < -c.limy ? -c.limy : (c.limy < uy ? c.limy : uy);
+  {
+    // Frustum pre-test: lambda_max(cov2) <= trace(J Sigma J^T) + 2 dil^2 <=
+    // trace(Sigma) |J|_F^2 + 2 dil^2, so r <= rub; a particle outside the
+    // frustum by more than rub is culled below anyway -- skip projecting Sigma.
+    const double gx = fx * inv_z, gy = fy * inv_z;
+    const double jf = gx * gx * (1.0 + ux * ux) + gy * gy * (1.0 + uy * uy);
+    const double rub = 3.0 * sqrt((S.trace * jf + 2.0 * dilation * dilation) * 1.000001) + 1e-9;
+    if (mx < -rub || mx > c.width + rub || my < -rub || my > c.height + rub) return false;
+  }
   const double jx = ux * t2;
   const double jy = uy * t2;
   // W = R^T, cov_cam = (W Sigma) W^T ; W(r,k) = R(k,r) = c.R[k*3+r]
@@ -354,6 +365,30 @@ void launch_emit_keys(const EmitArgs& a, cudaStream_t s) {
 void launch_ranges(const RangesArgs& a, cudaStream_t s) {
   if (a.K == 0) return;
   ranges_kernel<<<blocks_for(a.K, 256), 256, 0, s>>>(a);
+}
+
+// Scene upload: host SoA (positions [N][3], opacities [N], scales [N][3],
+// colours [N][3][nb], is_virtual [N]) staged raw in device memory -> the device
+// layout (float4 pos|opacity, float4 scale, colour rows padded to nbp, 0/1 mask).
+__global__ void pack_scene_kernel(PackSceneArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  a.pos_op[i] = make_float4(a.pos[3 * i], a.pos[3 * i + 1], a.pos[3 * i + 2], a.op[i]);
+  a.scale4[i] = make_float4(a.scale[3 * i], a.scale[3 * i + 1], a.scale[3 * i + 2], 0.f);
+  a.virt_out[i] = a.virt ? (a.virt[i] ? 1 : 0) : 0;
+  if (a.colors) {
+    float* dst = a.colors_out + i * a.cstride;
+    const float* src = a.colors + i * 3 * a.nb;
+    for (int k = 0; k < a.cstride; ++k) {
+      const int ch = k / a.nbp, m = k - ch * a.nbp;
+      dst[k] = (ch < 3 && m < a.nb) ? src[ch * a.nb + m] : 0.f;
+    }
+  }
+}
+
+void launch_pack_scene(const PackSceneArgs& a, cudaStream_t s) {
+  if (a.n == 0) return;
+  pack_scene_kernel<<<(unsigned)((a.n + 255) / 256), 256, 0, s>>>(a);
 }
 
 void launch_query(const QueryArgs& a, cudaStream_t s) {

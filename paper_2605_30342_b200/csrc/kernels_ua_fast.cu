@@ -1,0 +1,541 @@
+// kernels_ua_fast.cu -- certified fp32 UA blend (K7f), its fp64 redo (K7r) and
+// the image score (K8).
+//
+// K7f computes the same two tracks as the exact fp64 kernel (kernels_ua.cu;
+// rasterize raster.hpp:191-229 and render_entropy_core uncertainty.hpp:177-236)
+// in fp32, except for the quadratic form q, which stays fp64 (a thin splat's
+// conic is ill-conditioned: q cancels in fp32). exp and ln run on the SFU
+// (ex2/lg2.approx). The only discrete decision of the loop that fp32 can get
+// wrong is early termination (T < cutoff; coverage is integer and exact), so
+// the kernel carries an error bound for each transmittance and flags a pixel
+// when a termination test it made was closer to the cutoff than that bound.
+// Flagged pixels are recomputed with the exact fp64 steps by K7r; every other
+// pixel's stop point -- hence contributor counts -- is that of the fp64
+// reference.
+//
+// Error bound (relative, T_fp32 vs T_fp64, u = 2^-24). A composited entry
+// multiplies T by (1 - a). fp32 perturbs a by |da| <= a (1.5 q + 8) u (q -> fp32
+// and the ln2 scaling 1.5 q u, ex2.approx <= 4u, products and the A/B/v
+// roundings of a* <= 4u), so the factor is off by |da| / (1 - a) + 2u (its own
+// rounding and the product's). On the splat's support q <= 2 ln(o/a), hence
+//   a < 1/2 :  a (1.5 q + 8) / (1 - a) <= 2 (3/e + 8 a)   <= 2.2 + 16 a/(1-a)
+//   a >= 1/2:  q <= 2 ln 2, a (1.5 q + 8) / (1 - a)        <= 10.1 a/(1-a)
+// and for a* = clamp(A a + B): [A a (1.5 q + 8) + 3 a*] / (1 - a*) <= 2.2 +
+// 22 a*/(1-a*) (A a (1.5 q + 8) <= 8 A o <= 16 a* when a* >= 1/2). After k
+// entries, with S = sum a/(1-a) over them, the relative error is at most
+//   u (22 S + 4.2 k + 16).
+// The kernel accumulates S per track (one rcp.approx + one FMA per entry) and
+// flags a pixel when min |T/cutoff - 1| over the two tests bracketing its stop
+// (or its final T, if it never stops) is within twice that bound
+// (cert_base + cert_per_step k + cert_sum S, from the host).
+#include "ua_common.cuh"
+
+namespace gavis {
+
+namespace {
+
+constexpr int kFastBatch = 192;
+constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
+constexpr float kLn2f = 0.69314718055994531f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One staged splat: fp64 mean/conic for q, fp32 opacity and depth.
+struct __align__(16) FGeo {
+  double mx, my, ca, cb2, cc;
+  float o, depth;
+};
+
+template <int LC, bool RGB, bool ENT>
+struct FStage {
+  static constexpr size_t bytes(int batch) {
+    return (size_t)batch * (sizeof(FGeo) + sizeof(int4) + (ENT ? sizeof(float4) : 0) +
+                            (RGB ? sizeof(float) * Col<LC>::STRIDE : 0));
+  }
+};
+
+// Stage entries [base, base+n) of the tile list: the fp32 forms are rounded
+// once here, per tile, not per pixel.
+template <int LC, bool RGB, bool ENT>
+__device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec* geo,
+                                             const UaRec* uar, uint32_t base, int n, FGeo* s_geo,
+                                             int4* s_rect, float4* s_ua, float* s_col) {
+  constexpr int V4 = Col<LC>::STRIDE / 4;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const uint32_t g = a.vals[base + j];
+    const GeoRec r = geo[g];
+    FGeo f;
+    f.mx = r.mx;
+    f.my = r.my;
+    f.ca = r.ca;
+    f.cb2 = r.cb2;
+    f.cc = r.cc;
+    f.o = r.opacity;
+    f.depth = (float)r.depth;
+    s_geo[j] = f;
+    s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
+    if (ENT) {
+      const UaRec u = uar[g];
+      s_ua[j] = make_float4((float)u.A, (float)u.B, (float)u.v, (float)(u.hl + kGaussEntropy));
+    }
+  }
+  if (RGB) {
+    const float4* colors4 = reinterpret_cast<const float4*>(a.scene.colors);
+    for (int k = threadIdx.x; k < n * V4; k += blockDim.x) {
+      const int j = k / V4, qd = k - j * V4;
+      const uint32_t g = a.vals[base + j];
+      reinterpret_cast<float4*>(s_col)[k] = __ldg(colors4 + (int64_t)g * V4 + qd);
+    }
+  }
+}
+
+template <int LC>
+struct FPix {
+  // fp32 running state; the sums are folded into fp64 after every 32-entry chunk
+  float T, Tp, r0, r1, r2, dp;
+  float Te, Tep, h, w0, ed;
+  float S, Se;  // sum a/(1-a) over composited entries, per track (error bound)
+  double R0, R1, R2, DP, H, W0, ED;
+  int n_rgb, n_ent;
+  bool rd, edn;
+  float2 bp[Col<LC>::NP];
+};
+
+template <int LC, bool EXTRA>
+__device__ __forceinline__ void fold(FPix<LC>& P) {
+  P.R0 += (double)P.r0;
+  P.R1 += (double)P.r1;
+  P.R2 += (double)P.r2;
+  P.H += (double)P.h;
+  P.W0 += (double)P.w0;
+  P.r0 = P.r1 = P.r2 = P.h = P.w0 = 0.f;
+  if (EXTRA) {
+    P.DP += (double)P.dp;
+    P.ED += (double)P.ed;
+    P.dp = P.ed = 0.f;
+  }
+}
+
+// Distance of a track's termination tests from the cutoff, relative.
+__device__ __forceinline__ float stop_margin(bool done, float T, float Tprev, float cutoff) {
+  const float d = done ? fminf(cutoff - T, Tprev - cutoff) : T - cutoff;
+  return d / cutoff;
+}
+
+// ---------------------------------------------------------------------------
+// K7f: 16x16 tiles, 256 threads, one pixel each (warp = 8x4 patch), 192-entry
+// shared-memory batches, warp pre-filter, list entries two at a time in
+// straight-line code (masks instead of branches, as in the exact ILP kernel).
+template <int LC, bool RGB, bool ENT, bool EXTRA>
+__global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
+  constexpr int CS = Col<LC>::STRIDE;
+  constexpr int B = kFastBatch;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  FGeo* s_geo = reinterpret_cast<FGeo*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + B * sizeof(FGeo));
+  float4* s_ua = reinterpret_cast<float4*>(s_dyn + B * (sizeof(FGeo) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + B * (sizeof(FGeo) + sizeof(int4) +
+                                                       (ENT ? sizeof(float4) : 0)));
+
+  const float amax = (float)a.amax, cutoff = (float)a.cutoff;
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = a.scene.n;
+  const GeoRec* geo = a.geo + (int64_t)v * N;
+  const UaRec* uar = a.ua + (int64_t)v * N;
+
+  const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 4;
+  const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+  const bool inside = px < c.width && py < c.height;
+  const double cxp = px + 0.5, cyp = py + 0.5;
+  FPix<LC> P;
+  if (RGB) pixel_basis<LC>(c, px, py, P.bp);
+  P.T = P.Te = 1.f;
+  P.Tp = P.Tep = 1.f;
+  P.r0 = P.r1 = P.r2 = P.dp = P.h = P.w0 = P.ed = 0.f;
+  P.R0 = P.R1 = P.R2 = P.DP = P.H = P.W0 = P.ED = 0.0;
+  P.n_rgb = P.n_ent = 0;
+  P.S = P.Se = 0.f;
+  P.rd = !(RGB && inside);
+  P.edn = !(ENT && inside);
+
+  for (uint32_t base = rg.x; base < rg.y; base += B) {
+    const bool live = !(P.rd && P.edn);
+    if (__syncthreads_count(live) == 0) break;
+    const int n = min((uint32_t)B, rg.y - base);
+    fstage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
+    __syncthreads();
+    if (__all_sync(0xffffffffu, !live)) continue;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      bool hit = false;
+      if (j0 + lane < n) {
+        const int4 r = s_rect[j0 + lane];
+        hit = r.x <= bx0 + 7 && r.x + r.y >= bx0 && r.z <= by0 + 3 && r.z + r.w >= by0;
+      }
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      if (hits == 0u) continue;
+      while (hits != 0u) {
+        const int ja = j0 + __ffs(hits) - 1;
+        hits &= hits - 1u;
+        const bool has_b = hits != 0u;
+        const int jb = has_b ? j0 + __ffs(hits) - 1 : ja;
+        if (has_b) hits &= hits - 1u;
+        const bool ca = in_rect4(s_rect[ja], px, py);
+        const bool cb = has_b && in_rect4(s_rect[jb], px, py);
+        const FGeo& ea = s_geo[ja];
+        const FGeo& eb = s_geo[jb];
+        // q in fp64 (splat_alpha, raster.hpp:101-108), then exp on the SFU
+        const double dxa = cxp - ea.mx, dya = cyp - ea.my;
+        const double dxb = cxp - eb.mx, dyb = cyp - eb.my;
+        const double qa = fma(dxa, fma(ea.cb2, dya, ea.ca * dxa), ea.cc * dya * dya);
+        const double qb = fma(dxb, fma(eb.cb2, dyb, eb.ca * dxb), eb.cc * dyb * dyb);
+        const float ala = fminf(ea.o * ex2_approx((float)qa * kNegHalfLog2e), amax);
+        const float alb = fminf(eb.o * ex2_approx((float)qb * kNegHalfLog2e), amax);
+        if (RGB) {
+          const bool ra = ca && !P.rd;
+          float a0, a1, a2, b0, b1, b2;
+          sh_color<LC>(reinterpret_cast<const float2*>(s_col + ja * CS), P.bp, a0, a1, a2);
+          sh_color<LC>(reinterpret_cast<const float2*>(s_col + jb * CS), P.bp, b0, b1, b2);
+          const float aa = ra ? ala : 0.f;
+          const float wa = aa * P.T;
+          P.r0 = fmaf(wa, a0, P.r0);
+          P.r1 = fmaf(wa, a1, P.r1);
+          P.r2 = fmaf(wa, a2, P.r2);
+          if (EXTRA) P.dp = fmaf(wa, ea.depth, P.dp);
+          const float fa = 1.f - aa;
+          P.S = fmaf(aa, rcp_approx(fa), P.S);
+          const float Ta = P.T * fa;
+          const bool sa = ra && Ta < cutoff;
+          P.Tp = sa ? P.T : P.Tp;
+          P.T = Ta;
+          const bool rb = cb && !(P.rd || sa);
+          const float ab = rb ? alb : 0.f;
+          const float wb = ab * P.T;
+          P.r0 = fmaf(wb, b0, P.r0);
+          P.r1 = fmaf(wb, b1, P.r1);
+          P.r2 = fmaf(wb, b2, P.r2);
+          if (EXTRA) P.dp = fmaf(wb, eb.depth, P.dp);
+          const float fb = 1.f - ab;
+          P.S = fmaf(ab, rcp_approx(fb), P.S);
+          const float Tb = P.T * fb;
+          const bool sb = rb && Tb < cutoff;
+          P.Tp = sb ? P.T : P.Tp;
+          P.T = Tb;
+          P.rd = P.rd || sa || sb;
+          P.n_rgb += (int)ra + (int)rb;
+        }
+        if (ENT) {
+          // compensated_alpha (uncertainty.hpp:55-59) and the entropy step (:198-222)
+          const float4 ua = s_ua[ja], ub = s_ua[jb];  // A, B, v, hl + C_H
+          const bool oa = ca && !P.edn;
+          const float xa = fminf(fmaxf(fmaf(ua.x, ala, ua.y), 0.f), amax);
+          const float xb = fminf(fmaxf(fmaf(ub.x, alb, ub.y), 0.f), amax);
+          const float asa = oa ? xa : 0.f;
+          const float wa = asa * P.Te;
+          const float sa = wa * ua.z;
+          P.w0 = fmaf(wa, 1.f - ua.z, P.w0);
+          if (EXTRA) P.ed = fmaf(wa, ea.depth, P.ed);
+          const float fa = 1.f - asa;
+          P.Se = fmaf(asa, rcp_approx(fa), P.Se);
+          const float Ta = P.Te * fa;
+          const bool ta = oa && Ta < cutoff;
+          P.Tep = ta ? P.Te : P.Tep;
+          P.Te = Ta;
+          const bool ob = cb && !(P.edn || ta);
+          const float asb = ob ? xb : 0.f;
+          const float wb = asb * P.Te;
+          const float sb = wb * ub.z;
+          P.w0 = fmaf(wb, 1.f - ub.z, P.w0);
+          if (EXTRA) P.ed = fmaf(wb, eb.depth, P.ed);
+          const float fb = 1.f - asb;
+          P.Se = fmaf(asb, rcp_approx(fb), P.Se);
+          const float Tb = P.Te * fb;
+          const bool tb = ob && Tb < cutoff;
+          P.Tep = tb ? P.Te : P.Tep;
+          P.Te = Tb;
+          P.edn = P.edn || ta || tb;
+          P.n_ent += (int)oa + (int)ob;
+          // H += s (-ln s + 1/2 ln|Qc| + C_H); s == 0 adds exactly 0
+          const float la = lg2_approx(fmaxf(sa, 1e-37f));
+          const float lb = lg2_approx(fmaxf(sb, 1e-37f));
+          P.h = fmaf(sa, fmaf(-la, kLn2f, ua.w), P.h);
+          P.h = fmaf(sb, fmaf(-lb, kLn2f, ub.w), P.h);
+        }
+      }
+      fold<LC, EXTRA>(P);
+    }
+  }
+
+  // certification of the stop decisions
+  bool flag = false;
+  if (inside) {
+    if (RGB)
+      flag |= stop_margin(P.rd, P.T, P.Tp, cutoff) <=
+              a.cert_base + a.cert_per_step * (float)P.n_rgb + a.cert_sum * P.S;
+    if (ENT)
+      flag |= stop_margin(P.edn, P.Te, P.Tep, cutoff) <=
+              a.cert_base + a.cert_per_step * (float)P.n_ent + a.cert_sum * P.Se;
+  }
+  const int64_t pix = c.pix_base + (int64_t)py * c.width + px;
+  const unsigned fm = __ballot_sync(0xffffffffu, flag);
+  if (fm != 0u) {
+    const int leader = __ffs(fm) - 1;
+    uint32_t slot = 0;
+    if (lane == leader) slot = atomicAdd(a.flag_count, (uint32_t)__popc(fm));
+    slot = __shfl_sync(0xffffffffu, slot, leader);
+    if (flag) a.flag_list[slot + __popc(fm & ((1u << lane) - 1u))] = (uint32_t)pix;
+  }
+  if (!inside) return;
+  if (RGB) {
+    if (a.rgb) {
+      a.rgb[pix * 3 + 0] = P.R0;
+      a.rgb[pix * 3 + 1] = P.R1;
+      a.rgb[pix * 3 + 2] = P.R2;
+    }
+    if (EXTRA && a.depth) a.depth[pix] = P.DP;
+    if (a.trans) a.trans[pix] = (double)P.T;
+    if (EXTRA && a.rgb_contrib) a.rgb_contrib[pix] = P.n_rgb;
+  }
+  if (ENT) {
+    double H = P.H;
+    if (P.W0 > 0.0) H += P.W0 * (-log(P.W0) + a.hl_q0 + kGaussEntropy);  // :224-225
+    if (a.entropy) a.entropy[pix] = H;
+    if (a.w0) a.w0[pix] = P.W0;
+    if (EXTRA && a.edepth) a.edepth[pix] = P.ED;
+    if (EXTRA && a.ent_contrib) a.ent_contrib[pix] = P.n_ent;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7r: exact fp64 recomputation of the flagged pixels, one warp per pixel.
+// The lanes walk the pixel's tile list 32 entries at a time: each lane loads
+// its entry, tests coverage and, if covered, evaluates the entry's fp64 alpha,
+// compensated alpha and fp32 SH colour (independent of the transmittance).
+// The covered entries are then composited in list order with the exact
+// path's operations (rgb_step / ent_step, ua_common.cuh), every lane carrying
+// the same pixel state, so the outputs equal the exact kernels' bit for bit.
+template <int LC, bool RGB, bool ENT>
+__global__ void __launch_bounds__(256) ua_redo_kernel(UaBlendArgs a) {
+  load_math_tables();
+  __syncthreads();
+  constexpr int CS = Col<LC>::STRIDE;
+  const uint32_t n = *a.flag_count;
+  const double amax = a.amax, cutoff = a.cutoff;
+  const int64_t N = a.scene.n;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nwarps) {
+    const int64_t pix = a.flag_list[i];
+    int v = 0;
+    while (v + 1 < a.V && a.cams[v + 1].pix_base <= pix) ++v;
+    const DevCam& c = a.cams[v];
+    const int64_t local = pix - c.pix_base;
+    const int py = (int)(local / c.width), px = (int)(local - (int64_t)py * c.width);
+    const int64_t tile = c.tile_base + (int64_t)(py / a.tile_size) * c.tiles_x + px / a.tile_size;
+    const uint2 rg = a.ranges[tile];
+    const GeoRec* geo = a.geo + (int64_t)v * N;
+    const UaRec* uar = a.ua + (int64_t)v * N;
+    const double cxp = px + 0.5, cyp = py + 0.5;
+    Pixel<LC> P;
+    pixel_init<LC, RGB, ENT>(P, c, px, py, true);
+    for (uint32_t base = rg.x; base < rg.y; base += 32) {
+      if (P.rgb_done && P.ent_done) break;
+      const uint32_t j = base + lane;
+      bool cov = false;
+      double al = 0.0, as = 0.0, dep = 0.0, vv = 0.0, hl = 0.0;
+      float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+      if (j < rg.y) {
+        const uint32_t g = a.vals[j];
+        const GeoRec e = geo[g];
+        cov = in_rect4(cover_rect4(e.cov_x, e.cov_y), px, py);
+        if (cov) {
+          al = splat_alpha(e, cxp, cyp, amax);
+          dep = e.depth;
+          if (RGB)
+            sh_color<LC>(reinterpret_cast<const float2*>(a.scene.colors + (int64_t)g * CS), P.bp, c0,
+                         c1, c2);
+          if (ENT) {
+            const UaRec u = uar[g];
+            const double x = u.A * al + u.B;  // compensated_alpha (uncertainty.hpp:55-59)
+            as = x < 0.0 ? 0.0 : (amax < x ? amax : x);
+            vv = u.v;
+            hl = u.hl;
+          }
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, cov);
+      double my_s = 0.0;  // s of this lane's entry if the entropy track composited it
+      unsigned mm = m;
+      while (mm != 0u) {
+        const int src = __ffs(mm) - 1;
+        mm &= mm - 1u;
+        const double eal = __shfl_sync(0xffffffffu, al, src);
+        const double edep = __shfl_sync(0xffffffffu, dep, src);
+        if (RGB && !P.rgb_done) {  // rgb_step (raster.hpp:209-221)
+          const float e0 = __shfl_sync(0xffffffffu, c0, src);
+          const float e1 = __shfl_sync(0xffffffffu, c1, src);
+          const float e2 = __shfl_sync(0xffffffffu, c2, src);
+          ++P.n_rgb;
+          const double w = eal * P.T;
+          if (w > 0.0) {
+            P.rgb0 += w * (double)e0;
+            P.rgb1 += w * (double)e1;
+            P.rgb2 += w * (double)e2;
+            P.dep += w * edep;
+          }
+          P.T *= 1.0 - eal;
+          if (P.T < cutoff) P.rgb_done = true;
+        }
+        if (ENT && !P.ent_done) {  // ent_step (uncertainty.hpp:198-222), H deferred
+          const double eas = __shfl_sync(0xffffffffu, as, src);
+          const double ev = __shfl_sync(0xffffffffu, vv, src);
+          ++P.n_ent;
+          const double w = eas * P.Te;
+          const double s = w * ev;
+          if (lane == src) my_s = s;
+          P.w0 += w * (1.0 - ev);
+          P.edep += w * edep;
+          P.Te *= 1.0 - eas;
+          if (P.Te < cutoff) P.ent_done = true;
+        }
+        if (P.rgb_done && P.ent_done) break;
+      }
+      if (ENT) {
+        // H += s (-ln s + 1/2 ln|Qc| + C_H) in list order: the logs in parallel
+        // (one per lane), the sum serial; entries not composited add +0.0
+        const double term = my_s > 0.0 ? my_s * (-log_pos(my_s) + hl + kGaussEntropy) : 0.0;
+        mm = m;
+        while (mm != 0u) {
+          const int src = __ffs(mm) - 1;
+          mm &= mm - 1u;
+          P.H += __shfl_sync(0xffffffffu, term, src);
+        }
+      }
+    }
+    if (lane == 0) pixel_finish<LC, RGB, ENT, true>(P, a, c, px, py, true);
+  }
+}
+
+// K8: image_entropy (uncertainty.hpp:264-278) per view, one block per view:
+// thread t folds pixels t, t+512, ... in order, then a fixed reduction tree.
+__global__ void __launch_bounds__(512) score_image_kernel(const DevCam* cams, const double* entropy,
+                                                          const double* edepth, double lambda,
+                                                          double* scores) {
+  __shared__ double s_red[16];
+  const DevCam& c = cams[blockIdx.x];
+  const int64_t P = (int64_t)c.width * c.height;
+  const double* H = entropy + c.pix_base;
+  double sum = 0.0;
+  if (lambda > 0.0) {
+    const double* d = edepth + c.pix_base;
+    for (int64_t i = threadIdx.x; i < P; i += 512) sum += H[i] - H[i] * exp(-d[i] / lambda);
+  } else {
+    for (int64_t i = threadIdx.x; i < P; i += 512) sum += H[i];
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 16; ++w) s += s_red[w];
+    scores[blockIdx.x] = s;
+  }
+}
+
+template <int LC, bool RGB, bool ENT, bool EXTRA>
+void launch_fast_one(const UaBlendArgs& a, cudaStream_t s) {
+  const size_t sm = FStage<LC, RGB, ENT>::bytes(kFastBatch);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ua_blend_fast_kernel<LC, RGB, ENT, EXTRA>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  ua_blend_fast_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+}
+
+template <int LC, bool EXTRA>
+void launch_fast_lc(const UaBlendArgs& a, cudaStream_t s) {
+  if (a.do_rgb && a.do_ent)
+    launch_fast_one<LC, true, true, EXTRA>(a, s);
+  else if (a.do_rgb)
+    launch_fast_one<LC, true, false, EXTRA>(a, s);
+  else if (a.do_ent)
+    launch_fast_one<LC, false, true, EXTRA>(a, s);
+}
+
+template <int LC>
+void launch_redo_lc(const UaBlendArgs& a, cudaStream_t s) {
+  const unsigned grid = 148 * 8;
+  if (a.do_rgb && a.do_ent)
+    ua_redo_kernel<LC, true, true><<<grid, 256, 0, s>>>(a);
+  else if (a.do_rgb)
+    ua_redo_kernel<LC, true, false><<<grid, 256, 0, s>>>(a);
+  else if (a.do_ent)
+    ua_redo_kernel<LC, false, true><<<grid, 256, 0, s>>>(a);
+}
+
+}  // namespace
+
+bool ua_fast_supported(int tile_size, double amax) { return tile_size == 16 && amax <= 0.999; }
+
+void launch_ua_blend_fast(const UaBlendArgs& a, cudaStream_t s) {
+  if (a.total_tiles == 0) return;
+  const bool extra = a.depth || a.edepth || a.rgb_contrib || a.ent_contrib || a.corr_lambda > 0.0;
+  switch (a.scene.color_degree) {
+#define GAVIS_FAST_LC(L)                \
+  case L:                               \
+    if (extra)                          \
+      launch_fast_lc<L, true>(a, s);    \
+    else                                \
+      launch_fast_lc<L, false>(a, s);   \
+    break;
+    GAVIS_FAST_LC(0)
+    GAVIS_FAST_LC(1)
+    GAVIS_FAST_LC(2)
+    GAVIS_FAST_LC(3)
+#undef GAVIS_FAST_LC
+    default: break;
+  }
+}
+
+void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s) {
+  if (a.total_tiles == 0) return;
+  switch (a.scene.color_degree) {
+    case 0: launch_redo_lc<0>(a, s); break;
+    case 1: launch_redo_lc<1>(a, s); break;
+    case 2: launch_redo_lc<2>(a, s); break;
+    case 3: launch_redo_lc<3>(a, s); break;
+    default: break;
+  }
+}
+
+void launch_score_image(const DevCam* cams, int V, const double* entropy, const double* edepth,
+                        double corr_lambda, double* scores, cudaStream_t s) {
+  if (V == 0) return;
+  score_image_kernel<<<V, 512, 0, s>>>(cams, entropy, edepth, corr_lambda, scores);
+}
+
+}  // namespace gavis

@@ -1,0 +1,209 @@
+// ua_common.cuh -- device helpers shared by the UA blend kernels (K7): the fp64
+// per-pixel state and steps of the exact path (kernels_ua.cu, also used by the
+// certified path's fp64 redo in kernels_ua_fast.cu), the packed fp32 SH colour
+// and the shared-memory staging of tile-list batches.
+#pragma once
+
+#include "fast_math.cuh"
+#include "kernels.h"
+
+namespace gavis {
+namespace {
+
+constexpr int kBatch = 128;
+
+__device__ __forceinline__ int find_view(const DevCam* cams, int V, int64_t tile) {
+  int v = 0;
+  while (v + 1 < V && cams[v + 1].tile_base <= tile) ++v;
+  return v;
+}
+
+template <int LC>
+struct Col {
+  static constexpr int NB = (LC + 1) * (LC + 1);
+  static constexpr int NBP = NB + (NB & 1);      // even-padded channel row
+  static constexpr int NP = NBP / 2;              // coefficient pairs per channel
+  static constexpr int STRIDE = ((3 * NBP + 3) / 4) * 4;
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra, rb, rc, rd;
+  ra = *reinterpret_cast<unsigned long long*>(&a);
+  rb = *reinterpret_cast<unsigned long long*>(&b);
+  rc = *reinterpret_cast<unsigned long long*>(&c);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2*>(&rd);
+}
+
+template <int LC>
+struct Pixel {
+  double T, rgb0, rgb1, rgb2, dep;
+  double Te, H, w0, edep;
+  bool rgb_done, ent_done;
+  int32_t n_rgb, n_ent;
+  float2 bp[Col<LC>::NP];  // SH basis at the pixel ray, as pairs
+};
+
+// SH basis at the pixel ray as fp32 pairs: CameraView::pixel_ray
+// (model.hpp:83-86) + eval_real_sh_block at the ray (raster.hpp:200-201).
+template <int LC>
+__device__ __forceinline__ void pixel_basis(const DevCam& c, int px, int py, float2* bp) {
+  constexpr int NB = Col<LC>::NB;
+  const double cxp = px + 0.5, cyp = py + 0.5;
+  const double dc0 = (cxp - c.cx) / c.fx, dc1 = (cyp - c.cy) / c.fy, dc2 = 1.0;
+  const double r0 = c.R[0] * dc0 + c.R[1] * dc1 + c.R[2] * dc2;
+  const double r1 = c.R[3] * dc0 + c.R[4] * dc1 + c.R[5] * dc2;
+  const double r2 = c.R[6] * dc0 + c.R[7] * dc1 + c.R[8] * dc2;
+  const double n2 = r0 * r0 + r1 * r1 + r2 * r2;
+  const double nn = n2 > 0.0 ? sqrt(n2) : 1.0;
+  double bd[Col<LC>::NBP];
+  eval_sh<LC>(r0 / nn, r1 / nn, r2 / nn, bd);
+  if (Col<LC>::NBP != NB) bd[Col<LC>::NBP - 1] = 0.0;
+#pragma unroll
+  for (int i = 0; i < Col<LC>::NP; ++i) bp[i] = make_float2((float)bd[2 * i], (float)bd[2 * i + 1]);
+}
+
+template <int LC, bool RGB, bool ENT>
+__device__ __forceinline__ void pixel_init(Pixel<LC>& P, const DevCam& c, int px, int py,
+                                           bool inside) {
+  if (RGB) pixel_basis<LC>(c, px, py, P.bp);
+  P.T = 1.0;
+  P.rgb0 = P.rgb1 = P.rgb2 = P.dep = 0.0;
+  P.Te = 1.0;
+  P.H = P.w0 = P.edep = 0.0;
+  P.rgb_done = !(RGB && inside);
+  P.ent_done = !(ENT && inside);
+  P.n_rgb = P.n_ent = 0;
+}
+
+// SH colour of one splat at one pixel ray, clamped to [0,1] (model.hpp:49-62):
+// packed pairs of coefficients, even/odd partial sums folded at the end.
+template <int LC>
+__device__ __forceinline__ void sh_color(const float2* col2, const float2* bp, float& c0, float& c1,
+                                         float& c2) {
+  constexpr int NP = Col<LC>::NP;
+  float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0;
+#pragma unroll
+  for (int m = 0; m < NP; ++m) {
+    a0 = ffma2(col2[m], bp[m], a0);
+    a1 = ffma2(col2[NP + m], bp[m], a1);
+    a2 = ffma2(col2[2 * NP + m], bp[m], a2);
+  }
+  c0 = __saturatef(a0.x + a0.y);
+  c1 = __saturatef(a1.x + a1.y);
+  c2 = __saturatef(a2.x + a2.y);
+}
+
+// alpha of splat e at the pixel (splat_alpha, raster.hpp:101-108).
+__device__ __forceinline__ double splat_alpha(const GeoRec& e, double cxp, double cyp, double amax) {
+  const double dx = cxp - e.mx;
+  const double dy = cyp - e.my;
+  const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
+  double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
+  if (q <= kQSkip) {
+    al = (double)e.opacity * exp_neg(-0.5 * q);
+    al = al > amax ? amax : al;
+  }
+  return al;
+}
+
+// RGB track update given alpha and (if w > 0) the colour (raster.hpp:209-221).
+// EXTRA: depth and contributor counts (only when an output asks for them).
+template <int LC, bool EXTRA>
+__device__ __forceinline__ void rgb_step(Pixel<LC>& P, double al, double depth, const float2* col2,
+                                         double cutoff) {
+  if (EXTRA) ++P.n_rgb;
+  const double w = al * P.T;
+  if (w > 0.0) {
+    float c0, c1, c2;
+    sh_color<LC>(col2, P.bp, c0, c1, c2);
+    P.rgb0 += w * (double)c0;
+    P.rgb1 += w * (double)c1;
+    P.rgb2 += w * (double)c2;
+    if (EXTRA) P.dep += w * depth;
+  }
+  P.T *= 1.0 - al;
+  if (P.T < cutoff) P.rgb_done = true;
+}
+
+// Entropy track update (uncertainty.hpp:198-222).
+template <int LC, bool EXTRA>
+__device__ __forceinline__ void ent_step(Pixel<LC>& P, double al, double depth, const UaRec& u,
+                                         double amax, double cutoff, double hl_qc) {
+  if (EXTRA) ++P.n_ent;
+  double as = u.A * al + u.B;
+  as = as < 0.0 ? 0.0 : (amax < as ? amax : as);
+  const double w = as * P.Te;
+  const double s = w * u.v;
+  if (s > 0.0) P.H += s * (-log_pos(s) + u.hl + kGaussEntropy);
+  P.w0 += w * (1.0 - u.v);
+  if (EXTRA) P.edep += w * depth;
+  P.Te *= 1.0 - as;
+  if (P.Te < cutoff) P.ent_done = true;
+}
+
+template <int LC, bool RGB, bool ENT, bool EXTRA>
+__device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a, const DevCam& c,
+                                             int px, int py, bool inside) {
+  if (ENT && P.w0 > 0.0) P.H += P.w0 * (-log_pos(P.w0) + a.hl_q0 + kGaussEntropy);
+  if (!inside) return;
+  const int64_t pix = c.pix_base + (int64_t)py * c.width + px;
+  if (RGB) {
+    if (a.rgb) {
+      a.rgb[pix * 3 + 0] = P.rgb0;
+      a.rgb[pix * 3 + 1] = P.rgb1;
+      a.rgb[pix * 3 + 2] = P.rgb2;
+    }
+    if (EXTRA && a.depth) a.depth[pix] = P.dep;
+    if (a.trans) a.trans[pix] = P.T;
+    if (EXTRA && a.rgb_contrib) a.rgb_contrib[pix] = P.n_rgb;
+  }
+  if (ENT) {
+    if (a.entropy) a.entropy[pix] = P.H;
+    if (a.w0) a.w0[pix] = P.w0;
+    if (EXTRA && a.edepth) a.edepth[pix] = P.edep;
+    if (EXTRA && a.ent_contrib) a.ent_contrib[pix] = P.n_ent;
+  }
+}
+
+// Per-pixel contribution to image_entropy (uncertainty.hpp:264-278): H, or with
+// the correlation hook H - H exp(-d / lambda), d the entropy-track depth.
+template <int LC>
+__device__ __forceinline__ double score_term(const Pixel<LC>& P, const UaBlendArgs& a) {
+  if (a.corr_lambda > 0.0) return P.H - P.H * exp(-P.edep / a.corr_lambda);
+  return P.H;
+}
+
+template <int LC, bool RGB, bool ENT>
+struct Stage {
+  static constexpr size_t bytes(int batch) {
+    return (size_t)batch * (sizeof(GeoRec) + sizeof(int4) + (ENT ? sizeof(UaRec) : 0) +
+                            (RGB ? sizeof(float) * Col<LC>::STRIDE : 0));
+  }
+};
+
+// Stage entries [base, base+n) of the tile list into shared memory.
+template <int LC, bool RGB, bool ENT>
+__device__ __forceinline__ void stage_batch(const UaBlendArgs& a, const GeoRec* geo, const UaRec* uar,
+                                            uint32_t base, int n, GeoRec* s_geo, int4* s_rect,
+                                            UaRec* s_ua, float* s_col) {
+  constexpr int V4 = Col<LC>::STRIDE / 4;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const uint32_t g = a.vals[base + j];
+    const GeoRec r = geo[g];
+    s_geo[j] = r;
+    s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
+    if (ENT) s_ua[j] = uar[g];
+  }
+  if (RGB) {
+    const float4* colors4 = reinterpret_cast<const float4*>(a.scene.colors);
+    for (int k = threadIdx.x; k < n * V4; k += blockDim.x) {
+      const int j = k / V4, qd = k - j * V4;
+      const uint32_t g = a.vals[base + j];
+      reinterpret_cast<float4*>(s_col)[k] = __ldg(colors4 + (int64_t)g * V4 + qd);
+    }
+  }
+}
+
+}  // namespace
+}  // namespace gavis

@@ -1,0 +1,165 @@
+"""Certified fp32 UA blend (GAVIS_PRECISION_CERTIFIED, the default) against the CPU
+oracle and against the exact fp64 device path.
+
+What the certified path guarantees (kernels_ua_fast.cu header):
+  * per-pixel contributor counts of both tracks are bit-exact (uncertified
+    early-termination tests are recomputed in fp64);
+  * the selected next-best view is the fp64 argmax (candidates within 1e-4 of
+    the best are re-scored exactly);
+  * RGB / entropy images within the north_star's 1e-4 max-abs (asserted), in
+    practice ~1e-6 (asserted at 2e-5), scores within 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2605_30342_b200 import api, synth
+from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig, VmfParams
+
+pytestmark = pytest.mark.gpu
+
+RC = RasterConfig()
+UC = UncertaintyConfig()
+NS_IMAGE_ABS = 1e-4   # north_star: RGB / uncertainty images within 1e-4 max-abs
+IMG_ABS = 2e-5        # what the fp32 blend holds on these scenes
+SCORE_REL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = api.Context(0)
+    c.set_precision("certified")
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_exact():
+    c = api.Context(0)
+    c.set_precision("exact")
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def room():
+    """Config-3 structure (thin wall slabs + clutter) at oracle-friendly size."""
+    return synth.config3(0, n=60_000, n_train=12, n_candidates=6, res=160)
+
+
+def test_certified_rasterize_parity(ctx):
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    for cam in c["candidates"][:3]:
+        r = api.render(ctx, scene, None, [cam], RC, UC, rgb=True, depth=True, transmittance=True,
+                       contributors=True)
+        rgb, depth, T, cc = O.rasterize(osc, cam, RC, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], cc)
+        assert np.max(np.abs(r["transmittance"] - T)) <= 1e-6
+        assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+        assert np.max(np.abs(r["rgb"] - rgb)) <= NS_IMAGE_ABS
+        assert np.max(np.abs(r["depth"] - depth)) <= 1e-4
+
+
+def _entropy_parity(ctx, scene, train, cams, degree):
+    osc = O.OracleScene(scene)
+    f = api.construct_field(ctx, scene, train, VmfParams(1.0), degree, RC)
+    g = f.download().gamma
+    r = api.render(ctx, scene, f, cams, RC, UC, entropy=True, invisible_mass=True, entropy_depth=True,
+                   scores=True, contributors=True, rgb=True)
+    P = cams[0].width * cams[0].height
+    for k, cam in enumerate(cams):
+        H, w0, depth, cc = O.render_entropy(osc, g, degree, len(train), cam, RC, UC, contrib=True)
+        sl = slice(k * P, (k + 1) * P)
+        assert np.array_equal(r["entropy_contributors"][sl], cc)
+        assert np.max(np.abs(r["entropy"][sl] - H)) <= IMG_ABS
+        assert np.max(np.abs(r["entropy"][sl] - H)) <= NS_IMAGE_ABS
+        assert np.max(np.abs(r["invisible_mass"][sl] - w0)) <= 1e-5
+        ref = O.image_entropy(H)
+        assert abs(r["scores"][k] - ref) <= SCORE_REL * max(1.0, abs(ref))
+        rgb, _, _, rc_cc = O.rasterize(osc, cam, RC, contrib=True)
+        assert np.array_equal(r["rgb_contributors"][sl], rc_cc)
+        assert np.max(np.abs(r["rgb"][3 * k * P:3 * (k + 1) * P] - rgb)) <= IMG_ABS
+
+
+def test_certified_entropy_parity_config1(ctx):
+    c = synth.config1(0)
+    _entropy_parity(ctx, c["scene"], c["train"], c["candidates"][:4], 2)
+
+
+def test_certified_entropy_parity_room(ctx, room):
+    _entropy_parity(ctx, room["scene"], room["train"], room["candidates"][:4], 2)
+
+
+def test_certified_select_nbv_matches_oracle(ctx, room):
+    scene = room["scene"]
+    f = api.construct_field(ctx, scene, room["train"], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    res = api.select_nbv(ctx, scene, f, room["candidates"], RC, UC)
+    best, scores = O.select_nbv(O.OracleScene(scene), g, 2, len(room["train"]), room["candidates"], RC, UC,
+                                threads=8)
+    assert res.best_index == best
+    assert np.max(np.abs(res.scores - scores) / np.maximum(1.0, np.abs(scores))) <= SCORE_REL
+
+
+def test_certified_argmax_rescoring(ctx):
+    """Identical candidates score identically; the tie goes to the lowest index
+    after the contenders are re-scored in fp64 (test_planner.cpp:170-180)."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    f = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC)
+    cam = c["candidates"][5]
+    other = c["candidates"][6]
+    before = ctx.counters()[1]
+    r = api.select_nbv(ctx, scene, f, [cam, cam, cam], RC, UC)
+    assert r.best_index == 0 and r.scores[0] == r.scores[1] == r.scores[2]
+    assert ctx.counters()[1] - before == 3
+    ex = api.select_nbv(ctx, scene, f, [other, cam], RC, UC)
+    r = api.select_nbv(ctx, scene, f, [other, cam, cam], RC, UC)
+    assert r.best_index == (1 if ex.scores[1] > ex.scores[0] else 0)
+    assert r.scores[1] == r.scores[2]
+
+
+def test_forced_redo_is_exact(ctx, ctx_exact, monkeypatch, room):
+    """With every pixel handed to the fp64 redo the certified path must reproduce
+    the exact path bit for bit (the redo runs the exact steps)."""
+    scene = room["scene"]
+    f = api.construct_field(ctx_exact, scene, room["train"], VmfParams(1.0), 2, RC)
+    cams = room["candidates"][:2]
+    kw = dict(rgb=True, depth=True, transmittance=True, entropy=True, invisible_mass=True,
+              entropy_depth=True, scores=True, contributors=True)
+    ex = api.render(ctx_exact, scene, f, cams, RC, UC, **kw)
+    monkeypatch.setenv("GAVIS_CERT_FORCE_REDO", "1")
+    fr = api.render(ctx_exact, scene, f, cams, RC, UC, **kw)  # exact context: knob ignored
+    ctx_f = api.Context(0)
+    try:
+        fd = api.upload_field(ctx_f, scene, f.download())
+        red0 = ctx_f.counters()[0]
+        got = api.render(ctx_f, scene, fd, cams, RC, UC, **kw)
+        assert ctx_f.counters()[0] - red0 == 2 * cams[0].width * cams[0].height
+    finally:
+        ctx_f.close()
+    assert set(ex) == set(got)
+    for k in ex:
+        assert np.array_equal(ex[k], fr[k])
+        assert np.array_equal(ex[k], got[k]), k
+
+
+def test_certified_vs_exact_full_size(ctx, ctx_exact):
+    """Config 3 at full size (1M Gaussians, 800^2): size-independent agreement of
+    the certified and the exact device paths (the exact path is pinned to the oracle)."""
+    c = synth.config3(0, n_candidates=4)
+    scene = c["scene"]
+    f = api.construct_field(ctx_exact, scene, c["train"][:30], VmfParams(1.0), 2, RC)
+    cams = c["candidates"][:4]
+    kw = dict(rgb=True, transmittance=True, entropy=True, invisible_mass=True, scores=True, contributors=True)
+    ex = api.render(ctx_exact, scene, f, cams, RC, UC, **kw)
+    fd = api.upload_field(ctx, scene, f.download())
+    got = api.render(ctx, scene, fd, cams, RC, UC, **kw)
+    assert np.array_equal(ex["rgb_contributors"], got["rgb_contributors"])
+    assert np.array_equal(ex["entropy_contributors"], got["entropy_contributors"])
+    assert np.max(np.abs(ex["rgb"] - got["rgb"])) <= IMG_ABS
+    assert np.max(np.abs(ex["entropy"] - got["entropy"])) <= IMG_ABS
+    assert np.max(np.abs(ex["transmittance"] - got["transmittance"])) <= 1e-6
+    assert np.max(np.abs(ex["scores"] - got["scores"]) / np.abs(ex["scores"])) <= SCORE_REL

@@ -26,6 +26,7 @@ NS_IMAGE_ABS = 1e-4   # north_star: RGB / uncertainty images within 1e-4 max-abs
 @pytest.fixture(scope="module")
 def ctx():
     c = api.Context(0)
+    c.set_precision("exact")  # fp64 blend: tolerances at rounding level
     yield c
     c.close()
 

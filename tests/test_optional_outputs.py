@@ -37,6 +37,7 @@ def test_oracle_propagated_constant_matches_constant_provider():
 def ctx():
     from paper_2605_30342_b200 import api
     c = api.Context(0)
+    c.set_precision("exact")  # fp64 blend: tolerances at rounding level
     yield c
     c.close()
 

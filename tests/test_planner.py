@@ -91,6 +91,7 @@ def test_vis_coverage_matches_oracle_and_kat():
 @pytest.fixture(scope="module")
 def ctx():
     c = api.Context(0)
+    c.set_precision("exact")  # fp64 blend: tolerances at rounding level
     yield c
     c.close()
 

@@ -20,8 +20,10 @@ if timeout 600 python $SMALL > $OUT/${TAG}_small.json 2>&1; then
     --log-file $OUT/${TAG}_launches.csv python $SMALL > $OUT/${TAG}_ncu_launches.log 2>&1
 fi
 if timeout 300 python tools/profile_driver.py ua > $OUT/${TAG}_ua.log 2>&1; then
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ua_blend -s 1 -c 1 \
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ua_blend_fast -s 1 -c 1 \
     -o $OUT/${TAG}_ua python tools/profile_driver.py ua > $OUT/${TAG}_ncu_ua.log 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ua_redo -s 1 -c 1 \
+    -o $OUT/${TAG}_redo python tools/profile_driver.py ua > $OUT/${TAG}_ncu_redo.log 2>&1
 fi
 if timeout 300 python tools/profile_driver.py vf > $OUT/${TAG}_vf.log 2>&1; then
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:vf_blend -s 1 -c 1 \
