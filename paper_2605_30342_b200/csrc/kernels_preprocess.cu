@@ -143,36 +143,104 @@ __device__ __forceinline__ double query_row(const double* row, int num_views, do
   return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
 }
 
+// Cheap visibility screen of one (view, particle): the near-plane test exactly as
+// project_particle makes it (fp64, same operations), then a conservative fp32
+// frustum test with the radius bound r <= 3 sqrt(trace(Sigma) |J|_F^2 + 2 dil^2)
+// (lambda_max(cov2) <= trace(cov2)) and a margin 100x above the fp32 error: a
+// particle it rejects is culled by project() as well.
+__device__ __forceinline__ bool screen(const DevCam& c, double px, double py, double pz,
+                                       float trace, float dil2x2) {
+  const double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
+  const double t2 = c.R[2] * d0 + c.R[5] * d1 + c.R[8] * d2;
+  if (t2 < c.near_plane) return false;
+  const float f0 = (float)d0, f1 = (float)d1, f2 = (float)d2;
+  const float t0 = __fmaf_rn((float)c.R[0], f0, __fmaf_rn((float)c.R[3], f1, (float)c.R[6] * f2));
+  const float t1 = __fmaf_rn((float)c.R[1], f0, __fmaf_rn((float)c.R[4], f1, (float)c.R[7] * f2));
+  const float iz = 1.f / (float)t2;
+  const float ux = t0 * iz, uy = t1 * iz;
+  const float fx = (float)c.fx, fy = (float)c.fy;
+  const float mx = __fmaf_rn(fx, ux, (float)c.cx), my = __fmaf_rn(fy, uy, (float)c.cy);
+  const float lx = (float)c.limx, ly = (float)c.limy;
+  const float uxc = fminf(fmaxf(ux, -lx), lx), uyc = fminf(fmaxf(uy, -ly), ly);
+  const float gx = fx * iz, gy = fy * iz;
+  const float jf = gx * gx * (1.f + uxc * uxc) + gy * gy * (1.f + uyc * uyc);
+  const float rub = 3.f * sqrtf(__fmaf_rn(trace, jf, dil2x2));
+  const float W = (float)c.width, H = (float)c.height;
+  const float M = 1e-3f * (fabsf(mx) + fabsf(my) + rub + W + H) + 1e-2f;
+  return !(mx + rub < -M || mx - rub > W + M || my + rub < -M || my - rub > H + M);
+}
+
+// K1. One thread per particle screens it against every view of the batch; the
+// surviving (view, particle) items of a warp are compacted in shared memory and
+// projected 32 at a time, so the fp64 projection runs on full warps (~10% of the
+// items survive in an indoor scene; without compaction almost every warp holds
+// a survivor for every view and runs the projection for all its lanes).
+constexpr int kPreThreads = 128;
+
 template <int QDEG>
-__global__ void __launch_bounds__(128) preprocess_kernel(PreprocessArgs a) {
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs a) {
+  constexpr int kWarps = kPreThreads / 32;
   __shared__ DevCam s_cam[kMaxBatchViews];
+  __shared__ uint16_t s_q[kWarps][32 * kMaxBatchViews];
+  __shared__ Sigma s_sig[kPreThreads];
   for (int i = threadIdx.x; i < a.V * (int)(sizeof(DevCam) / 8); i += blockDim.x)
     reinterpret_cast<double*>(s_cam)[i] = reinterpret_cast<const double*>(a.cams)[i];
-  __syncthreads();
   const int64_t N = a.scene.n;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= N) return;
-  const float4 po = a.scene.pos_op[g];
-  const float4 q = a.scene.rot[g];
-  const float4 sc = a.scene.scale[g];
-  const uint8_t virt = a.scene.virt ? a.scene.virt[g] : 0;
-  const Sigma S = covariance(q, sc);
-  const double px = po.x, py = po.y, pz = po.z;
-  constexpr int NBQ = QDEG >= 0 ? (QDEG + 1) * (QDEG + 1) : 1;
-  double row[NBQ];
-  bool have_row = false;
-  if (QDEG >= 0 && a.query_mode == kQueryField && !virt && a.num_views > 0) {
-    const double* gr = a.gamma + g * NBQ;
-#pragma unroll
-    for (int i = 0; i < NBQ; ++i) row[i] = gr[i];
-    have_row = true;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = (int64_t)blockIdx.x * kPreThreads + warp * 32;
+  const int64_t g = wbase + lane;
+  const bool valid = g < N;
+  double px = 0.0, py = 0.0, pz = 0.0;
+  float trace = 0.f;
+  if (valid) {
+    const float4 po = a.scene.pos_op[g];
+    const Sigma S = covariance(a.scene.rot[g], a.scene.scale[g]);
+    s_sig[threadIdx.x] = S;
+    px = po.x;
+    py = po.y;
+    pz = po.z;
+    trace = (float)S.trace;
   }
+  __syncthreads();
+  const float dil2x2 = (float)(2.0 * a.dilation * a.dilation);
+  const uint2 empty_rect = make_uint2(1u, 1u);  // tx0 = 1 > tx1 = 0
+  int qn = 0;
   for (int v = 0; v < a.V; ++v) {
+    bool surv = false;
+    if (valid) {
+      surv = screen(s_cam[v], px, py, pz, trace, dil2x2);
+      if (!surv) {
+        const int64_t slot = (int64_t)v * N + g;
+        a.counts[slot] = 0;
+        a.trect[slot] = empty_rect;
+        if (a.write_culled) {
+          GeoRec r = {};
+          r.cov_x = 1;
+          r.cov_y = 1;
+          a.geo[slot] = r;
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, surv);
+    if (surv) s_q[warp][qn + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(lane | (v << 5));
+    qn += __popc(m);
+  }
+  __syncwarp();
+  constexpr int NBQ = QDEG >= 0 ? (QDEG + 1) * (QDEG + 1) : 1;
+  for (int k = lane; k < qn + ((32 - qn % 32) % 32); k += 32) {
+    if (k >= qn) continue;
+    const int item = s_q[warp][k];
+    const int src = item & 31, v = item >> 5;
+    const int64_t gi = wbase + src;
+    const float4 po = a.scene.pos_op[gi];
+    const uint8_t virt = a.scene.virt ? a.scene.virt[gi] : 0;
+    const Sigma S = s_sig[warp * 32 + src];
+    const double qx = po.x, qy = po.y, qz = po.z;
     const DevCam& c = s_cam[v];
-    const int64_t slot = (int64_t)v * N + g;
+    const int64_t slot = (int64_t)v * N + gi;
     Projected p;
     int tx0 = 1, tx1 = 0, ty0 = 1, ty1 = 0;
-    bool ok = project(c, px, py, pz, S, a.dilation, p);
+    const bool ok = project(c, qx, qy, qz, S, a.dilation, p);
     int32_t count = 0;
     if (ok) {
       int x0, x1, y0, y1;
@@ -201,9 +269,13 @@ __global__ void __launch_bounds__(128) preprocess_kernel(PreprocessArgs a) {
       if (a.ua) {
         double vis = 0.0;
         if (a.query_mode == kQueryGiven) {
-          vis = a.vis_in[g];
-        } else if (QDEG >= 0 && have_row) {
-          const double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
+          vis = a.vis_in[gi];
+        } else if (QDEG >= 0 && a.query_mode == kQueryField && !virt && a.num_views > 0) {
+          double row[NBQ];
+          const double* gr = a.gamma + gi * NBQ;
+#pragma unroll
+          for (int i = 0; i < NBQ; ++i) row[i] = gr[i];
+          const double d0 = qx - c.pos[0], d1 = qy - c.pos[1], d2 = qz - c.pos[2];
           const double norm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
           if (!(norm < 1e-12))
             vis = query_row<(QDEG >= 0 ? QDEG : 0)>(row, a.num_views, d0 / norm, d1 / norm,
@@ -217,7 +289,7 @@ __global__ void __launch_bounds__(128) preprocess_kernel(PreprocessArgs a) {
         if (a.var) {
           // sh_variance_propagation (uncertainty.hpp:63-83) at the camera-to-centre
           // direction, half log-determinant of the diagonal Q_c (:149-163).
-          double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
+          double d0 = qx - c.pos[0], d1 = qy - c.pos[1], d2 = qz - c.pos[2];
           const double n2 = d0 * d0 + d1 * d1 + d2 * d2;
           if (n2 > 0.0) {
             const double nn = sqrt(n2);
@@ -228,7 +300,7 @@ __global__ void __launch_bounds__(128) preprocess_kernel(PreprocessArgs a) {
           double basis[(kMaxFieldDegree + 1) * (kMaxFieldDegree + 1)];
           eval_sh_rt(a.var_degree, d0, d1, d2, basis);
           const int nbv = (a.var_degree + 1) * (a.var_degree + 1);
-          const float* vr = a.var + g * 3 * nbv;
+          const float* vr = a.var + gi * 3 * nbv;
           double q0 = 0.0, q1 = 0.0, q2 = 0.0;
           for (int i = 0; i < nbv; ++i) {
             const double y2 = basis[i] * basis[i];
@@ -343,15 +415,15 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
   if (a.scene.n == 0 || a.V == 0) return;
-  const unsigned grid = blocks_for(a.scene.n, 128);
+  const unsigned grid = blocks_for(a.scene.n, kPreThreads);
   const int qd = a.query_mode == kQueryField ? a.degree : -1;
   switch (qd) {
-    case -1: preprocess_kernel<-1><<<grid, 128, 0, s>>>(a); break;
-    case 0: preprocess_kernel<0><<<grid, 128, 0, s>>>(a); break;
-    case 1: preprocess_kernel<1><<<grid, 128, 0, s>>>(a); break;
-    case 2: preprocess_kernel<2><<<grid, 128, 0, s>>>(a); break;
-    case 3: preprocess_kernel<3><<<grid, 128, 0, s>>>(a); break;
-    case 4: preprocess_kernel<4><<<grid, 128, 0, s>>>(a); break;
+    case -1: preprocess_kernel<-1><<<grid, kPreThreads, 0, s>>>(a); break;
+    case 0: preprocess_kernel<0><<<grid, kPreThreads, 0, s>>>(a); break;
+    case 1: preprocess_kernel<1><<<grid, kPreThreads, 0, s>>>(a); break;
+    case 2: preprocess_kernel<2><<<grid, kPreThreads, 0, s>>>(a); break;
+    case 3: preprocess_kernel<3><<<grid, kPreThreads, 0, s>>>(a); break;
+    case 4: preprocess_kernel<4><<<grid, kPreThreads, 0, s>>>(a); break;
     default: break;
   }
 }
