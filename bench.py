@@ -275,7 +275,11 @@ def run_ours(args):
     cands = c["candidates"][lo:hi]
 
     def step():
-        return api.select_nbv(ctx, ds, field, cands, rc, uc, with_rgb=True)
+        if world == 1:
+            return api.select_nbv(ctx, ds, field, cands, rc, uc, with_rgb=True)
+        # global argmax: scores all-gathered, contenders re-scored in fp64 on their ranks
+        return api.select_nbv_sharded(ctx, ds, field, c["candidates"], rank, world, dist, rc, uc,
+                                      with_rgb=True)
 
     for _ in range(args.warmup):
         res = step()
@@ -450,7 +454,7 @@ def run_ours(args):
             "select_nbv_entropy_only_views_per_s": select_only,
             "vf_build_ms": vf_ms, "vf_build_views": len(train), "vf_build_200_views_ms": vf200_ms,
             "vf_build_other_configs": vf_other,
-            "best_index_last_step": int(res.best_index) + lo,
+            "best_index_last_step": int(res.best_index) + (lo if world == 1 else 0),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
         }
         print(json.dumps(line))

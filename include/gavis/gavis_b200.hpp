@@ -166,6 +166,22 @@ struct EntropyMap {
   std::vector<double> invisible_mass;
 };
 
+// uncertainty.hpp:90-102
+struct PixelMixtureComponent {
+  double weight = 0.0;  // w* = alpha* T
+  double vis = 0.0;     // particle visibility v
+  Vec3 mean{};
+  Vec3 var{};           // diagonal of Q_c
+};
+
+struct PixelMixture {
+  int x = 0, y = 0;
+  double prior_weight = 0.0;            // w0
+  double residual_transmittance = 0.0;  // T after the loop
+  double entropy = 0.0;
+  std::vector<PixelMixtureComponent> components;
+};
+
 struct RenderOutput {
   int width = 0, height = 0;
   std::vector<double> color, depth, transmittance;
@@ -407,7 +423,8 @@ inline RenderOutput rasterize(const Scene& scene, const CameraView& cam, const R
 inline EntropyMap render_entropy(const Scene& scene, const VisibilityField& field,
                                  const CameraView& cam, const RasterConfig& rc,
                                  const UncertaintyConfig& uc, int /*threads*/ = 1,
-                                 std::vector<double>* depth_out = nullptr) {
+                                 std::vector<double>* depth_out = nullptr,
+                                 std::vector<PixelMixture>* mixtures_out = nullptr) {
   if (field.num_particles != scene.particles.size())
     throw ParameterError("render_entropy: field was built for a different scene");
   auto ds = detail::upload(scene);
@@ -427,6 +444,31 @@ inline EntropyMap render_entropy(const Scene& scene, const VisibilityField& fiel
   o.invisible_mass = m.invisible_mass.data();
   o.entropy_depth = depth_out ? depth_out->data() : nullptr;
   check(gavis_ua_render(detail::holder().get(), ds->h, df->h, nullptr, &c, 1, &r, &u, &o));
+  if (mixtures_out) {
+    // uncertainty.hpp:207-230: per-pixel components (exact fp64 track on the device)
+    std::vector<int64_t> off(P + 1);
+    std::vector<double> prior(P), resid(P), ent(P);
+    check(gavis_ua_mixtures(detail::holder().get(), ds->h, df->h, nullptr, &c, &r, &u, off.data(),
+                            nullptr, 0, prior.data(), resid.data(), ent.data()));
+    std::vector<gavis_mixture_component> comp((std::size_t)off[P]);
+    if (!comp.empty())
+      check(gavis_ua_mixtures(detail::holder().get(), ds->h, df->h, nullptr, &c, &r, &u, off.data(),
+                              comp.data(), (int64_t)comp.size(), nullptr, nullptr, nullptr));
+    mixtures_out->assign(P, PixelMixture{});
+    for (std::size_t p = 0; p < P; ++p) {
+      PixelMixture& mx = (*mixtures_out)[p];
+      mx.x = (int)(p % (std::size_t)cam.width);
+      mx.y = (int)(p / (std::size_t)cam.width);
+      mx.prior_weight = prior[p];
+      mx.residual_transmittance = resid[p];
+      mx.entropy = ent[p];
+      for (int64_t k = off[p]; k < off[p + 1]; ++k) {
+        const gavis_mixture_component& g = comp[(std::size_t)k];
+        mx.components.push_back({g.weight, g.vis, Vec3{g.mean[0], g.mean[1], g.mean[2]},
+                                 Vec3{g.var[0], g.var[1], g.var[2]}});
+      }
+    }
+  }
   return m;
 }
 

@@ -219,6 +219,27 @@ gavis_status gavis_ua_render(gavis_ctx* ctx, const gavis_scene* scene,
                              const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
                              gavis_render_outputs* out);
 
+/* render_entropy's mixtures_out (uncertainty.hpp:90-102, :207-230) for one
+ * camera: the components of every pixel (composited entries with w* > 0, in
+ * compositing order) in CSR form. offsets [W*H+1] is always written;
+ * components are written when non-NULL and capacity >= offsets[W*H] (call once
+ * with components = NULL to size the buffer). prior_weight (w0),
+ * residual_transmittance (T*) and entropy per pixel are optional. Field or
+ * splat_visibility as in gavis_ua_render. Computed with the exact fp64 track. */
+typedef struct {
+  double weight;  /* w* = alpha* T */
+  double vis;     /* particle visibility v */
+  double mean[3]; /* clamped SH colour at the pixel ray */
+  double var[3];  /* diagonal of Q_c */
+} gavis_mixture_component;
+
+gavis_status gavis_ua_mixtures(gavis_ctx* ctx, const gavis_scene* scene, const gavis_field* field,
+                               const double* splat_visibility, const gavis_camera* cam,
+                               const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
+                               int64_t* offsets, gavis_mixture_component* components,
+                               int64_t capacity, double* prior_weight,
+                               double* residual_transmittance, double* entropy);
+
 /* select_nbv (planner.hpp:117-137): scores [n] and the first maximum. */
 gavis_status gavis_select_nbv(gavis_ctx* ctx, const gavis_scene* scene,
                               const gavis_field* field, const gavis_camera* cams,

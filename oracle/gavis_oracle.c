@@ -741,6 +741,108 @@ void gor_render_entropy_core(const gor_scene* s, const gor_camera* cam, const go
   free_view(&b);
 }
 
+/* render_entropy_core's per-pixel mixtures (uncertainty.hpp:90-102, :185-230):
+ * for every composited entry with w* > 0, in list order, the component
+ * {w*, v, clamp(SH colour at the pixel ray), diag Q_c}; per pixel the prior
+ * weight w0, the residual T* and the entropy. offsets[P+1] always; comps only
+ * when non-NULL (capacity >= offsets[P] checked by the caller). */
+void gor_render_mixtures(const gor_scene* s, const gor_camera* cam, const gor_raster* rc,
+                         const gor_unc* uc, const double* vis_by_particle, int64_t* offsets,
+                         gor_mixture_component* comps, double* prior, double* resid,
+                         double* entropy) {
+  binned_view b = bin_view(s, cam, rc);
+  cam_derived cd = derive(cam);
+  const double hl_const = 3.0 * log(uc->color_sigma);
+  const double hl_q0 = 0.5 * logdet_spd3(uc->prior_cov);
+  const double var_const = uc->color_sigma * uc->color_sigma;
+  const int degree = s->color_degree;
+  const int nb = (degree + 1) * (degree + 1);
+  const int W = cam->width, H = cam->height, ts = rc->tile_size;
+  const int nbv = (g_coeff_var_degree + 1) * (g_coeff_var_degree + 1);
+  int64_t* count = (int64_t*)calloc((size_t)W * H + 1, sizeof(int64_t));
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      offsets[0] = 0;
+      for (int64_t p = 0; p < (int64_t)W * H; ++p) offsets[p + 1] = offsets[p] + count[p];
+      if (!comps) break;
+    }
+    for (int tile = 0; tile < b.tx_n * b.ty_n; ++tile) {
+      int tx = tile % b.tx_n, ty = tile / b.tx_n;
+      int px0 = tx * ts, px1 = px0 + ts < W ? px0 + ts : W;
+      int py0 = ty * ts, py1 = py0 + ts < H ? py0 + ts : H;
+      for (int py = py0; py < py1; ++py) {
+        for (int px = px0; px < px1; ++px) {
+          const double cxp = px + 0.5, cyp = py + 0.5;
+          const int64_t pix = (int64_t)py * W + px;
+          double ray[3], basis[MAX_SH];
+          pixel_ray(cam, &cd, cxp, cyp, ray);
+          gor_eval_sh(degree, ray, basis);
+          double t_cur = 1.0, h = 0.0, w0 = 0.0;
+          int64_t k = 0;
+          for (int64_t e = b.off[tile]; e < b.off[tile + 1]; ++e) {
+            const gor_splat* sp = &b.splats[b.ent[e]];
+            if (!splat_covers(sp, cxp, cyp)) continue;
+            const int64_t i = sp->particle_index;
+            double a = splat_alpha(sp, cxp, cyp, rc->alpha_clamp_max);
+            double v = vis_by_particle[i];
+            double astar = compensated_alpha(a, v, uc, rc->alpha_clamp_max);
+            double w = astar * t_cur;
+            double seen = w * v;
+            double qd[3] = {var_const, var_const, var_const}, hl_qc = hl_const;
+            if (uc->variance_provider == 1) {
+              double d[3] = {s->positions[3 * i] - cam->position[0],
+                             s->positions[3 * i + 1] - cam->position[1],
+                             s->positions[3 * i + 2] - cam->position[2]};
+              double n2 = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+              if (n2 > 0.0) {
+                double nn = sqrt(n2);
+                d[0] /= nn;
+                d[1] /= nn;
+                d[2] /= nn;
+              }
+              double bv[MAX_SH];
+              gor_eval_sh(g_coeff_var_degree, d, bv);
+              qd[0] = qd[1] = qd[2] = 0.0;
+              for (int j = 0; j < nbv; ++j)
+                for (int c = 0; c < 3; ++c) qd[c] += bv[j] * bv[j] * g_coeff_var[i * 3 * nbv + c * nbv + j];
+              hl_qc = 0.5 * (log(qd[0]) + log(qd[1]) + log(qd[2]));
+            }
+            if (seen > 0.0) h += seen * (-log(seen) + hl_qc + K_GAUSS_ENTROPY);
+            w0 += w * (1.0 - v);
+            if (w > 0.0) {
+              if (pass == 0) {
+                ++count[pix];
+              } else {
+                gor_mixture_component* m = &comps[offsets[pix] + k];
+                m->weight = w;
+                m->vis = v;
+                const double* col = s->colors + i * 3 * nb;
+                for (int c = 0; c < 3; ++c) {
+                  double acc = 0.0;
+                  for (int j = 0; j < nb; ++j) acc += col[c * nb + j] * basis[j];
+                  m->mean[c] = clamp01(acc);
+                  m->var[c] = qd[c];
+                }
+              }
+              ++k;
+            }
+            t_cur *= 1.0 - astar;
+            if (t_cur < rc->transmittance_cutoff) break;
+          }
+          if (w0 > 0.0) h += w0 * (-log(w0) + hl_q0 + K_GAUSS_ENTROPY);
+          if (pass == 0) {
+            if (prior) prior[pix] = w0;
+            if (resid) resid[pix] = t_cur;
+            if (entropy) entropy[pix] = h;
+          }
+        }
+      }
+    }
+  }
+  free(count);
+  free_view(&b);
+}
+
 /* render_entropy uncertainty.hpp:242-260: per-splat visibility from the field */
 void gor_splat_visibility(const double* gamma, int degree, int num_views, const gor_scene* s,
                           const gor_camera* cam, double dilation, double* vis) {

@@ -94,6 +94,14 @@ int64_t gor_query_view(const double* gamma, int degree, int num_views, const gor
                        const gor_camera* cam, double dilation, int32_t* idx, double* vis);
 
 /* uncertainty.hpp: vis_by_particle indexed by particle id */
+/* PixelMixtureComponent (uncertainty.hpp:90-95) */
+typedef struct {
+  double weight, vis, mean[3], var[3];
+} gor_mixture_component;
+void gor_render_mixtures(const gor_scene* s, const gor_camera* cam, const gor_raster* rc,
+                         const gor_unc* uc, const double* vis_by_particle, int64_t* offsets,
+                         gor_mixture_component* comps, double* prior, double* resid,
+                         double* entropy);
 void gor_render_entropy_core(const gor_scene* s, const gor_camera* cam, const gor_raster* rc,
                              const gor_unc* uc, const double* vis_by_particle, double* entropy,
                              double* w0, double* depth, int32_t* contrib);

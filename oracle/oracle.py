@@ -285,6 +285,23 @@ def render_entropy_core(scene, cam, rc, uc, vis_by_particle, contrib: bool = Fal
     return (H, w0, depth, cc) if contrib else (H, w0, depth)
 
 
+def render_mixtures(scene, cam, rc, uc, vis_by_particle):
+    """Per-pixel mixtures of render_entropy_core (uncertainty.hpp:185-230):
+    (offsets[P+1], components[K, 8] = w, v, mean rgb, var rgb, prior w0, residual T, H)."""
+    s = _scene(scene)
+    P = cam.width * cam.height
+    off = np.zeros(P + 1, np.int64)
+    prior, resid, H = np.zeros(P), np.zeros(P), np.zeros(P)
+    v = np.ascontiguousarray(vis_by_particle, np.float64)
+    if v.size == 0:
+        v = np.zeros(1)
+    args = (C.byref(s.c), C.byref(camera_struct(cam)), C.byref(raster_struct(rc)), C.byref(unc_struct(uc)), _p(v))
+    lib().gor_render_mixtures(*args, _p(off), None, _p(prior), _p(resid), _p(H))
+    comps = np.zeros((max(1, int(off[-1])), 8))
+    lib().gor_render_mixtures(*args, _p(off), _p(comps), None, None, None)
+    return off, comps[: int(off[-1])], prior, resid, H
+
+
 def render_entropy(scene, gamma, degree: int, num_views: int, cam, rc, uc, contrib: bool = False):
     s = _scene(scene)
     P = cam.width * cam.height

@@ -78,7 +78,7 @@ EXPORTS = [
     "gavis_scene_num_particles", "gavis_vf_construct", "gavis_vf_create",
     "gavis_vf_accumulate_views", "gavis_vf_accumulate_visibility", "gavis_vf_upload",
     "gavis_vf_download", "gavis_vf_set_num_views", "gavis_vf_device_gamma", "gavis_vf_destroy",
-    "gavis_single_view_visibility", "gavis_vf_query", "gavis_vf_query_view", "gavis_ua_render",
+    "gavis_single_view_visibility", "gavis_vf_query", "gavis_vf_query_view", "gavis_ua_render", "gavis_ua_mixtures",
     "gavis_select_nbv", "gavis_nbv_loop", "gavis_density_control", "gavis_sample_candidates",
     "gavis_vis_coverage", "gavis_active_mapping", "gavis_ply_info",
     "gavis_read_splat_ply", "gavis_field_json_write", "gavis_field_json_read", "gavis_debug_project", "gavis_debug_binning",

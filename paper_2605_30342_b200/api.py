@@ -83,6 +83,7 @@ class Context:
         # device objects of this context, released before it (the C ABI requires
         # scenes and fields to be destroyed before their context)
         self._children = weakref.WeakSet()
+        self.precision = "certified"
 
     def close(self) -> None:
         if self.h:
@@ -119,6 +120,7 @@ class Context:
         modes = {"certified": N.PRECISION_CERTIFIED, "exact": N.PRECISION_EXACT}
         require(precision in modes, "precision must be 'certified' or 'exact'")
         N.check(self.lib.gavis_ctx_set_precision(self.h, C.c_int32(modes[precision])))
+        self.precision = precision
 
     def counters(self):
         """(pixels recomputed in fp64 by the certified blend, candidates re-scored
@@ -386,6 +388,29 @@ def render(ctx: Context, scene, field: Optional[DeviceField], cams: Sequence[Cam
     return out
 
 
+def render_mixtures(ctx: Context, scene, field: Optional[DeviceField], cam: CameraView,
+                    rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(),
+                    splat_visibility=None):
+    """render_entropy's mixtures_out (uncertainty.hpp:207-230) via gavis_ua_mixtures:
+    (offsets[P+1], components[K, 8] = w*, v, mean rgb, var rgb, prior w0, residual T*, H)."""
+    ds = _as_dev(ctx, scene)
+    P = cam.width * cam.height
+    off = np.zeros(P + 1, np.int64)
+    prior, resid, H = np.zeros(max(1, P)), np.zeros(max(1, P)), np.zeros(max(1, P))
+    vis = None if splat_visibility is None else np.ascontiguousarray(splat_visibility, np.float64)
+    if vis is not None and vis.size == 0:
+        vis = np.zeros(1)
+    cc = camera_c(cam)
+    args = (ctx.h, ds.h, field.h if field is not None else None, _ptr(vis), C.byref(cc),
+            C.byref(raster_c(rc)), C.byref(unc_c(uc)))
+    N.check(ctx.lib.gavis_ua_mixtures(*args, _ptr(off), None, C.c_int64(0), _ptr(prior), _ptr(resid), _ptr(H)))
+    K = int(off[-1])
+    comps = np.zeros((max(1, K), 8))
+    if K > 0:
+        N.check(ctx.lib.gavis_ua_mixtures(*args, _ptr(off), _ptr(comps), C.c_int64(K), None, None, None))
+    return off, comps[:K], prior[:P], resid[:P], H[:P]
+
+
 def rasterize(ctx: Context, scene, cam: CameraView, rc: RasterConfig = RasterConfig()) -> RenderOutput:
     r = render(ctx, scene, None, [cam], rc, UncertaintyConfig(), rgb=True, depth=True, transmittance=True)
     return RenderOutput(cam.width, cam.height, r["rgb"], r["depth"], r["transmittance"])
@@ -429,6 +454,39 @@ def select_nbv(ctx: Context, scene, field: DeviceField, candidates: Sequence[Cam
                                      C.byref(raster_c(rc)), C.byref(unc_c(uc)), C.c_int32(1 if with_rgb else 0),
                                      _ptr(scores), C.byref(best)))
     return NbvResult(best.value, scores)
+
+
+def score_views(ctx: Context, scene, field: DeviceField, cams: Sequence[CameraView],
+                rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(),
+                with_rgb: bool = False, exact: bool = False) -> np.ndarray:
+    """image_entropy(render_entropy(cam)) per camera (planner.hpp:125-131), with the
+    context's precision or, with exact=True, the fp64 blend."""
+    if len(cams) == 0:
+        return np.zeros(0)
+    prev = ctx.precision
+    if exact and prev != "exact":
+        ctx.set_precision("exact")
+    try:
+        return render(ctx, scene, field, cams, rc, uc, scores=True, with_rgb=with_rgb)["scores"]
+    finally:
+        if exact and prev != "exact":
+            ctx.set_precision(prev)
+
+
+def select_nbv_sharded(ctx: Context, scene, field: DeviceField, candidates: Sequence[CameraView],
+                       rank: int, world: int, dist=None, rc: RasterConfig = RasterConfig(),
+                       uc: UncertaintyConfig = UncertaintyConfig(), with_rgb: bool = False) -> NbvResult:
+    """select_nbv over candidates sharded across ranks (one process per GPU): each
+    rank scores its contiguous block, the scores are all-gathered, contenders of the
+    certified argmax are re-scored in fp64 on their owning ranks (parallel.py)."""
+    from . import parallel
+    require(len(candidates) > 0, "select_nbv: candidate list must be nonempty")
+    best, scores = parallel.select_nbv_sharded(
+        lambda lo, hi: score_views(ctx, scene, field, candidates[lo:hi], rc, uc, with_rgb),
+        len(candidates), rank, world, dist,
+        rescore=None if ctx.precision == "exact" else
+        (lambda idx: score_views(ctx, scene, field, [candidates[i] for i in idx], rc, uc, exact=True)))
+    return NbvResult(best, scores)
 
 
 def nbv_loop(ctx: Context, scene, field: DeviceField, candidates: Sequence[CameraView], steps: int,

@@ -1502,6 +1502,99 @@ gavis_status gavis_ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_fie
   });
 }
 
+gavis_status gavis_ua_mixtures(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
+                               const double* splat_visibility, const gavis_camera* cam,
+                               const gavis_raster_config* rc, const gavis_uncertainty_config* uc,
+                               int64_t* offsets, gavis_mixture_component* components,
+                               int64_t capacity, double* prior_weight,
+                               double* residual_transmittance, double* entropy) {
+  return guard([&] {
+    require(c && s && cam && rc && uc && offsets, "null argument");
+    validate_raster(rc);
+    double hl_q0 = 0.0;
+    validate_unc(uc, &hl_q0);
+    validate_camera(*cam);
+    check_scene_field(s, f);
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    c->use();
+    const int64_t N = s->dev.n;
+    const int64_t P = (int64_t)cam->width * cam->height;
+    BinOpts o;
+    o.ua = true;
+    o.field = f;
+    if (!f) {
+      require(splat_visibility != nullptr || N == 0,
+              "mixtures need a field or per-particle splat visibility");
+      if (N > 0) {
+        double* d = (double*)c->buf("vis_given", sizeof(double) * N);
+        CK(cudaMemcpyAsync(d, splat_visibility, sizeof(double) * N, cudaMemcpyHostToDevice,
+                           c->stream));
+        o.vis_given_dev = d;
+      }
+    }
+    o.beta = uc->beta;
+    o.o0b = uc->prior_opacity * (1.0 - uc->beta);
+    o.hl_const = 3.0 * std::log(uc->color_sigma);
+    int* err = nullptr;
+    if (uc->variance_provider == 1) {
+      require(s->var != nullptr || N == 0,
+              "variance_provider sh_propagation requires coeff_variances");
+      o.var = s->var;
+      o.var_degree = s->var_degree;
+      err = (int*)c->buf("err_flag", sizeof(int));
+      CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+      o.err_flag = err;
+    }
+    Binned b = bin_batch(c, s, cam, 1, rc, o);
+    if (err) {
+      CK(cudaMemcpyAsync(c->pinned + 2, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      require(c->pinned[2] == 0, "propagated color variance must be positive");
+    }
+    MixtureArgs m;
+    m.scene = s->dev;
+    m.cam = b.dcams;
+    m.tile_size = rc->tile_size;
+    m.cutoff = rc->transmittance_cutoff;
+    m.amax = rc->alpha_clamp_max;
+    m.hl_q0 = hl_q0;
+    m.var_const = uc->color_sigma * uc->color_sigma;
+    m.geo = b.geo;
+    m.ua = b.ua;
+    m.ranges = b.ranges;
+    m.vals = b.vals;
+    m.var = o.var;
+    m.var_degree = o.var_degree;
+    m.counts = (int64_t*)c->buf("mix_counts", sizeof(int64_t) * std::max<int64_t>(1, P));
+    m.prior = (double*)c->buf("mix_prior", sizeof(double) * std::max<int64_t>(1, P));
+    m.resid = (double*)c->buf("mix_resid", sizeof(double) * std::max<int64_t>(1, P));
+    m.entropy = (double*)c->buf("mix_entropy", sizeof(double) * std::max<int64_t>(1, P));
+    c->run("mixtures", [&] { launch_mixtures(m, P, c->stream); });
+    std::vector<int64_t> cnt((size_t)P);
+    if (P > 0)
+      CK(cudaMemcpyAsync(cnt.data(), m.counts, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, c->stream));
+    copy_out(c, prior_weight, m.prior, P);
+    copy_out(c, residual_transmittance, m.resid, P);
+    copy_out(c, entropy, m.entropy, P);
+    c->sync();
+    offsets[0] = 0;
+    for (int64_t p = 0; p < P; ++p) offsets[p + 1] = offsets[p] + cnt[p];
+    const int64_t K = offsets[P];
+    if (components && K > 0) {
+      require(capacity >= K, "mixtures: capacity is smaller than offsets[W*H]");
+      int64_t* doff = (int64_t*)c->buf("mix_offsets", sizeof(int64_t) * (P + 1));
+      CK(cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, c->stream));
+      m.offsets = doff;
+      m.comps = (double*)c->buf("mix_comps", sizeof(double) * 8 * K);
+      c->run("mixtures", [&] { launch_mixtures(m, P, c->stream); });
+      static_assert(sizeof(gavis_mixture_component) == 8 * sizeof(double), "component layout");
+      CK(cudaMemcpyAsync(components, m.comps, sizeof(double) * 8 * K, cudaMemcpyDeviceToHost,
+                         c->stream));
+      c->sync();
+    }
+  });
+}
+
 gavis_status gavis_select_nbv(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
                               const gavis_camera* cams, int32_t n_cams,
                               const gavis_raster_config* rc, const gavis_uncertainty_config* uc,

@@ -137,6 +137,27 @@ struct UaBlendArgs {
   float cert_sum = 0.f;            // relative window per unit of sum a/(1-a)
 };
 
+// Per-pixel mixtures of the entropy track for one view (kernels_mixture.cu).
+struct MixtureArgs {
+  SceneDev scene;
+  const DevCam* cam = nullptr;
+  int tile_size = 16;
+  double cutoff = 1e-4, amax = 0.99, hl_q0 = 0.0, var_const = 0.01;
+  const GeoRec* geo = nullptr;
+  const UaRec* ua = nullptr;
+  const uint2* ranges = nullptr;
+  const uint32_t* vals = nullptr;
+  const float* var = nullptr;  // sh_propagation coefficient variances or null
+  int var_degree = -1;
+  // pass 1 (comps == null): counts, prior, resid, entropy; pass 2: comps at offsets
+  int64_t* counts = nullptr;
+  double* prior = nullptr;
+  double* resid = nullptr;
+  double* entropy = nullptr;
+  const int64_t* offsets = nullptr;
+  double* comps = nullptr;  // [K][8]
+};
+
 struct QueryArgs {
   const double* gamma = nullptr;
   const uint8_t* virt = nullptr;
@@ -183,6 +204,7 @@ int ua_score_parts(int tile_size);
 void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,
                   cudaStream_t s);
 void launch_query(const QueryArgs& a, cudaStream_t s);
+void launch_mixtures(const MixtureArgs& a, int64_t P, cudaStream_t s);
 // unseen[k] *= 1 - vis[v*N + n_real + k] for v = 0..V-1 in order.
 void launch_density_update(double* unseen, const double* vis, int V, int64_t N, int64_t n_real,
                            int64_t n_virtual, cudaStream_t s);

@@ -44,8 +44,21 @@ struct Pixel {
   float2 bp[Col<LC>::NP];  // SH basis at the pixel ray, as pairs
 };
 
-// SH basis at the pixel ray as fp32 pairs: CameraView::pixel_ray
-// (model.hpp:83-86) + eval_real_sh_block at the ray (raster.hpp:200-201).
+// SH basis at the pixel ray in fp64: CameraView::pixel_ray (model.hpp:83-86)
+// + eval_real_sh_block at the ray (raster.hpp:200-201).
+template <int LC>
+__device__ __forceinline__ void pixel_basis_d(const DevCam& c, int px, int py, double* bd) {
+  const double cxp = px + 0.5, cyp = py + 0.5;
+  const double dc0 = (cxp - c.cx) / c.fx, dc1 = (cyp - c.cy) / c.fy, dc2 = 1.0;
+  const double r0 = c.R[0] * dc0 + c.R[1] * dc1 + c.R[2] * dc2;
+  const double r1 = c.R[3] * dc0 + c.R[4] * dc1 + c.R[5] * dc2;
+  const double r2 = c.R[6] * dc0 + c.R[7] * dc1 + c.R[8] * dc2;
+  const double n2 = r0 * r0 + r1 * r1 + r2 * r2;
+  const double nn = n2 > 0.0 ? sqrt(n2) : 1.0;
+  eval_sh<LC>(r0 / nn, r1 / nn, r2 / nn, bd);
+}
+
+// The same basis as fp32 pairs (the packed colour dot products).
 template <int LC>
 __device__ __forceinline__ void pixel_basis(const DevCam& c, int px, int py, float2* bp) {
   constexpr int NB = Col<LC>::NB;

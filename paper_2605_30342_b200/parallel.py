@@ -15,7 +15,7 @@ library in production and over gloo on CPU in the tests.
 """
 from __future__ import annotations
 
-from typing import Callable, List, Sequence, Tuple
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -54,13 +54,53 @@ def gather_scores(local: np.ndarray, n_total: int, rank: int, world: int, dist=N
     return np.concatenate(out) if out else np.zeros(0)
 
 
+CERT_SCORE_REL = 1e-4  # same window as the library's single-GPU select (gavis_abi.cu)
+
+
+def contenders(scores: np.ndarray, window: float = CERT_SCORE_REL) -> List[int]:
+    """Candidates whose certified fp32 score lies within `window` (relative) of the
+    best: the only ones that can be the fp64 argmax."""
+    b = first_max(scores)
+    lo = scores[b] - window * abs(scores[b])
+    return [i for i in range(len(scores)) if scores[i] >= lo]
+
+
 def select_nbv_sharded(score_block: Callable[[int, int], np.ndarray], n_candidates: int, rank: int,
-                       world: int, dist=None) -> Tuple[int, np.ndarray]:
-    """score_block(lo, hi) scores candidates [lo, hi) on this rank."""
+                       world: int, dist=None,
+                       rescore: Optional[Callable[[List[int]], np.ndarray]] = None,
+                       window: float = CERT_SCORE_REL) -> Tuple[int, np.ndarray]:
+    """score_block(lo, hi) scores candidates [lo, hi) on this rank (certified fp32
+    path). With `rescore(indices)` (exact fp64 scores of global candidate indices
+    of this rank's block), every contender within `window` of the best is re-scored
+    on the rank that owns it and the first-max is taken again, so the argmax is
+    the fp64 one whatever the rank count (the library does the same on one GPU)."""
     lo, hi = shard_range(n_candidates, rank, world)
     local = score_block(lo, hi) if hi > lo else np.zeros(0)
     scores = gather_scores(local, n_candidates, rank, world, dist)
+    if rescore is None or n_candidates == 0:
+        return first_max(scores), scores
+    cont = contenders(scores, window)
+    if len(cont) < 2:
+        return first_max(scores), scores
+    mine = [i for i in cont if lo <= i < hi]
+    exact = np.zeros(n_candidates)
+    if mine:
+        exact[mine] = np.asarray(rescore(mine), np.float64)
+    if world > 1 and dist is not None:
+        exact = _allreduce_sum_host(exact, dist)
+    scores = scores.copy()
+    scores[cont] = exact[cont]
     return first_max(scores), scores
+
+
+def _allreduce_sum_host(x: np.ndarray, dist) -> np.ndarray:
+    """Sum of per-rank vectors whose non-zero entries are disjoint (exact: x + 0 = x)."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" \
+        else torch.device("cpu")
+    t = torch.as_tensor(np.asarray(x, np.float64), device=dev).clone()
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().numpy()
 
 
 def construct_field_sharded(partial_field: Callable[[int, int], object], n_views: int, rank: int,

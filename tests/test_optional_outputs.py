@@ -102,3 +102,39 @@ def test_device_correlation_hook_scores(ctx):
     assert np.max(np.abs(res.scores - scores) / np.maximum(1.0, np.abs(scores))) <= 1e-9
     plain = api.select_nbv(ctx, scene, f, c["candidates"][:6], RC, UncertaintyConfig())
     assert np.all(res.scores < plain.scores)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("provider", [0, 1])
+def test_device_mixtures_match_oracle(ctx, provider):
+    """gavis_ua_mixtures (render_entropy mixtures_out, uncertainty.hpp:207-230)
+    against the oracle restatement: CSR offsets bit-exact, components and the
+    per-pixel prior weight / residual transmittance / entropy to fp64 rounding."""
+    from paper_2605_30342_b200 import api
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    cam = c["candidates"][1]
+    rng = np.random.default_rng(3)
+    vis = rng.uniform(0, 1, scene.num_particles)
+    vis[rng.uniform(size=scene.num_particles) < 0.2] = 0.0
+    uc = UncertaintyConfig(variance_provider=provider)
+    ds = ctx.upload(scene)
+    if provider == 1:
+        var = rng.uniform(0.01, 0.2, size=(scene.num_particles, 3, 4)).astype(np.float32)
+        ds.set_coeff_variances(var, 1)
+        O.set_coeff_variances(var.astype(np.float64), 1)
+    try:
+        off, comp, prior, resid, H = api.render_mixtures(ctx, ds, None, cam, RC, uc, splat_visibility=vis)
+        ooff, ocomp, oprior, oresid, oH = O.render_mixtures(osc, cam, RC, uc, vis)
+    finally:
+        O.set_coeff_variances(None, -1)
+    assert np.array_equal(off, ooff) and off[-1] > 1000
+    assert np.max(np.abs(comp[:, :2] - ocomp[:, :2])) <= 1e-12
+    assert np.max(np.abs(comp[:, 2:5] - ocomp[:, 2:5])) <= 1e-12
+    assert np.max(np.abs(comp[:, 5:] - ocomp[:, 5:]) / ocomp[:, 5:]) <= 1e-12
+    assert np.max(np.abs(prior - oprior)) <= 1e-12 and np.max(np.abs(resid - oresid)) <= 1e-12
+    assert np.max(np.abs(H - oH)) <= 1e-10
+    # consistent with the regular render of the same pixels
+    r = api.render(ctx, ds, None, [cam], RC, uc, entropy=True, invisible_mass=True, splat_visibility=vis)
+    assert np.max(np.abs(r["entropy"] - H)) <= 1e-10

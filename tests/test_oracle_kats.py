@@ -435,3 +435,40 @@ def test_compensated_alpha_closed_forms():
         H, w0, depth = O.render_entropy_core(sc, EXACT_CAM, EXACT_RC, uc, [v])
         # depth = w * z with w = alpha* * 1 at the centre, z = 1
         assert abs(depth[CENTER] - expect) <= 1e-12
+
+
+@pytest.mark.parametrize("provider", [0, 1])
+def test_mixture_dump_consistency(provider):
+    """render_entropy_core's mixtures_out (uncertainty.hpp:207-230): the components
+    reproduce the pixel's entropy, prior weight and residual transmittance
+    (sum w* + T* = 1, sum w* (1 - v) = w0) and match the entropy map."""
+    sc = synth.random_scene(0x5EED, 40)
+    cam = synth.z_camera(48, 40)
+    vis = np.array([synth.SplitMix64(99 + i).next_double() for i in range(40)])
+    vis[::7] = 0.0
+    vis[3::9] = 1.0
+    uc = UncertaintyConfig(color_sigma=0.3, variance_provider=provider)
+    rc = RasterConfig()
+    if provider == 1:
+        O.set_coeff_variances(np.full((40, 3, 4), 0.05) + np.arange(40)[:, None, None] * 1e-3, 1)
+    try:
+        off, comp, prior, resid, H = O.render_mixtures(sc, cam, rc, uc, vis)
+        Href, w0ref, _ = O.render_entropy_core(sc, cam, rc, uc, vis)
+    finally:
+        O.set_coeff_variances(None, -1)
+    assert np.array_equal(H, Href) and np.array_equal(prior, w0ref)
+    assert off[-1] == len(comp) and off[-1] > 100
+    for p in range(cam.width * cam.height):
+        c = comp[off[p]:off[p + 1]]
+        w, v = c[:, 0], c[:, 1]
+        assert np.all(w > 0) and np.all((c[:, 2:5] >= 0) & (c[:, 2:5] <= 1))
+        assert abs(w.sum() + resid[p] - 1.0) <= 1e-12
+        assert abs((w * (1 - v)).sum() - prior[p]) <= 1e-12
+        s = w * v
+        hl = 0.5 * np.log(c[:, 5:8]).sum(axis=1)
+        h = (s[s > 0] * (-np.log(s[s > 0]) + hl[s > 0] + K_GAUSS_ENTROPY)).sum()
+        if prior[p] > 0:
+            h += prior[p] * (-math.log(prior[p]) + K_GAUSS_ENTROPY)
+        assert abs(h - H[p]) <= 1e-12 * max(1.0, abs(H[p]))
+        if provider == 0:
+            assert np.all(c[:, 5:8] == 0.09)

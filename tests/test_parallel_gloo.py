@@ -56,7 +56,27 @@ def _worker(rank, world, port, out_dir):
         return O.select_nbv(osc, gamma, 2, len(views), cands[lo:hi], RC, UC)[1]
 
     best, scores = parallel.select_nbv_sharded(score_block, len(cands), rank, world, dist)
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), gamma=gamma, best=best, scores=scores)
+
+    # certified argmax across shards: an fp32-like score block whose error pushes the
+    # cross-shard duplicate (index 7, rank 1) above its twin (index 2, rank 0); the
+    # contenders are re-scored exactly on their owning ranks and the tie goes back to 2
+    exact = O.select_nbv(osc, gamma, 2, len(views), cands, RC, UC)[1]
+
+    def approx_block(lo, hi):
+        out = exact[lo:hi].copy()
+        for i in range(lo, hi):
+            out[i - lo] *= 1.0 + (1e-9 if i == 7 else -1e-9 * (i % 3))
+        return out
+
+    calls = []
+
+    def rescore(idx):
+        calls.append(list(idx))
+        return exact[idx]
+
+    cbest, cscores = parallel.select_nbv_sharded(approx_block, len(cands), rank, world, dist, rescore=rescore)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), gamma=gamma, best=best, scores=scores,
+             cbest=cbest, cscores=cscores, ncalls=len(calls))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -81,6 +101,22 @@ def test_sharded_field_and_nbv_match_single_process(tmp_path):
     assert int(r0["best"]) == int(r1["best"]) == best_ref
     assert np.max(np.abs(r0["scores"] - scores_ref) / np.maximum(1.0, np.abs(scores_ref))) <= 1e-12
     assert r0["scores"][2] == r0["scores"][7]
+    # certified sharded argmax equals the exact one, identical on both ranks
+    assert int(r0["cbest"]) == int(r1["cbest"]) == best_ref
+    assert np.array_equal(r0["cscores"], r1["cscores"])
+
+
+def test_certified_contenders_rescored_across_shards():
+    """Host logic without processes: a perturbation that would flip the argmax
+    across a shard boundary is undone by re-scoring the contenders."""
+    exact = np.array([1.0, 5.0, 3.0, 5.0, 2.0])
+    approx = exact.copy()
+    approx[3] *= 1 + 1e-8  # fp32 error favours the later duplicate
+    assert parallel.first_max(approx) == 3
+    best, sc = parallel.select_nbv_sharded(lambda lo, hi: approx[lo:hi], len(exact), 0, 1, None,
+                                           rescore=lambda idx: exact[idx])
+    assert best == 1 and sc[3] == exact[3]
+    assert parallel.contenders(approx) == [1, 3]
 
 
 def test_shard_range_partition():
