@@ -30,11 +30,15 @@
 // (cert_base + cert_per_step k + cert_sum S, from the host).
 #include "ua_common.cuh"
 
+#include <cuda_fp16.h>
+#include <cstdlib>
+
 namespace gavis {
 
 namespace {
 
 constexpr int kFastBatch = 192;
+constexpr int kFastBatchMma = 128;
 constexpr float kNegHalfLog2e = -0.72134752044448170f;  // -0.5 / ln 2
 constexpr float kLn2f = 0.69314718055994531f;
 
@@ -62,21 +66,60 @@ struct __align__(16) FGeo {
   float o, depth;
 };
 
-template <int LC, bool RGB, bool ENT>
+// Colour of a (pixel, entry) pair, clamp(sum_i c_i Y_i(ray), 0, 1) per channel
+// (model.hpp:49-62), two ways:
+//  * FFMA: fp32 coefficient rows staged per entry, packed fp32x2 FMAs per pixel
+//    against the pixel's SH basis (48 MACs per pair at degree 3);
+//  * MMA (default): per group of 8 hit entries the warp computes the 32 x 24
+//    colour block [pixels x (entry, channel)] = Y[32 x 16] C[16 x 24] on the
+//    tensor cores with mma.sync m16n8k16 in split fp16 (x = hi + lo, products
+//    hi*hi + hi*lo + lo*hi accumulated in fp32: ~22-bit operands, colour error
+//    ~1e-6), then transposes it through shared memory so each lane reads its
+//    own pixel's colours. Coefficients are split once per tile when staged.
+constexpr int kColWords = 52;  // per staged entry: hi [3][16] f16 (24 words), lo (24), pad (4)
+constexpr int kTrStride = 36;  // floats per pixel row of the warp's colour block (8 entries x 4)
+
+template <int LC, bool RGB, bool ENT, bool MMA>
 struct FStage {
+  static constexpr size_t col_bytes() {
+    return MMA ? sizeof(uint32_t) * kColWords : sizeof(float) * Col<LC>::STRIDE;
+  }
+  static constexpr size_t tr_bytes() { return (RGB && MMA) ? 8 * 32 * kTrStride * sizeof(float) : 0; }
   static constexpr size_t bytes(int batch) {
     return (size_t)batch * (sizeof(FGeo) + sizeof(int4) + (ENT ? sizeof(float4) : 0) +
-                            (RGB ? sizeof(float) * Col<LC>::STRIDE : 0));
+                            (RGB ? col_bytes() : 0)) + tr_bytes();
   }
 };
 
-// Stage entries [base, base+n) of the tile list: the fp32 forms are rounded
-// once here, per tile, not per pixel.
-template <int LC, bool RGB, bool ENT>
+__device__ __forceinline__ uint32_t pack_half2(float x, float y) {
+  const __half2 h = __floats2half2_rn(x, y);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// x = hi + lo with hi, lo fp16 (lo rounds the exact fp32 residual)
+__device__ __forceinline__ void split_half2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x, y);
+  const float2 f = __half22float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack_half2(x - f.x, y - f.y);
+}
+
+__device__ __forceinline__ void hmma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                          uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Stage entries [base, base+n) of the tile list: the fp32 forms (and the fp16
+// colour splits) are computed once here, per tile, not per pixel.
+template <int LC, bool RGB, bool ENT, bool MMA>
 __device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec* geo,
                                              const UaRec* uar, uint32_t base, int n, FGeo* s_geo,
-                                             int4* s_rect, float4* s_ua, float* s_col) {
-  constexpr int V4 = Col<LC>::STRIDE / 4;
+                                             int4* s_rect, float4* s_ua, void* s_col) {
+  constexpr int CS = Col<LC>::STRIDE;
+  constexpr int V4 = CS / 4;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const uint32_t g = a.vals[base + j];
     const GeoRec r = geo[g];
@@ -95,12 +138,39 @@ __device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec*
       s_ua[j] = make_float4((float)u.A, (float)u.B, (float)u.v, (float)(u.hl + kGaussEntropy));
     }
   }
-  if (RGB) {
+  if (RGB && !MMA) {
     const float4* colors4 = reinterpret_cast<const float4*>(a.scene.colors);
     for (int k = threadIdx.x; k < n * V4; k += blockDim.x) {
       const int j = k / V4, qd = k - j * V4;
       const uint32_t g = a.vals[base + j];
       reinterpret_cast<float4*>(s_col)[k] = __ldg(colors4 + (int64_t)g * V4 + qd);
+    }
+  }
+  if (RGB && MMA) {
+    // per (entry, channel, 4 coefficients): hi/lo fp16 words at [j][ch][k/2]
+    constexpr int NB = Col<LC>::NB, NBP = Col<LC>::NBP;
+    uint32_t* w = reinterpret_cast<uint32_t*>(s_col);
+    for (int k = threadIdx.x; k < n * 12; k += blockDim.x) {
+      const int j = k / 12, r = k - j * 12, ch = r >> 2, q = r & 3;
+      const uint32_t g = a.vals[base + j];
+      const float* src = a.scene.colors + (int64_t)g * CS + ch * NBP;
+      float x[4];
+      if (NB == 16) {
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(src) + q);
+        x[0] = v4.x;
+        x[1] = v4.y;
+        x[2] = v4.z;
+        x[3] = v4.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = (4 * q + i < NB) ? __ldg(src + 4 * q + i) : 0.f;
+      }
+      uint32_t h0, l0, h1, l1;
+      split_half2(x[0], x[1], h0, l0);
+      split_half2(x[2], x[3], h1, l1);
+      uint32_t* dst = w + j * kColWords + ch * 8 + 2 * q;
+      *reinterpret_cast<uint2*>(dst) = make_uint2(h0, h1);
+      *reinterpret_cast<uint2*>(dst + 24) = make_uint2(l0, l1);
     }
   }
 }
@@ -114,7 +184,6 @@ struct FPix {
   double R0, R1, R2, DP, H, W0, ED;
   int n_rgb, n_ent;
   bool rd, edn;
-  float2 bp[Col<LC>::NP];
 };
 
 template <int LC, bool EXTRA>
@@ -138,20 +207,105 @@ __device__ __forceinline__ float stop_margin(bool done, float T, float Tprev, fl
   return d / cutoff;
 }
 
-// ---------------------------------------------------------------------------
-// K7f: 16x16 tiles, 256 threads, one pixel each (warp = 8x4 patch), 192-entry
-// shared-memory batches, warp pre-filter, list entries two at a time in
-// straight-line code (masks instead of branches, as in the exact ILP kernel).
+// Two list entries a, b (in list order) composited into one pixel, straight-line:
+// an entry the pixel does not cover, or one past its termination, gets alpha = 0.
 template <int LC, bool RGB, bool ENT, bool EXTRA>
+__device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FGeo& eb,
+                                           const float4& ua, const float4& ub, bool ca, bool cb,
+                                           double cxp, double cyp, float3 cola, float3 colb,
+                                           float amax, float cutoff) {
+  // q in fp64 (splat_alpha, raster.hpp:101-108), then exp on the SFU
+  const double dxa = cxp - ea.mx, dya = cyp - ea.my;
+  const double dxb = cxp - eb.mx, dyb = cyp - eb.my;
+  const double qa = fma(dxa, fma(ea.cb2, dya, ea.ca * dxa), ea.cc * dya * dya);
+  const double qb = fma(dxb, fma(eb.cb2, dyb, eb.ca * dxb), eb.cc * dyb * dyb);
+  const float ala = fminf(ea.o * ex2_approx((float)qa * kNegHalfLog2e), amax);
+  const float alb = fminf(eb.o * ex2_approx((float)qb * kNegHalfLog2e), amax);
+  if (RGB) {
+    const bool ra = ca && !P.rd;
+    const float aa = ra ? ala : 0.f;
+    const float wa = aa * P.T;
+    P.r0 = fmaf(wa, cola.x, P.r0);
+    P.r1 = fmaf(wa, cola.y, P.r1);
+    P.r2 = fmaf(wa, cola.z, P.r2);
+    if (EXTRA) P.dp = fmaf(wa, ea.depth, P.dp);
+    const float fa = 1.f - aa;
+    P.S = fmaf(aa, rcp_approx(fa), P.S);
+    const float Ta = P.T * fa;
+    const bool sa = ra && Ta < cutoff;
+    P.Tp = sa ? P.T : P.Tp;
+    P.T = Ta;
+    const bool rb = cb && !(P.rd || sa);
+    const float ab = rb ? alb : 0.f;
+    const float wb = ab * P.T;
+    P.r0 = fmaf(wb, colb.x, P.r0);
+    P.r1 = fmaf(wb, colb.y, P.r1);
+    P.r2 = fmaf(wb, colb.z, P.r2);
+    if (EXTRA) P.dp = fmaf(wb, eb.depth, P.dp);
+    const float fb = 1.f - ab;
+    P.S = fmaf(ab, rcp_approx(fb), P.S);
+    const float Tb = P.T * fb;
+    const bool sb = rb && Tb < cutoff;
+    P.Tp = sb ? P.T : P.Tp;
+    P.T = Tb;
+    P.rd = P.rd || sa || sb;
+    P.n_rgb += (int)ra + (int)rb;
+  }
+  if (ENT) {
+    // compensated_alpha (uncertainty.hpp:55-59) and the entropy step (:198-222);
+    // ua = (A, B, v, hl + C_H)
+    const bool oa = ca && !P.edn;
+    const float xa = fminf(fmaxf(fmaf(ua.x, ala, ua.y), 0.f), amax);
+    const float xb = fminf(fmaxf(fmaf(ub.x, alb, ub.y), 0.f), amax);
+    const float asa = oa ? xa : 0.f;
+    const float wa = asa * P.Te;
+    const float sa = wa * ua.z;
+    P.w0 = fmaf(wa, 1.f - ua.z, P.w0);
+    if (EXTRA) P.ed = fmaf(wa, ea.depth, P.ed);
+    const float fa = 1.f - asa;
+    P.Se = fmaf(asa, rcp_approx(fa), P.Se);
+    const float Ta = P.Te * fa;
+    const bool ta = oa && Ta < cutoff;
+    P.Tep = ta ? P.Te : P.Tep;
+    P.Te = Ta;
+    const bool ob = cb && !(P.edn || ta);
+    const float asb = ob ? xb : 0.f;
+    const float wb = asb * P.Te;
+    const float sb = wb * ub.z;
+    P.w0 = fmaf(wb, 1.f - ub.z, P.w0);
+    if (EXTRA) P.ed = fmaf(wb, eb.depth, P.ed);
+    const float fb = 1.f - asb;
+    P.Se = fmaf(asb, rcp_approx(fb), P.Se);
+    const float Tb = P.Te * fb;
+    const bool tb = ob && Tb < cutoff;
+    P.Tep = tb ? P.Te : P.Tep;
+    P.Te = Tb;
+    P.edn = P.edn || ta || tb;
+    P.n_ent += (int)oa + (int)ob;
+    // H += s (-ln s + 1/2 ln|Qc| + C_H); s == 0 adds exactly 0
+    const float la = lg2_approx(fmaxf(sa, 1e-37f));
+    const float lb = lg2_approx(fmaxf(sb, 1e-37f));
+    P.h = fmaf(sa, fmaf(-la, kLn2f, ua.w), P.h);
+    P.h = fmaf(sb, fmaf(-lb, kLn2f, ub.w), P.h);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7f: 16x16 tiles, 256 threads, one pixel each (warp = 8x4 patch, lane = GEMM
+// row), shared-memory batches of the tile list, warp pre-filter (one lane per
+// entry against the warp's patch), hit entries in groups of 8 (colours for the
+// group on the tensor cores when MMA), composited two at a time.
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA>
 __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
+  using St = FStage<LC, RGB, ENT, MMA>;
+  constexpr int B = MMA ? kFastBatchMma : kFastBatch;
   constexpr int CS = Col<LC>::STRIDE;
-  constexpr int B = kFastBatch;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   FGeo* s_geo = reinterpret_cast<FGeo*>(s_dyn);
   int4* s_rect = reinterpret_cast<int4*>(s_dyn + B * sizeof(FGeo));
   float4* s_ua = reinterpret_cast<float4*>(s_dyn + B * (sizeof(FGeo) + sizeof(int4)));
-  float* s_col = reinterpret_cast<float*>(s_dyn + B * (sizeof(FGeo) + sizeof(int4) +
-                                                       (ENT ? sizeof(float4) : 0)));
+  unsigned char* s_col = s_dyn + B * (sizeof(FGeo) + sizeof(int4) + (ENT ? sizeof(float4) : 0));
+  float* s_tr = reinterpret_cast<float*>(s_col + (RGB ? B * St::col_bytes() : 0));
 
   const float amax = (float)a.amax, cutoff = (float)a.cutoff;
   const int64_t gt = blockIdx.x;
@@ -161,6 +315,7 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
   const uint2 rg = a.ranges[gt];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tig = lane & 3;  // mma fragment coordinates
   const int64_t N = a.scene.n;
   const GeoRec* geo = a.geo + (int64_t)v * N;
   const UaRec* uar = a.ua + (int64_t)v * N;
@@ -170,7 +325,39 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   const bool inside = px < c.width && py < c.height;
   const double cxp = px + 0.5, cyp = py + 0.5;
   FPix<LC> P;
-  if (RGB) pixel_basis<LC>(c, px, py, P.bp);
+  float2 bp[Col<LC>::NP];           // FFMA colour: SH basis at the pixel ray
+  uint32_t aH[2][4], aL[2][4];      // MMA colour: A fragments (rows = lanes), fp16 hi / lo
+  float* tr = s_tr + warp * 32 * kTrStride;
+  if (RGB && !MMA) pixel_basis<LC>(c, px, py, bp);
+  if (RGB && MMA) {
+    constexpr int NB = Col<LC>::NB;
+    double bd[Col<LC>::NBP];
+    pixel_basis_d<LC>(c, px, py, bd);
+    uint32_t* wb = reinterpret_cast<uint32_t*>(tr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float x0 = 2 * i < NB ? (float)bd[2 * i] : 0.f;
+      const float x1 = 2 * i + 1 < NB ? (float)bd[2 * i + 1] : 0.f;
+      uint32_t h, l;
+      split_half2(x0, x1, h, l);
+      wb[lane * 17 + i] = h;
+      wb[lane * 17 + 8 + i] = l;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int r0 = 16 * m + gq, r1 = r0 + 8;
+      aH[m][0] = wb[r0 * 17 + tig];
+      aH[m][1] = wb[r1 * 17 + tig];
+      aH[m][2] = wb[r0 * 17 + tig + 4];
+      aH[m][3] = wb[r1 * 17 + tig + 4];
+      aL[m][0] = wb[r0 * 17 + 8 + tig];
+      aL[m][1] = wb[r1 * 17 + 8 + tig];
+      aL[m][2] = wb[r0 * 17 + 8 + tig + 4];
+      aL[m][3] = wb[r1 * 17 + 8 + tig + 4];
+    }
+    __syncwarp();
+  }
   P.T = P.Te = 1.f;
   P.Tp = P.Tep = 1.f;
   P.r0 = P.r1 = P.r2 = P.dp = P.h = P.w0 = P.ed = 0.f;
@@ -184,10 +371,11 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
     const bool live = !(P.rd && P.edn);
     if (__syncthreads_count(live) == 0) break;
     const int n = min((uint32_t)B, rg.y - base);
-    fstage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
+    fstage_batch<LC, RGB, ENT, MMA>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
     __syncthreads();
     if (__all_sync(0xffffffffu, !live)) continue;
     for (int j0 = 0; j0 < n; j0 += 32) {
+      if (__all_sync(0xffffffffu, P.rd && P.edn)) break;  // every pixel of the warp finished
       bool hit = false;
       if (j0 + lane < n) {
         const int4 r = s_rect[j0 + lane];
@@ -196,92 +384,73 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
       unsigned hits = __ballot_sync(0xffffffffu, hit);
       if (hits == 0u) continue;
       while (hits != 0u) {
-        const int ja = j0 + __ffs(hits) - 1;
-        hits &= hits - 1u;
-        const bool has_b = hits != 0u;
-        const int jb = has_b ? j0 + __ffs(hits) - 1 : ja;
-        if (has_b) hits &= hits - 1u;
-        const bool ca = in_rect4(s_rect[ja], px, py);
-        const bool cb = has_b && in_rect4(s_rect[jb], px, py);
-        const FGeo& ea = s_geo[ja];
-        const FGeo& eb = s_geo[jb];
-        // q in fp64 (splat_alpha, raster.hpp:101-108), then exp on the SFU
-        const double dxa = cxp - ea.mx, dya = cyp - ea.my;
-        const double dxb = cxp - eb.mx, dyb = cyp - eb.my;
-        const double qa = fma(dxa, fma(ea.cb2, dya, ea.ca * dxa), ea.cc * dya * dya);
-        const double qb = fma(dxb, fma(eb.cb2, dyb, eb.ca * dxb), eb.cc * dyb * dyb);
-        const float ala = fminf(ea.o * ex2_approx((float)qa * kNegHalfLog2e), amax);
-        const float alb = fminf(eb.o * ex2_approx((float)qb * kNegHalfLog2e), amax);
-        if (RGB) {
-          const bool ra = ca && !P.rd;
-          float a0, a1, a2, b0, b1, b2;
-          sh_color<LC>(reinterpret_cast<const float2*>(s_col + ja * CS), P.bp, a0, a1, a2);
-          sh_color<LC>(reinterpret_cast<const float2*>(s_col + jb * CS), P.bp, b0, b1, b2);
-          const float aa = ra ? ala : 0.f;
-          const float wa = aa * P.T;
-          P.r0 = fmaf(wa, a0, P.r0);
-          P.r1 = fmaf(wa, a1, P.r1);
-          P.r2 = fmaf(wa, a2, P.r2);
-          if (EXTRA) P.dp = fmaf(wa, ea.depth, P.dp);
-          const float fa = 1.f - aa;
-          P.S = fmaf(aa, rcp_approx(fa), P.S);
-          const float Ta = P.T * fa;
-          const bool sa = ra && Ta < cutoff;
-          P.Tp = sa ? P.T : P.Tp;
-          P.T = Ta;
-          const bool rb = cb && !(P.rd || sa);
-          const float ab = rb ? alb : 0.f;
-          const float wb = ab * P.T;
-          P.r0 = fmaf(wb, b0, P.r0);
-          P.r1 = fmaf(wb, b1, P.r1);
-          P.r2 = fmaf(wb, b2, P.r2);
-          if (EXTRA) P.dp = fmaf(wb, eb.depth, P.dp);
-          const float fb = 1.f - ab;
-          P.S = fmaf(ab, rcp_approx(fb), P.S);
-          const float Tb = P.T * fb;
-          const bool sb = rb && Tb < cutoff;
-          P.Tp = sb ? P.T : P.Tp;
-          P.T = Tb;
-          P.rd = P.rd || sa || sb;
-          P.n_rgb += (int)ra + (int)rb;
+        // the next (up to) 8 hit entries, in list order
+        int je[8];
+        int ng = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          je[q] = hits != 0u ? j0 + __ffs(hits) - 1 : -1;
+          ng += hits != 0u ? 1 : 0;
+          hits &= hits - 1u;
         }
-        if (ENT) {
-          // compensated_alpha (uncertainty.hpp:55-59) and the entropy step (:198-222)
-          const float4 ua = s_ua[ja], ub = s_ua[jb];  // A, B, v, hl + C_H
-          const bool oa = ca && !P.edn;
-          const float xa = fminf(fmaxf(fmaf(ua.x, ala, ua.y), 0.f), amax);
-          const float xb = fminf(fmaxf(fmaf(ub.x, alb, ub.y), 0.f), amax);
-          const float asa = oa ? xa : 0.f;
-          const float wa = asa * P.Te;
-          const float sa = wa * ua.z;
-          P.w0 = fmaf(wa, 1.f - ua.z, P.w0);
-          if (EXTRA) P.ed = fmaf(wa, ea.depth, P.ed);
-          const float fa = 1.f - asa;
-          P.Se = fmaf(asa, rcp_approx(fa), P.Se);
-          const float Ta = P.Te * fa;
-          const bool ta = oa && Ta < cutoff;
-          P.Tep = ta ? P.Te : P.Tep;
-          P.Te = Ta;
-          const bool ob = cb && !(P.edn || ta);
-          const float asb = ob ? xb : 0.f;
-          const float wb = asb * P.Te;
-          const float sb = wb * ub.z;
-          P.w0 = fmaf(wb, 1.f - ub.z, P.w0);
-          if (EXTRA) P.ed = fmaf(wb, eb.depth, P.ed);
-          const float fb = 1.f - asb;
-          P.Se = fmaf(asb, rcp_approx(fb), P.Se);
-          const float Tb = P.Te * fb;
-          const bool tb = ob && Tb < cutoff;
-          P.Tep = tb ? P.Te : P.Tep;
-          P.Te = Tb;
-          P.edn = P.edn || ta || tb;
-          P.n_ent += (int)oa + (int)ob;
-          // H += s (-ln s + 1/2 ln|Qc| + C_H); s == 0 adds exactly 0
-          const float la = lg2_approx(fmaxf(sa, 1e-37f));
-          const float lb = lg2_approx(fmaxf(sb, 1e-37f));
-          P.h = fmaf(sa, fmaf(-la, kLn2f, ua.w), P.h);
-          P.h = fmaf(sb, fmaf(-lb, kLn2f, ub.w), P.h);
+        if (RGB && MMA && __any_sync(0xffffffffu, !P.rd)) {
+          int my_e = -1;  // B fragment column gq = entry gq of the group
+#pragma unroll
+          for (int q = 0; q < 8; ++q) my_e = gq == q ? je[q] : my_e;
+          uint32_t bh[3][2], bl[3][2];
+          const uint32_t* cw = reinterpret_cast<const uint32_t*>(s_col) + max(my_e, 0) * kColWords;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            bh[ch][0] = my_e >= 0 ? cw[ch * 8 + tig] : 0u;
+            bh[ch][1] = my_e >= 0 ? cw[ch * 8 + tig + 4] : 0u;
+            bl[ch][0] = my_e >= 0 ? cw[24 + ch * 8 + tig] : 0u;
+            bl[ch][1] = my_e >= 0 ? cw[24 + ch * 8 + tig + 4] : 0u;
+          }
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              float d[4] = {0.f, 0.f, 0.f, 0.f};
+              hmma16816(d, aH[m], bh[ch][0], bh[ch][1]);
+              hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
+              hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
+              // C fragment: (row gq | gq+8, cols 2 tig, 2 tig + 1) -> [pixel][entry][channel]
+              const int r0 = 16 * m + gq, r1 = r0 + 8;
+              tr[r0 * kTrStride + (2 * tig) * 4 + ch] = d[0];
+              tr[r0 * kTrStride + (2 * tig + 1) * 4 + ch] = d[1];
+              tr[r1 * kTrStride + (2 * tig) * 4 + ch] = d[2];
+              tr[r1 * kTrStride + (2 * tig + 1) * 4 + ch] = d[3];
+            }
+          }
+          __syncwarp();
         }
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          if (q < ng) {
+            const int ja = je[q];
+            const bool has_b = q + 1 < ng;
+            const int jb = has_b ? je[q + 1] : ja;
+            const bool ca = in_rect4(s_rect[ja], px, py);
+            const bool cb = has_b && in_rect4(s_rect[jb], px, py);
+            float3 cola = make_float3(0.f, 0.f, 0.f), colb = cola;
+            if (RGB && MMA) {
+              const float4 c4a = reinterpret_cast<const float4*>(tr + lane * kTrStride)[q];
+              const float4 c4b = reinterpret_cast<const float4*>(tr + lane * kTrStride)[q + 1];
+              cola = make_float3(__saturatef(c4a.x), __saturatef(c4a.y), __saturatef(c4a.z));
+              colb = make_float3(__saturatef(c4b.x), __saturatef(c4b.y), __saturatef(c4b.z));
+            }
+            if (RGB && !MMA) {
+              const float* sc = reinterpret_cast<const float*>(s_col);
+              sh_color<LC>(reinterpret_cast<const float2*>(sc + ja * CS), bp, cola.x, cola.y, cola.z);
+              sh_color<LC>(reinterpret_cast<const float2*>(sc + jb * CS), bp, colb.x, colb.y, colb.z);
+            }
+            const float4 ua = ENT ? s_ua[ja] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 ub = ENT ? s_ua[jb] : make_float4(0.f, 0.f, 0.f, 0.f);
+            blend_pair<LC, RGB, ENT, EXTRA>(P, s_geo[ja], s_geo[jb], ua, ub, ca, cb, cxp, cyp, cola,
+                                            colb, amax, cutoff);
+          }
+        }
+        if (RGB && MMA) __syncwarp();  // the next group overwrites the colour block
       }
       fold<LC, EXTRA>(P);
     }
@@ -464,16 +633,35 @@ __global__ void __launch_bounds__(512) score_image_kernel(const DevCam* cams, co
   }
 }
 
-template <int LC, bool RGB, bool ENT, bool EXTRA>
-void launch_fast_one(const UaBlendArgs& a, cudaStream_t s) {
-  const size_t sm = FStage<LC, RGB, ENT>::bytes(kFastBatch);
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA>
+void launch_fast_kernel(const UaBlendArgs& a, cudaStream_t s) {
+  using St = FStage<LC, RGB, ENT, MMA>;
+  const size_t sm = St::bytes(MMA ? kFastBatchMma : kFastBatch);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(ua_blend_fast_kernel<LC, RGB, ENT, EXTRA>,
+    cudaFuncSetAttribute(ua_blend_fast_kernel<LC, RGB, ENT, EXTRA, MMA>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  ua_blend_fast_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+  ua_blend_fast_kernel<LC, RGB, ENT, EXTRA, MMA><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+}
+
+// Colour path: the tensor-core GEMM by default, GAVIS_UA_COLOR=ffma selects the
+// packed-FFMA dot products (A/B measurements).
+inline bool colour_mma() {
+  static const bool mma = [] {
+    const char* e = std::getenv("GAVIS_UA_COLOR");
+    return !(e && e[0] == 'f');
+  }();
+  return mma;
+}
+
+template <int LC, bool RGB, bool ENT, bool EXTRA>
+void launch_fast_one(const UaBlendArgs& a, cudaStream_t s) {
+  if (RGB && colour_mma())
+    launch_fast_kernel<LC, RGB, ENT, EXTRA, true>(a, s);
+  else
+    launch_fast_kernel<LC, RGB, ENT, EXTRA, false>(a, s);
 }
 
 template <int LC, bool EXTRA>
