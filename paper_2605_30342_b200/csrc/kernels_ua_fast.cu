@@ -77,7 +77,10 @@ struct __align__(16) FGeo {
 //    ~1e-6), then transposes it through shared memory so each lane reads its
 //    own pixel's colours. Coefficients are split once per tile when staged.
 constexpr int kColWords = 52;  // per staged entry: hi [3][16] f16 (24 words), lo (24), pad (4)
-constexpr int kTrStride = 36;  // floats per pixel row of the warp's colour block (8 entries x 4)
+// floats per pixel row of the warp's colour block, laid out [channel][8 entries]:
+// 26 makes both the fragment stores (STS.64, a (row, entry pair) per lane) and
+// the per-pixel reads (LDS.64, an entry pair per channel) bank-conflict free
+constexpr int kTrStride = 26;
 
 template <int LC, bool RGB, bool ENT, bool MMA>
 struct FStage {
@@ -414,12 +417,10 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
               hmma16816(d, aH[m], bh[ch][0], bh[ch][1]);
               hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
               hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
-              // C fragment: (row gq | gq+8, cols 2 tig, 2 tig + 1) -> [pixel][entry][channel]
+              // C fragment: (row gq | gq+8, cols 2 tig, 2 tig + 1) -> [pixel][channel][entry]
               const int r0 = 16 * m + gq, r1 = r0 + 8;
-              tr[r0 * kTrStride + (2 * tig) * 4 + ch] = d[0];
-              tr[r0 * kTrStride + (2 * tig + 1) * 4 + ch] = d[1];
-              tr[r1 * kTrStride + (2 * tig) * 4 + ch] = d[2];
-              tr[r1 * kTrStride + (2 * tig + 1) * 4 + ch] = d[3];
+              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
             }
           }
           __syncwarp();
@@ -433,11 +434,12 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
             const bool ca = in_rect4(s_rect[ja], px, py);
             const bool cb = has_b && in_rect4(s_rect[jb], px, py);
             float3 cola = make_float3(0.f, 0.f, 0.f), colb = cola;
-            if (RGB && MMA) {
-              const float4 c4a = reinterpret_cast<const float4*>(tr + lane * kTrStride)[q];
-              const float4 c4b = reinterpret_cast<const float4*>(tr + lane * kTrStride)[q + 1];
-              cola = make_float3(__saturatef(c4a.x), __saturatef(c4a.y), __saturatef(c4a.z));
-              colb = make_float3(__saturatef(c4b.x), __saturatef(c4b.y), __saturatef(c4b.z));
+            if (RGB && MMA) {  // entries q, q+1 of the group, own pixel row
+              const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
+              const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
+              const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+              cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
+              colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
             }
             if (RGB && !MMA) {
               const float* sc = reinterpret_cast<const float*>(s_col);
