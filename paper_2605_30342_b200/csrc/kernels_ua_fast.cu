@@ -293,15 +293,119 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
   }
 }
 
+// Word index of the fp16 hi pair w (k = 2w, 2w+1) of entry e, channel ch in a
+// staged colour area, and the offset of the matching lo pair.
+struct ColWordsStaged {  // fstage_batch: [e][hi: ch][8] [lo: ch][8], 52 words per entry
+  static constexpr int kLo = 24;
+  __device__ __forceinline__ int operator()(int e, int ch, int w) const {
+    return e * kColWords + ch * 8 + w;
+  }
+};
+
+// One staged batch of n list entries composited into the warp's 32 pixels: warp
+// pre-filter per 32-entry chunk, hit entries in groups of 8 (their colours on the
+// tensor cores when MMA), two entries at a time through blend_pair.
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA, class CW>
+__device__ __forceinline__ void blend_batch(FPix<LC>& P, int n, const FGeo* s_geo, const int4* s_rect,
+                                            const float4* s_ua, const void* s_col, CW colword,
+                                            float* tr, const uint32_t (&aH)[2][4],
+                                            const uint32_t (&aL)[2][4], const float2* bp, int lane,
+                                            int bx0, int by0, int bx1, int by1, int px, int py,
+                                            double cxp,
+                                            double cyp, float amax, float cutoff) {
+  constexpr int CS = Col<LC>::STRIDE;
+  const int gq = lane >> 2, tig = lane & 3;  // mma fragment coordinates
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      if (__all_sync(0xffffffffu, P.rd && P.edn)) break;  // every pixel of the warp finished
+      bool hit = false;
+      if (j0 + lane < n) {
+        const int4 r = s_rect[j0 + lane];
+        hit = r.x <= bx1 && r.x + r.y >= bx0 && r.z <= by1 && r.z + r.w >= by0;
+      }
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      if (hits == 0u) continue;
+      while (hits != 0u) {
+        // the next (up to) 8 hit entries, in list order
+        int je[8];
+        int ng = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          je[q] = hits != 0u ? j0 + __ffs(hits) - 1 : -1;
+          ng += hits != 0u ? 1 : 0;
+          hits &= hits - 1u;
+        }
+        if (RGB && MMA && __any_sync(0xffffffffu, !P.rd)) {
+          int my_e = -1;  // B fragment column gq = entry gq of the group
+#pragma unroll
+          for (int q = 0; q < 8; ++q) my_e = gq == q ? je[q] : my_e;
+          uint32_t bh[3][2], bl[3][2];
+          const uint32_t* cw = reinterpret_cast<const uint32_t*>(s_col);
+          const int e = max(my_e, 0);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const int w0 = colword(e, ch, tig), w1 = colword(e, ch, tig + 4);
+            bh[ch][0] = my_e >= 0 ? cw[w0] : 0u;
+            bh[ch][1] = my_e >= 0 ? cw[w1] : 0u;
+            bl[ch][0] = my_e >= 0 ? cw[w0 + CW::kLo] : 0u;
+            bl[ch][1] = my_e >= 0 ? cw[w1 + CW::kLo] : 0u;
+          }
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              float d[4] = {0.f, 0.f, 0.f, 0.f};
+              hmma16816(d, aH[m], bh[ch][0], bh[ch][1]);
+              hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
+              hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
+              // C fragment: (row gq | gq+8, cols 2 tig, 2 tig + 1) -> [pixel][channel][entry]
+              const int r0 = 16 * m + gq, r1 = r0 + 8;
+              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
+            }
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          if (q < ng) {
+            const int ja = je[q];
+            const bool has_b = q + 1 < ng;
+            const int jb = has_b ? je[q + 1] : ja;
+            const bool ca = in_rect4(s_rect[ja], px, py);
+            const bool cb = has_b && in_rect4(s_rect[jb], px, py);
+            float3 cola = make_float3(0.f, 0.f, 0.f), colb = cola;
+            if (RGB && MMA) {  // entries q, q+1 of the group, own pixel row
+              const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
+              const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
+              const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+              cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
+              colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
+            }
+            if (RGB && !MMA) {
+              const float* sc = reinterpret_cast<const float*>(s_col);
+              sh_color<LC>(reinterpret_cast<const float2*>(sc + ja * CS), bp, cola.x, cola.y, cola.z);
+              sh_color<LC>(reinterpret_cast<const float2*>(sc + jb * CS), bp, colb.x, colb.y, colb.z);
+            }
+            const float4 ua = ENT ? s_ua[ja] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 ub = ENT ? s_ua[jb] : make_float4(0.f, 0.f, 0.f, 0.f);
+            blend_pair<LC, RGB, ENT, EXTRA>(P, s_geo[ja], s_geo[jb], ua, ub, ca, cb, cxp, cyp, cola,
+                                            colb, amax, cutoff);
+          }
+        }
+        if (RGB && MMA) __syncwarp();  // the next group overwrites the colour block
+      }
+      fold<LC, EXTRA>(P);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K7f: 16x16 tiles, 256 threads, one pixel each (warp = 8x4 patch, lane = GEMM
 // row), shared-memory batches of the tile list, warp pre-filter (one lane per
 // entry against the warp's patch), hit entries in groups of 8 (colours for the
 // group on the tensor cores when MMA), composited two at a time.
-template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA>
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA, int B>
 __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   using St = FStage<LC, RGB, ENT, MMA>;
-  constexpr int B = MMA ? kFastBatchMma : kFastBatch;
   constexpr int CS = Col<LC>::STRIDE;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   FGeo* s_geo = reinterpret_cast<FGeo*>(s_dyn);
@@ -323,8 +427,19 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   const GeoRec* geo = a.geo + (int64_t)v * N;
   const UaRec* uar = a.ua + (int64_t)v * N;
 
+  // warp -> an 8x4 pixel patch of the tile (tried: 16x2 strips 9% slower, rows w
+  // and w+8 39% slower -- the pre-filter box matters more than warp balance)
   const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 4;
+  const int bx1 = bx0 + 7, by1 = by0 + 3;
   const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+else {
+    bx0 = tx * 16;
+    by0 = ty * 16 + warp;
+    bx1 = bx0 + 15;
+    by1 = by0 + 8;
+    px = bx0 + (lane & 15);
+    py = by0 + 8 * (lane >> 4);
+  }
   const bool inside = px < c.width && py < c.height;
   const double cxp = px + 0.5, cyp = py + 0.5;
   FPix<LC> P;
@@ -377,85 +492,9 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
     fstage_batch<LC, RGB, ENT, MMA>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
     __syncthreads();
     if (__all_sync(0xffffffffu, !live)) continue;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      if (__all_sync(0xffffffffu, P.rd && P.edn)) break;  // every pixel of the warp finished
-      bool hit = false;
-      if (j0 + lane < n) {
-        const int4 r = s_rect[j0 + lane];
-        hit = r.x <= bx0 + 7 && r.x + r.y >= bx0 && r.z <= by0 + 3 && r.z + r.w >= by0;
-      }
-      unsigned hits = __ballot_sync(0xffffffffu, hit);
-      if (hits == 0u) continue;
-      while (hits != 0u) {
-        // the next (up to) 8 hit entries, in list order
-        int je[8];
-        int ng = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          je[q] = hits != 0u ? j0 + __ffs(hits) - 1 : -1;
-          ng += hits != 0u ? 1 : 0;
-          hits &= hits - 1u;
-        }
-        if (RGB && MMA && __any_sync(0xffffffffu, !P.rd)) {
-          int my_e = -1;  // B fragment column gq = entry gq of the group
-#pragma unroll
-          for (int q = 0; q < 8; ++q) my_e = gq == q ? je[q] : my_e;
-          uint32_t bh[3][2], bl[3][2];
-          const uint32_t* cw = reinterpret_cast<const uint32_t*>(s_col) + max(my_e, 0) * kColWords;
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            bh[ch][0] = my_e >= 0 ? cw[ch * 8 + tig] : 0u;
-            bh[ch][1] = my_e >= 0 ? cw[ch * 8 + tig + 4] : 0u;
-            bl[ch][0] = my_e >= 0 ? cw[24 + ch * 8 + tig] : 0u;
-            bl[ch][1] = my_e >= 0 ? cw[24 + ch * 8 + tig + 4] : 0u;
-          }
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              float d[4] = {0.f, 0.f, 0.f, 0.f};
-              hmma16816(d, aH[m], bh[ch][0], bh[ch][1]);
-              hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
-              hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
-              // C fragment: (row gq | gq+8, cols 2 tig, 2 tig + 1) -> [pixel][channel][entry]
-              const int r0 = 16 * m + gq, r1 = r0 + 8;
-              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
-              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
-            }
-          }
-          __syncwarp();
-        }
-#pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-          if (q < ng) {
-            const int ja = je[q];
-            const bool has_b = q + 1 < ng;
-            const int jb = has_b ? je[q + 1] : ja;
-            const bool ca = in_rect4(s_rect[ja], px, py);
-            const bool cb = has_b && in_rect4(s_rect[jb], px, py);
-            float3 cola = make_float3(0.f, 0.f, 0.f), colb = cola;
-            if (RGB && MMA) {  // entries q, q+1 of the group, own pixel row
-              const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
-              const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
-              const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
-              cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
-              colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
-            }
-            if (RGB && !MMA) {
-              const float* sc = reinterpret_cast<const float*>(s_col);
-              sh_color<LC>(reinterpret_cast<const float2*>(sc + ja * CS), bp, cola.x, cola.y, cola.z);
-              sh_color<LC>(reinterpret_cast<const float2*>(sc + jb * CS), bp, colb.x, colb.y, colb.z);
-            }
-            const float4 ua = ENT ? s_ua[ja] : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 ub = ENT ? s_ua[jb] : make_float4(0.f, 0.f, 0.f, 0.f);
-            blend_pair<LC, RGB, ENT, EXTRA>(P, s_geo[ja], s_geo[jb], ua, ub, ca, cb, cxp, cyp, cola,
-                                            colb, amax, cutoff);
-          }
-        }
-        if (RGB && MMA) __syncwarp();  // the next group overwrites the colour block
-      }
-      fold<LC, EXTRA>(P);
-    }
+    blend_batch<LC, RGB, ENT, EXTRA, MMA>(P, n, s_geo, s_rect, s_ua, s_col, ColWordsStaged{}, tr, aH, aL,
+                                          bp, lane, bx0, by0, bx1, by1, px, py, cxp, cyp, amax,
+                                          cutoff);
   }
 
   // certification of the stop decisions
@@ -635,17 +674,19 @@ __global__ void __launch_bounds__(512) score_image_kernel(const DevCam* cams, co
   }
 }
 
+// batch of 128 list entries (tried 96: +2%, 160: +3%; 192 leaves 2 CTAs per SM)
 template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA>
 void launch_fast_kernel(const UaBlendArgs& a, cudaStream_t s) {
+  constexpr int B = MMA ? kFastBatchMma : kFastBatch;
   using St = FStage<LC, RGB, ENT, MMA>;
-  const size_t sm = St::bytes(MMA ? kFastBatchMma : kFastBatch);
+  const size_t sm = St::bytes(B);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(ua_blend_fast_kernel<LC, RGB, ENT, EXTRA, MMA>,
+    cudaFuncSetAttribute(ua_blend_fast_kernel<LC, RGB, ENT, EXTRA, MMA, B>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = true;
   }
-  ua_blend_fast_kernel<LC, RGB, ENT, EXTRA, MMA><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+  ua_blend_fast_kernel<LC, RGB, ENT, EXTRA, MMA, B><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
 }
 
 // Colour path: the tensor-core GEMM by default, GAVIS_UA_COLOR=ffma selects the
