@@ -432,14 +432,6 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 4;
   const int bx1 = bx0 + 7, by1 = by0 + 3;
   const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
-else {
-    bx0 = tx * 16;
-    by0 = ty * 16 + warp;
-    bx1 = bx0 + 15;
-    by1 = by0 + 8;
-    px = bx0 + (lane & 15);
-    py = by0 + 8 * (lane >> 4);
-  }
   const bool inside = px < c.width && py < c.height;
   const double cxp = px + 0.5, cyp = py + 0.5;
   FPix<LC> P;
