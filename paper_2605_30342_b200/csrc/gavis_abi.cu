@@ -365,7 +365,12 @@ struct Binned {
   uint32_t* vals = nullptr;
   uint32_t* pair_gid = nullptr;
   uint2* ranges = nullptr;
+  bool narrow = false;  // keys are 32-bit (local tile << rb | depth rank); b.keys == null
 };
+
+// pinned host scratch layout (int32 words)
+constexpr int kPinItems = 4;
+constexpr int kPinWords = 64;
 
 struct BinOpts {
   bool vf_mode = false;
@@ -378,6 +383,7 @@ struct BinOpts {
   const float* var = nullptr;
   int var_degree = -1;
   int* err_flag = nullptr;
+  bool force_wide = false;  // 64-bit (tile << 32 | fp32 depth) keys (reference-form debug keys)
 };
 
 // K1..K5 for one batch of cameras.
@@ -437,39 +443,103 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
   }
   c->run("preprocess", [&] { launch_preprocess(pa, c->stream); }, N > 0 ? 1 : 0);
 
-  int32_t total = 0;
-  if (VN > 0) {
+  // GAVIS_BIN_WIDE=1 selects the 64-bit (tile << 32 | fp32 depth) key path (A/B and
+  // the equivalence test); it is also the path of the reference-form debug keys
+  const char* wide_env = std::getenv("GAVIS_BIN_WIDE");
+  const bool narrow = !o.force_wide && !(wide_env && wide_env[0] == '1');
+  int32_t* P32 = c->pinned;
+  int64_t K = 0, n_items = 0;
+  NarrowArgs na;
+  if (VN > 0 && narrow) {
+    // visible items -> sorted by (view, depth) -> tile counts in that order -> pair offsets
+    uint32_t* items = (uint32_t*)c->buf("items", sizeof(uint32_t) * VN);
+    int32_t* dnum = (int32_t*)c->buf("items_num", sizeof(int32_t));
+    const size_t selb = select_temp_bytes(VN);
+    void* seltmp = c->buf("select_tmp", selb);
+    c->run("select", [&] { select_visible(b.counts, VN, items, dnum, seltmp, selb, c->stream); });
+    CK(cudaMemcpyAsync(P32 + kPinItems, dnum, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    n_items = P32[kPinItems];
+    na.N = N;
+    na.geo = b.geo;
+    na.counts = b.counts;
+    na.n_items = n_items;
+    na.item_slot = items;
+    if (n_items > 0) {
+      uint64_t* ik_a = (uint64_t*)c->buf("item_key_a", sizeof(uint64_t) * n_items);
+      uint64_t* ik_b = (uint64_t*)c->buf("item_key_b", sizeof(uint64_t) * n_items);
+      uint32_t* is_b = (uint32_t*)c->buf("item_slot_b", sizeof(uint32_t) * n_items);
+      na.item_key = ik_a;
+      c->run("item_keys", [&] { launch_item_keys(na, c->stream); });
+      const size_t isb = sort_temp_bytes(n_items);
+      void* itmp = c->buf("sort_tmp", isb);
+      c->run("sort", [&] {
+        uint64_t* kout;
+        uint32_t* vout;
+        radix_sort_pairs(ik_a, ik_b, items, is_b, n_items, 32 + std::max(1, bits_for(V)), itmp, isb,
+                         c->stream, &kout, &vout);
+        na.item_key = kout;
+        na.item_slot_sorted = vout;
+      });
+      na.item_count = (int32_t*)c->buf("item_count", sizeof(int32_t) * (n_items + 1));
+      int32_t* ioff = (int32_t*)c->buf("item_offset", sizeof(int32_t) * (n_items + 1));
+      CK(cudaMemsetAsync(na.item_count + n_items, 0, sizeof(int32_t), c->stream));
+      c->run("depth_order", [&] { launch_depth_order(na, c->stream); });
+      const size_t scb = scan_temp_bytes(n_items + 1);
+      void* stmp = c->buf("scan_tmp", scb);
+      c->run("scan", [&] { exclusive_scan(na.item_count, ioff, n_items + 1, stmp, scb, c->stream); });
+      na.item_offset = ioff;
+      CK(cudaMemcpyAsync(P32, ioff + n_items, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+      c->sync();
+      K = P32[0];
+    }
+  } else if (VN > 0) {
     const size_t sb = scan_temp_bytes(VN);
     void* tmp = c->buf("scan_tmp", sb);
     c->run("scan", [&] { exclusive_scan(b.counts, b.offsets, VN, tmp, sb, c->stream); });
-    CK(cudaMemcpyAsync(c->pinned, b.offsets + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       c->stream));
-    CK(cudaMemcpyAsync(c->pinned + 1, b.counts + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       c->stream));
+    CK(cudaMemcpyAsync(P32, b.offsets + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(P32 + 1, b.counts + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     c->sync();
-    const int64_t K64 = (int64_t)c->pinned[0] + (int64_t)c->pinned[1];
-    invariant(K64 >= 0 && K64 < (int64_t(1) << 31), "pair count overflow in one batch");
-    total = (int32_t)K64;
+    K = (int64_t)P32[0] + (int64_t)P32[1];
   }
-  b.K = total;
-  const int64_t K = b.K;
-  uint64_t* ka = (uint64_t*)c->buf("keys_a", sizeof(uint64_t) * K);
-  uint64_t* kb = (uint64_t*)c->buf("keys_b", sizeof(uint64_t) * K);
+  invariant(K >= 0 && K < (int64_t(1) << 31), "pair count overflow in one batch");
+  b.K = K;
+
   uint32_t* va = (uint32_t*)c->buf("vals_a", sizeof(uint32_t) * K);
   uint32_t* vb = (uint32_t*)c->buf("vals_b", sizeof(uint32_t) * K);
   if (o.vf_mode) b.pair_gid = (uint32_t*)c->buf("pair_gid", sizeof(uint32_t) * K);
-  if (K > 0) {
-    EmitArgs ea;
-    ea.cams = b.dcams;
-    ea.V = V;
-    ea.N = N;
-    ea.geo = b.geo;
-    ea.counts = b.counts;
-    ea.offsets = b.offsets;
-    ea.trect = trect;
+  b.ranges = (uint2*)c->buf("ranges", sizeof(uint2) * std::max<int64_t>(1, b.total_tiles));
+  CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.total_tiles, c->stream));
+  EmitArgs ea;
+  ea.cams = b.dcams;
+  ea.V = V;
+  ea.N = N;
+  ea.geo = b.geo;
+  ea.counts = b.counts;
+  ea.offsets = b.offsets;
+  ea.trect = trect;
+  ea.vals = va;
+  ea.pair_gid = b.pair_gid;
+  if (narrow && K > 0) {
+    b.narrow = true;
+    uint32_t* k32a = (uint32_t*)c->buf("keys32_a", sizeof(uint32_t) * K);
+    uint32_t* k32b = (uint32_t*)c->buf("keys32_b", sizeof(uint32_t) * K);
+    na.keys32 = k32a;
+    na.slot_offset = b.offsets;  // per-slot pair offsets (VF finalize)
+    c->run("emit_keys", [&] { launch_emit_tiles(ea, na, c->stream); });
+    const size_t sb32 = sort32_temp_bytes(K);
+    void* tmp = c->buf("sort32_tmp", sb32);
+    c->run("sort", [&] {
+      radix_sort_pairs32(k32a, k32b, va, vb, K, std::max(1, bits_for(b.total_tiles)), tmp, sb32,
+                         c->stream);
+    });
+    c->run("ranges", [&] { launch_ranges32(k32a, K, b.ranges, c->stream); });
+    b.vals = va;
+    b.keys = nullptr;
+  } else if (K > 0) {
+    uint64_t* ka = (uint64_t*)c->buf("keys_a", sizeof(uint64_t) * K);
+    uint64_t* kb = (uint64_t*)c->buf("keys_b", sizeof(uint64_t) * K);
     ea.keys = ka;
-    ea.vals = va;
-    ea.pair_gid = b.pair_gid;
     c->run("emit_keys", [&] { launch_emit_keys(ea, c->stream); });
     const size_t sb = sort_temp_bytes(K);
     void* tmp = c->buf("sort_tmp", sb);
@@ -477,13 +547,6 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     c->run("sort", [&] {
       radix_sort_pairs(ka, kb, va, vb, K, end_bit, tmp, sb, c->stream, &b.keys, &b.vals);
     });
-  } else {
-    b.keys = ka;
-    b.vals = va;
-  }
-  b.ranges = (uint2*)c->buf("ranges", sizeof(uint2) * std::max<int64_t>(1, b.total_tiles));
-  CK(cudaMemsetAsync(b.ranges, 0, sizeof(uint2) * b.total_tiles, c->stream));
-  if (K > 0) {
     RangesArgs ra;
     ra.cams = b.dcams;
     ra.V = V;
@@ -495,6 +558,8 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     ra.geo = b.geo;
     ra.ranges = b.ranges;
     c->run("ranges", [&] { launch_ranges(ra, c->stream); });
+  } else {
+    b.vals = va;
   }
   return b;
 }
@@ -809,7 +874,7 @@ gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
       }
-      CK(cudaMallocHost(&c->pinned, 64));
+      CK(cudaMallocHost(&c->pinned, sizeof(int32_t) * kPinWords));
       // keep freed scene/field memory in the device pool between uploads
       cudaMemPool_t pool;
       CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1678,8 +1743,18 @@ gavis_status gavis_debug_binning(gavis_ctx* c, const gavis_scene* s, const gavis
     BinOpts o;
     Binned b = bin_batch(c, s, cam, 1, rc, o);
     *n_pairs = b.K;
-    if (keys && b.K > 0)
-      CK(cudaMemcpyAsync(keys, b.keys, sizeof(uint64_t) * b.K, cudaMemcpyDeviceToHost, c->stream));
+    if (keys && b.K > 0) {
+      const uint64_t* dk = b.keys;
+      if (b.narrow) {  // reference-form (tile << 32 | fp32 depth) keys of the sorted pairs
+        uint64_t* wk = (uint64_t*)c->buf("keys_a", sizeof(uint64_t) * b.K);
+        c->run("wide_keys", [&] {
+          launch_wide_keys(b.ranges, b.total_tiles, b.vals, b.pair_gid, b.dcams, b.V, s->dev.n, b.geo,
+                           wk, c->stream);
+        });
+        dk = wk;
+      }
+      CK(cudaMemcpyAsync(keys, dk, sizeof(uint64_t) * b.K, cudaMemcpyDeviceToHost, c->stream));
+    }
     if (particle_ids && b.K > 0)
       CK(cudaMemcpyAsync(particle_ids, b.vals, sizeof(uint32_t) * b.K, cudaMemcpyDeviceToHost,
                          c->stream));

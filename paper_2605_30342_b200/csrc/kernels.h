@@ -59,6 +59,22 @@ struct EmitArgs {
   uint32_t* pair_gid = nullptr;  // VF mode: vals = pair index, pair_gid[pair] = particle
 };
 
+// Depth-ordered binning (kernels_preprocess.cu): particles sorted by depth per
+// view, pairs emitted in that order, then stably sorted by tile id.
+struct NarrowArgs {
+  int64_t N = 0;
+  const GeoRec* geo = nullptr;
+  const int32_t* counts = nullptr;     // [V*N] tiles touched
+  int64_t n_items = 0;                 // visible (view, particle) items
+  const uint32_t* item_slot = nullptr; // [n_items] slots in slot order (selection output)
+  uint64_t* item_key = nullptr;        // [n_items] view << 32 | fp32 depth (sorted)
+  uint32_t* item_slot_sorted = nullptr;
+  int32_t* item_count = nullptr;       // [n_items + 1] tiles of each item, depth order
+  const int32_t* item_offset = nullptr;  // exclusive scan of item_count
+  int32_t* slot_offset = nullptr;      // [V*N] pair offset of each visible slot
+  uint32_t* keys32 = nullptr;          // [K] global tile ids
+};
+
 struct RangesArgs {
   const DevCam* cams = nullptr;
   int V = 0;
@@ -187,6 +203,14 @@ void launch_pack_scene(const PackSceneArgs& a, cudaStream_t s);
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 void launch_emit_keys(const EmitArgs& a, cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
+void launch_item_keys(const NarrowArgs& a, cudaStream_t s);
+void launch_depth_order(const NarrowArgs& a, cudaStream_t s);
+void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s);
+void launch_ranges32(const uint32_t* keys32, int64_t K, uint2* ranges, cudaStream_t s);
+void launch_wide_keys(const uint2* ranges, int64_t total_tiles, const uint32_t* vals,
+                      const uint32_t* pair_gid, const DevCam* cams, int V, int64_t N, const GeoRec* geo,
+                      uint64_t* keys, cudaStream_t s);
+
 void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s);
 void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s);
 void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s);
@@ -219,5 +243,13 @@ size_t sort_temp_bytes(int64_t n);
 void radix_sort_pairs(uint64_t* keys_a, uint64_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
                       int64_t n, int end_bit, void* temp, size_t temp_bytes, cudaStream_t s,
                       uint64_t** keys_out, uint32_t** vals_out);
+size_t sort32_temp_bytes(int64_t n);
+// 32-bit keys (stable); the sorted pairs always end in (keys_a, vals_a).
+void radix_sort_pairs32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                        int64_t n, int end_bit, void* temp, size_t temp_bytes, cudaStream_t s);
+// slots s in [0, n) with counts[s] > 0, in order; *num_out (device) = how many
+size_t select_temp_bytes(int64_t n);
+void select_visible(const int32_t* counts, int64_t n, uint32_t* out, int32_t* num_out, void* temp,
+                    size_t temp_bytes, cudaStream_t s);
 
 }  // namespace gavis

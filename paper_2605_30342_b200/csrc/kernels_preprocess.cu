@@ -393,6 +393,113 @@ __global__ void ranges_kernel(RangesArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Depth-ordered binning (NarrowArgs): instead of sorting 64-bit (tile << 32 |
+// fp32 depth) pair keys, the visible particles of each view are sorted once by
+// (fp64 depth, index) -- the order of project_scene (raster.hpp:124-128) --, the
+// pairs are emitted in that order and then stably radix-sorted by tile id alone
+// (2-3 digit passes over 8-byte pairs instead of 6 over 12-byte pairs). Stability
+// keeps the depth order inside every tile, which is exactly the reference's
+// per-tile list order (splat_binning, raster.hpp:145-164).
+
+// K2b: keys of the visible (view, particle) items, (view << 32 | fp32 depth rtz).
+__global__ void item_keys_kernel(NarrowArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_items) return;
+  const uint32_t slot = a.item_slot[i];
+  const uint32_t v = slot / (uint32_t)a.N;
+  const float df = __double2float_rz(a.geo[slot].depth);
+  a.item_key[i] = ((uint64_t)v << 32) | (uint64_t)__float_as_uint(df);
+}
+
+// K2c: runs of equal fp32 keys ordered by (fp64 depth, index) by the thread at
+// the run's start (the stable sort left them in index order); then every item's
+// tile count, in depth order, for the pair-offset scan.
+__global__ void depth_order_kernel(NarrowArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_items) return;
+  const uint64_t key = a.item_key[i];
+  const bool run_start = i + 1 < a.n_items && a.item_key[i + 1] == key &&
+                         (i == 0 || a.item_key[i - 1] != key);
+  if (run_start) {
+    int64_t j = i;
+    while (j + 1 < a.n_items && a.item_key[j + 1] == key) ++j;
+    uint32_t* sl = a.item_slot_sorted;
+    for (int64_t x = i + 1; x <= j; ++x) {
+      const uint32_t sx = sl[x];
+      const double dx = a.geo[sx].depth;
+      int64_t y = x - 1;
+      while (y >= i) {
+        const uint32_t sy = sl[y];
+        const double dy = a.geo[sy].depth;
+        if (dy < dx || (dy == dx && sy < sx)) break;  // same view: slot order = index order
+        sl[y + 1] = sy;
+        --y;
+      }
+      sl[y + 1] = sx;
+    }
+  }
+}
+
+__global__ void item_counts_kernel(NarrowArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_items) return;
+  a.item_count[i] = a.counts[a.item_slot_sorted[i]];
+}
+
+// K3n: one thread per visible item (depth order) writes its tile pairs (key =
+// global tile id) and records its pair offset under its slot (VF finalize).
+__global__ void emit_tiles_kernel(EmitArgs a, NarrowArgs n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n.n_items) return;
+  const uint32_t slot = n.item_slot_sorted[i];
+  const int v = (int)(slot / (uint32_t)a.N);
+  const uint32_t g = slot - (uint32_t)v * (uint32_t)a.N;
+  const DevCam& c = a.cams[v];
+  const uint2 tr = a.trect[slot];
+  const int tx0 = tr.x & 0xFFFF, tx1 = tr.x >> 16, ty0 = tr.y & 0xFFFF, ty1 = tr.y >> 16;
+  int64_t o = n.item_offset[i];
+  n.slot_offset[slot] = (int32_t)o;
+  for (int ty = ty0; ty <= ty1; ++ty) {
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      n.keys32[o] = (uint32_t)(c.tile_base + (int64_t)ty * c.tiles_x + tx);
+      if (a.pair_gid) {
+        a.vals[o] = (uint32_t)o;
+        a.pair_gid[o] = g;
+      } else {
+        a.vals[o] = g;
+      }
+      ++o;
+    }
+  }
+}
+
+// K5n: tile ranges of the tile-sorted pairs.
+__global__ void ranges32_kernel(const uint32_t* keys32, int64_t K, uint2* ranges) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const uint32_t t = keys32[i];
+  if (i == 0 || keys32[i - 1] != t) ranges[t].x = (uint32_t)i;
+  if (i == K - 1 || keys32[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+}
+
+// Reference-form 64-bit keys (tile << 32 | fp32 depth) of the sorted pairs, for
+// gavis_debug_binning.
+__global__ void wide_keys_kernel(const uint2* ranges, int64_t total_tiles, const uint32_t* vals,
+                                 const uint32_t* pair_gid, const DevCam* cams, int V, int64_t N,
+                                 const GeoRec* geo, uint64_t* keys) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total_tiles) return;
+  int v = 0;
+  while (v + 1 < V && cams[v + 1].tile_base <= t) ++v;
+  const uint2 r = ranges[t];
+  for (uint32_t i = r.x; i < r.y; ++i) {
+    const uint32_t g = pair_gid ? pair_gid[vals[i]] : vals[i];
+    const float df = __double2float_rz(geo[(int64_t)v * N + g].depth);
+    keys[i] = ((uint64_t)t << 32) | (uint64_t)__float_as_uint(df);
+  }
+}
+
 template <int DEG>
 __global__ void query_kernel(QueryArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -432,6 +539,32 @@ void launch_emit_keys(const EmitArgs& a, cudaStream_t s) {
   const int64_t n = (int64_t)a.V * a.N;
   if (n == 0) return;
   emit_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(a);
+}
+
+void launch_item_keys(const NarrowArgs& a, cudaStream_t s) {
+  if (a.n_items > 0) item_keys_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
+}
+
+void launch_depth_order(const NarrowArgs& a, cudaStream_t s) {
+  if (a.n_items == 0) return;
+  depth_order_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
+  item_counts_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
+}
+
+void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s) {
+  if (n.n_items > 0) emit_tiles_kernel<<<blocks_for(n.n_items, 256), 256, 0, s>>>(a, n);
+}
+
+void launch_ranges32(const uint32_t* keys32, int64_t K, uint2* ranges, cudaStream_t s) {
+  if (K > 0) ranges32_kernel<<<blocks_for(K, 256), 256, 0, s>>>(keys32, K, ranges);
+}
+
+void launch_wide_keys(const uint2* ranges, int64_t total_tiles, const uint32_t* vals,
+                      const uint32_t* pair_gid, const DevCam* cams, int V, int64_t N, const GeoRec* geo,
+                      uint64_t* keys, cudaStream_t s) {
+  if (total_tiles > 0)
+    wide_keys_kernel<<<blocks_for(total_tiles, 128), 128, 0, s>>>(ranges, total_tiles, vals, pair_gid,
+                                                                 cams, V, N, geo, keys);
 }
 
 void launch_ranges(const RangesArgs& a, cudaStream_t s) {

@@ -3,6 +3,8 @@
 // tile counts and K4 stable LSD radix sort of (tile << 32 | fp32 depth) keys.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "kernels.h"
 
@@ -37,6 +39,46 @@ void radix_sort_pairs(uint64_t* keys_a, uint64_t* keys_b, uint32_t* vals_a, uint
   if (n > 0) cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, s);
   *keys_out = k.Current();
   *vals_out = v.Current();
+}
+
+size_t sort32_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v, (int)n, 0, 32);
+  return bytes;
+}
+
+void radix_sort_pairs32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
+                        int64_t n, int end_bit, void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (n <= 0) return;
+  cub::DoubleBuffer<uint32_t> k(keys_a, keys_b);
+  cub::DoubleBuffer<uint32_t> v(vals_a, vals_b);
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k, v, (int)n, 0, end_bit, s);
+  if (k.Current() != keys_a) {
+    cudaMemcpyAsync(keys_a, k.Current(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(vals_a, v.Current(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
+  }
+}
+
+namespace {
+struct Touches {
+  const int32_t* counts;
+  __host__ __device__ bool operator()(const uint32_t& s) const { return counts[s] > 0; }
+};
+}  // namespace
+
+size_t select_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceSelect::If(nullptr, bytes, cub::CountingInputIterator<uint32_t>(0), (uint32_t*)nullptr,
+                        (int32_t*)nullptr, (int)n, Touches{nullptr});
+  return bytes;
+}
+
+void select_visible(const int32_t* counts, int64_t n, uint32_t* out, int32_t* num_out, void* temp,
+                    size_t temp_bytes, cudaStream_t s) {
+  cub::DeviceSelect::If(temp, temp_bytes, cub::CountingInputIterator<uint32_t>(0), out, num_out,
+                        (int)n, Touches{counts}, s);
 }
 
 }  // namespace gavis

@@ -404,3 +404,30 @@ def test_parameter_errors(ctx):
         api.render_entropy(ctx, bigger, f, cam, RC, UC)
     with pytest.raises(InvariantError):
         api.accumulate_views(ctx, f, bigger, [cam], RC)
+
+
+def test_narrow_and_wide_binning_agree(ctx, monkeypatch):
+    """The narrow-key binning (depth ranks + 32-bit pair keys, the default) and the
+    64-bit (tile << 32 | fp32 depth) key path produce the same sorted tile lists,
+    hence bit-identical renders and fields (config 3 structure, 4 views per batch)."""
+    c = synth.config3(0, n=80_000, n_train=6, n_candidates=5, res=200)
+    scene, cams = c["scene"], c["candidates"]
+    kw = dict(rgb=True, transmittance=True, entropy=True, invisible_mass=True, scores=True, contributors=True)
+    ds = ctx.upload(scene)
+    ctx.set_batch(4)
+    try:
+        f = api.construct_field(ctx, ds, c["train"], VmfParams(1.0), 2, RC)
+        narrow = api.render(ctx, ds, f, cams, RC, UC, **kw)
+        g_n = f.download().gamma
+        keys_n, ids_n, rng_n = api.debug_binning(ctx, ds, cams[0], RC)
+        monkeypatch.setenv("GAVIS_BIN_WIDE", "1")
+        f2 = api.construct_field(ctx, ds, c["train"], VmfParams(1.0), 2, RC)
+        wide = api.render(ctx, ds, f2, cams, RC, UC, **kw)
+        keys_w, ids_w, rng_w = api.debug_binning(ctx, ds, cams[0], RC)
+    finally:
+        ctx.set_batch(0)
+    assert np.array_equal(g_n, f2.download().gamma)
+    assert set(narrow) == set(wide)
+    for k in narrow:
+        assert np.array_equal(narrow[k], wide[k]), k
+    assert np.array_equal(keys_n, keys_w) and np.array_equal(ids_n, ids_w) and np.array_equal(rng_n, rng_w)
