@@ -466,21 +466,18 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     na.n_items = n_items;
     na.item_slot = items;
     if (n_items > 0) {
-      uint64_t* ik_a = (uint64_t*)c->buf("item_key_a", sizeof(uint64_t) * n_items);
-      uint64_t* ik_b = (uint64_t*)c->buf("item_key_b", sizeof(uint64_t) * n_items);
+      uint32_t* ik_a = (uint32_t*)c->buf("item_key_a", sizeof(uint32_t) * n_items);
+      uint32_t* ik_b = (uint32_t*)c->buf("item_key_b", sizeof(uint32_t) * n_items);
       uint32_t* is_b = (uint32_t*)c->buf("item_slot_b", sizeof(uint32_t) * n_items);
       na.item_key = ik_a;
+      na.view_bits = std::max(1, bits_for(V));
       c->run("item_keys", [&] { launch_item_keys(na, c->stream); });
-      const size_t isb = sort_temp_bytes(n_items);
+      const size_t isb = sort32_temp_bytes(n_items);
       void* itmp = c->buf("sort_tmp", isb);
       c->run("sort", [&] {
-        uint64_t* kout;
-        uint32_t* vout;
-        radix_sort_pairs(ik_a, ik_b, items, is_b, n_items, 32 + std::max(1, bits_for(V)), itmp, isb,
-                         c->stream, &kout, &vout);
-        na.item_key = kout;
-        na.item_slot_sorted = vout;
+        radix_sort_pairs32(ik_a, ik_b, items, is_b, n_items, 32, itmp, isb, c->stream);
       });
+      na.item_slot_sorted = items;
       na.item_count = (int32_t*)c->buf("item_count", sizeof(int32_t) * (n_items + 1));
       int32_t* ioff = (int32_t*)c->buf("item_offset", sizeof(int32_t) * (n_items + 1));
       CK(cudaMemsetAsync(na.item_count + n_items, 0, sizeof(int32_t), c->stream));

@@ -67,7 +67,8 @@ struct NarrowArgs {
   const int32_t* counts = nullptr;     // [V*N] tiles touched
   int64_t n_items = 0;                 // visible (view, particle) items
   const uint32_t* item_slot = nullptr; // [n_items] slots in slot order (selection output)
-  uint64_t* item_key = nullptr;        // [n_items] view << 32 | fp32 depth (sorted)
+  uint32_t* item_key = nullptr;        // [n_items] view | leading depth bits (sorted)
+  int view_bits = 1;                   // bits of the view index in item_key (>= 1)
   uint32_t* item_slot_sorted = nullptr;
   int32_t* item_count = nullptr;       // [n_items + 1] tiles of each item, depth order
   const int32_t* item_offset = nullptr;  // exclusive scan of item_count

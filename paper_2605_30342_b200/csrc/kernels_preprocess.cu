@@ -402,14 +402,17 @@ __global__ void ranges_kernel(RangesArgs a) {
 // keeps the depth order inside every tile, which is exactly the reference's
 // per-tile list order (splat_binning, raster.hpp:145-164).
 
-// K2b: keys of the visible (view, particle) items, (view << 32 | fp32 depth rtz).
+// K2b: 32-bit keys of the visible (view, particle) items: the view in the top
+// view_bits, then the leading bits of the fp32 depth (rounded toward zero, sign
+// bit dropped: depth > near > 0). Monotone in the fp64 depth; runs of equal keys
+// are ordered exactly by depth_order_kernel.
 __global__ void item_keys_kernel(NarrowArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n_items) return;
   const uint32_t slot = a.item_slot[i];
   const uint32_t v = slot / (uint32_t)a.N;
-  const float df = __double2float_rz(a.geo[slot].depth);
-  a.item_key[i] = ((uint64_t)v << 32) | (uint64_t)__float_as_uint(df);
+  const uint32_t db = __float_as_uint(__double2float_rz(a.geo[slot].depth));  // < 2^31
+  a.item_key[i] = (v << (32 - a.view_bits)) | (db >> (a.view_bits - 1));
 }
 
 // K2c: runs of equal fp32 keys ordered by (fp64 depth, index) by the thread at
@@ -418,7 +421,7 @@ __global__ void item_keys_kernel(NarrowArgs a) {
 __global__ void depth_order_kernel(NarrowArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n_items) return;
-  const uint64_t key = a.item_key[i];
+  const uint32_t key = a.item_key[i];
   const bool run_start = i + 1 < a.n_items && a.item_key[i + 1] == key &&
                          (i == 0 || a.item_key[i - 1] != key);
   if (run_start) {
