@@ -284,7 +284,8 @@ def run_ours(args):
     for _ in range(args.warmup):
         res = step()
     ctx.set_profiling(True)
-    KERNELS = ("ua_blend", "ua_redo", "preprocess", "sort", "emit_keys", "ranges", "scan", "score")
+    KERNELS = ("ua_blend", "ua_redo", "preprocess", "select", "item_keys", "sort", "depth_order", "scan",
+               "emit_keys", "ranges", "score")
     for k in KERNELS:
         ctx.kernel_time(k, reset=True)
     redo0, resc0 = ctx.counters()

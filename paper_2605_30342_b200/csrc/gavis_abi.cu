@@ -768,8 +768,9 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     double* dscores = nullptr;
     if (do_ent) {
       dscores = (double*)c->buf("scores", sizeof(double) * V);
+      double* part = (double*)c->buf("score_partial", sizeof(double) * V * score_partials_per_view());
       c->run("score", [&] {
-        launch_score_image(b.dcams, V, ua.entropy, ua.edepth, ua.corr_lambda, dscores, c->stream);
+        launch_score_image(b.dcams, V, ua.entropy, ua.edepth, ua.corr_lambda, part, dscores, c->stream);
       });
     }
     copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P);

@@ -141,7 +141,6 @@ struct UaBlendArgs {
   double* edepth = nullptr;
   int32_t* rgb_contrib = nullptr;
   int32_t* ent_contrib = nullptr;
-  double* tile_score = nullptr;  // [total_tiles] per-tile entropy sum
   double corr_lambda = 0.0;      // > 0: correlation hook in the image score
   bool do_rgb = true, do_ent = true;
   // Certified fp32 path (kernels_ua_fast.cu): pixels whose early-termination
@@ -223,11 +222,8 @@ void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s);
 // image_entropy per view: fixed-order fold of the per-pixel entropy image
 // (with the correlation hook when corr_lambda > 0; edepth must then be set).
 void launch_score_image(const DevCam* cams, int V, const double* entropy, const double* edepth,
-                        double corr_lambda, double* scores, cudaStream_t s);
-// Entropy partials per tile written by the UA blend (8 patches per 16x16 tile).
-int ua_score_parts(int tile_size);
-void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,
-                  cudaStream_t s);
+                        double corr_lambda, double* partial, double* scores, cudaStream_t s);
+int score_partials_per_view();
 void launch_query(const QueryArgs& a, cudaStream_t s);
 void launch_mixtures(const MixtureArgs& a, int64_t P, cudaStream_t s);
 // unseen[k] *= 1 - vis[v*N + n_real + k] for v = 0..V-1 in order.

@@ -40,7 +40,6 @@ __global__ void __launch_bounds__(128, 5) ua_blend_tile2_kernel(UaBlendArgs a) {
   UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
   float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
                                                             (ENT ? sizeof(UaRec) : 0)));
-  __shared__ double s_red[4];
   load_math_tables();
 
   const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
@@ -106,14 +105,6 @@ __global__ void __launch_bounds__(128, 5) ua_blend_tile2_kernel(UaBlendArgs a) {
   }
   pixel_finish<LC, RGB, ENT, EXTRA>(P0, a, c, px, py0, in0);
   pixel_finish<LC, RGB, ENT, EXTRA>(P1, a, c, px, py1, in1);
-  if (ENT && a.tile_score) {
-    double h = (in0 ? score_term(P0, a) : 0.0) + (in1 ? score_term(P1, a) : 0.0);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
-    if (lane == 0) s_red[warp] = h;
-    __syncthreads();
-    if (tid == 0) a.tile_score[gt] = ((s_red[0] + s_red[1]) + s_red[2]) + s_red[3];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -128,7 +119,6 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
   float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
                                                             (ENT ? sizeof(UaRec) : 0)));
-  __shared__ double s_red[kWarps];
   load_math_tables();
 
   const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
@@ -144,7 +134,6 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   const int64_t N = a.scene.n;
   const GeoRec* geo = a.geo + (int64_t)v * N;
   const UaRec* uar = a.ua + (int64_t)v * N;
-  double tile_h = 0.0;
 
   for (int round = 0; round < rounds; ++round) {
     const int li = round * kThreads + tid;
@@ -172,22 +161,8 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
       }
     }
     pixel_finish<LC, RGB, ENT, EXTRA>(P, a, c, px, py, inside);
-    if (ENT && a.tile_score) {
-      double h = inside ? score_term(P, a) : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
-      if (lane == 0) s_red[warp] = h;
-      __syncthreads();
-      if (tid == 0) {
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) sum += s_red[w];
-        tile_h += sum;
-      }
-    }
     __syncthreads();
   }
-  if (ENT && a.tile_score && tid == 0) a.tile_score[gt] = tile_h;
 }
 
 // ---------------------------------------------------------------------------
@@ -207,7 +182,6 @@ __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
   UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + BATCH * (sizeof(GeoRec) + sizeof(int4)));
   float* s_col = reinterpret_cast<float*>(s_dyn + BATCH * (sizeof(GeoRec) + sizeof(int4) +
                                                            (ENT ? sizeof(UaRec) : 0)));
-  __shared__ double s_red[8];
   load_math_tables();
 
   const double amax = a.amax, cutoff = a.cutoff;
@@ -323,34 +297,6 @@ __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
     }
   }
   pixel_finish<LC, RGB, ENT, EXTRA>(P, a, c, px, py, inside);
-  if (ENT && a.tile_score) {
-    double h = inside ? score_term(P, a) : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
-    if (lane == 0) s_red[warp] = h;
-    __syncthreads();
-    if (tid == 0) {
-      double sum = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) sum += s_red[w];
-      a.tile_score[gt] = sum;
-    }
-  }
-}
-
-// K8: image score per view = fold of its per-tile partials in tile order, one warp
-// per view (lane-contiguous chunks, then a fixed shuffle tree).
-__global__ void score_kernel(const DevCam* cams, int V, const double* tile_score, double* scores) {
-  const int v = blockIdx.x;
-  const int lane = threadIdx.x;
-  const DevCam& c = cams[v];
-  const int64_t nt = (int64_t)c.tiles_x * c.tiles_y;
-  const int64_t lo = nt * lane / 32, hi = nt * (lane + 1) / 32;
-  double sum = 0.0;
-  for (int64_t i = lo; i < hi; ++i) sum += tile_score[c.tile_base + i];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-  if (lane == 0) scores[v] = sum;
 }
 
 template <class K>
@@ -415,8 +361,6 @@ void launch_lc(const UaBlendArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-int ua_score_parts(int /*tile_size*/) { return 1; }
-
 void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s) {
   if (a.total_tiles == 0) return;
   switch (a.scene.color_degree) {
@@ -428,11 +372,5 @@ void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s) {
   }
 }
 
-void launch_score(const DevCam* cams, int V, int parts, const double* tile_score, double* scores,
-                  cudaStream_t s) {
-  (void)parts;
-  if (V == 0) return;
-  score_kernel<<<V, 32, 0, s>>>(cams, V, tile_score, scores);
-}
 
 }  // namespace gavis

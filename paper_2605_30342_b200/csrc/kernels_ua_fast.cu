@@ -639,21 +639,26 @@ __global__ void __launch_bounds__(256) ua_redo_kernel(UaBlendArgs a) {
   }
 }
 
-// K8: image_entropy (uncertainty.hpp:264-278) per view, one block per view:
-// thread t folds pixels t, t+512, ... in order, then a fixed reduction tree.
-__global__ void __launch_bounds__(512) score_image_kernel(const DevCam* cams, const double* entropy,
+// K8: image_entropy (uncertainty.hpp:264-278) per view in two fixed-order
+// stages: block (chunk, view) folds its pixels (thread t: t, t + 256, ...), a
+// shuffle tree and the 8 warp sums in order; then one warp per view folds the
+// chunk partials (lane-contiguous blocks, shuffle tree). Deterministic.
+constexpr int kScoreChunks = 64;
+
+__global__ void __launch_bounds__(256) score_image_kernel(const DevCam* cams, const double* entropy,
                                                           const double* edepth, double lambda,
-                                                          double* scores) {
-  __shared__ double s_red[16];
-  const DevCam& c = cams[blockIdx.x];
+                                                          double* partial) {
+  __shared__ double s_red[8];
+  const DevCam& c = cams[blockIdx.y];
   const int64_t P = (int64_t)c.width * c.height;
+  const int64_t lo = P * blockIdx.x / kScoreChunks, hi = P * (blockIdx.x + 1) / kScoreChunks;
   const double* H = entropy + c.pix_base;
   double sum = 0.0;
   if (lambda > 0.0) {
     const double* d = edepth + c.pix_base;
-    for (int64_t i = threadIdx.x; i < P; i += 512) sum += H[i] - H[i] * exp(-d[i] / lambda);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += 256) sum += H[i] - H[i] * exp(-d[i] / lambda);
   } else {
-    for (int64_t i = threadIdx.x; i < P; i += 512) sum += H[i];
+    for (int64_t i = lo + threadIdx.x; i < hi; i += 256) sum += H[i];
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
@@ -661,9 +666,19 @@ __global__ void __launch_bounds__(512) score_image_kernel(const DevCam* cams, co
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < 16; ++w) s += s_red[w];
-    scores[blockIdx.x] = s;
+    for (int w = 0; w < 8; ++w) s += s_red[w];
+    partial[(int64_t)blockIdx.y * kScoreChunks + blockIdx.x] = s;
   }
+}
+
+__global__ void score_fold_kernel(const double* partial, double* scores) {
+  const int v = blockIdx.x, lane = threadIdx.x;
+  const double* p = partial + (int64_t)v * kScoreChunks;
+  double sum = 0.0;
+  for (int i = lane * (kScoreChunks / 32); i < (lane + 1) * (kScoreChunks / 32); ++i) sum += p[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  if (lane == 0) scores[v] = sum;
 }
 
 // batch of 128 list entries (tried 96: +2%, 160: +3%; 192 leaves 2 CTAs per SM)
@@ -756,9 +771,12 @@ void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s) {
 }
 
 void launch_score_image(const DevCam* cams, int V, const double* entropy, const double* edepth,
-                        double corr_lambda, double* scores, cudaStream_t s) {
+                        double corr_lambda, double* partial, double* scores, cudaStream_t s) {
   if (V == 0) return;
-  score_image_kernel<<<V, 512, 0, s>>>(cams, entropy, edepth, corr_lambda, scores);
+  score_image_kernel<<<dim3(kScoreChunks, V), 256, 0, s>>>(cams, entropy, edepth, corr_lambda, partial);
+  score_fold_kernel<<<V, 32, 0, s>>>(partial, scores);
 }
+
+int score_partials_per_view() { return kScoreChunks; }
 
 }  // namespace gavis

@@ -179,14 +179,6 @@ __device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a,
   }
 }
 
-// Per-pixel contribution to image_entropy (uncertainty.hpp:264-278): H, or with
-// the correlation hook H - H exp(-d / lambda), d the entropy-track depth.
-template <int LC>
-__device__ __forceinline__ double score_term(const Pixel<LC>& P, const UaBlendArgs& a) {
-  if (a.corr_lambda > 0.0) return P.H - P.H * exp(-P.edep / a.corr_lambda);
-  return P.H;
-}
-
 template <int LC, bool RGB, bool ENT>
 struct Stage {
   static constexpr size_t bytes(int batch) {
