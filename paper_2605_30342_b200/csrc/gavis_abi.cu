@@ -201,6 +201,12 @@ struct gavis_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // UA renders run two batches in flight: batch k's redo / score / copy-outs on
+  // `side` overlap batch k+1's binning on `stream`; per-batch buffers alternate
+  // between two sets (bufset), events order the reuse.
+  cudaStream_t side = nullptr;
+  int bufset = 0;
+  cudaEvent_t ev_blend[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   std::map<std::string, DevBuf> bufs;
   int max_batch = 0;
   bool profiling = false;
@@ -210,6 +216,8 @@ struct gavis_ctx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   int64_t launches = 0;
   int32_t* pinned = nullptr;
+  double* pin_scores = nullptr;  // pinned staging of per-view scores (async D2H on `side`)
+  int64_t pin_scores_cap = 0;
   int precision = GAVIS_PRECISION_CERTIFIED;
   int64_t redo_pixels = 0;       // pixels the certified blend handed to the fp64 redo
   int64_t rescored_views = 0;    // candidates re-scored exactly to certify an argmax
@@ -218,7 +226,7 @@ struct gavis_ctx {
   void use() { CK(cudaSetDevice(device)); }
 
   void* buf(const std::string& name, size_t bytes) {
-    DevBuf& b = bufs[name];
+    DevBuf& b = bufs[bufset ? name + "#1" : name];
     if (bytes == 0) bytes = 16;
     if (b.bytes < bytes) {
       if (b.p) CK(cudaFree(b.p));
@@ -264,25 +272,32 @@ struct gavis_ctx {
   }
 
   template <class F>
-  void run(const char* name, F&& launch, int nlaunch = 1) {
+  void run(const char* name, F&& launch, int nlaunch = 1, cudaStream_t st = nullptr) {
+    if (!st) st = stream;
     cudaEvent_t a = nullptr, b = nullptr;
     if (profiling) {
       a = event();
       b = event();
-      CK(cudaEventRecord(a, stream));
+      CK(cudaEventRecord(a, st));
     }
     launch();
     CK(cudaGetLastError());
     if (profiling) {
-      CK(cudaEventRecord(b, stream));
+      CK(cudaEventRecord(b, st));
       pending.emplace_back(name, a, b);
     }
     launches += nlaunch;
   }
 
-  void sync() {
-    CK(cudaStreamSynchronize(stream));
+  // Collect the kernel timings whose events have completed (all when `all`).
+  void collect(bool all) {
+    std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> keep;
     for (auto& p : pending) {
+      if (!all && cudaEventQuery(std::get<2>(p)) != cudaSuccess) {
+        (void)cudaGetLastError();
+        keep.push_back(p);
+        continue;
+      }
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, std::get<1>(p), std::get<2>(p)));
       Timing& t = timing[std::get<0>(p)];
@@ -291,7 +306,19 @@ struct gavis_ctx {
       spare_events.push_back(std::get<1>(p));
       spare_events.push_back(std::get<2>(p));
     }
-    pending.clear();
+    pending.swap(keep);
+  }
+
+  // The main stream (side-stream work of an in-flight UA batch may continue).
+  void sync() {
+    CK(cudaStreamSynchronize(stream));
+    collect(false);
+  }
+
+  void sync_all() {
+    CK(cudaStreamSynchronize(stream));
+    if (side) CK(cudaStreamSynchronize(side));
+    collect(true);
   }
 };
 
@@ -370,6 +397,7 @@ struct Binned {
 
 // pinned host scratch layout (int32 words)
 constexpr int kPinItems = 4;
+constexpr int kPinRedo = 6;  // u64
 constexpr int kPinWords = 64;
 
 struct BinOpts {
@@ -643,9 +671,11 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
   if (f) f->num_views += n_views;
 }
 
-void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t count) {
+void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t count,
+              cudaStream_t st = nullptr) {
   if (host && count > 0)
-    CK(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(host, dev, sizeof(double) * count, cudaMemcpyDeviceToHost,
+                       st ? st : c->stream));
 }
 
 // Certification window of the fp32 blend, relative to the cutoff: twice the
@@ -688,9 +718,35 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     }
   }
   const int bv = batch_views(c, N, n);
+  const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED &&
+                    ua_fast_supported(rc->tile_size, rc->alpha_clamp_max);
+  unsigned long long* redo_total = nullptr;
+  if (fast) {
+    redo_total = (unsigned long long*)c->buf("redo_total", sizeof(unsigned long long));
+    CK(cudaMemsetAsync(redo_total, 0, sizeof(unsigned long long), c->stream));
+  }
+  if (out->scores && n > c->pin_scores_cap) {
+    c->sync_all();
+    if (c->pin_scores) CK(cudaFreeHost(c->pin_scores));
+    c->pin_scores = nullptr;
+    c->pin_scores_cap = 0;
+    CK(cudaMallocHost(&c->pin_scores, sizeof(double) * n));
+    c->pin_scores_cap = n;
+  }
+  CK(cudaEventRecord(c->ev_done[0], c->stream));  // side work may start after this point
+  CK(cudaStreamWaitEvent(c->side, c->ev_done[0], 0));
+  struct BufsetReset {
+    gavis_ctx* c;
+    ~BufsetReset() { c->bufset = 0; }
+  } reset{c};
   int64_t pix_done = 0;
-  for (int v0 = 0; v0 < n; v0 += bv) {
+  int batch = 0;
+  for (int v0 = 0; v0 < n; v0 += bv, ++batch) {
     const int V = std::min(bv, n - v0);
+    const int par = batch & 1;
+    c->bufset = par;
+    // the buffers of this set were last read by batch - 2's side-stream work
+    if (batch >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_done[par], 0));
     BinOpts o;
     o.ua = do_ent;
     o.field = f;
@@ -750,8 +806,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       if (out->entropy_contributors)
         ua.ent_contrib = (int32_t*)c->buf("img_nent", sizeof(int32_t) * P);
     }
-    const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED &&
-                      ua_fast_supported(rc->tile_size, rc->alpha_clamp_max);
+    cudaStream_t side = c->side;
     if (fast && b.total_tiles > 0) {
       invariant(P < (int64_t(1) << 32), "too many pixels in one batch");
       ua.flag_list = (uint32_t*)c->buf("flag_list", sizeof(uint32_t) * P);
@@ -759,37 +814,52 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       CK(cudaMemsetAsync(ua.flag_count, 0, sizeof(uint32_t), c->stream));
       cert_window(&ua);
       c->run("ua_blend", [&] { launch_ua_blend_fast(ua, c->stream); });
-      c->run("ua_redo", [&] { launch_ua_redo(ua, c->stream); });
-      CK(cudaMemcpyAsync(c->pinned + 3, ua.flag_count, sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                         c->stream));
+      CK(cudaEventRecord(c->ev_blend[par], c->stream));
+      CK(cudaStreamWaitEvent(side, c->ev_blend[par], 0));
+      c->run("ua_redo", [&] { launch_ua_redo(ua, side); }, 1, side);
+      launch_add_count(redo_total, ua.flag_count, side);
     } else {
       c->run("ua_blend", [&] { launch_ua_blend(ua, c->stream); }, b.total_tiles > 0 ? 1 : 0);
+      CK(cudaEventRecord(c->ev_blend[par], c->stream));
+      CK(cudaStreamWaitEvent(side, c->ev_blend[par], 0));
     }
     double* dscores = nullptr;
     if (do_ent) {
       dscores = (double*)c->buf("scores", sizeof(double) * V);
       double* part = (double*)c->buf("score_partial", sizeof(double) * V * score_partials_per_view());
       c->run("score", [&] {
-        launch_score_image(b.dcams, V, ua.entropy, ua.edepth, ua.corr_lambda, part, dscores, c->stream);
-      });
+        launch_score_image(b.dcams, V, ua.entropy, ua.edepth, ua.corr_lambda, part, dscores, side);
+      }, 1, side);
     }
-    copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P);
-    copy_out(c, out->depth ? out->depth + pix_done : nullptr, ua.depth, P);
-    copy_out(c, out->transmittance ? out->transmittance + pix_done : nullptr, ua.trans, P);
-    copy_out(c, out->entropy ? out->entropy + pix_done : nullptr, ua.entropy, P);
-    copy_out(c, out->invisible_mass ? out->invisible_mass + pix_done : nullptr, ua.w0, P);
-    copy_out(c, out->entropy_depth ? out->entropy_depth + pix_done : nullptr, ua.edepth, P);
-    copy_out(c, out->scores ? out->scores + v0 : nullptr, dscores, V);
+    copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P, side);
+    copy_out(c, out->depth ? out->depth + pix_done : nullptr, ua.depth, P, side);
+    copy_out(c, out->transmittance ? out->transmittance + pix_done : nullptr, ua.trans, P, side);
+    copy_out(c, out->entropy ? out->entropy + pix_done : nullptr, ua.entropy, P, side);
+    copy_out(c, out->invisible_mass ? out->invisible_mass + pix_done : nullptr, ua.w0, P, side);
+    copy_out(c, out->entropy_depth ? out->entropy_depth + pix_done : nullptr, ua.edepth, P, side);
+    // scores through pinned staging: a D2H copy into pageable memory would block
+    // the host on this batch's side-stream work and serialise the batches
+    copy_out(c, out->scores ? c->pin_scores + v0 : nullptr, dscores, V, side);
     if (out->rgb_contributors)
       CK(cudaMemcpyAsync(out->rgb_contributors + pix_done, ua.rgb_contrib, sizeof(int32_t) * P,
-                         cudaMemcpyDeviceToHost, c->stream));
+                         cudaMemcpyDeviceToHost, side));
     if (out->entropy_contributors)
       CK(cudaMemcpyAsync(out->entropy_contributors + pix_done, ua.ent_contrib,
-                         sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    if (fast && b.total_tiles > 0) c->redo_pixels += (uint32_t)c->pinned[3];
+                         sizeof(int32_t) * P, cudaMemcpyDeviceToHost, side));
+    CK(cudaEventRecord(c->ev_done[par], side));
     pix_done += P;
   }
+  c->bufset = 0;
+  // the main stream continues after the side stream's last batch
+  CK(cudaEventRecord(c->ev_done[0], c->side));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_done[0], 0));
+  if (redo_total) {
+    CK(cudaMemcpyAsync(c->pinned + kPinRedo, redo_total, sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, c->stream));
+  }
+  c->sync_all();
+  if (out->scores && n > 0) std::memcpy(out->scores, c->pin_scores, sizeof(double) * n);
+  if (redo_total) c->redo_pixels += (int64_t)*reinterpret_cast<unsigned long long*>(c->pinned + kPinRedo);
 }
 
 // select_nbv's argmax (planner.hpp:132-136: first strictly greater score) over
@@ -873,6 +943,11 @@ gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
         c->own_stream = true;
       }
       CK(cudaMallocHost(&c->pinned, sizeof(int32_t) * kPinWords));
+      CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        CK(cudaEventCreateWithFlags(&c->ev_blend[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
+      }
       // keep freed scene/field memory in the device pool between uploads
       cudaMemPool_t pool;
       CK(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -903,6 +978,15 @@ gavis_status gavis_ctx_destroy(gavis_ctx* c) {
     if (c->t0) cudaEventDestroy(c->t0);
     if (c->t1) cudaEventDestroy(c->t1);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pin_scores) cudaFreeHost(c->pin_scores);
+    if (c->side) {
+      cudaStreamSynchronize(c->side);
+      cudaStreamDestroy(c->side);
+    }
+    for (int k = 0; k < 2; ++k) {
+      if (c->ev_blend[k]) cudaEventDestroy(c->ev_blend[k]);
+      if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+    }
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
   });
@@ -913,7 +997,7 @@ gavis_status gavis_ctx_synchronize(gavis_ctx* c) {
     require(c != nullptr, "context must not be null");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
-    c->sync();
+    c->sync_all();
   });
 }
 
@@ -949,7 +1033,7 @@ gavis_status gavis_ctx_set_profiling(gavis_ctx* c, int32_t enabled) {
     require(c != nullptr, "context must not be null");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
-    c->sync();
+    c->sync_all();
     c->profiling = enabled != 0;
   });
 }
@@ -960,7 +1044,7 @@ gavis_status gavis_ctx_kernel_time(gavis_ctx* c, const char* kernel, double* ms,
     require(c != nullptr && kernel != nullptr, "context and kernel name must not be null");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
-    c->sync();
+    c->sync_all();
     Timing t;
     auto it = c->timing.find(kernel);
     if (it != c->timing.end()) t = it->second;

@@ -224,6 +224,7 @@ void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s);
 void launch_score_image(const DevCam* cams, int V, const double* entropy, const double* edepth,
                         double corr_lambda, double* partial, double* scores, cudaStream_t s);
 int score_partials_per_view();
+void launch_add_count(unsigned long long* total, const uint32_t* count, cudaStream_t s);
 void launch_query(const QueryArgs& a, cudaStream_t s);
 void launch_mixtures(const MixtureArgs& a, int64_t P, cudaStream_t s);
 // unseen[k] *= 1 - vis[v*N + n_real + k] for v = 0..V-1 in order.

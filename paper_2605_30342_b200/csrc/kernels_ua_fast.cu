@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
 // path's operations (rgb_step / ent_step, ua_common.cuh), every lane carrying
 // the same pixel state, so the outputs equal the exact kernels' bit for bit.
 template <int LC, bool RGB, bool ENT>
-__global__ void __launch_bounds__(256) ua_redo_kernel(UaBlendArgs a) {
+__global__ void __launch_bounds__(32) ua_redo_kernel(UaBlendArgs a) {
   load_math_tables();
   __syncthreads();
   constexpr int CS = Col<LC>::STRIDE;
@@ -726,13 +726,16 @@ void launch_fast_lc(const UaBlendArgs& a, cudaStream_t s) {
 
 template <int LC>
 void launch_redo_lc(const UaBlendArgs& a, cudaStream_t s) {
-  const unsigned grid = 148 * 8;
+  // one-warp blocks: they fit beside the next batch's blend CTAs (3 x 20k
+  // registers per SM leave room for one redo warp), so the redo of batch k runs
+  // on the side stream underneath batch k+1 instead of holding whole SMs
+  const unsigned grid = 148 * 32;
   if (a.do_rgb && a.do_ent)
-    ua_redo_kernel<LC, true, true><<<grid, 256, 0, s>>>(a);
+    ua_redo_kernel<LC, true, true><<<grid, 32, 0, s>>>(a);
   else if (a.do_rgb)
-    ua_redo_kernel<LC, true, false><<<grid, 256, 0, s>>>(a);
+    ua_redo_kernel<LC, true, false><<<grid, 32, 0, s>>>(a);
   else if (a.do_ent)
-    ua_redo_kernel<LC, false, true><<<grid, 256, 0, s>>>(a);
+    ua_redo_kernel<LC, false, true><<<grid, 32, 0, s>>>(a);
 }
 
 }  // namespace
@@ -778,5 +781,13 @@ void launch_score_image(const DevCam* cams, int V, const double* entropy, const 
 }
 
 int score_partials_per_view() { return kScoreChunks; }
+
+namespace {
+__global__ void add_count_kernel(unsigned long long* total, const uint32_t* count) { *total += *count; }
+}  // namespace
+
+void launch_add_count(unsigned long long* total, const uint32_t* count, cudaStream_t s) {
+  add_count_kernel<<<1, 1, 0, s>>>(total, count);
+}
 
 }  // namespace gavis
