@@ -205,8 +205,10 @@ struct gavis_ctx {
   // `side` overlap batch k+1's binning on `stream`; per-batch buffers alternate
   // between two sets (bufset), events order the reuse.
   cudaStream_t side = nullptr;
+  cudaStream_t front = nullptr;  // binning of batch k+1 under batch k's blend (high priority)
   int bufset = 0;
   cudaEvent_t ev_blend[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  cudaEvent_t ev_bin[2] = {nullptr, nullptr};
   std::map<std::string, DevBuf> bufs;
   int max_batch = 0;
   bool profiling = false;
@@ -318,6 +320,7 @@ struct gavis_ctx {
   void sync_all() {
     CK(cudaStreamSynchronize(stream));
     if (side) CK(cudaStreamSynchronize(side));
+    if (front) CK(cudaStreamSynchronize(front));
     collect(true);
   }
 };
@@ -733,20 +736,28 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     CK(cudaMallocHost(&c->pin_scores, sizeof(double) * n));
     c->pin_scores_cap = n;
   }
-  CK(cudaEventRecord(c->ev_done[0], c->stream));  // side work may start after this point
+  CK(cudaEventRecord(c->ev_done[0], c->stream));  // side / front work start after this point
   CK(cudaStreamWaitEvent(c->side, c->ev_done[0], 0));
+  CK(cudaStreamWaitEvent(c->front, c->ev_done[0], 0));
+  cudaStream_t main_stream = c->stream;
   struct BufsetReset {
     gavis_ctx* c;
-    ~BufsetReset() { c->bufset = 0; }
-  } reset{c};
+    cudaStream_t main;
+    ~BufsetReset() {
+      c->bufset = 0;
+      c->stream = main;
+    }
+  } reset{c, main_stream};
   int64_t pix_done = 0;
   int batch = 0;
   for (int v0 = 0; v0 < n; v0 += bv, ++batch) {
     const int V = std::min(bv, n - v0);
     const int par = batch & 1;
     c->bufset = par;
-    // the buffers of this set were last read by batch - 2's side-stream work
-    if (batch >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_done[par], 0));
+    // binning runs on the front stream, under the previous batch's blend; the
+    // buffers of this set were last read by batch - 2's side-stream work
+    c->stream = c->front;
+    if (batch >= 2) CK(cudaStreamWaitEvent(c->front, c->ev_done[par], 0));
     BinOpts o;
     o.ua = do_ent;
     o.field = f;
@@ -770,6 +781,9 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       c->sync();
       require(c->pinned[2] == 0, "propagated color variance must be positive");
     }
+    CK(cudaEventRecord(c->ev_bin[par], c->front));
+    c->stream = main_stream;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_bin[par], 0));
     const int64_t P = b.total_pix;
     UaBlendArgs ua;
     ua.scene = s->dev;
@@ -944,9 +958,13 @@ gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
       }
       CK(cudaMallocHost(&c->pinned, sizeof(int32_t) * kPinWords));
       CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      int lo_prio = 0, hi_prio = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      CK(cudaStreamCreateWithPriority(&c->front, cudaStreamNonBlocking, hi_prio));
       for (int k = 0; k < 2; ++k) {
         CK(cudaEventCreateWithFlags(&c->ev_blend[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_bin[k], cudaEventDisableTiming));
       }
       // keep freed scene/field memory in the device pool between uploads
       cudaMemPool_t pool;
@@ -979,13 +997,15 @@ gavis_status gavis_ctx_destroy(gavis_ctx* c) {
     if (c->t1) cudaEventDestroy(c->t1);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pin_scores) cudaFreeHost(c->pin_scores);
-    if (c->side) {
-      cudaStreamSynchronize(c->side);
-      cudaStreamDestroy(c->side);
-    }
+    for (cudaStream_t st : {c->side, c->front})
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
     for (int k = 0; k < 2; ++k) {
       if (c->ev_blend[k]) cudaEventDestroy(c->ev_blend[k]);
       if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
+      if (c->ev_bin[k]) cudaEventDestroy(c->ev_bin[k]);
     }
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
