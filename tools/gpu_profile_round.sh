@@ -14,6 +14,8 @@ timeout 900 python -m pytest tests -m gpu -x -q > $OUT/${TAG}_pytest.log 2>&1
 echo "pytest exit $?" >> $OUT/${TAG}_pytest.log
 timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
 echo "bench exit $?" >> $OUT/${TAG}_bench.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/${TAG}_bench_reference.json 2>> $OUT/${TAG}_bench.err
+timeout 900 python bench.py --precision exact --steps 3 --warmup 3 --no-cpu-baseline --no-extra-vf > $OUT/${TAG}_bench_exact.json 2>> $OUT/${TAG}_bench.err
 SMALL="bench.py --steps 1 --warmup 3 --per-gpu 64 --no-cpu-baseline --no-e2e --no-extra-vf"
 if timeout 600 python $SMALL > $OUT/${TAG}_small.json 2>&1; then
   timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
