@@ -450,29 +450,54 @@ __global__ void item_counts_kernel(NarrowArgs a) {
   a.item_count[i] = a.counts[a.item_slot_sorted[i]];
 }
 
-// K3n: one thread per visible item (depth order) writes its tile pairs (key =
-// global tile id) and records its pair offset under its slot (VF finalize).
-__global__ void emit_tiles_kernel(EmitArgs a, NarrowArgs n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n.n_items) return;
-  const uint32_t slot = n.item_slot_sorted[i];
-  const int v = (int)(slot / (uint32_t)a.N);
-  const uint32_t g = slot - (uint32_t)v * (uint32_t)a.N;
-  const DevCam& c = a.cams[v];
-  const uint2 tr = a.trect[slot];
-  const int tx0 = tr.x & 0xFFFF, tx1 = tr.x >> 16, ty0 = tr.y & 0xFFFF, ty1 = tr.y >> 16;
-  int64_t o = n.item_offset[i];
-  n.slot_offset[slot] = (int32_t)o;
-  for (int ty = ty0; ty <= ty1; ++ty) {
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      n.keys32[o] = (uint32_t)(c.tile_base + (int64_t)ty * c.tiles_x + tx);
-      if (a.pair_gid) {
-        a.vals[o] = (uint32_t)o;
-        a.pair_gid[o] = g;
-      } else {
-        a.vals[o] = g;
-      }
-      ++o;
+// K3n: visible items in depth order write their tile pairs (key = global tile
+// id) and record their pair offset under their slot (VF finalize). A warp takes
+// 32 consecutive items, whose pairs form one contiguous range, and writes that
+// range lane-strided (coalesced): each pair finds its item by a binary search
+// over the 32 item offsets and its tile from the item's rectangle.
+__global__ void __launch_bounds__(256) emit_tiles_kernel(EmitArgs a, NarrowArgs n) {
+  __shared__ int32_t s_off[8][33];
+  __shared__ int32_t s_tb[8][32], s_tx[8][32], s_x0[8][32], s_y0[8][32], s_w[8][32];
+  __shared__ uint32_t s_g[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i0 = ((int64_t)blockIdx.x * 8 + warp) * 32;
+  if (i0 >= n.n_items) return;
+  const int nv = (int)min((int64_t)32, n.n_items - i0);
+  const int64_t i = i0 + lane;
+  if (lane < nv) {
+    const uint32_t slot = n.item_slot_sorted[i];
+    const int v = (int)(slot / (uint32_t)a.N);
+    const DevCam& c = a.cams[v];
+    const uint2 tr = a.trect[slot];
+    const int tx0 = tr.x & 0xFFFF, tx1 = tr.x >> 16, ty0 = tr.y & 0xFFFF;
+    const int32_t o = n.item_offset[i];
+    n.slot_offset[slot] = o;
+    s_off[warp][lane] = o;
+    s_tb[warp][lane] = (int32_t)c.tile_base;
+    s_tx[warp][lane] = c.tiles_x;
+    s_x0[warp][lane] = tx0;
+    s_y0[warp][lane] = ty0;
+    s_w[warp][lane] = tx1 - tx0 + 1;
+    s_g[warp][lane] = slot - (uint32_t)v * (uint32_t)a.N;
+    if (lane == nv - 1) s_off[warp][32] = o + n.item_count[i];
+  }
+  __syncwarp();
+  const int32_t start = s_off[warp][0], end = s_off[warp][32];
+  for (int32_t p = start + lane; p < end; p += 32) {
+    int j = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (j + step < nv && s_off[warp][j + step] <= p) j += step;
+    const int k = p - s_off[warp][j];
+    const int w = s_w[warp][j];
+    const int dy = k / w, dx = k - dy * w;
+    n.keys32[p] = (uint32_t)(s_tb[warp][j] + (s_y0[warp][j] + dy) * s_tx[warp][j] + s_x0[warp][j] + dx);
+    const uint32_t g = s_g[warp][j];
+    if (a.pair_gid) {
+      a.vals[p] = (uint32_t)p;
+      a.pair_gid[p] = g;
+    } else {
+      a.vals[p] = g;
     }
   }
 }
@@ -555,7 +580,7 @@ void launch_depth_order(const NarrowArgs& a, cudaStream_t s) {
 }
 
 void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s) {
-  if (n.n_items > 0) emit_tiles_kernel<<<blocks_for(n.n_items, 256), 256, 0, s>>>(a, n);
+  if (n.n_items > 0) emit_tiles_kernel<<<blocks_for(n.n_items, 256), 256, 0, s>>>(a, n);  // 32 items per warp
 }
 
 void launch_ranges32(const uint32_t* keys32, int64_t K, uint2* ranges, cudaStream_t s) {
