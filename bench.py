@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="candidates in the CPU sample")
     p.add_argument("--no-extra-vf", action="store_true", help="skip the config-2/4 VF-build timings")
+    p.add_argument("--sweep5", action="store_true",
+                   help="config-5 active-mapping sweep: 20 incremental rounds x 512..4096 candidates at 400^2")
     p.add_argument("--precision", default="certified", choices=["certified", "exact"],
                    help="UA blend arithmetic (certified fp32 + fp64 redo, or fp64 throughout)")
     return p.parse_args()
@@ -406,6 +408,30 @@ def run_ours(args):
             dsc.close()
             del cc
 
+    # ---------------- config 5: active-mapping iteration sweep (1 GPU) ---------
+    sweep5 = None
+    if args.sweep5 and world == 1:
+        from paper_2605_30342_b200 import synth
+        c5 = synth.config5(0, n_candidates=4096)
+        ds5 = ctx.upload(c5["scene"])
+        sweep5 = {"scene": "config2 (500k Gaussians)", "training_views": len(c5["train"]),
+                  "candidate_resolution": [400, 400], "rounds": c5["rounds"], "per_count": {}}
+        for count in (512, 1024, 2048, 4096):
+            f5 = build_field(c5["train"], ds5, c5["degree"])
+            api.nbv_loop(ctx, ds5, f5, c5["candidates"][:count], 1, rc, uc)  # warm-up round
+            f5.close()
+            f5 = build_field(c5["train"], ds5, c5["degree"])
+            barrier(ctx, dist)
+            ctx.timer_start()
+            chosen, _, _ = api.nbv_loop(ctx, ds5, f5, c5["candidates"][:count], c5["rounds"], rc, uc)
+            ms5 = ctx.timer_stop()
+            sweep5["per_count"][str(count)] = {
+                "ms_per_round": ms5 / c5["rounds"],
+                "candidate_views_per_s": count * c5["rounds"] / (ms5 / 1000.0),
+                "chosen_first_rounds": [int(x) for x in chosen[:5]]}
+            f5.close()
+        ds5.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         model, cores = cpu_info()
@@ -457,6 +483,7 @@ def run_ours(args):
             "vf_build_other_configs": vf_other,
             "best_index_last_step": int(res.best_index) + (lo if world == 1 else 0),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            **({"config5_sweep": sweep5} if sweep5 else {}),
         }
         print(json.dumps(line))
     if dist is not None:
