@@ -14,7 +14,7 @@ import pytest
 
 import oracle as O
 from paper_2605_30342_b200 import api, synth
-from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig, VmfParams
+from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig, VmfParams, make_lookat
 
 pytestmark = pytest.mark.gpu
 
@@ -163,3 +163,79 @@ def test_certified_vs_exact_full_size(ctx, ctx_exact):
     assert np.max(np.abs(ex["entropy"] - got["entropy"])) <= IMG_ABS
     assert np.max(np.abs(ex["transmittance"] - got["transmittance"])) <= 1e-6
     assert np.max(np.abs(ex["scores"] - got["scores"]) / np.abs(ex["scores"])) <= SCORE_REL
+
+
+def test_certified_variants_match_oracle(ctx):
+    """Every instantiation the certified path selects -- entropy only, RGB only,
+    extra outputs (depths, counts), the correlation hook, sh_propagation -- and
+    the configurations it hands to the exact kernels (tile 13, alpha_clamp_max 1)."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    f = api.construct_field(ctx, scene, c["train"], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    cam = c["candidates"][2]
+    H, w0, edep, cc = O.render_entropy(osc, g, 2, 16, cam, RC, UC, contrib=True)
+    rgb, dep, T, rcc = O.rasterize(osc, cam, RC, contrib=True)
+    # entropy only (select_nbv without RGB), with contributor counts and depth
+    r = api.render(ctx, scene, f, [cam], RC, UC, entropy=True, entropy_depth=True, contributors=True)
+    assert np.array_equal(r["entropy_contributors"], cc)
+    assert np.max(np.abs(r["entropy"] - H)) <= IMG_ABS
+    assert np.max(np.abs(r["entropy_depth"] - edep)) <= 1e-4
+    # RGB only
+    r = api.render(ctx, scene, None, [cam], RC, UC, rgb=True, transmittance=True, contributors=True)
+    assert np.array_equal(r["rgb_contributors"], rcc)
+    assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+    # correlation hook (needs the entropy-track depth inside the score)
+    uc = UncertaintyConfig(correlation=1, correlation_lambda=2.0)
+    res = api.select_nbv(ctx, scene, f, c["candidates"][:6], RC, uc)
+    best, sc = O.select_nbv(osc, g, 2, 16, c["candidates"][:6], RC, uc, threads=8)
+    assert res.best_index == best
+    assert np.max(np.abs(res.scores - sc) / np.maximum(1.0, np.abs(sc))) <= SCORE_REL
+    # tile 13 and alpha_clamp_max 1.0 run the exact kernels: fp64-level agreement
+    for rc in (RasterConfig(tile_size=13), RasterConfig(alpha_clamp_max=1.0)):
+        r = api.render(ctx, scene, f, [cam], rc, UC, entropy=True, contributors=True)
+        He, _, _, cce = O.render_entropy(osc, g, 2, 16, cam, rc, UC, contrib=True)
+        assert np.array_equal(r["entropy_contributors"], cce)
+        assert np.max(np.abs(r["entropy"] - He)) <= 1e-10
+
+
+def test_certified_sh_propagation(ctx):
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    rng = np.random.default_rng(11)
+    var = rng.uniform(0.01, 0.2, size=(scene.num_particles, 3, 9)).astype(np.float32)
+    ds = ctx.upload(scene)
+    ds.set_coeff_variances(var, 2)
+    f = api.construct_field(ctx, ds, c["train"][:4], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    uc = UncertaintyConfig(variance_provider=1)
+    cam = c["candidates"][0]
+    r = api.render(ctx, ds, f, [cam], RC, uc, entropy=True, contributors=True, scores=True)
+    O.set_coeff_variances(var.astype(np.float64), 2)
+    try:
+        H, _, _, cc = O.render_entropy(osc, g, 2, 4, cam, RC, uc, contrib=True)
+    finally:
+        O.set_coeff_variances(None, -1)
+    assert np.array_equal(r["entropy_contributors"], cc)
+    assert np.max(np.abs(r["entropy"] - H)) <= IMG_ABS
+
+
+def test_certified_edge_cases(ctx):
+    """1x1 camera, camera inside the cloud, nothing visible, empty scene."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    tiny = make_lookat((0, 0, 3), (0, 0, 0), (0, 1, 0), 1, 1)
+    inside = make_lookat((0.1, 0.05, 0.0), (1, 0, 0), (0, 0, 1), 64, 48)
+    away = make_lookat((0, 0, 10), (0, 0, 20), (0, 1, 0), 32, 32)
+    for cam in (tiny, inside, away):
+        r = api.render(ctx, scene, None, [cam], RC, UC, rgb=True, transmittance=True, contributors=True)
+        rgb, _, T, cc = O.rasterize(osc, cam, RC, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], cc)
+        assert np.max(np.abs(r["transmittance"] - T)) <= 1e-6
+        assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+    from paper_2605_30342_b200.model import Scene
+    r = api.render(ctx, Scene.empty(), None, [synth.z_camera()], RC, UC, rgb=True, transmittance=True)
+    assert np.all(r["rgb"] == 0) and np.all(r["transmittance"] == 1)
