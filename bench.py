@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="candidates in the CPU sample")
     p.add_argument("--no-extra-vf", action="store_true", help="skip the config-2/4 VF-build timings")
+    p.add_argument("--batch", type=int, default=0, help="views per launch batch (0 = library default)")
     p.add_argument("--sweep5", action="store_true",
                    help="config-5 active-mapping sweep: 20 incremental rounds x 512..4096 candidates at 400^2")
     p.add_argument("--precision", default="certified", choices=["certified", "exact"],
@@ -232,6 +233,8 @@ def run_ours(args):
     scene = c["scene"]
     ctx = api.Context(local)
     ctx.set_precision(args.precision)
+    if args.batch:
+        ctx.set_batch(args.batch)
     ds = ctx.upload(scene)
     vmf = VmfParams(1.0)
     degree = c["degree"]

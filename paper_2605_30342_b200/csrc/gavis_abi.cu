@@ -370,7 +370,7 @@ DevCam make_devcam(const gavis_camera& c, int ts, int64_t tile_base, int64_t pix
 }
 
 int batch_views(gavis_ctx* c, int64_t N, int n_views) {
-  int vmax = c->max_batch > 0 ? c->max_batch : 16;
+  int vmax = c->max_batch > 0 ? c->max_batch : 32;
   if (N > 0) {
     // ~112 B of per-(view, particle) state; keep a batch under ~6 GB of it.
     const int64_t by_mem = (int64_t)(6.0e9 / (112.0 * (double)N));
