@@ -400,8 +400,9 @@ struct Binned {
 
 // pinned host scratch layout (int32 words)
 constexpr int kPinItems = 4;
-constexpr int kPinRedo = 6;  // u64
-constexpr int kPinWords = 64;
+constexpr int kPinRedo = 6;     // u64
+constexpr int kPinStarts = 16;  // int64 [V + 1] (V <= 64)
+constexpr int kPinWords = 256;
 
 struct BinOpts {
   bool vf_mode = false;
@@ -517,9 +518,13 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
       void* stmp = c->buf("scan_tmp", scb);
       c->run("scan", [&] { exclusive_scan(na.item_count, ioff, n_items + 1, stmp, scb, c->stream); });
       na.item_offset = ioff;
-      CK(cudaMemcpyAsync(P32, ioff + n_items, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+      na.view_bits = std::max(1, bits_for(V));
+      int64_t* dstarts = (int64_t*)c->buf("view_pair_starts", sizeof(int64_t) * (V + 1));
+      c->run("depth_order", [&] { launch_view_pair_starts(na, V, dstarts, c->stream); });
+      CK(cudaMemcpyAsync(c->pinned + kPinStarts, dstarts, sizeof(int64_t) * (V + 1),
+                         cudaMemcpyDeviceToHost, c->stream));
       c->sync();
-      K = P32[0];
+      K = reinterpret_cast<int64_t*>(c->pinned + kPinStarts)[V];
     }
   } else if (VN > 0) {
     const size_t sb = scan_temp_bytes(VN);
@@ -554,14 +559,43 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     uint32_t* k32b = (uint32_t*)c->buf("keys32_b", sizeof(uint32_t) * K);
     na.keys32 = k32a;
     na.slot_offset = b.offsets;  // per-slot pair offsets (VF finalize)
+    // chunks of consecutive views with <= 2^16 tiles: 16-bit local tile keys, two
+    // 8-bit radix passes per chunk (the pairs of a chunk are contiguous: views
+    // were emitted in order)
+    const int64_t* vstart = reinterpret_cast<const int64_t*>(c->pinned + kPinStarts);
+    std::vector<int> chunk_first;
+    std::vector<int64_t> hbase((size_t)V);
+    int64_t acc = 0;
+    for (int v = 0; v < V; ++v) {
+      const int64_t tv = (int64_t)b.hcams[v].tiles_x * b.hcams[v].tiles_y;
+      if (v == 0 || acc + tv > (int64_t(1) << 16)) {
+        chunk_first.push_back(v);
+        acc = 0;
+      }
+      acc += tv;
+      hbase[v] = b.hcams[chunk_first.back()].tile_base;
+    }
+    chunk_first.push_back(V);
+    int64_t* dbase = (int64_t*)c->buf("chunk_tile_base", sizeof(int64_t) * V);
+    CK(cudaMemcpyAsync(dbase, hbase.data(), sizeof(int64_t) * V, cudaMemcpyHostToDevice, c->stream));
+    na.chunk_tile_base = dbase;
     c->run("emit_keys", [&] { launch_emit_tiles(ea, na, c->stream); });
     const size_t sb32 = sort32_temp_bytes(K);
     void* tmp = c->buf("sort32_tmp", sb32);
-    c->run("sort", [&] {
-      radix_sort_pairs32(k32a, k32b, va, vb, K, std::max(1, bits_for(b.total_tiles)), tmp, sb32,
-                         c->stream);
-    });
-    c->run("ranges", [&] { launch_ranges32(k32a, K, b.ranges, c->stream); });
+    for (size_t k = 0; k + 1 < chunk_first.size(); ++k) {
+      const int v0 = chunk_first[k], v1 = chunk_first[k + 1];
+      const int64_t lo = vstart[v0], hi = vstart[v1];
+      const int64_t tiles = b.hcams[v1 - 1].tile_base +
+                            (int64_t)b.hcams[v1 - 1].tiles_x * b.hcams[v1 - 1].tiles_y -
+                            b.hcams[v0].tile_base;
+      c->run("sort", [&] {
+        radix_sort_pairs32(k32a + lo, k32b + lo, va + lo, vb + lo, hi - lo,
+                           std::max(1, bits_for(tiles)), tmp, sb32, c->stream);
+      });
+      c->run("ranges", [&] {
+        launch_ranges32(k32a, lo, hi, b.hcams[v0].tile_base, b.ranges, c->stream);
+      });
+    }
     b.vals = va;
     b.keys = nullptr;
   } else if (K > 0) {

@@ -73,7 +73,8 @@ struct NarrowArgs {
   int32_t* item_count = nullptr;       // [n_items + 1] tiles of each item, depth order
   const int32_t* item_offset = nullptr;  // exclusive scan of item_count
   int32_t* slot_offset = nullptr;      // [V*N] pair offset of each visible slot
-  uint32_t* keys32 = nullptr;          // [K] global tile ids
+  const int64_t* chunk_tile_base = nullptr;  // [V] first tile of the view's sort chunk
+  uint32_t* keys32 = nullptr;          // [K] tile ids relative to the chunk's first tile
 };
 
 struct RangesArgs {
@@ -206,7 +207,9 @@ void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_item_keys(const NarrowArgs& a, cudaStream_t s);
 void launch_depth_order(const NarrowArgs& a, cudaStream_t s);
 void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s);
-void launch_ranges32(const uint32_t* keys32, int64_t K, uint2* ranges, cudaStream_t s);
+void launch_ranges32(const uint32_t* keys32, int64_t lo, int64_t hi, int64_t tile_base, uint2* ranges,
+                     cudaStream_t s);
+void launch_view_pair_starts(const NarrowArgs& a, int V, int64_t* out, cudaStream_t s);
 void launch_wide_keys(const uint2* ranges, int64_t total_tiles, const uint32_t* vals,
                       const uint32_t* pair_gid, const DevCam* cams, int V, int64_t N, const GeoRec* geo,
                       uint64_t* keys, cudaStream_t s);

@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256) emit_tiles_kernel(EmitArgs a, NarrowArgs 
     const int32_t o = n.item_offset[i];
     n.slot_offset[slot] = o;
     s_off[warp][lane] = o;
-    s_tb[warp][lane] = (int32_t)c.tile_base;
+    s_tb[warp][lane] = (int32_t)(c.tile_base - n.chunk_tile_base[v]);
     s_tx[warp][lane] = c.tiles_x;
     s_x0[warp][lane] = tx0;
     s_y0[warp][lane] = ty0;
@@ -502,13 +502,33 @@ __global__ void __launch_bounds__(256) emit_tiles_kernel(EmitArgs a, NarrowArgs 
   }
 }
 
-// K5n: tile ranges of the tile-sorted pairs.
-__global__ void ranges32_kernel(const uint32_t* keys32, int64_t K, uint2* ranges) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= K) return;
+// K5n: tile ranges of the tile-sorted pairs [lo, hi) of one chunk of views
+// (keys = tile id - tile_base).
+__global__ void ranges32_kernel(const uint32_t* keys32, int64_t lo, int64_t hi, int64_t tile_base,
+                                uint2* ranges) {
+  const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hi) return;
   const uint32_t t = keys32[i];
-  if (i == 0 || keys32[i - 1] != t) ranges[t].x = (uint32_t)i;
-  if (i == K - 1 || keys32[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+  if (i == lo || keys32[i - 1] != t) ranges[tile_base + t].x = (uint32_t)i;
+  if (i == hi - 1 || keys32[i + 1] != t) ranges[tile_base + t].y = (uint32_t)(i + 1);
+}
+
+// Pair offset of the first item of every view (lower bound of the view's key
+// prefix in the depth-sorted items); out[V] = K.
+__global__ void view_pair_starts_kernel(NarrowArgs a, int V, int64_t* out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > V) return;
+  if (v == V) {
+    out[V] = a.item_offset[a.n_items];
+    return;
+  }
+  const uint32_t key = (uint32_t)v << (32 - a.view_bits);
+  int64_t lo = 0, hi = a.n_items;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (a.item_key[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  out[v] = a.item_offset[lo];
 }
 
 // Reference-form 64-bit keys (tile << 32 | fp32 depth) of the sorted pairs, for
@@ -583,8 +603,14 @@ void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s) {
   if (n.n_items > 0) emit_tiles_kernel<<<blocks_for(n.n_items, 256), 256, 0, s>>>(a, n);  // 32 items per warp
 }
 
-void launch_ranges32(const uint32_t* keys32, int64_t K, uint2* ranges, cudaStream_t s) {
-  if (K > 0) ranges32_kernel<<<blocks_for(K, 256), 256, 0, s>>>(keys32, K, ranges);
+void launch_ranges32(const uint32_t* keys32, int64_t lo, int64_t hi, int64_t tile_base, uint2* ranges,
+                     cudaStream_t s) {
+  if (hi > lo)
+    ranges32_kernel<<<blocks_for(hi - lo, 256), 256, 0, s>>>(keys32, lo, hi, tile_base, ranges);
+}
+
+void launch_view_pair_starts(const NarrowArgs& a, int V, int64_t* out, cudaStream_t s) {
+  view_pair_starts_kernel<<<blocks_for(V + 1, 64), 64, 0, s>>>(a, V, out);
 }
 
 void launch_wide_keys(const uint2* ranges, int64_t total_tiles, const uint32_t* vals,
