@@ -15,12 +15,11 @@
 //   * ua_blend_ilp_kernel (16x16 tiles, default): 256 threads, one pixel each,
 //     warp pre-filter of the tile list, list entries walked two at a time in
 //     straight-line code (fp64 instruction-level parallelism).
-//   * ua_blend_tile2_kernel (16x16 tiles): 128 threads, two pixels per thread.
 //   * ua_blend_kernel (any tile size): 256 threads, one pixel each, in rounds.
 // The SH colour dot products run as packed fp32x2 FMAs (FFMA2, sm_100) over
 // coefficient pairs; colour rows are padded to an even length on upload.
-// Per-tile entropy partials feed K8, which folds them in tile order into the
-// image score (image_entropy, uncertainty.hpp:264-272).
+// The image score (image_entropy, uncertainty.hpp:264-272) folds the entropy
+// image (K8, kernels_ua_fast.cu).
 #include "ua_common.cuh"
 
 #include <cstdlib>
@@ -28,84 +27,6 @@
 namespace gavis {
 
 namespace {
-
-// ---------------------------------------------------------------------------
-// 16x16 tiles, 128 threads, two pixels per thread.
-template <int LC, bool RGB, bool ENT, bool EXTRA>
-__global__ void __launch_bounds__(128, 5) ua_blend_tile2_kernel(UaBlendArgs a) {
-  constexpr int CS = Col<LC>::STRIDE;
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
-  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
-  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
-  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
-                                                            (ENT ? sizeof(UaRec) : 0)));
-  load_math_tables();
-
-  const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
-  const int64_t gt = blockIdx.x;
-  const int v = find_view(a.cams, a.V, gt);
-  const DevCam& c = a.cams[v];
-  const int64_t t = gt - c.tile_base;
-  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
-  const uint2 rg = a.ranges[gt];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t N = a.scene.n;
-  const GeoRec* geo = a.geo + (int64_t)v * N;
-  const UaRec* uar = a.ua + (int64_t)v * N;
-
-  const int px = tx * 16 + (warp & 1) * 8 + (lane & 7);
-  const int py0 = ty * 16 + (warp >> 1) * 8 + (lane >> 3);
-  const int py1 = py0 + 4;
-  const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 8;
-  const bool in0 = px < c.width && py0 < c.height;
-  const bool in1 = px < c.width && py1 < c.height;
-  const double cxp = px + 0.5, cyp0 = py0 + 0.5, cyp1 = py1 + 0.5;
-  Pixel<LC> P0, P1;
-  pixel_init<LC, RGB, ENT>(P0, c, px, py0, in0);
-  pixel_init<LC, RGB, ENT>(P1, c, px, py1, in1);
-
-  for (uint32_t base = rg.x; base < rg.y; base += kBatch) {
-    const bool live = !(P0.rgb_done && P0.ent_done && P1.rgb_done && P1.ent_done);
-    if (__syncthreads_count(live) == 0) break;
-    const int n = min((uint32_t)kBatch, rg.y - base);
-    stage_batch<LC, RGB, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
-    __syncthreads();
-    if (__all_sync(0xffffffffu, !live)) continue;
-    // warp pre-filter: one lane per entry tests the entry's coverage rectangle
-    // against the warp's 8x8 pixel block; only hits are walked (in list order).
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      bool hit = false;
-      if (j0 + lane < n) {
-        const int4 r = s_rect[j0 + lane];
-        hit = r.x <= bx0 + 7 && r.x + r.y >= bx0 && r.z <= by0 + 7 && r.z + r.w >= by0;
-      }
-      unsigned hits = __ballot_sync(0xffffffffu, hit);
-      while (hits != 0u) {
-      const int j = j0 + __ffs(hits) - 1;
-      hits &= hits - 1u;
-      const int4 rr = s_rect[j];
-      const bool c0 = !(P0.rgb_done && P0.ent_done) && in_rect4(rr, px, py0);
-      const bool c1 = !(P1.rgb_done && P1.ent_done) && in_rect4(rr, px, py1);
-      if (!(c0 || c1)) continue;
-      const GeoRec& e = s_geo[j];
-      const float2* col2 = reinterpret_cast<const float2*>(s_col + j * CS);
-      if (c0) {
-        const double al = splat_alpha(e, cxp, cyp0, amax);
-        if (RGB && !P0.rgb_done) rgb_step<LC, EXTRA>(P0, al, e.depth, col2, cutoff);
-        if (ENT && !P0.ent_done) ent_step<LC, EXTRA>(P0, al, e.depth, s_ua[j], amax, cutoff, hl_qc);
-      }
-      if (c1) {
-        const double al = splat_alpha(e, cxp, cyp1, amax);
-        if (RGB && !P1.rgb_done) rgb_step<LC, EXTRA>(P1, al, e.depth, col2, cutoff);
-        if (ENT && !P1.ent_done) ent_step<LC, EXTRA>(P1, al, e.depth, s_ua[j], amax, cutoff, hl_qc);
-      }
-      }
-    }
-  }
-  pixel_finish<LC, RGB, ENT, EXTRA>(P0, a, c, px, py0, in0);
-  pixel_finish<LC, RGB, ENT, EXTRA>(P1, a, c, px, py1, in1);
-}
 
 // ---------------------------------------------------------------------------
 // Any tile size: 256 threads, one pixel each, pixels in rounds of 256.
@@ -311,25 +232,16 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
     const char* e = getenv("GAVIS_UA_KERNEL");
     return e ? atoi(e) : 0;
   }();
-  // default for 16x16 tiles: the entry-pair (ILP) kernel; GAVIS_UA_KERNEL=3 selects
-  // the two-pixel kernel, =1 the generic per-pixel kernel (A/B measurements).
-  // (batch 192: fewer block barriers per tile list than 128; 3 CTAs of 58 KB fit)
-  if (a.tile_size == 16 && (choice == 0 || choice == 2)) {
+  // default for 16x16 tiles: the entry-pair (ILP) kernel; GAVIS_UA_KERNEL=1 selects
+  // the generic per-pixel kernel (A/B measurements). (batch 192: fewer block
+  // barriers per tile list than 128; 3 CTAs of 58 KB fit)
+  if (a.tile_size == 16 && choice != 1) {
     constexpr int kIlpBatch = 192;
     const size_t sm = Stage<LC, RGB, ENT>::bytes(kIlpBatch);
     static bool configured = false;
     if (!configured) set_smem(ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, kIlpBatch>, sm);
     configured = true;
     ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, kIlpBatch><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
-    return;
-  }
-  if (a.tile_size == 16 && choice == 3) {
-    static bool configured = false;
-    if (!configured) {
-      set_smem(ua_blend_tile2_kernel<LC, RGB, ENT, EXTRA>, smem);
-      configured = true;
-    }
-    ua_blend_tile2_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 128, smem, s>>>(a);
     return;
   }
   static bool configured = false;

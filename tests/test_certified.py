@@ -146,12 +146,14 @@ def test_forced_redo_is_exact(ctx, ctx_exact, monkeypatch, room):
         assert np.array_equal(ex[k], got[k]), k
 
 
-def test_certified_vs_exact_full_size(ctx, ctx_exact):
-    """Config 3 at full size (1M Gaussians, 800^2): size-independent agreement of
-    the certified and the exact device paths (the exact path is pinned to the oracle)."""
-    c = synth.config3(0, n_candidates=4)
+@pytest.mark.parametrize("cfg", [3, 2])
+def test_certified_vs_exact_full_size(ctx, ctx_exact, cfg):
+    """Configs 3 (1M Gaussians, indoor) and 2 (500k, object) at full size, 800^2:
+    size-independent agreement of the certified and the exact device paths (the
+    exact path is pinned to the oracle)."""
+    c = synth.config3(0, n_candidates=4) if cfg == 3 else synth.config2(0, n_candidates=4)
     scene = c["scene"]
-    f = api.construct_field(ctx_exact, scene, c["train"][:30], VmfParams(1.0), 2, RC)
+    f = api.construct_field(ctx_exact, scene, c["train"][:30], VmfParams(1.0), c["degree"], RC)
     cams = c["candidates"][:4]
     kw = dict(rgb=True, transmittance=True, entropy=True, invisible_mass=True, scores=True, contributors=True)
     ex = api.render(ctx_exact, scene, f, cams, RC, UC, **kw)
