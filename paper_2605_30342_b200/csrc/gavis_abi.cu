@@ -716,12 +716,12 @@ void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t count,
 }
 
 // Certification window of the fp32 blend, relative to the cutoff: twice the
-// bound u (16 + 4.2 k + 22 S) derived in kernels_ua_fast.cu (k composited
+// bound u (16 + 3.2 k + 22 S) derived in kernels_ua_fast.cu (k composited
 // entries, S = sum a/(1-a) over them).
 void cert_window(UaBlendArgs* ua) {
   const double u = std::ldexp(1.0, -24);
   ua->cert_base = (float)(2.0 * u * 16.0);
-  ua->cert_per_step = (float)(2.0 * u * 4.2);
+  ua->cert_per_step = (float)(2.0 * u * 3.2);
   ua->cert_sum = (float)(2.0 * u * 22.0);
   // test hook (tests/test_certified.py): hand every pixel to the fp64 redo
   const char* force = std::getenv("GAVIS_CERT_FORCE_REDO");

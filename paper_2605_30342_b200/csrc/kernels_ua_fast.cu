@@ -16,14 +16,14 @@
 // Error bound (relative, T_fp32 vs T_fp64, u = 2^-24). A composited entry
 // multiplies T by (1 - a). fp32 perturbs a by |da| <= a (1.5 q + 8) u (q -> fp32
 // and the ln2 scaling 1.5 q u, ex2.approx <= 4u, products and the A/B/v
-// roundings of a* <= 4u), so the factor is off by |da| / (1 - a) + 2u (its own
-// rounding and the product's). On the splat's support q <= 2 ln(o/a), hence
+// roundings of a* <= 4u), so the new T = fma(-T, a, T) (one rounding) is off by
+// |da| / (1 - a) + u. On the splat's support q <= 2 ln(o/a), hence
 //   a < 1/2 :  a (1.5 q + 8) / (1 - a) <= 2 (3/e + 8 a)   <= 2.2 + 16 a/(1-a)
 //   a >= 1/2:  q <= 2 ln 2, a (1.5 q + 8) / (1 - a)        <= 10.1 a/(1-a)
 // and for a* = clamp(A a + B): [A a (1.5 q + 8) + 3 a*] / (1 - a*) <= 2.2 +
 // 22 a*/(1-a*) (A a (1.5 q + 8) <= 8 A o <= 16 a* when a* >= 1/2). After k
 // entries, with S = sum a/(1-a) over them, the relative error is at most
-//   u (22 S + 4.2 k + 16).
+//   u (22 S + 3.2 k + 16).
 // The kernel accumulates S per track (one rcp.approx + one FMA per entry) and
 // flags a pixel when min |T/cutoff - 1| over the two tests bracketing its stop
 // (or its final T, if it never stops) is within twice that bound
@@ -234,7 +234,7 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
     if (EXTRA) P.dp = fmaf(wa, ea.depth, P.dp);
     const float fa = 1.f - aa;
     P.S = fmaf(aa, rcp_approx(fa), P.S);
-    const float Ta = P.T * fa;
+    const float Ta = fmaf(-P.T, aa, P.T);  // T (1 - a), one rounding
     const bool sa = ra && Ta < cutoff;
     P.Tp = sa ? P.T : P.Tp;
     P.T = Ta;
@@ -247,7 +247,7 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
     if (EXTRA) P.dp = fmaf(wb, eb.depth, P.dp);
     const float fb = 1.f - ab;
     P.S = fmaf(ab, rcp_approx(fb), P.S);
-    const float Tb = P.T * fb;
+    const float Tb = fmaf(-P.T, ab, P.T);
     const bool sb = rb && Tb < cutoff;
     P.Tp = sb ? P.T : P.Tp;
     P.T = Tb;
@@ -267,7 +267,7 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
     if (EXTRA) P.ed = fmaf(wa, ea.depth, P.ed);
     const float fa = 1.f - asa;
     P.Se = fmaf(asa, rcp_approx(fa), P.Se);
-    const float Ta = P.Te * fa;
+    const float Ta = fmaf(-P.Te, asa, P.Te);
     const bool ta = oa && Ta < cutoff;
     P.Tep = ta ? P.Te : P.Tep;
     P.Te = Ta;
@@ -279,7 +279,7 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
     if (EXTRA) P.ed = fmaf(wb, eb.depth, P.ed);
     const float fb = 1.f - asb;
     P.Se = fmaf(asb, rcp_approx(fb), P.Se);
-    const float Tb = P.Te * fb;
+    const float Tb = fmaf(-P.Te, asb, P.Te);
     const bool tb = ob && Tb < cutoff;
     P.Tep = tb ? P.Te : P.Tep;
     P.Te = Tb;
