@@ -18,7 +18,7 @@ constexpr int kMaxBatchViews = 64;
 
 struct Sigma {
   double s00, s01, s02, s11, s12, s22;
-  double trace;  // >= lambda_max(Sigma): bounds the screen radius before projecting Sigma
+  double lam;  // >= lambda_max(Sigma) (Gershgorin): bounds the screen radius before projecting
 };
 
 // GaussianParticle::covariance (model.hpp:42-45), Eigen toRotationMatrix order.
@@ -42,7 +42,10 @@ __device__ __forceinline__ Sigma covariance(float4 q, float4 sc) {
   s.s11 = m10 * m10 + m11 * m11 + m12 * m12;
   s.s12 = m10 * m20 + m11 * m21 + m12 * m22;
   s.s22 = m20 * m20 + m21 * m21 + m22 * m22;
-  s.trace = s.s00 + s.s11 + s.s22;
+  const double r0 = s.s00 + fabs(s.s01) + fabs(s.s02);
+  const double r1 = fabs(s.s01) + s.s11 + fabs(s.s12);
+  const double r2 = fabs(s.s02) + fabs(s.s12) + s.s22;
+  s.lam = fmax(r0, fmax(r1, r2));
   return s;
 }
 
@@ -66,12 +69,12 @@ __device__ __forceinline__ bool project(const DevCam& c, double px, double py, d
   ux = ux < -c.limx ? -c.limx : (c.limx < ux ? c.limx : ux);
   uy = uy < -c.limy ? -c.limy : (c.limy < uy ? c.limy : uy);
   {
-    // Frustum pre-test: lambda_max(cov2) <= trace(J Sigma J^T) + 2 dil^2 <=
-    // trace(Sigma) |J|_F^2 + 2 dil^2, so r <= rub; a particle outside the
-    // frustum by more than rub is culled below anyway -- skip projecting Sigma.
+    // Frustum pre-test: lambda_max(cov2) <= lambda_max(Sigma) |J|_F^2 + dil^2, so
+    // r <= rub; a particle outside the frustum by more than rub is culled below
+    // anyway -- skip projecting Sigma.
     const double gx = fx * inv_z, gy = fy * inv_z;
     const double jf = gx * gx * (1.0 + ux * ux) + gy * gy * (1.0 + uy * uy);
-    const double rub = 3.0 * sqrt((S.trace * jf + 2.0 * dilation * dilation) * 1.000001) + 1e-9;
+    const double rub = 3.0 * sqrt((S.lam * jf + 2.0 * dilation * dilation) * 1.000001) + 1e-9;
     if (mx < -rub || mx > c.width + rub || my < -rub || my > c.height + rub) return false;
   }
   const double jx = ux * t2;
@@ -145,11 +148,13 @@ __device__ __forceinline__ double query_row(const double* row, int num_views, do
 
 // Cheap visibility screen of one (view, particle): the near-plane test exactly as
 // project_particle makes it (fp64, same operations), then a conservative fp32
-// frustum test with the radius bound r <= 3 sqrt(trace(Sigma) |J|_F^2 + 2 dil^2)
-// (lambda_max(cov2) <= trace(cov2)) and a margin 100x above the fp32 error: a
-// particle it rejects is culled by project() as well.
+// frustum test with the radius bound r <= 3 sqrt(lambda_max(Sigma) lambda_max(J J^T)
+// + dil^2) (J C J^T <= lambda_max(C) J J^T in the Loewner order, C = W Sigma W^T
+// has Sigma's spectrum; lam >= lambda_max(Sigma) by Gershgorin), inflated by 0.1 %,
+// and a position margin 100x above the fp32 error: a particle it rejects is
+// culled by project() as well.
 __device__ __forceinline__ bool screen(const DevCam& c, double px, double py, double pz,
-                                       float trace, float dil2x2) {
+                                       float lam, float dil2) {
   const double d0 = px - c.pos[0], d1 = py - c.pos[1], d2 = pz - c.pos[2];
   const double t2 = c.R[2] * d0 + c.R[5] * d1 + c.R[8] * d2;
   if (t2 < c.near_plane) return false;
@@ -163,8 +168,11 @@ __device__ __forceinline__ bool screen(const DevCam& c, double px, double py, do
   const float lx = (float)c.limx, ly = (float)c.limy;
   const float uxc = fminf(fmaxf(ux, -lx), lx), uyc = fminf(fmaxf(uy, -ly), ly);
   const float gx = fx * iz, gy = fy * iz;
-  const float jf = gx * gx * (1.f + uxc * uxc) + gy * gy * (1.f + uyc * uyc);
-  const float rub = 3.f * sqrtf(__fmaf_rn(trace, jf, dil2x2));
+  const float j00 = gx * gx * (1.f + uxc * uxc), j11 = gy * gy * (1.f + uyc * uyc);
+  const float j01 = gx * gy * uxc * uyc;
+  const float hd = 0.5f * (j00 - j11);
+  const float lj = 0.5f * (j00 + j11) + sqrtf(hd * hd + j01 * j01);  // lambda_max(J J^T), no cancellation
+  const float rub = 3.f * sqrtf(__fmaf_rn(lam, lj, dil2) * 1.002f);
   const float W = (float)c.width, H = (float)c.height;
   const float M = 1e-3f * (fabsf(mx) + fabsf(my) + rub + W + H) + 1e-2f;
   return !(mx + rub < -M || mx - rub > W + M || my + rub < -M || my - rub > H + M);
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
   const int64_t g = wbase + lane;
   const bool valid = g < N;
   double px = 0.0, py = 0.0, pz = 0.0;
-  float trace = 0.f;
+  float lam = 0.f;
   if (valid) {
     const float4 po = a.scene.pos_op[g];
     const Sigma S = covariance(a.scene.rot[g], a.scene.scale[g]);
@@ -199,16 +207,16 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
     px = po.x;
     py = po.y;
     pz = po.z;
-    trace = (float)S.trace;
+    lam = (float)S.lam;
   }
   __syncthreads();
-  const float dil2x2 = (float)(2.0 * a.dilation * a.dilation);
+  const float dil2 = (float)(a.dilation * a.dilation);
   const uint2 empty_rect = make_uint2(1u, 1u);  // tx0 = 1 > tx1 = 0
   int qn = 0;
   for (int v = 0; v < a.V; ++v) {
     bool surv = false;
     if (valid) {
-      surv = screen(s_cam[v], px, py, pz, trace, dil2x2);
+      surv = screen(s_cam[v], px, py, pz, lam, dil2);
       if (!surv) {
         const int64_t slot = (int64_t)v * N + g;
         a.counts[slot] = 0;
