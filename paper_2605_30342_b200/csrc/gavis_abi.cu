@@ -646,11 +646,32 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
   const int bv = batch_views(c, N, n_views);
   double scales[kMaxFieldDegree + 1] = {0};
   if (f) vmf_scales(f->kappa, f->degree, scales);
-  for (int v0 = 0; v0 < n_views; v0 += bv) {
+  // binning of batch k+1 on the front stream under batch k's blend (as ua_render)
+  cudaStream_t main_stream = c->stream;
+  struct Restore {
+    gavis_ctx* c;
+    cudaStream_t main;
+    ~Restore() {
+      c->bufset = 0;
+      c->stream = main;
+    }
+  } restore{c, main_stream};
+  CK(cudaEventRecord(c->ev_done[0], main_stream));
+  CK(cudaStreamWaitEvent(c->front, c->ev_done[0], 0));
+  const bool host_out = vis_host || touch_host || contrib_host;
+  int batch = 0;
+  for (int v0 = 0; v0 < n_views; v0 += bv, ++batch) {
     const int V = std::min(bv, n_views - v0);
+    const int par = batch & 1;
+    c->bufset = par;
+    c->stream = c->front;
+    if (batch >= 2) CK(cudaStreamWaitEvent(c->front, c->ev_done[par], 0));
     BinOpts o;
     o.vf_mode = true;
     Binned b = bin_batch(c, s, views + v0, V, rc, o);
+    CK(cudaEventRecord(c->ev_bin[par], c->front));
+    c->stream = main_stream;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_bin[par], 0));
     double* psum = (double*)c->buf("pair_sum", sizeof(double) * b.K);
     int32_t* pcnt = (int32_t*)c->buf("pair_cnt", sizeof(int32_t) * b.K);
     if (b.K > 0) {
@@ -703,8 +724,11 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
     if (contrib_host)
       CK(cudaMemcpyAsync(contrib_host, dcontrib, sizeof(int32_t) * b.total_pix,
                          cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
+    CK(cudaEventRecord(c->ev_done[par], c->stream));
+    if (host_out) c->sync();
   }
+  c->bufset = 0;
+  c->sync_all();
   if (f) f->num_views += n_views;
 }
 
