@@ -16,10 +16,10 @@ timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err
 echo "bench exit $?" >> $OUT/${TAG}_bench.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/${TAG}_bench_reference.json 2>> $OUT/${TAG}_bench.err
 timeout 900 python bench.py --precision exact --steps 3 --warmup 3 --no-cpu-baseline --no-extra-vf > $OUT/${TAG}_bench_exact.json 2>> $OUT/${TAG}_bench.err
-SMALL="bench.py --steps 1 --warmup 3 --per-gpu 64 --no-cpu-baseline --no-e2e --no-extra-vf"
-if timeout 600 python $SMALL > $OUT/${TAG}_small.json 2>&1; then
-  timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file $OUT/${TAG}_launches.csv python $SMALL > $OUT/${TAG}_ncu_launches.log 2>&1
+# launch list of one 16-view field build + two 16-candidate UA renders (all kernels)
+if timeout 300 python tools/profile_driver.py ua > $OUT/${TAG}_small.log 2>&1; then
+  timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/${TAG}_launches.csv python tools/profile_driver.py ua > $OUT/${TAG}_ncu_launches.log 2>&1
 fi
 if timeout 300 python tools/profile_driver.py ua > $OUT/${TAG}_ua.log 2>&1; then
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ua_blend_fast -s 1 -c 1 \
