@@ -222,6 +222,7 @@ struct gavis_ctx {
   int64_t pin_scores_cap = 0;
   int precision = GAVIS_PRECISION_CERTIFIED;
   int64_t redo_pixels = 0;       // pixels the certified blend handed to the fp64 redo
+  double batch_budget = 0.0;     // bytes of per-(view, particle) state one batch may use
   int64_t rescored_views = 0;    // candidates re-scored exactly to certify an argmax
   std::recursive_mutex mu;
 
@@ -372,8 +373,14 @@ DevCam make_devcam(const gavis_camera& c, int ts, int64_t tile_base, int64_t pix
 int batch_views(gavis_ctx* c, int64_t N, int n_views) {
   int vmax = c->max_batch > 0 ? c->max_batch : 32;
   if (N > 0) {
-    // ~112 B of per-(view, particle) state; keep a batch under ~6 GB of it.
-    const int64_t by_mem = (int64_t)(6.0e9 / (112.0 * (double)N));
+    // ~112 B of per-(view, particle) state per batch, two batches in flight: one
+    // batch may use a sixth of the free device memory, within [2, 16] GB
+    if (c->batch_budget == 0.0) {
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      c->batch_budget = std::min(16.0e9, std::max(2.0e9, (double)free_b / 6.0));
+    }
+    const int64_t by_mem = (int64_t)(c->batch_budget / (112.0 * (double)N));
     vmax = (int)std::max<int64_t>(1, std::min<int64_t>(vmax, by_mem));
   }
   vmax = std::min(vmax, 64);
