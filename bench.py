@@ -315,6 +315,25 @@ def run_ours(args):
     total_cands = sum_over_ranks(float(len(cands) * args.steps), dist)
     value = total_cands / (ms_max / 1000.0)
 
+    # parity gate of this run: certified scores/argmax against the exact fp64 path on
+    # the first 8 candidates, contributor counts of one view (tests hold the oracle)
+    gate_cams = cands[: min(8, len(cands))]
+    cert = api.render(ctx, ds, field, gate_cams[:1], rc, uc, entropy=True, rgb=True, contributors=True)
+    cert_scores = api.score_views(ctx, ds, field, gate_cams, rc, uc, with_rgb=True)
+    ctx.set_precision("exact")
+    exact = api.render(ctx, ds, field, gate_cams[:1], rc, uc, entropy=True, rgb=True, contributors=True)
+    exact_scores = api.score_views(ctx, ds, field, gate_cams, rc, uc, with_rgb=True)
+    ctx.set_precision(args.precision)
+    parity_gate = {
+        "candidates": len(gate_cams),
+        "scores_max_rel": float(np.max(np.abs(cert_scores - exact_scores) / np.abs(exact_scores))),
+        "argmax_equal": bool(parallel.first_max(cert_scores) == parallel.first_max(exact_scores)),
+        "contributors_equal": bool(np.array_equal(cert["rgb_contributors"], exact["rgb_contributors"]) and
+                                   np.array_equal(cert["entropy_contributors"], exact["entropy_contributors"])),
+        "images_max_abs": float(max(np.max(np.abs(cert["rgb"] - exact["rgb"])),
+                                    np.max(np.abs(cert["entropy"] - exact["entropy"])))),
+        "reference": "exact fp64 device path (pinned to the CPU oracle by tests/test_gpu_parity.py)"}
+
     # secondary: the reference planner's own select_nbv work (entropy + score, no RGB)
     barrier(ctx, dist)
     ctx.timer_start()
@@ -390,8 +409,8 @@ def run_ours(args):
     vf_other = {}
     if not args.no_extra_vf:
         from paper_2605_30342_b200 import synth
-        for cid, gen in ((2, lambda: synth.config2(0, n_candidates=0)),
-                         (4, lambda: synth.config4(0, n_candidates=0))):
+        for cid, gen in ((2, lambda: synth.config2(0, n_candidates=256)),
+                         (4, lambda: synth.config4(0, n_candidates=64))):
             cc = gen()
             dsc = ctx.upload(cc["scene"])
             fld = build_field(cc["train"], dsc, cc["degree"])  # warm-up
@@ -403,9 +422,22 @@ def run_ours(args):
                 fld = build_field(cc["train"], dsc, cc["degree"])
                 barrier(ctx, dist)
                 times.append((time.perf_counter() - t0) * 1000.0)
-                fld.close()
+                if _ == 0:
+                    fld.close()
+            # UA render + score of this config's candidates (per rank block, device time)
+            clo, chi = parallel.shard_range(len(cc["candidates"]), rank, world)
+            ccands = cc["candidates"][clo:chi]
+            api.select_nbv(ctx, dsc, fld, ccands, rc, uc, with_rgb=True)  # warm-up (buffer sizes)
+            barrier(ctx, dist)
+            ctx.timer_start()
+            api.select_nbv(ctx, dsc, fld, ccands, rc, uc, with_rgb=True)
+            ua_ms = max_over_ranks(ctx.timer_stop(), dist)
+            fld.close()
             cam = cc["train"][0]
             vf_other[f"config{cid}"] = {"vf_build_ms": max_over_ranks(min(times), dist),
+                                        "ua_views_per_s": sum_over_ranks(float(len(ccands)), dist) / (ua_ms / 1000.0),
+                                        "ua_candidates": len(cc["candidates"]),
+                                        "ua_resolution": [cc["candidates"][0].width, cc["candidates"][0].height],
                                         "views": len(cc["train"]), "particles": cc["scene"].num_particles,
                                         "resolution": [cam.width, cam.height], "field_degree": cc["degree"]}
             dsc.close()
@@ -486,6 +518,7 @@ def run_ours(args):
             "vf_build_other_configs": vf_other,
             "best_index_last_step": int(res.best_index) + (lo if world == 1 else 0),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "parity_gate": parity_gate,
             **({"config5_sweep": sweep5} if sweep5 else {}),
         }
         print(json.dumps(line))

@@ -107,7 +107,7 @@ gavis_status gavis_ctx_set_batch(gavis_ctx* ctx, int32_t max_views_per_batch);
  *    on the early-termination tests; pixels the bound cannot certify are
  *    recomputed in fp64, so contributor counts equal the fp64 reference's;
  *    images agree with it to ~1e-6 (north_star: 1e-4); select_nbv re-scores in
- *    fp64 every candidate within 1e-4 (relative) of the best, so the argmax is
+ *    fp64 every candidate within 1e-3 (relative) of the best, so the argmax is
  *    the fp64 one. Used for 16x16 tiles and alpha_clamp_max <= 0.999.
  *  GAVIS_PRECISION_EXACT: every blend in fp64 with the reference's operation
  *    order (images to ~1e-12 of the reference). */

@@ -945,8 +945,9 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
 // scores from the certified fp32 blend: every candidate within kCertScoreRel
 // (relative) of the best is re-scored with the exact fp64 blend and the argmax
 // is taken again, so it is the exact path's argmax (the fp32 scores agree with
-// the fp64 ones to ~1e-7 relative, three orders of magnitude inside the window).
-constexpr double kCertScoreRel = 1e-4;
+// the fp64 ones to a few 1e-6 relative -- 3e-6 at config 3 -- over two orders of
+// magnitude inside the window).
+constexpr double kCertScoreRel = 1e-3;
 
 int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
                         const gavis_camera* cams, int n, const gavis_raster_config* rc,
