@@ -336,6 +336,7 @@ struct gavis_scene {
   float* colors = nullptr;
   float* var = nullptr;  // coefficient variances for the sh_propagation provider
   int var_degree = -1;
+  float max_opacity = 1.f;  // enters the certified blend's error bound (q <= 2 ln(o / alpha))
 };
 
 struct gavis_field {
@@ -749,11 +750,15 @@ void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t count,
 // Certification window of the fp32 blend, relative to the cutoff: twice the
 // bound u (16 + 3.2 k + 22 S) derived in kernels_ua_fast.cu (k composited
 // entries, S = sum a/(1-a) over them).
-void cert_window(UaBlendArgs* ua) {
+// Opacities above 1 (not excluded by the reference) weaken the alpha-error
+// bounds (q <= 2 ln(o_max / a); A a (1.5 q + 8) <= 8 o_max A): the S coefficient
+// becomes 22 o_max + 6 ln(o_max) (22 for o_max <= 1).
+void cert_window(UaBlendArgs* ua, float max_opacity) {
   const double u = std::ldexp(1.0, -24);
+  const double om = std::max(1.0, (double)max_opacity);
   ua->cert_base = (float)(2.0 * u * 16.0);
   ua->cert_per_step = (float)(2.0 * u * 3.2);
-  ua->cert_sum = (float)(2.0 * u * 22.0);
+  ua->cert_sum = (float)(2.0 * u * (22.0 * om + 6.0 * std::log(om)));
   // test hook (tests/test_certified.py): hand every pixel to the fp64 redo
   const char* force = std::getenv("GAVIS_CERT_FORCE_REDO");
   if (force && force[0] == '1') ua->cert_base = 3.0e38f;
@@ -891,7 +896,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       ua.flag_list = (uint32_t*)c->buf("flag_list", sizeof(uint32_t) * P);
       ua.flag_count = (uint32_t*)c->buf("flag_count", sizeof(uint32_t));
       CK(cudaMemsetAsync(ua.flag_count, 0, sizeof(uint32_t), c->stream));
-      cert_window(&ua);
+      cert_window(&ua, s->max_opacity);
       c->run("ua_blend", [&] { launch_ua_blend_fast(ua, c->stream); });
       CK(cudaEventRecord(c->ev_blend[par], c->stream));
       CK(cudaStreamWaitEvent(side, c->ev_blend[par], 0));
@@ -1322,6 +1327,7 @@ gavis_status gavis_density_control(gavis_ctx* c, const gavis_scene* scene, const
     std::vector<int64_t> all(n_virtual);
     for (int64_t k = 0; k < n_virtual; ++k) all[k] = k;
     gavis_scene* probe = alloc_scene(c, n_real + n_virtual, scene->dev.color_degree);
+    probe->max_opacity = scene->max_opacity;
     std::vector<double> unseen((size_t)std::max<int64_t>(1, n_virtual), 1.0);
     try {
       copy_particles(c, probe, 0, scene, n_real);
@@ -1351,6 +1357,7 @@ gavis_status gavis_density_control(gavis_ctx* c, const gavis_scene* scene, const
       keep.push_back(k);
     }
     gavis_scene* o = alloc_scene(c, n_real + (int64_t)keep.size(), scene->dev.color_degree);
+    o->max_opacity = scene->max_opacity;
     try {
       copy_particles(c, o, 0, scene, n_real);
       upload_probes(c, o, n_real, p, keep);
@@ -1380,6 +1387,7 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
     gavis_scene* s = alloc_scene(c, N, d->color_degree);
+    for (int64_t i = 0; i < N; ++i) s->max_opacity = std::max(s->max_opacity, d->opacities[i]);
     const int nb = s->dev.nb;
     const int nbp = nb + (nb & 1);
     const int cstride = s->dev.cstride;
