@@ -241,3 +241,19 @@ def test_certified_edge_cases(ctx):
     from paper_2605_30342_b200.model import Scene
     r = api.render(ctx, Scene.empty(), None, [synth.z_camera()], RC, UC, rgb=True, transmittance=True)
     assert np.all(r["rgb"] == 0) and np.all(r["transmittance"] == 1)
+
+
+def test_certified_opacity_above_one(ctx):
+    """The reference does not clamp opacities; the certified bound scales with the
+    scene's largest opacity, so counts stay exact with o up to 3."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    boosted = scene.__class__(scene.positions, scene.rotations, scene.scales,
+                              (scene.opacities * 3.0).astype(np.float32), scene.colors, scene.is_virtual,
+                              scene.color_degree, scene.bounds_min, scene.bounds_max)
+    osc = O.OracleScene(boosted)
+    for cam in c["candidates"][:2]:
+        r = api.render(ctx, boosted, None, [cam], RC, UC, rgb=True, contributors=True)
+        rgb, _, _, cc = O.rasterize(osc, cam, RC, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], cc)
+        assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
