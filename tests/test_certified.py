@@ -257,3 +257,23 @@ def test_certified_opacity_above_one(ctx):
         rgb, _, _, cc = O.rasterize(osc, cam, RC, contrib=True)
         assert np.array_equal(r["rgb_contributors"], cc)
         assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+
+
+@pytest.mark.parametrize("cutoff,amax", [(1e-2, 0.99), (1e-7, 0.99), (1e-4, 0.999), (1e-4, 0.5)])
+def test_certified_raster_configs(ctx, cutoff, amax):
+    """Other transmittance cutoffs and alpha clamps: the window is relative to the
+    cutoff and the clamp bounds a/(1-a); counts stay exact."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    rc = RasterConfig(transmittance_cutoff=cutoff, alpha_clamp_max=amax)
+    f = api.construct_field(ctx, scene, c["train"][:6], VmfParams(1.0), 2, rc)
+    g = f.download().gamma
+    cam = c["candidates"][3]
+    r = api.render(ctx, scene, f, [cam], rc, UC, rgb=True, entropy=True, contributors=True)
+    rgb, _, _, rcc = O.rasterize(osc, cam, rc, contrib=True)
+    H, _, _, ecc = O.render_entropy(osc, g, 2, 6, cam, rc, UC, contrib=True)
+    assert np.array_equal(r["rgb_contributors"], rcc)
+    assert np.array_equal(r["entropy_contributors"], ecc)
+    assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+    assert np.max(np.abs(r["entropy"] - H)) <= IMG_ABS
