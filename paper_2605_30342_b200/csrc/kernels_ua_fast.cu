@@ -258,8 +258,9 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
     // compensated_alpha (uncertainty.hpp:55-59) and the entropy step (:198-222);
     // ua = (A, B, v, hl + C_H)
     const bool oa = ca && !P.edn;
-    const float xa = fminf(fmaxf(fmaf(ua.x, ala, ua.y), 0.f), amax);
-    const float xb = fminf(fmaxf(fmaf(ub.x, alb, ub.y), 0.f), amax);
+    // A, B >= 0 (A = v + beta (1 - v), B = o0 (1 - beta)(1 - v)): no lower clamp needed
+    const float xa = fminf(fmaf(ua.x, ala, ua.y), amax);
+    const float xb = fminf(fmaf(ub.x, alb, ub.y), amax);
     const float asa = oa ? xa : 0.f;
     const float wa = asa * P.Te;
     const float sa = wa * ua.z;
