@@ -277,3 +277,47 @@ def test_certified_raster_configs(ctx, cutoff, amax):
     assert np.array_equal(r["entropy_contributors"], ecc)
     assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
     assert np.max(np.abs(r["entropy"] - H)) <= IMG_ABS
+
+
+def _fuzz_scene(seed: int, n: int):
+    """Mixed populations: thin slabs, near-opaque splats (alpha at the clamp), faint
+    large splats, degree-3 colours -- the regimes that stress the error bound."""
+    rng = np.random.default_rng(seed)
+    pos = np.stack([rng.uniform(-1.2, 1.2, n), rng.uniform(-1.2, 1.2, n), rng.uniform(2.0, 5.0, n)], 1)
+    kind = rng.integers(0, 3, n)
+    sc = np.exp(rng.normal(-3.5, 0.6, (n, 3)))
+    sc[kind == 0, 2] = np.exp(rng.normal(-7.0, 0.3, int((kind == 0).sum())))  # slabs
+    sc[kind == 2] *= 3.0                                                      # large, faint
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    op = np.where(kind == 1, rng.uniform(0.95, 1.0, n), rng.uniform(0.02, 0.9, n))
+    op[kind == 2] *= 0.2
+    col = rng.normal(0.0, 0.3, (n, 3, 16))
+    col[:, :, 0] += 0.5 / 0.28209479177387814
+    from paper_2605_30342_b200.model import Scene
+    return Scene(pos.astype(np.float32), q.astype(np.float32), sc.astype(np.float32), op.astype(np.float32),
+                 col.astype(np.float32), np.zeros(n, np.uint8), 3, np.array([-2.0, -2, 1]), np.array([2.0, 2, 7]))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_certified_fuzz(ctx, seed):
+    """Randomised scenes and cameras: contributor counts of both tracks exact,
+    images within tolerance, against the oracle (given per-particle visibility)."""
+    scene = _fuzz_scene(seed, 3000)
+    osc = O.OracleScene(scene)
+    rng = np.random.default_rng(100 + seed)
+    vis = rng.uniform(0, 1, scene.num_particles)
+    vis[rng.uniform(size=scene.num_particles) < 0.3] = 0.0
+    vis[rng.uniform(size=scene.num_particles) < 0.2] = 1.0
+    for k in range(2):
+        eye = (rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5))
+        cam = make_lookat(eye, (rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), 3.5), (0, 1, 0), 96, 80)
+        r = api.render(ctx, scene, None, [cam], RC, UC, rgb=True, entropy=True, contributors=True,
+                       splat_visibility=vis)
+        rgb, _, _, rcc = O.rasterize(osc, cam, RC, contrib=True)
+        H, _, _ = O.render_entropy_core(osc, cam, RC, UC, vis)
+        _, _, _, ecc = O.render_entropy_core(osc, cam, RC, UC, vis, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], rcc)
+        assert np.array_equal(r["entropy_contributors"], ecc)
+        assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+        assert np.max(np.abs(r["entropy"] - H)) <= IMG_ABS
