@@ -324,6 +324,10 @@ def run_ours(args):
     exact = api.render(ctx, ds, field, gate_cams[:1], rc, uc, entropy=True, rgb=True, contributors=True)
     exact_scores = api.score_views(ctx, ds, field, gate_cams, rc, uc, with_rgb=True)
     ctx.set_precision(args.precision)
+    # covered (pixel, list entry) pairs composited per view (SURVEY 8d secondary metric):
+    # the per-pixel contributor counts of both tracks, averaged over the gate views
+    cov_rgb = float(np.sum(exact["rgb_contributors"]))
+    cov_ent = float(np.sum(exact["entropy_contributors"]))
     parity_gate = {
         "candidates": len(gate_cams),
         "scores_max_rel": float(np.max(np.abs(cert_scores - exact_scores) / np.abs(exact_scores))),
@@ -519,6 +523,9 @@ def run_ours(args):
             "best_index_last_step": int(res.best_index) + (lo if world == 1 else 0),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
             "parity_gate": parity_gate,
+            "covered_pairs": {"rgb_per_view": cov_rgb, "entropy_per_view": cov_ent,
+                              "per_s": (cov_rgb + cov_ent) * value,
+                              "note": "pixel-entry evaluations until each track terminates, view 0 of the step"},
             **({"config5_sweep": sweep5} if sweep5 else {}),
         }
         print(json.dumps(line))
