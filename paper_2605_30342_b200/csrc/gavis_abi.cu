@@ -759,6 +759,8 @@ void cert_window(UaBlendArgs* ua, float max_opacity) {
   ua->cert_base = (float)(2.0 * u * 16.0);
   ua->cert_per_step = (float)(2.0 * u * 3.2);
   ua->cert_sum = (float)(2.0 * u * (22.0 * om + 6.0 * std::log(om)));
+  ua->cert_per_step2 = (float)(2.0 * u * (1.004 + 3e-4 * std::log(om)));
+  ua->cert_sum2 = (float)(2.0 * u * (41.0 + 3.0 * std::log(om)) * om);
   // test hook (tests/test_certified.py): hand every pixel to the fp64 redo
   const char* force = std::getenv("GAVIS_CERT_FORCE_REDO");
   if (force && force[0] == '1') ua->cert_base = 3.0e38f;

@@ -152,6 +152,8 @@ struct UaBlendArgs {
   float cert_base = 0.f;           // relative window, constant part
   float cert_per_step = 0.f;       // relative window per composited entry
   float cert_sum = 0.f;            // relative window per unit of sum a/(1-a)
+  float cert_per_step2 = 0.f;      // second bound (small-alpha steps folded into S)
+  float cert_sum2 = 0.f;
 };
 
 // Per-pixel mixtures of the entropy track for one view (kernels_mixture.cu).

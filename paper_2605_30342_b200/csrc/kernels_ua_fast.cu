@@ -24,6 +24,10 @@
 // 22 a*/(1-a*) (A a (1.5 q + 8) <= 8 A o <= 16 a* when a* >= 1/2). After k
 // entries, with S = sum a/(1-a) over them, the relative error is at most
 //   u (22 S + 3.2 k + 16).
+// A second bound splits the steps at a = e^-10 instead of 1/2: above it
+// q <= 20 gives a (1.5 q + 8)/(1 - a) <= 38 a/(1-a) (41 for a*), below it the
+// term is < 2e-3 (< 4e-3 for a*), so the error is also <= u (41 S + 1.004 k + 16);
+// the window uses the smaller (deep pixels: many steps, few of them opaque).
 // The kernel accumulates S per track (one rcp.approx + one FMA per entry) and
 // flags a pixel when min |T/cutoff - 1| over the two tests bracketing its stop
 // (or its final T, if it never stops) is within twice that bound
@@ -202,6 +206,13 @@ __device__ __forceinline__ void fold(FPix<LC>& P) {
     P.ED += (double)P.ed;
     P.dp = P.ed = 0.f;
   }
+}
+
+// The certification window of a track after k composited entries with
+// S = sum a/(1-a): the smaller of the two bounds (header; twice each).
+__device__ __forceinline__ float cert_window_of(const UaBlendArgs& a, float k, float S) {
+  return a.cert_base + fminf(fmaf(a.cert_per_step, k, a.cert_sum * S),
+                             fmaf(a.cert_per_step2, k, a.cert_sum2 * S));
 }
 
 // Distance of a track's termination tests from the cutoff, relative.
@@ -495,10 +506,10 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   if (inside) {
     if (RGB)
       flag |= stop_margin(P.rd, P.T, P.Tp, cutoff) <=
-              a.cert_base + a.cert_per_step * (float)P.n_rgb + a.cert_sum * P.S;
+              cert_window_of(a, (float)P.n_rgb, P.S);
     if (ENT)
       flag |= stop_margin(P.edn, P.Te, P.Tep, cutoff) <=
-              a.cert_base + a.cert_per_step * (float)P.n_ent + a.cert_sum * P.Se;
+              cert_window_of(a, (float)P.n_ent, P.Se);
   }
   const int64_t pix = c.pix_base + (int64_t)py * c.width + px;
   const unsigned fm = __ballot_sync(0xffffffffu, flag);
