@@ -33,7 +33,7 @@ namespace {
 template <int LC, bool RGB, bool ENT, bool EXTRA>
 __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
-  constexpr int kThreads = 256, kWarps = 8;
+  constexpr int kThreads = 256;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
   int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   const uint2 rg = a.ranges[gt];
   const int ts = a.tile_size;
   const int rounds = (ts * ts + kThreads - 1) / kThreads;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int64_t N = a.scene.n;
   const GeoRec* geo = a.geo + (int64_t)v * N;
   const UaRec* uar = a.ua + (int64_t)v * N;

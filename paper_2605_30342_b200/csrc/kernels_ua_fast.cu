@@ -418,7 +418,6 @@ __device__ __forceinline__ void blend_batch(FPix<LC>& P, int n, const FGeo* s_ge
 template <int LC, bool RGB, bool ENT, bool EXTRA, bool MMA, int B>
 __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   using St = FStage<LC, RGB, ENT, MMA>;
-  constexpr int CS = Col<LC>::STRIDE;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   FGeo* s_geo = reinterpret_cast<FGeo*>(s_dyn);
   int4* s_rect = reinterpret_cast<int4*>(s_dyn + B * sizeof(FGeo));

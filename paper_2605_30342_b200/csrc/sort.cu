@@ -4,7 +4,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "kernels.h"
 
@@ -70,14 +70,14 @@ struct Touches {
 
 size_t select_temp_bytes(int64_t n) {
   size_t bytes = 0;
-  cub::DeviceSelect::If(nullptr, bytes, cub::CountingInputIterator<uint32_t>(0), (uint32_t*)nullptr,
+  cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<uint32_t>(0), (uint32_t*)nullptr,
                         (int32_t*)nullptr, (int)n, Touches{nullptr});
   return bytes;
 }
 
 void select_visible(const int32_t* counts, int64_t n, uint32_t* out, int32_t* num_out, void* temp,
                     size_t temp_bytes, cudaStream_t s) {
-  cub::DeviceSelect::If(temp, temp_bytes, cub::CountingInputIterator<uint32_t>(0), out, num_out,
+  cub::DeviceSelect::If(temp, temp_bytes, thrust::counting_iterator<uint32_t>(0), out, num_out,
                         (int)n, Touches{counts}, s);
 }
 
