@@ -411,7 +411,9 @@ def run_ours(args):
 
     # ---------------- VF-build ms on configs 2 and 4 (BASELINE metric) ------
     vf_other = {}
-    if not args.no_extra_vf:
+    # configs 2 and 4 (scene generation on every rank's host is slow at 3M
+    # Gaussians): one GPU only; the config-3 VF build above is measured at every N
+    if not args.no_extra_vf and world == 1:
         from paper_2605_30342_b200 import synth
         for cid, gen in ((2, lambda: synth.config2(0, n_candidates=256)),
                          (4, lambda: synth.config4(0, n_candidates=64))):
