@@ -54,6 +54,10 @@ def parse():
 
 
 def dist_init(gpus: int):
+    """One process per GPU (torchrun env). GAVIS_DIST_BACKEND=gloo runs the same
+    host logic over gloo (code-path smoke test with fewer GPUs than ranks: ranks
+    then share devices round-robin; the collectives are host-side, no kernel of
+    one rank waits on another)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -61,9 +65,15 @@ def dist_init(gpus: int):
     if world > 1:
         import torch
         import torch.distributed as d
+        backend = os.environ.get("GAVIS_DIST_BACKEND", "nccl")
+        if backend != "nccl":
+            local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        d.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            d.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            d.init_process_group(backend)
         dist = d
     return rank, local, world, dist
 
@@ -134,11 +144,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def _coll_device(dist):
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(x: float, dist) -> float:
     if dist is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -147,7 +161,7 @@ def sum_over_ranks(x: float, dist) -> float:
     if dist is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device(dist))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 

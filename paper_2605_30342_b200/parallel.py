@@ -124,10 +124,16 @@ class DeviceArray:
 
 
 def allreduce_device_field(field, dist) -> None:
-    """In-place NCCL all-reduce(sum) of a DeviceField's fp64 coefficients."""
+    """In-place NCCL all-reduce(sum) of a DeviceField's fp64 coefficients (aliasing
+    the library's device buffer); over gloo through a host copy."""
     import torch
     ptr, count = field.device_gamma()
     field.ctx.synchronize()
     t = torch.as_tensor(DeviceArray(ptr, count), device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    if dist.get_backend() == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM)
+        t.copy_(h)
     torch.cuda.synchronize()
