@@ -334,6 +334,7 @@ struct gavis_scene {
   float4* scale = nullptr;
   uint8_t* virt = nullptr;
   float* colors = nullptr;
+  uint4* colors_split = nullptr;  // tensor-core colour form, built on first certified RGB render
   float* var = nullptr;  // coefficient variances for the sh_propagation provider
   int var_degree = -1;
   float max_opacity = 1.f;  // enters the certified blend's error bound (q <= 2 ln(o / alpha))
@@ -764,6 +765,12 @@ void cert_window(UaBlendArgs* ua, float max_opacity) {
   // test hook (tests/test_certified.py): hand every pixel to the fp64 redo
   const char* force = std::getenv("GAVIS_CERT_FORCE_REDO");
   if (force && force[0] == '1') ua->cert_base = 3.0e38f;
+  // timing hook only (uncertified results): flag no pixel, to measure what the
+  // redo costs the step
+  if (force && force[0] == 'n') {
+    ua->cert_base = ua->cert_per_step = ua->cert_sum = 0.0f;
+    ua->cert_per_step2 = ua->cert_sum2 = 0.0f;
+  }
 }
 
 void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const double* vis_host,
@@ -795,6 +802,17 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   const int bv = batch_views(c, N, n);
   const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED &&
                     ua_fast_supported(rc->tile_size, rc->alpha_clamp_max);
+  if (fast && do_rgb && !s->colors_split) {
+    // the staged colour records of the tensor-core colour path, once per scene
+    // (scenes are immutable once built; calls on a context are serialised)
+    const size_t bytes = ua_colors_split_bytes(s->dev);
+    if (bytes > 0) {
+      auto* ms = const_cast<gavis_scene*>(s);
+      ms->colors_split = (uint4*)c->dalloc(bytes, "scene colour splits");
+      ms->dev.colors_split = ms->colors_split;
+      c->run("split_colors", [&] { launch_split_colors(ms->dev, ms->colors_split, c->stream); });
+    }
+  }
   unsigned long long* redo_total = nullptr;
   if (fast) {
     redo_total = (unsigned long long*)c->buf("redo_total", sizeof(unsigned long long));
@@ -1454,6 +1472,7 @@ gavis_status gavis_scene_destroy(gavis_scene* s) {
     c->dfree(s->scale);
     c->dfree(s->virt);
     c->dfree(s->colors);
+    c->dfree(s->colors_split);
     c->dfree(s->var);
     delete s;
   });

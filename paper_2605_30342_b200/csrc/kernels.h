@@ -19,6 +19,9 @@ struct SceneDev {
   const float4* scale = nullptr;   // sx, sy, sz, 0
   const uint8_t* virt = nullptr;
   const float* colors = nullptr;
+  // the colours as the tensor-core colour path stages them (kernels_ua_fast.cu):
+  // per particle 13 x 16 B, fp16 hi/lo splits; built once per scene, or null
+  const uint4* colors_split = nullptr;
 };
 
 enum QueryMode : int { kQueryNone = 0, kQueryField = 1, kQueryGiven = 2 };
@@ -224,6 +227,10 @@ void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s);
 bool ua_fast_supported(int tile_size, double amax);
 void launch_ua_blend_fast(const UaBlendArgs& a, cudaStream_t s);
 void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s);
+// The staged colour form of the tensor-core colour path: its size in bytes, 0
+// when the fast blend stages fp32 colours instead (GAVIS_UA_COLOR=ffma).
+size_t ua_colors_split_bytes(const SceneDev& scene);
+void launch_split_colors(const SceneDev& scene, uint4* out, cudaStream_t s);
 // image_entropy per view: fixed-order fold of the per-pixel entropy image
 // (with the correlation hook when corr_lambda > 0; edepth must then be set).
 void launch_score_image(const DevCam* cams, int V, const double* entropy, const double* edepth,

@@ -119,15 +119,80 @@ __device__ __forceinline__ void hmma16816(float (&d)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// Stage entries [base, base+n) of the tile list: the fp32 forms (and the fp16
-// colour splits) are computed once here, per tile, not per pixel.
+// Per (particle, channel, 4 coefficients): the hi/lo fp16 words of the staged
+// colour record ([hi: ch][8] [lo: ch][8] [pad 4], 52 words), as fstage_batch
+// stages them; coefficients past NB are 0.
+template <int LC>
+__device__ __forceinline__ void split_colour_quad(const float* colors, int64_t g, int ch, int q,
+                                                  uint32_t* rec) {
+  constexpr int NB = Col<LC>::NB, NBP = Col<LC>::NBP, CS = Col<LC>::STRIDE;
+  const float* src = colors + g * CS + ch * NBP;
+  float x[4];
+  if (NB == 16) {
+    const float4 v4 = __ldg(reinterpret_cast<const float4*>(src) + q);
+    x[0] = v4.x;
+    x[1] = v4.y;
+    x[2] = v4.z;
+    x[3] = v4.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = (4 * q + i < NB) ? __ldg(src + 4 * q + i) : 0.f;
+  }
+  uint32_t h0, l0, h1, l1;
+  split_half2(x[0], x[1], h0, l0);
+  split_half2(x[2], x[3], h1, l1);
+  uint32_t* dst = rec + ch * 8 + 2 * q;
+  *reinterpret_cast<uint2*>(dst) = make_uint2(h0, h1);
+  *reinterpret_cast<uint2*>(dst + 24) = make_uint2(l0, l1);
+}
+
+// Builds SceneDev::colors_split: one thread per (particle, channel, quad); the
+// padding words are zeroed by the (ch, q) = (0, 0) thread.
+template <int LC>
+__global__ void split_colors_kernel(const float* colors, int64_t n, uint32_t* out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n * 12) return;
+  const int64_t g = k / 12;
+  const int r = (int)(k - g * 12), ch = r >> 2, q = r & 3;
+  uint32_t* rec = out + g * kColWords;
+  split_colour_quad<LC>(colors, g, ch, q, rec);
+  if (r == 0) *reinterpret_cast<uint4*>(rec + 48) = make_uint4(0u, 0u, 0u, 0u);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Stage entries [base, base+n) of the tile list: the fp32 forms are computed
+// once here, per tile, not per pixel. With the tensor-core colour path the
+// colours come pre-split (SceneDev::colors_split): threads [0, 128) stage the
+// geometry, threads [128, 256) copy the colour records with cp.async (13
+// independent 16-byte copies per entry in flight, no register round trip).
 template <int LC, bool RGB, bool ENT, bool MMA>
 __device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec* geo,
                                              const UaRec* uar, uint32_t base, int n, FGeo* s_geo,
                                              int4* s_rect, float4* s_ua, void* s_col) {
   constexpr int CS = Col<LC>::STRIDE;
   constexpr int V4 = CS / 4;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+  constexpr int kHalf = 128;
+  if (RGB && MMA) {
+    const int t = threadIdx.x;
+    if (t >= kHalf) {
+      uint4* dst = reinterpret_cast<uint4*>(s_col);
+      for (int j = t - kHalf; j < n; j += kHalf) {
+        const uint4* src = a.scene.colors_split + (int64_t)a.vals[base + j] * (kColWords / 4);
+#pragma unroll
+        for (int w = 0; w < kColWords / 4; ++w) cp_async16(dst + j * (kColWords / 4) + w, src + w);
+      }
+      cp_async_wait_all();
+      return;
+    }
+  }
+  const int t0 = threadIdx.x, nt = (RGB && MMA) ? kHalf : blockDim.x;
+  for (int j = t0; j < n; j += nt) {
     const uint32_t g = a.vals[base + j];
     const GeoRec r = geo[g];
     FGeo f;
@@ -151,33 +216,6 @@ __device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec*
       const int j = k / V4, qd = k - j * V4;
       const uint32_t g = a.vals[base + j];
       reinterpret_cast<float4*>(s_col)[k] = __ldg(colors4 + (int64_t)g * V4 + qd);
-    }
-  }
-  if (RGB && MMA) {
-    // per (entry, channel, 4 coefficients): hi/lo fp16 words at [j][ch][k/2]
-    constexpr int NB = Col<LC>::NB, NBP = Col<LC>::NBP;
-    uint32_t* w = reinterpret_cast<uint32_t*>(s_col);
-    for (int k = threadIdx.x; k < n * 12; k += blockDim.x) {
-      const int j = k / 12, r = k - j * 12, ch = r >> 2, q = r & 3;
-      const uint32_t g = a.vals[base + j];
-      const float* src = a.scene.colors + (int64_t)g * CS + ch * NBP;
-      float x[4];
-      if (NB == 16) {
-        const float4 v4 = __ldg(reinterpret_cast<const float4*>(src) + q);
-        x[0] = v4.x;
-        x[1] = v4.y;
-        x[2] = v4.z;
-        x[3] = v4.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) x[i] = (4 * q + i < NB) ? __ldg(src + 4 * q + i) : 0.f;
-      }
-      uint32_t h0, l0, h1, l1;
-      split_half2(x[0], x[1], h0, l0);
-      split_half2(x[2], x[3], h1, l1);
-      uint32_t* dst = w + j * kColWords + ch * 8 + 2 * q;
-      *reinterpret_cast<uint2*>(dst) = make_uint2(h0, h1);
-      *reinterpret_cast<uint2*>(dst + 24) = make_uint2(l0, l1);
     }
   }
 }
@@ -725,7 +763,7 @@ inline bool colour_mma() {
 
 template <int LC, bool RGB, bool ENT, bool EXTRA>
 void launch_fast_one(const UaBlendArgs& a, cudaStream_t s) {
-  if (RGB && colour_mma())
+  if (RGB && a.scene.colors_split)  // built when colour_mma() (ua_colors_split_bytes)
     launch_fast_kernel<LC, RGB, ENT, EXTRA, true>(a, s);
   else
     launch_fast_kernel<LC, RGB, ENT, EXTRA, false>(a, s);
@@ -798,6 +836,25 @@ void launch_score_image(const DevCam* cams, int V, const double* entropy, const 
 }
 
 int score_partials_per_view() { return kScoreChunks; }
+
+size_t ua_colors_split_bytes(const SceneDev& scene) {
+  if (!colour_mma() || scene.color_degree < 0 || scene.color_degree > 3) return 0;
+  return sizeof(uint32_t) * kColWords * (size_t)std::max<int64_t>(scene.n, 1);
+}
+
+void launch_split_colors(const SceneDev& scene, uint4* out, cudaStream_t s) {
+  if (scene.n == 0) return;
+  const int64_t work = scene.n * 12;
+  const unsigned grid = (unsigned)((work + 255) / 256);
+  uint32_t* o = reinterpret_cast<uint32_t*>(out);
+  switch (scene.color_degree) {
+    case 0: split_colors_kernel<0><<<grid, 256, 0, s>>>(scene.colors, scene.n, o); break;
+    case 1: split_colors_kernel<1><<<grid, 256, 0, s>>>(scene.colors, scene.n, o); break;
+    case 2: split_colors_kernel<2><<<grid, 256, 0, s>>>(scene.colors, scene.n, o); break;
+    case 3: split_colors_kernel<3><<<grid, 256, 0, s>>>(scene.colors, scene.n, o); break;
+    default: break;
+  }
+}
 
 namespace {
 __global__ void add_count_kernel(unsigned long long* total, const uint32_t* count) { *total += *count; }
