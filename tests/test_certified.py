@@ -321,3 +321,49 @@ def test_certified_fuzz(ctx, seed):
         assert np.array_equal(r["entropy_contributors"], ecc)
         assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
         assert np.max(np.abs(r["entropy"] - H)) <= IMG_ABS
+
+
+@pytest.mark.parametrize("degree", [0, 1, 2])
+def test_certified_color_degrees(ctx, degree):
+    """Colour degrees below 3: the tensor-core colour path zero-pads the 1/4/9
+    coefficients of each channel to the GEMM's k = 16 (pre-split colour records)."""
+    scene = synth._gaussian_cloud(7, 10_000, (-1, -1, -1), (1, 1, 1), -4.0, 0.5, color_degree=degree)
+    osc = O.OracleScene(scene)
+    for cam in synth.config1(0)["candidates"][:2]:
+        r = api.render(ctx, scene, None, [cam], RC, UC, rgb=True, contributors=True)
+        rgb, _, _, cc = O.rasterize(osc, cam, RC, contrib=True)
+        assert np.array_equal(r["rgb_contributors"], cc)
+        assert np.max(np.abs(r["rgb"] - rgb)) <= IMG_ABS
+
+
+_FFMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/oracle']
+import oracle as O
+from paper_2605_30342_b200 import api, synth
+from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
+c = synth.config1(0)
+osc = O.OracleScene(c['scene'])
+with api.Context(0) as ctx:
+    for cam in c['candidates'][:2]:
+        r = api.render(ctx, c['scene'], None, [cam], RasterConfig(), UncertaintyConfig(), rgb=True,
+                       contributors=True)
+        rgb, _, _, cc = O.rasterize(osc, cam, RasterConfig(), contrib=True)
+        assert np.array_equal(r['rgb_contributors'], cc)
+        assert np.max(np.abs(r['rgb'] - rgb)) <= 2e-5, np.max(np.abs(r['rgb'] - rgb))
+print('ok')
+"""
+
+
+def test_certified_ffma_colour_variant(tmp_path):
+    """GAVIS_UA_COLOR=ffma (read once per process): the packed-FFMA colour path."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "ffma.py"
+    script.write_text(_FFMA_SCRIPT)
+    env = dict(os.environ, GAVIS_UA_COLOR="ffma")
+    r = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
