@@ -54,7 +54,7 @@ def gather_scores(local: np.ndarray, n_total: int, rank: int, world: int, dist=N
     return np.concatenate(out) if out else np.zeros(0)
 
 
-CERT_SCORE_REL = 1e-3  # same window as the library's single-GPU select (gavis_abi.cu)
+CERT_SCORE_REL = 1e-3  # same window as the library's single-GPU select (ua_host.cu)
 
 
 def contenders(scores: np.ndarray, window: float = CERT_SCORE_REL) -> List[int]:

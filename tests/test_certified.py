@@ -146,12 +146,13 @@ def test_forced_redo_is_exact(ctx, ctx_exact, monkeypatch, room):
         assert np.array_equal(ex[k], got[k]), k
 
 
-@pytest.mark.parametrize("cfg", [3, 2])
+@pytest.mark.parametrize("cfg", [3, 2, 4])
 def test_certified_vs_exact_full_size(ctx, ctx_exact, cfg):
-    """Configs 3 (1M Gaussians, indoor) and 2 (500k, object) at full size, 800^2:
-    size-independent agreement of the certified and the exact device paths (the
-    exact path is pinned to the oracle)."""
-    c = synth.config3(0, n_candidates=4) if cfg == 3 else synth.config2(0, n_candidates=4)
+    """Configs 3 (1M Gaussians, indoor), 2 (500k, object) at 800^2 and 4 (3M,
+    1920x1080) at full size: size-independent agreement of the certified and the
+    exact device paths (the exact path is pinned to the oracle)."""
+    c = {3: lambda: synth.config3(0, n_candidates=4), 2: lambda: synth.config2(0, n_candidates=4),
+         4: lambda: synth.config4(0, n_train=30, n_candidates=4)}[cfg]()
     scene = c["scene"]
     f = api.construct_field(ctx_exact, scene, c["train"][:30], VmfParams(1.0), c["degree"], RC)
     cams = c["candidates"][:4]
