@@ -368,3 +368,28 @@ def test_certified_ffma_colour_variant(tmp_path):
     r = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_certified_deterministic_and_batch_invariant(ctx, room):
+    """Run to run and for any views-per-batch the certified outputs are bit-identical
+    (per-view work is independent, the flagged-pixel redo is per pixel, the score
+    fold has a fixed order) -- what makes sharded candidates agree at 1/2/4/8 GPUs."""
+    scene = room["scene"]
+    ds = ctx.upload(scene)
+    f = api.construct_field(ctx, ds, room["train"], VmfParams(1.0), 2, RC)
+    cams = room["candidates"]
+    kw = dict(rgb=True, transmittance=True, entropy=True, invisible_mass=True, scores=True, contributors=True)
+    a = api.render(ctx, ds, f, cams, RC, UC, **kw)
+    b = api.render(ctx, ds, f, cams, RC, UC, **kw)
+    ctx.set_batch(2)
+    try:
+        c = api.render(ctx, ds, f, cams, RC, UC, **kw)
+        sel_b = api.select_nbv(ctx, ds, f, cams, RC, UC)
+    finally:
+        ctx.set_batch(0)
+    sel_a = api.select_nbv(ctx, ds, f, cams, RC, UC)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+        assert np.array_equal(a[k], c[k]), k
+    assert sel_a.best_index == sel_b.best_index
+    assert np.array_equal(sel_a.scores, sel_b.scores)

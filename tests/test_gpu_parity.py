@@ -431,3 +431,50 @@ def test_narrow_and_wide_binning_agree(ctx, monkeypatch):
     for k in narrow:
         assert np.array_equal(narrow[k], wide[k]), k
     assert np.array_equal(keys_n, keys_w) and np.array_equal(ids_n, ids_w) and np.array_equal(rng_n, rng_w)
+
+
+_NCCL_SCRIPT = r"""
+import os, socket, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import torch
+import torch.distributed as dist
+from paper_2605_30342_b200 import api, parallel, synth
+from paper_2605_30342_b200.model import RasterConfig, VmfParams
+s = socket.socket(); s.bind(('127.0.0.1', 0)); port = s.getsockname()[1]; s.close()
+os.environ.update(MASTER_ADDR='127.0.0.1', MASTER_PORT=str(port), RANK='0', WORLD_SIZE='1')
+torch.cuda.set_device(0)
+dist.init_process_group('nccl', rank=0, world_size=1, device_id=torch.device('cuda', 0))
+c = synth.config1(0)
+with api.Context(0) as ctx:
+    ds = ctx.upload(c['scene'])
+    ref = api.construct_field(ctx, ds, c['train'], VmfParams(1.0), 2, RasterConfig()).download().gamma
+    f = parallel.construct_field_sharded(
+        lambda lo, hi: api.construct_field(ctx, ds, c['train'][lo:hi], VmfParams(1.0), 2, RasterConfig()),
+        len(c['train']), 0, 1, lambda fld: None)
+    parallel.allreduce_device_field(f, dist)      # NCCL over the aliased library buffer
+    g = f.download().gamma
+    assert np.array_equal(g, ref)
+    ptr, n = f.device_gamma()
+    t = torch.as_tensor(parallel.DeviceArray(ptr, n), device='cuda')
+    t.mul_(2.0)                                   # torch writes land in the library's field
+    torch.cuda.synchronize()
+    assert np.array_equal(f.download().gamma, 2.0 * ref)
+dist.destroy_process_group()
+print('ok')
+"""
+
+
+def test_nccl_allreduce_aliases_field(tmp_path):
+    """The VF all-reduce path on one GPU (NCCL, world size 1): torch aliases the
+    library's device coefficients zero-copy, the collective leaves them intact and
+    writes through the alias reach the field (multi-GPU runs sum partial fields
+    through exactly this buffer)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "nccl1.py"
+    script.write_text(_NCCL_SCRIPT)
+    r = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
