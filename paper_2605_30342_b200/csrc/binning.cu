@@ -29,12 +29,12 @@ DevCam make_devcam(const gavis_camera& c, int ts, int64_t tile_base, int64_t pix
 int batch_views(gavis_ctx* c, int64_t N, int n_views) {
   int vmax = c->max_batch > 0 ? c->max_batch : 32;
   if (N > 0) {
-    // ~112 B of per-(view, particle) state per batch, two batches in flight: one
-    // batch may use a sixth of the free device memory, within [2, 16] GB
+    // ~112 B of per-(view, particle) state per batch, up to three buffer sets in
+    // flight: one batch may use a ninth of the free device memory, within [2, 16] GB
     if (c->batch_budget == 0.0) {
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
-      c->batch_budget = std::min(16.0e9, std::max(2.0e9, (double)free_b / 6.0));
+      c->batch_budget = std::min(16.0e9, std::max(2.0e9, (double)free_b / 9.0));
     }
     const int64_t by_mem = (int64_t)(c->batch_budget / (112.0 * (double)N));
     vmax = (int)std::max<int64_t>(1, std::min<int64_t>(vmax, by_mem));

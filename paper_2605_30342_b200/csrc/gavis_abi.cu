@@ -43,7 +43,7 @@ gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
       int lo_prio = 0, hi_prio = 0;
       CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
       CK(cudaStreamCreateWithPriority(&c->front, cudaStreamNonBlocking, hi_prio));
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < gavis_ctx::kSets; ++k) {
         CK(cudaEventCreateWithFlags(&c->ev_blend[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_done[k], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_bin[k], cudaEventDisableTiming));
@@ -84,7 +84,7 @@ gavis_status gavis_ctx_destroy(gavis_ctx* c) {
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
       }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < gavis_ctx::kSets; ++k) {
       if (c->ev_blend[k]) cudaEventDestroy(c->ev_blend[k]);
       if (c->ev_done[k]) cudaEventDestroy(c->ev_done[k]);
       if (c->ev_bin[k]) cudaEventDestroy(c->ev_bin[k]);

@@ -216,8 +216,8 @@ struct gavis_ctx {
   cudaStream_t side = nullptr;
   cudaStream_t front = nullptr;  // binning of batch k+1 under batch k's blend (high priority)
   int bufset = 0;
-  cudaEvent_t ev_blend[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
-  cudaEvent_t ev_bin[2] = {nullptr, nullptr};
+  static constexpr int kSets = 3;  // per-batch buffer sets (UA renders rotate over all three)
+  cudaEvent_t ev_blend[kSets] = {}, ev_done[kSets] = {}, ev_bin[kSets] = {};
   std::map<std::string, DevBuf> bufs;
   int max_batch = 0;
   bool profiling = false;
@@ -238,7 +238,7 @@ struct gavis_ctx {
   void use() { CK(cudaSetDevice(device)); }
 
   void* buf(const std::string& name, size_t bytes) {
-    DevBuf& b = bufs[bufset ? name + "#1" : name];
+    DevBuf& b = bufs[bufset ? name + "#" + std::to_string(bufset) : name];
     if (bytes == 0) bytes = 16;
     if (b.bytes < bytes) {
       if (b.p) CK(cudaFree(b.p));

@@ -99,14 +99,20 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   } reset{c, main_stream};
   int64_t pix_done = 0;
   int batch = 0;
+  // buffer sets in rotation: batch k's binning reuses the set of batch k - nsets,
+  // whose side-stream redo reads its binning outputs (A/B: GAVIS_BUFSETS=2)
+  static const int nsets = [] {
+    const char* e = std::getenv("GAVIS_BUFSETS");
+    return (e && e[0] == '2') ? 2 : gavis_ctx::kSets;
+  }();
   for (int v0 = 0; v0 < n; v0 += bv, ++batch) {
     const int V = std::min(bv, n - v0);
-    const int par = batch & 1;
+    const int par = batch % nsets;
     c->bufset = par;
     // binning runs on the front stream, under the previous batch's blend; the
-    // buffers of this set were last read by batch - 2's side-stream work
+    // buffers of this set were last read by batch - nsets's side-stream work
     c->stream = c->front;
-    if (batch >= 2) CK(cudaStreamWaitEvent(c->front, c->ev_done[par], 0));
+    if (batch >= nsets) CK(cudaStreamWaitEvent(c->front, c->ev_done[par], 0));
     BinOpts o;
     o.ua = do_ent;
     o.field = f;
