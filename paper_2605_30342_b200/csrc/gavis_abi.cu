@@ -245,6 +245,16 @@ static gavis_scene* alloc_scene(gavis_ctx* c, int64_t n, int color_degree) {
   return s;
 }
 
+// The staged colour records of the certified blend's tensor-core colour path
+// (SceneDev::colors_split), built once when a scene is finalised.
+static void build_colour_split(gavis_ctx* c, gavis_scene* s) {
+  const size_t bytes = ua_colors_split_bytes(s->dev);
+  if (bytes == 0 || s->dev.n == 0) return;
+  s->colors_split = (uint4*)c->dalloc(bytes, "scene colour splits");
+  s->dev.colors_split = s->colors_split;
+  c->run("split_colors", [&] { launch_split_colors(s->dev, s->colors_split, c->stream); });
+}
+
 // Copies particles [0, n) of src into dst at offset `at` (device to device).
 static void copy_particles(gavis_ctx* c, gavis_scene* dst, int64_t at, const gavis_scene* src,
                            int64_t n) {
@@ -372,6 +382,7 @@ gavis_status gavis_density_control(gavis_ctx* c, const gavis_scene* scene, const
     try {
       copy_particles(c, o, 0, scene, n_real);
       upload_probes(c, o, n_real, p, keep);
+      build_colour_split(c, o);
       c->sync();
     } catch (...) {
       gavis_scene_destroy(o);
@@ -443,6 +454,7 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
         pk.virt_out = s->virt;
         c->run("pack_scene", [&] { launch_pack_scene(pk, c->stream); });
       }
+      build_colour_split(c, s);
       c->sync();  // the caller may release its host arrays on return
     } catch (...) {
       gavis_scene_destroy(s);

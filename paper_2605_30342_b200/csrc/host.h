@@ -343,7 +343,7 @@ struct gavis_scene {
   float4* scale = nullptr;
   uint8_t* virt = nullptr;
   float* colors = nullptr;
-  uint4* colors_split = nullptr;  // tensor-core colour form, built on first certified RGB render
+  uint4* colors_split = nullptr;  // tensor-core colour form, built when the scene is finalised
   float* var = nullptr;  // coefficient variances for the sh_propagation provider
   int var_degree = -1;
   float max_opacity = 1.f;  // enters the certified blend's error bound (q <= 2 ln(o / alpha))
@@ -408,9 +408,11 @@ int batch_views(gavis_ctx* c, int64_t N, int n_views);
 Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, int V,
                  const gavis_raster_config* rc, const BinOpts& o);
 
-inline void check_scene_field(const gavis_scene* s, const gavis_field* f) {
+inline void check_scene_field(const gavis_ctx* c, const gavis_scene* s, const gavis_field* f) {
   require(s != nullptr, "scene must not be null");
+  require(s->ctx->device == c->device, "scene was uploaded to another device");
   if (f) require(f->n == s->dev.n, "field was built for a different scene");
+  if (f) require(f->ctx->device == c->device, "field lives on another device");
 }
 
 // VF accumulation of views [0, n) into field (or only per-view outputs).

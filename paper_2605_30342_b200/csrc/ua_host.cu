@@ -40,7 +40,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   validate_unc(uc, &hl_q0);
   require(cams != nullptr || n == 0, "cameras must not be null");
   require(out != nullptr, "render outputs must not be null");
-  check_scene_field(s, f);
+  check_scene_field(c, s, f);
   for (int i = 0; i < n; ++i) validate_camera(cams[i]);
   const int64_t N = s->dev.n;
   const bool do_rgb = out->rgb || out->depth || out->transmittance || out->rgb_contributors ||
@@ -61,17 +61,6 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   const int bv = batch_views(c, N, n);
   const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED &&
                     ua_fast_supported(rc->tile_size, rc->alpha_clamp_max);
-  if (fast && do_rgb && !s->colors_split) {
-    // the staged colour records of the tensor-core colour path, once per scene
-    // (scenes are immutable once built; calls on a context are serialised)
-    const size_t bytes = ua_colors_split_bytes(s->dev);
-    if (bytes > 0) {
-      auto* ms = const_cast<gavis_scene*>(s);
-      ms->colors_split = (uint4*)c->dalloc(bytes, "scene colour splits");
-      ms->dev.colors_split = ms->colors_split;
-      c->run("split_colors", [&] { launch_split_colors(ms->dev, ms->colors_split, c->stream); });
-    }
-  }
   unsigned long long* redo_total = nullptr;
   if (fast) {
     redo_total = (unsigned long long*)c->buf("redo_total", sizeof(unsigned long long));
@@ -307,7 +296,7 @@ gavis_status gavis_ua_mixtures(gavis_ctx* c, const gavis_scene* s, const gavis_f
     double hl_q0 = 0.0;
     validate_unc(uc, &hl_q0);
     validate_camera(*cam);
-    check_scene_field(s, f);
+    check_scene_field(c, s, f);
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
     const int64_t N = s->dev.n;
