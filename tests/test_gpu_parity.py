@@ -478,3 +478,34 @@ def test_nccl_allreduce_aliases_field(tmp_path):
     script.write_text(_NCCL_SCRIPT)
     r = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_vf_full_size_properties(ctx, cfg):
+    """VF CONST at full scene size (config 3: 1M Gaussians, 800^2; config 4: 3M,
+    1920x1080), where the oracle is too slow: views accumulated in trajectory order
+    make prefix + suffix builds bit-identical to the one-shot build, any views per
+    batch give the same field, a repeated view doubles its contribution exactly
+    (test_vfield.cpp:91-131), and every coefficient row stays finite with the
+    virtual-free rows' gamma_00 within [0, 4 pi Y00 * views]."""
+    c = synth.config3(0, n_candidates=1) if cfg == 3 else synth.config4(0, n_train=20, n_candidates=1)
+    ds = ctx.upload(c["scene"])
+    views = c["train"][:20]
+    deg = c["degree"]
+    whole = api.construct_field(ctx, ds, views, VmfParams(1.0), deg, RC).download().gamma
+    f = api.empty_field(ctx, ds, VmfParams(1.0), deg)
+    api.accumulate_views(ctx, f, ds, views[:7], RC)
+    api.accumulate_views(ctx, f, ds, views[7:], RC)
+    assert np.array_equal(f.download().gamma, whole)
+    ctx.set_batch(3)
+    try:
+        batched = api.construct_field(ctx, ds, views, VmfParams(1.0), deg, RC).download().gamma
+    finally:
+        ctx.set_batch(0)
+    assert np.array_equal(batched, whole)
+    one = api.construct_field(ctx, ds, views[:1], VmfParams(1.0), deg, RC).download().gamma
+    two = api.construct_field(ctx, ds, [views[0], views[0]], VmfParams(1.0), deg, RC).download().gamma
+    assert np.array_equal(two, 2.0 * one)
+    assert np.all(np.isfinite(whole))
+    a0 = O.vmf_scales(1.0, deg)[0] * 0.28209479177387814
+    assert whole[:, 0].min() >= 0.0 and whole[:, 0].max() <= a0 * len(views) * (1 + 1e-12)
