@@ -79,7 +79,8 @@ struct __align__(16) FGeo {
 //    tensor cores with mma.sync m16n8k16 in split fp16 (x = hi + lo, products
 //    hi*hi + hi*lo + lo*hi accumulated in fp32: ~22-bit operands, colour error
 //    ~1e-6), then transposes it through shared memory so each lane reads its
-//    own pixel's colours. Coefficients are split once per tile when staged.
+//    own pixel's colours. Coefficients are split once per scene
+//    (SceneDev::colors_split) and staged as-is.
 constexpr int kColWords = 52;  // per staged entry: hi [3][16] f16 (24 words), lo (24), pad (4)
 // floats per pixel row of the warp's colour block, laid out [channel][8 entries]:
 // 26 makes both the fragment stores (STS.64, a (row, entry pair) per lane) and
