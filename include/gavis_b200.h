@@ -102,6 +102,10 @@ gavis_status gavis_ctx_destroy(gavis_ctx* ctx);
 gavis_status gavis_ctx_synchronize(gavis_ctx* ctx);
 /* Views processed per launch batch (0 = automatic from free memory). */
 gavis_status gavis_ctx_set_batch(gavis_ctx* ctx, int32_t max_views_per_batch);
+/* Tile pairs one batch may hold (0 = automatic: the batch memory budget / 32 B,
+ * at most 2^31 - 1). A batch of views whose pairs exceed it is re-binned with
+ * half the views (down to one view; one view may produce up to 2^31 - 1 pairs). */
+gavis_status gavis_ctx_set_pair_budget(gavis_ctx* ctx, int64_t max_pairs_per_batch);
 /* Arithmetic of the UA render (gavis_ua_render, gavis_select_nbv, loops):
  *  GAVIS_PRECISION_CERTIFIED (default): fp32 blend with a per-pixel error bound
  *    on the early-termination tests; pixels the bound cannot certify are

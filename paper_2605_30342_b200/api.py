@@ -114,6 +114,10 @@ class Context:
     def set_batch(self, n: int) -> None:
         N.check(self.lib.gavis_ctx_set_batch(self.h, C.c_int32(n)))
 
+    def set_pair_budget(self, n: int) -> None:
+        """Tile pairs one batch may hold (0 = automatic); larger batches are split."""
+        N.check(self.lib.gavis_ctx_set_pair_budget(self.h, C.c_int64(n)))
+
     def set_precision(self, precision: str) -> None:
         """'certified' (default: fp32 blend, fp64 redo of uncertified pixels,
         exact argmax) or 'exact' (fp64 throughout)."""

@@ -99,6 +99,23 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     }
   }
   c->run("preprocess", [&] { launch_preprocess(pa, c->stream); }, N > 0 ? 1 : 0);
+  // 64-bit pair total, read with the first host sync below: a batch whose pairs
+  // exceed the 32-bit pair indexing or the pair memory budget is split by the caller
+  unsigned long long* dtotal = (unsigned long long*)c->buf("pair_total", sizeof(unsigned long long));
+  if (VN > 0) c->run("select", [&] { launch_pair_total(b.counts, VN, dtotal, c->stream); });
+  const auto pairs_fit = [&]() {
+    const uint64_t total = *reinterpret_cast<const unsigned long long*>(c->pinned + kPinPairs);
+    // <= 32 B of pair state per pair (keys and values double-buffered, VF sums)
+    const int64_t limit = std::min<int64_t>(
+        (int64_t(1) << 31) - 1,
+        c->pair_budget > 0    ? c->pair_budget
+        : c->batch_budget > 0.0 ? (int64_t)(c->batch_budget / 32.0)
+                                : (int64_t(1) << 31) - 1);
+    if (V > 1 && total > (uint64_t)limit) return false;
+    invariant(total < (uint64_t(1) << 31),
+              "one view produces 2^31 or more tile pairs (the device path indexes pairs in 32 bits)");
+    return true;
+  };
 
   // GAVIS_BIN_WIDE=1 selects the 64-bit (tile << 32 | fp32 depth) key path (A/B and
   // the equivalence test); it is also the path of the reference-form debug keys
@@ -115,7 +132,13 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     void* seltmp = c->buf("select_tmp", selb);
     c->run("select", [&] { select_visible(b.counts, VN, items, dnum, seltmp, selb, c->stream); });
     CK(cudaMemcpyAsync(P32 + kPinItems, dnum, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(P32 + kPinPairs, dtotal, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       c->stream));
     c->sync();
+    if (!pairs_fit()) {
+      b.overflow = true;
+      return b;
+    }
     n_items = P32[kPinItems];
     na.N = N;
     na.geo = b.geo;
@@ -157,7 +180,13 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     c->run("scan", [&] { exclusive_scan(b.counts, b.offsets, VN, tmp, sb, c->stream); });
     CK(cudaMemcpyAsync(P32, b.offsets + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(P32 + 1, b.counts + VN - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(P32 + kPinPairs, dtotal, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       c->stream));
     c->sync();
+    if (!pairs_fit()) {
+      b.overflow = true;
+      return b;
+    }
     K = (int64_t)P32[0] + (int64_t)P32[1];
   }
   invariant(K >= 0 && K < (int64_t(1) << 31), "pair count overflow in one batch");

@@ -103,6 +103,14 @@ gavis_status gavis_ctx_synchronize(gavis_ctx* c) {
   });
 }
 
+gavis_status gavis_ctx_set_pair_budget(gavis_ctx* c, int64_t n) {
+  return guard([&] {
+    require(c != nullptr, "context must not be null");
+    require(n >= 0, "pair budget must be non-negative");
+    c->pair_budget = n;
+  });
+}
+
 gavis_status gavis_ctx_set_batch(gavis_ctx* c, int32_t n) {
   return guard([&] {
     require(c != nullptr, "context must not be null");

@@ -220,6 +220,7 @@ struct gavis_ctx {
   cudaEvent_t ev_blend[kSets] = {}, ev_done[kSets] = {}, ev_bin[kSets] = {};
   std::map<std::string, DevBuf> bufs;
   int max_batch = 0;
+  int64_t pair_budget = 0;       // tile pairs per batch (0: batch_budget / 32 B)
   bool profiling = false;
   std::map<std::string, Timing> timing;
   std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> pending;
@@ -380,11 +381,13 @@ struct Binned {
   uint32_t* pair_gid = nullptr;
   uint2* ranges = nullptr;
   bool narrow = false;  // keys are 32-bit (local tile << rb | depth rank); b.keys == null
+  bool overflow = false;  // more pairs than one batch may hold: nothing emitted, re-bin fewer views
 };
 
 // pinned host scratch layout (int32 words)
 constexpr int kPinItems = 4;
 constexpr int kPinRedo = 6;     // u64
+constexpr int kPinPairs = 8;    // u64: total tile pairs of the batch being binned
 constexpr int kPinStarts = 16;  // int64 [V + 1] (V <= 64)
 constexpr int kPinWords = 256;
 

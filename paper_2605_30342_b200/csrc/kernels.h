@@ -211,6 +211,8 @@ void launch_emit_keys(const EmitArgs& a, cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_item_keys(const NarrowArgs& a, cudaStream_t s);
 void launch_depth_order(const NarrowArgs& a, cudaStream_t s);
+// *total = sum of counts[0, n) (64-bit; zeroed first)
+void launch_pair_total(const int32_t* counts, int64_t n, unsigned long long* total, cudaStream_t s);
 void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s);
 void launch_ranges32(const uint32_t* keys32, int64_t lo, int64_t hi, int64_t tile_base, uint2* ranges,
                      cudaStream_t s);

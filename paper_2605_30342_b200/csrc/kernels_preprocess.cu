@@ -423,6 +423,19 @@ __global__ void item_keys_kernel(NarrowArgs a) {
   a.item_key[i] = (v << (32 - a.view_bits)) | (db >> (a.view_bits - 1));
 }
 
+// Total tile pairs of a batch (sum of the per-(view, particle) tile counts) in
+// 64 bits: the host checks it against the 32-bit pair indexing and the pair
+// memory budget before emitting (bin_batch splits oversized batches).
+__global__ void pair_total_kernel(const int32_t* counts, int64_t n, unsigned long long* total) {
+  unsigned long long sum = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    sum += (unsigned long long)counts[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  if ((threadIdx.x & 31) == 0 && sum != 0) atomicAdd(total, sum);
+}
+
 // K2c: runs of equal fp32 keys ordered by (fp64 depth, index) by the thread at
 // the run's start (the stable sort left them in index order); then every item's
 // tile count, in depth order, for the pair-offset scan.
@@ -599,6 +612,11 @@ void launch_emit_keys(const EmitArgs& a, cudaStream_t s) {
 
 void launch_item_keys(const NarrowArgs& a, cudaStream_t s) {
   if (a.n_items > 0) item_keys_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
+}
+
+void launch_pair_total(const int32_t* counts, int64_t n, unsigned long long* total, cudaStream_t s) {
+  cudaMemsetAsync(total, 0, sizeof(unsigned long long), s);
+  if (n > 0) pair_total_kernel<<<(unsigned)std::min<int64_t>(blocks_for(n, 256), 148 * 8), 256, 0, s>>>(counts, n, total);
 }
 
 void launch_depth_order(const NarrowArgs& a, cudaStream_t s) {

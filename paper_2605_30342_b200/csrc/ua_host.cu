@@ -94,8 +94,9 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     const char* e = std::getenv("GAVIS_BUFSETS");
     return (e && e[0] == '2') ? 2 : gavis_ctx::kSets;
   }();
-  for (int v0 = 0; v0 < n; v0 += bv, ++batch) {
-    const int V = std::min(bv, n - v0);
+  int bvv = bv;  // views per batch; halved for good when a batch holds too many pairs
+  for (int v0 = 0, V = 0; v0 < n; v0 += V, ++batch) {
+    V = std::min(bvv, n - v0);
     const int par = batch % nsets;
     c->bufset = par;
     // binning runs on the front stream, under the previous batch's blend; the
@@ -120,6 +121,10 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       o.err_flag = err;
     }
     Binned b = bin_batch(c, s, cams + v0, V, rc, o);
+    while (b.overflow) {
+      V = bvv = std::max(1, V / 2);
+      b = bin_batch(c, s, cams + v0, V, rc, o);
+    }
     if (err) {
       CK(cudaMemcpyAsync(c->pinned + 2, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
       c->sync();

@@ -28,8 +28,9 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
   CK(cudaStreamWaitEvent(c->front, c->ev_done[0], 0));
   const bool host_out = vis_host || touch_host || contrib_host;
   int batch = 0;
-  for (int v0 = 0; v0 < n_views; v0 += bv, ++batch) {
-    const int V = std::min(bv, n_views - v0);
+  int bvv = bv;  // views per batch; halved for good when a batch holds too many pairs
+  for (int v0 = 0, V = 0; v0 < n_views; v0 += V, ++batch) {
+    V = std::min(bvv, n_views - v0);
     const int par = batch & 1;
     c->bufset = par;
     c->stream = c->front;
@@ -37,6 +38,10 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
     BinOpts o;
     o.vf_mode = true;
     Binned b = bin_batch(c, s, views + v0, V, rc, o);
+    while (b.overflow) {
+      V = bvv = std::max(1, V / 2);
+      b = bin_batch(c, s, views + v0, V, rc, o);
+    }
     CK(cudaEventRecord(c->ev_bin[par], c->front));
     c->stream = main_stream;
     CK(cudaStreamWaitEvent(c->stream, c->ev_bin[par], 0));

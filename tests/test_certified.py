@@ -393,3 +393,28 @@ def test_certified_deterministic_and_batch_invariant(ctx, room):
         assert np.array_equal(a[k], c[k]), k
     assert sel_a.best_index == sel_b.best_index
     assert np.array_equal(sel_a.scores, sel_b.scores)
+
+
+def test_pair_budget_splits_batches(ctx, room):
+    """A batch whose tile pairs exceed the pair budget is re-binned with fewer
+    views (down to one); results are bit-identical to the unsplit run, for the
+    field build and the render."""
+    scene = room["scene"]
+    ds = ctx.upload(scene)
+    cams = room["candidates"]
+    kw = dict(rgb=True, transmittance=True, entropy=True, invisible_mass=True, scores=True, contributors=True)
+    f = api.construct_field(ctx, ds, room["train"], VmfParams(1.0), 2, RC)
+    g = f.download().gamma
+    a = api.render(ctx, ds, f, cams, RC, UC, **kw)
+    _, ids, _ = api.debug_binning(ctx, ds, cams[0], RC)
+    ctx.set_pair_budget(max(1, len(ids) + 1))  # about one view's pairs per batch
+    try:
+        f2 = api.construct_field(ctx, ds, room["train"], VmfParams(1.0), 2, RC)
+        b = api.render(ctx, ds, f2, cams, RC, UC, **kw)
+        sel = api.select_nbv(ctx, ds, f2, cams, RC, UC)
+    finally:
+        ctx.set_pair_budget(0)
+    assert np.array_equal(f2.download().gamma, g)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    assert sel.best_index == api.select_nbv(ctx, ds, f, cams, RC, UC).best_index

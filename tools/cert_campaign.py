@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--cases", type=int, default=400)
     ap.add_argument("--seconds", type=float, default=600.0)
     ap.add_argument("--seed", type=int, default=2026)
+    ap.add_argument("--large", action="store_true", help="3M splats, 1920x1080 cameras (config-4 scale)")
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     cert = api.Context(0)
@@ -67,17 +68,18 @@ def main():
     for case in range(args.cases):
         if time.time() - t0 > args.seconds:
             break
-        n = int(rng.choice([20_000, 100_000, 400_000]))
+        n = 3_000_000 if args.large else int(rng.choice([20_000, 100_000, 400_000]))
         scene = scene_for(rng, n)
         vis = rng.uniform(0, 1, n)
         vis[rng.uniform(size=n) < 0.25] = 0.0
         vis[rng.uniform(size=n) < 0.15] = 1.0
         res = int(rng.choice([256, 512, 800]))
+        w, h = (1920, 1080) if args.large else (res, res)
         cams = []
         for _ in range(8):
             eye = (rng.uniform(-0.6, 0.6), rng.uniform(-0.6, 0.6), rng.uniform(-0.8, 0.8))
             cams.append(make_lookat(eye, (rng.uniform(-0.4, 0.4), rng.uniform(-0.4, 0.4), 3.6), (0, 1, 0),
-                                    res, res, rng.uniform(0.6, 1.6), rng.uniform(0.6, 1.6)))
+                                    w, h, rng.uniform(0.6, 1.6), rng.uniform(0.6, 1.6)))
         uc = UncertaintyConfig(beta=float(rng.uniform(0.2, 0.8)), prior_opacity=float(rng.uniform(0.05, 0.3)))
         rc = RasterConfig(transmittance_cutoff=float(rng.choice([1e-4, 1e-4, 1e-3, 1e-5])),
                           alpha_clamp_max=float(rng.choice([0.99, 0.99, 0.999, 0.9, 0.5])))
@@ -104,7 +106,7 @@ def main():
         stats["rescored"] += r1[1] - r0[1]
         stats["cases"] += 1
         stats["views"] += len(cams)
-        stats["pixels"] += len(cams) * res * res
+        stats["pixels"] += len(cams) * w * h
         stats["particles_max"] = max(stats["particles_max"], n)
     stats["seconds"] = round(time.time() - t0, 1)
     stats["ok"] = (stats["count_mismatch_pixels"] == 0 and stats["argmax_mismatch"] == 0 and
