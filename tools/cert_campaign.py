@@ -26,9 +26,10 @@ from paper_2605_30342_b200.model import (RasterConfig, Scene, UncertaintyConfig,
                                          VmfParams, make_lookat)
 
 
-def scene_for(rng, n):
+def scene_for(rng, n, spread=1.0):
     kind = rng.integers(0, 5, n)
-    pos = np.stack([rng.uniform(-1.5, 1.5, n), rng.uniform(-1.5, 1.5, n), rng.uniform(2.0, 6.0, n)], 1)
+    pos = np.stack([rng.uniform(-1.5, 1.5, n) * spread, rng.uniform(-1.5, 1.5, n) * spread,
+                    2.0 + rng.uniform(0.0, 4.0, n) * spread], 1)
     dense = kind == 4                                        # tight cluster: deep pixels
     pos[dense] = rng.normal([0.2, -0.1, 3.5], 0.25, (int(dense.sum()), 3))
     sc = np.exp(rng.normal(rng.uniform(-4.5, -3.0), 0.6, (n, 3)))
@@ -69,7 +70,9 @@ def main():
         if time.time() - t0 > args.seconds:
             break
         n = 3_000_000 if args.large else int(rng.choice([20_000, 100_000, 400_000]))
-        scene = scene_for(rng, n)
+        # --large: 3M splats spread over a 4x wider volume (config-4 density per view:
+        # tens of millions of tile pairs per 1080p view, far below the 2^31 limit)
+        scene = scene_for(rng, n, 4.0 if args.large else 1.0)
         vis = rng.uniform(0, 1, n)
         vis[rng.uniform(size=n) < 0.25] = 0.0
         vis[rng.uniform(size=n) < 0.15] = 1.0
