@@ -14,7 +14,9 @@ namespace gavis {
 
 constexpr double kY00 = 0.28209479177387814;        // sh.hpp:28
 constexpr double kGaussEntropy = 4.256815599614018;  // uncertainty.hpp:19
-constexpr int kMaxFieldDegree = 4;                   // device instantiations
+constexpr int kMaxFieldDegree = 4;                   // device instantiations (registers)
+constexpr int kMaxFieldDegreeRT = 20;                // runtime-degree path (local memory), construct_field's limit
+constexpr int kDegRT = 99;                            // template tag of the runtime-degree path
 constexpr int kMaxColorDegree = 3;
 
 // Per-view camera block, precomputed on the host with the reference's own
@@ -111,8 +113,8 @@ __device__ __forceinline__ void eval_sh(double x, double y, double z, double* ou
   }
 }
 
-// Runtime-degree variant (degree <= kMaxFieldDegree) for the non-default
-// variance-propagation provider.
+// Runtime-degree variant (any degree; `out` holds (degree + 1)^2 values): the
+// variance-propagation provider and fields above degree 4.
 __device__ __forceinline__ void eval_sh_rt(int degree, double x, double y, double z, double* out) {
   const double s = sqrt(x * x + y * y);
   const double cphi = s > 1e-14 ? x / s : 1.0;

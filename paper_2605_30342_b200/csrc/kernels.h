@@ -119,7 +119,7 @@ struct VfFinalizeArgs {
   const double* vis_given = nullptr;  // [N] accumulate caller-provided v (V == 1)
   double* gamma = nullptr;            // null: do not accumulate
   int degree = 0;
-  double scales[kMaxFieldDegree + 1] = {0};
+  double scales[kMaxFieldDegreeRT + 1] = {0};
   double* vis_out = nullptr;          // [V*N]
   int64_t* touch_out = nullptr;       // [V*N]
 };

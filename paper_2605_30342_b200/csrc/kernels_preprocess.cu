@@ -146,6 +146,22 @@ __device__ __forceinline__ double query_row(const double* row, int num_views, do
   return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
 }
 
+// The same for any degree (fields above degree 4): the basis in local memory,
+// the dot product in the same index order straight from the field row.
+__device__ __noinline__ double query_row_rt(const double* gr, int degree, int num_views, double x,
+                                            double y, double z) {
+  double basis[(kMaxFieldDegreeRT + 1) * (kMaxFieldDegreeRT + 1)];
+  eval_sh_rt(degree, x, y, z, basis);
+  const int nb = (degree + 1) * (degree + 1);
+  double vt = 0.0;
+  for (int i = 0; i < nb; ++i) vt += gr[i] * basis[i];
+  const double p = (double)num_views;
+  if (vt < 0.0) vt = 0.0;
+  if (vt > p) vt = p;
+  double v = 1.0 - pow(1.0 - vt / p, p);
+  return v < 0.0 ? 0.0 : (1.0 < v ? 1.0 : v);
+}
+
 // Cheap visibility screen of one (view, particle): the near-plane test exactly as
 // project_particle makes it (fp64, same operations), then a conservative fp32
 // frustum test with the radius bound r <= 3 sqrt(lambda_max(Sigma) lambda_max(J J^T)
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
     qn += __popc(m);
   }
   __syncwarp();
-  constexpr int NBQ = QDEG >= 0 ? (QDEG + 1) * (QDEG + 1) : 1;
+  constexpr int NBQ = (QDEG >= 0 && QDEG != kDegRT) ? (QDEG + 1) * (QDEG + 1) : 1;
   for (int k = lane; k < qn + ((32 - qn % 32) % 32); k += 32) {
     if (k >= qn) continue;
     const int item = s_q[warp][k];
@@ -278,6 +294,12 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
         double vis = 0.0;
         if (a.query_mode == kQueryGiven) {
           vis = a.vis_in[gi];
+        } else if (QDEG == kDegRT && a.query_mode == kQueryField && !virt && a.num_views > 0) {
+          const int nb = (a.degree + 1) * (a.degree + 1);
+          const double d0 = qx - c.pos[0], d1 = qy - c.pos[1], d2 = qz - c.pos[2];
+          const double norm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+          if (!(norm < 1e-12))
+            vis = query_row_rt(a.gamma + gi * nb, a.degree, a.num_views, d0 / norm, d1 / norm, d2 / norm);
         } else if (QDEG >= 0 && a.query_mode == kQueryField && !virt && a.num_views > 0) {
           double row[NBQ];
           const double* gr = a.gamma + gi * NBQ;
@@ -286,7 +308,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
           const double d0 = qx - c.pos[0], d1 = qy - c.pos[1], d2 = qz - c.pos[2];
           const double norm = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
           if (!(norm < 1e-12))
-            vis = query_row<(QDEG >= 0 ? QDEG : 0)>(row, a.num_views, d0 / norm, d1 / norm,
+            vis = query_row<((QDEG >= 0 && QDEG != kDegRT) ? QDEG : 0)>(row, a.num_views, d0 / norm, d1 / norm,
                                                      d2 / norm);
         }
         UaRec u;
@@ -585,6 +607,18 @@ __global__ void query_kernel(QueryArgs a) {
   a.out[i] = out;
 }
 
+__global__ void query_rt_kernel(QueryArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const int nb = (a.degree + 1) * (a.degree + 1);
+  const int64_t g = a.idx[i];
+  double out = 0.0;
+  if (!(a.virt && a.virt[g]) && a.num_views > 0)
+    out = query_row_rt(a.gamma + g * nb, a.degree, a.num_views, a.dirs[3 * i], a.dirs[3 * i + 1],
+                       a.dirs[3 * i + 2]);
+  a.out[i] = out;
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -600,7 +634,7 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t s) {
     case 2: preprocess_kernel<2><<<grid, kPreThreads, 0, s>>>(a); break;
     case 3: preprocess_kernel<3><<<grid, kPreThreads, 0, s>>>(a); break;
     case 4: preprocess_kernel<4><<<grid, kPreThreads, 0, s>>>(a); break;
-    default: break;
+    default: preprocess_kernel<kDegRT><<<grid, kPreThreads, 0, s>>>(a); break;
   }
 }
 
@@ -685,7 +719,7 @@ void launch_query(const QueryArgs& a, cudaStream_t s) {
     case 2: query_kernel<2><<<grid, 128, 0, s>>>(a); break;
     case 3: query_kernel<3><<<grid, 128, 0, s>>>(a); break;
     case 4: query_kernel<4><<<grid, 128, 0, s>>>(a); break;
-    default: break;
+    default: query_rt_kernel<<<grid, 128, 0, s>>>(a); break;
   }
 }
 

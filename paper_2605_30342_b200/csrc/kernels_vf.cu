@@ -258,16 +258,19 @@ __global__ void __launch_bounds__(128) vf_blend_tile2_kernel(VfBlendArgs a) {
   }
 }
 
+// DEG = kDegRT: any degree up to construct_field's 20, the row updated in place
+// in global memory and the basis in local memory (same per-coefficient ops).
 template <int DEG>
 __global__ void vf_finalize_kernel(VfFinalizeArgs a, int64_t N) {
-  constexpr int NB = (DEG + 1) * (DEG + 1);
+  constexpr bool RT = DEG == kDegRT;
+  constexpr int NB = RT ? 1 : (DEG + 1) * (DEG + 1);
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= N) return;
   const bool virt = a.scene.virt ? a.scene.virt[g] != 0 : false;
   const float4 po = a.scene.pos_op[g];
   double row[NB];
   const bool acc = a.gamma != nullptr && !virt;
-  if (acc) {
+  if (acc && !RT) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) row[k] = a.gamma[g * NB + k];
   }
@@ -300,10 +303,23 @@ __global__ void vf_finalize_kernel(VfFinalizeArgs a, int64_t N) {
     d0 /= norm;
     d1 /= norm;
     d2 /= norm;
+    if (RT) {
+      double basis[(kMaxFieldDegreeRT + 1) * (kMaxFieldDegreeRT + 1)];
+      eval_sh_rt(a.degree, d0, d1, d2, basis);
+      double* gr = a.gamma + g * (int64_t)((a.degree + 1) * (a.degree + 1));
+      for (int l = 0; l <= a.degree; ++l) {
+        const double scale = vis * a.scales[l];
+        for (int m = -l; m <= l; ++m) {
+          const int idx = l * l + l + m;
+          gr[idx] += scale * basis[idx];
+        }
+      }
+      continue;
+    }
     double basis[NB];
-    eval_sh<DEG>(d0, d1, d2, basis);
+    eval_sh<(RT ? 0 : DEG)>(d0, d1, d2, basis);
 #pragma unroll
-    for (int l = 0; l <= DEG; ++l) {
+    for (int l = 0; l <= (RT ? 0 : DEG); ++l) {
       const double scale = vis * a.scales[l];
 #pragma unroll
       for (int m = -l; m <= l; ++m) {
@@ -313,7 +329,7 @@ __global__ void vf_finalize_kernel(VfFinalizeArgs a, int64_t N) {
     }
     touched_row = true;
   }
-  if (acc && touched_row) {
+  if (acc && touched_row && !RT) {
 #pragma unroll
     for (int k = 0; k < NB; ++k) a.gamma[g * NB + k] = row[k];
   }
@@ -356,7 +372,7 @@ void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s) {
     case 2: vf_finalize_kernel<2><<<grid, 128, 0, s>>>(a, N); break;
     case 3: vf_finalize_kernel<3><<<grid, 128, 0, s>>>(a, N); break;
     case 4: vf_finalize_kernel<4><<<grid, 128, 0, s>>>(a, N); break;
-    default: break;
+    default: vf_finalize_kernel<kDegRT><<<grid, 128, 0, s>>>(a, N); break;
   }
 }
 

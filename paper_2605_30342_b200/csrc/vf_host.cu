@@ -12,7 +12,7 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
   if (f) require(f->ctx->device == c->device, "field lives on another device");
   const int64_t N = s->dev.n;
   const int bv = batch_views(c, N, n_views);
-  double scales[kMaxFieldDegree + 1] = {0};
+  double scales[kMaxFieldDegreeRT + 1] = {0};
   if (f) vmf_scales(f->kappa, f->degree, scales);
   // binning of batch k+1 on the front stream under batch k's blend (as ua_render)
   cudaStream_t main_stream = c->stream;
@@ -112,7 +112,6 @@ extern "C" {
 
 static gavis_field* new_field(gavis_ctx* c, const gavis_scene* s, double kappa, int degree) {
   require(degree >= 0 && degree <= 20, "construct_field: degree out of range");
-  require(degree <= kMaxFieldDegree, "field degree above 4 is not supported by the device path");
   require(kappa >= 0.0 && kappa <= 50.0, "vmf kappa must lie in [0, 50]");
   auto* f = new gavis_field();
   f->ctx = c;

@@ -509,3 +509,29 @@ def test_vf_full_size_properties(ctx, cfg):
     assert np.all(np.isfinite(whole))
     a0 = O.vmf_scales(1.0, deg)[0] * 0.28209479177387814
     assert whole[:, 0].min() >= 0.0 and whole[:, 0].max() <= a0 * len(views) * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("degree", [5, 8, 20])
+def test_high_degree_fields(ctx, degree):
+    """Field degrees above 4 up to construct_field's limit of 20 (vfield.hpp:71-72)
+    run the runtime-degree kernels (basis in local memory, same recurrence and
+    summation order): gamma, query_view and the field-driven entropy render match
+    the oracle like the register-resident low-degree path."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    views = c["train"][:6]
+    f = api.construct_field(ctx, scene, views, VmfParams(1.0), degree, RC)
+    g = f.download().gamma
+    assert g.shape[1] == (degree + 1) ** 2
+    osc = O.OracleScene(scene)
+    og = O.construct_field(osc, views, 1.0, degree, RC, threads=8)
+    assert gamma_rel_err(g, og) <= 1e-12
+    cam = c["candidates"][1]
+    q = api.query_view(ctx, f, scene, cam)
+    idx, vis = O.query_view(og, degree, len(views), osc, cam)
+    assert np.array_equal(q.particle_indices, idx)
+    assert np.max(np.abs(q.visibilities - vis)) <= 1e-12
+    r = api.render(ctx, scene, f, [cam], RC, UC, entropy=True, contributors=True, scores=True)
+    H, _, _, cc = O.render_entropy(osc, og, degree, len(views), cam, RC, UC, contrib=True)
+    assert np.array_equal(r["entropy_contributors"], cc)
+    assert np.max(np.abs(r["entropy"] - H)) <= 2e-5
