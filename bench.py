@@ -303,7 +303,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         res = step()
     ctx.set_profiling(True)
-    KERNELS = ("ua_blend", "ua_redo", "preprocess", "select", "item_keys", "sort", "depth_order", "scan",
+    KERNELS = ("ua_blend", "ua_redo", "preprocess", "sort", "depth_order", "scan",
                "emit_keys", "ranges", "score")
     for k in KERNELS:
         ctx.kernel_time(k, reset=True)

@@ -98,11 +98,31 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
       pa.num_views = o.field->num_views;
     }
   }
-  c->run("preprocess", [&] { launch_preprocess(pa, c->stream); }, N > 0 ? 1 : 0);
-  // 64-bit pair total, read with the first host sync below: a batch whose pairs
-  // exceed the 32-bit pair indexing or the pair memory budget is split by the caller
+  // GAVIS_BIN_WIDE=1 selects the 64-bit (tile << 32 | fp32 depth) key path (A/B and
+  // the equivalence test); it is also the path of the reference-form debug keys
+  const char* wide_env = std::getenv("GAVIS_BIN_WIDE");
+  const bool narrow = !o.force_wide && !(wide_env && wide_env[0] == '1');
+  // 64-bit pair total (K1), read with the first host sync below: a batch whose
+  // pairs exceed the 32-bit pair indexing or the pair memory budget is split by
+  // the caller
   unsigned long long* dtotal = (unsigned long long*)c->buf("pair_total", sizeof(unsigned long long));
-  if (VN > 0) c->run("select", [&] { launch_pair_total(b.counts, VN, dtotal, c->stream); });
+  CK(cudaMemsetAsync(dtotal, 0, sizeof(unsigned long long), c->stream));
+  pa.pair_total = dtotal;
+  uint32_t* items = nullptr;
+  uint32_t* ik_a = nullptr;
+  uint32_t* dnum = nullptr;
+  if (VN > 0 && narrow) {
+    // K1 appends the visible (view, particle) items with their depth keys
+    items = (uint32_t*)c->buf("items", sizeof(uint32_t) * VN);
+    ik_a = (uint32_t*)c->buf("item_key_a", sizeof(uint32_t) * VN);
+    dnum = (uint32_t*)c->buf("items_num", sizeof(uint32_t));
+    CK(cudaMemsetAsync(dnum, 0, sizeof(uint32_t), c->stream));
+    pa.item_slot_out = items;
+    pa.item_key_out = ik_a;
+    pa.n_items_out = dnum;
+    pa.view_bits = std::max(1, bits_for(V));
+  }
+  c->run("preprocess", [&] { launch_preprocess(pa, c->stream); }, N > 0 ? 1 : 0);
   const auto pairs_fit = [&]() {
     const uint64_t total = *reinterpret_cast<const unsigned long long*>(c->pinned + kPinPairs);
     // <= 32 B of pair state per pair (keys and values double-buffered, VF sums)
@@ -117,21 +137,12 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     return true;
   };
 
-  // GAVIS_BIN_WIDE=1 selects the 64-bit (tile << 32 | fp32 depth) key path (A/B and
-  // the equivalence test); it is also the path of the reference-form debug keys
-  const char* wide_env = std::getenv("GAVIS_BIN_WIDE");
-  const bool narrow = !o.force_wide && !(wide_env && wide_env[0] == '1');
   int32_t* P32 = c->pinned;
   int64_t K = 0, n_items = 0;
   NarrowArgs na;
   if (VN > 0 && narrow) {
-    // visible items -> sorted by (view, depth) -> tile counts in that order -> pair offsets
-    uint32_t* items = (uint32_t*)c->buf("items", sizeof(uint32_t) * VN);
-    int32_t* dnum = (int32_t*)c->buf("items_num", sizeof(int32_t));
-    const size_t selb = select_temp_bytes(VN);
-    void* seltmp = c->buf("select_tmp", selb);
-    c->run("select", [&] { select_visible(b.counts, VN, items, dnum, seltmp, selb, c->stream); });
-    CK(cudaMemcpyAsync(P32 + kPinItems, dnum, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    // visible items (K1) -> sorted by (view, depth) -> tile counts in that order -> pair offsets
+    CK(cudaMemcpyAsync(P32 + kPinItems, dnum, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(P32 + kPinPairs, dtotal, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        c->stream));
     c->sync();
@@ -146,12 +157,10 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     na.n_items = n_items;
     na.item_slot = items;
     if (n_items > 0) {
-      uint32_t* ik_a = (uint32_t*)c->buf("item_key_a", sizeof(uint32_t) * n_items);
       uint32_t* ik_b = (uint32_t*)c->buf("item_key_b", sizeof(uint32_t) * n_items);
       uint32_t* is_b = (uint32_t*)c->buf("item_slot_b", sizeof(uint32_t) * n_items);
       na.item_key = ik_a;
       na.view_bits = std::max(1, bits_for(V));
-      c->run("item_keys", [&] { launch_item_keys(na, c->stream); });
       const size_t isb = sort32_temp_bytes(n_items);
       void* itmp = c->buf("sort_tmp", isb);
       c->run("sort", [&] {

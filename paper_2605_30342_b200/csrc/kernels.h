@@ -47,6 +47,14 @@ struct PreprocessArgs {
   int var_degree = -1;
   int* err_flag = nullptr;         // set to 1 when a propagated variance is not positive
   bool write_culled = false;
+  // depth-ordered binning: visible (view, particle) items appended (warp-aggregated,
+  // any order: the stable key sort + depth_order fix the final order) with their
+  // 32-bit keys (view | leading fp32 depth bits); null in the 64-bit key path
+  uint32_t* item_slot_out = nullptr;   // [V*N] capacity
+  uint32_t* item_key_out = nullptr;    // [V*N] capacity
+  uint32_t* n_items_out = nullptr;     // [1], zeroed by the caller
+  int view_bits = 1;
+  unsigned long long* pair_total = nullptr;  // [1] sum of tile counts, zeroed by the caller
 };
 
 struct EmitArgs {
@@ -209,10 +217,7 @@ void launch_pack_scene(const PackSceneArgs& a, cudaStream_t s);
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t s);
 void launch_emit_keys(const EmitArgs& a, cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
-void launch_item_keys(const NarrowArgs& a, cudaStream_t s);
 void launch_depth_order(const NarrowArgs& a, cudaStream_t s);
-// *total = sum of counts[0, n) (64-bit; zeroed first)
-void launch_pair_total(const int32_t* counts, int64_t n, unsigned long long* total, cudaStream_t s);
 void launch_emit_tiles(const EmitArgs& a, const NarrowArgs& n, cudaStream_t s);
 void launch_ranges32(const uint32_t* keys32, int64_t lo, int64_t hi, int64_t tile_base, uint2* ranges,
                      cudaStream_t s);
@@ -259,9 +264,5 @@ size_t sort32_temp_bytes(int64_t n);
 // 32-bit keys (stable); the sorted pairs always end in (keys_a, vals_a).
 void radix_sort_pairs32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, uint32_t* vals_b,
                         int64_t n, int end_bit, void* temp, size_t temp_bytes, cudaStream_t s);
-// slots s in [0, n) with counts[s] > 0, in order; *num_out (device) = how many
-size_t select_temp_bytes(int64_t n);
-void select_visible(const int32_t* counts, int64_t n, uint32_t* out, int32_t* num_out, void* temp,
-                    size_t temp_bytes, cudaStream_t s);
 
 }  // namespace gavis

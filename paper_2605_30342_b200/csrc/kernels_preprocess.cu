@@ -251,8 +251,11 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
   }
   __syncwarp();
   constexpr int NBQ = (QDEG >= 0 && QDEG != kDegRT) ? (QDEG + 1) * (QDEG + 1) : 1;
+  unsigned long long pairs = 0;  // this lane's tile pairs (pair_total)
   for (int k = lane; k < qn + ((32 - qn % 32) % 32); k += 32) {
-    if (k >= qn) continue;
+    bool emit = false;
+    uint32_t eslot = 0, ekey = 0;
+    if (k < qn) {
     const int item = s_q[warp][k];
     const int src = item & 31, v = item >> 5;
     const int64_t gi = wbase + src;
@@ -352,6 +355,36 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
     a.counts[slot] = count;
     a.trect[slot] = make_uint2((uint32_t)(tx0 & 0xFFFF) | ((uint32_t)(tx1 & 0xFFFF) << 16),
                                (uint32_t)(ty0 & 0xFFFF) | ((uint32_t)(ty1 & 0xFFFF) << 16));
+    pairs += (unsigned long long)count;
+    if (count > 0) {
+      // K2b, the item's 32-bit key: the view in the top view_bits, then the
+      // leading bits of the fp32 depth rounded toward zero, sign bit dropped
+      // (depth > near > 0): monotone in the fp64 depth; runs of equal keys are
+      // ordered exactly by depth_order_kernel
+      emit = true;
+      eslot = (uint32_t)slot;
+      const uint32_t db = __float_as_uint(__double2float_rz(p.depth));  // < 2^31
+      ekey = ((uint32_t)v << (32 - a.view_bits)) | (db >> (a.view_bits - 1));
+    }
+    }
+    if (a.item_slot_out) {
+      const unsigned em = __ballot_sync(0xffffffffu, emit);
+      if (em != 0u) {
+        const int leader = __ffs(em) - 1;
+        uint32_t at = 0;
+        if (lane == leader) at = atomicAdd(a.n_items_out, (uint32_t)__popc(em));
+        at = __shfl_sync(0xffffffffu, at, leader) + __popc(em & ((1u << lane) - 1u));
+        if (emit) {
+          a.item_slot_out[at] = eslot;
+          a.item_key_out[at] = ekey;
+        }
+      }
+    }
+  }
+  if (a.pair_total) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) pairs += __shfl_xor_sync(0xffffffffu, pairs, off);
+    if (lane == 0 && pairs != 0) atomicAdd(a.pair_total, pairs);
   }
 }
 
@@ -432,31 +465,7 @@ __global__ void ranges_kernel(RangesArgs a) {
 // keeps the depth order inside every tile, which is exactly the reference's
 // per-tile list order (splat_binning, raster.hpp:145-164).
 
-// K2b: 32-bit keys of the visible (view, particle) items: the view in the top
-// view_bits, then the leading bits of the fp32 depth (rounded toward zero, sign
-// bit dropped: depth > near > 0). Monotone in the fp64 depth; runs of equal keys
-// are ordered exactly by depth_order_kernel.
-__global__ void item_keys_kernel(NarrowArgs a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n_items) return;
-  const uint32_t slot = a.item_slot[i];
-  const uint32_t v = slot / (uint32_t)a.N;
-  const uint32_t db = __float_as_uint(__double2float_rz(a.geo[slot].depth));  // < 2^31
-  a.item_key[i] = (v << (32 - a.view_bits)) | (db >> (a.view_bits - 1));
-}
 
-// Total tile pairs of a batch (sum of the per-(view, particle) tile counts) in
-// 64 bits: the host checks it against the 32-bit pair indexing and the pair
-// memory budget before emitting (bin_batch splits oversized batches).
-__global__ void pair_total_kernel(const int32_t* counts, int64_t n, unsigned long long* total) {
-  unsigned long long sum = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    sum += (unsigned long long)counts[i];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-  if ((threadIdx.x & 31) == 0 && sum != 0) atomicAdd(total, sum);
-}
 
 // K2c: runs of equal fp32 keys ordered by (fp64 depth, index) by the thread at
 // the run's start (the stable sort left them in index order); then every item's
@@ -642,15 +651,6 @@ void launch_emit_keys(const EmitArgs& a, cudaStream_t s) {
   const int64_t n = (int64_t)a.V * a.N;
   if (n == 0) return;
   emit_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(a);
-}
-
-void launch_item_keys(const NarrowArgs& a, cudaStream_t s) {
-  if (a.n_items > 0) item_keys_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
-}
-
-void launch_pair_total(const int32_t* counts, int64_t n, unsigned long long* total, cudaStream_t s) {
-  cudaMemsetAsync(total, 0, sizeof(unsigned long long), s);
-  if (n > 0) pair_total_kernel<<<(unsigned)std::min<int64_t>(blocks_for(n, 256), 148 * 8), 256, 0, s>>>(counts, n, total);
 }
 
 void launch_depth_order(const NarrowArgs& a, cudaStream_t s) {

@@ -3,8 +3,6 @@
 // tile counts and K4 stable LSD radix sort of (tile << 32 | fp32 depth) keys.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
-#include <thrust/iterator/counting_iterator.h>
 
 #include "kernels.h"
 
@@ -59,26 +57,6 @@ void radix_sort_pairs32(uint32_t* keys_a, uint32_t* keys_b, uint32_t* vals_a, ui
     cudaMemcpyAsync(keys_a, k.Current(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(vals_a, v.Current(), sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
   }
-}
-
-namespace {
-struct Touches {
-  const int32_t* counts;
-  __host__ __device__ bool operator()(const uint32_t& s) const { return counts[s] > 0; }
-};
-}  // namespace
-
-size_t select_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  cub::DeviceSelect::If(nullptr, bytes, thrust::counting_iterator<uint32_t>(0), (uint32_t*)nullptr,
-                        (int32_t*)nullptr, (int)n, Touches{nullptr});
-  return bytes;
-}
-
-void select_visible(const int32_t* counts, int64_t n, uint32_t* out, int32_t* num_out, void* temp,
-                    size_t temp_bytes, cudaStream_t s) {
-  cub::DeviceSelect::If(temp, temp_bytes, thrust::counting_iterator<uint32_t>(0), out, num_out,
-                        (int)n, Touches{counts}, s);
 }
 
 }  // namespace gavis

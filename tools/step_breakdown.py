@@ -34,7 +34,7 @@ with api.Context(0) as ctx:
     print(f"render 32 / 1024 / 2048: {r32:.1f} / {r1k:.1f} / {r2k:.1f} ms;"
           f" marginal {(r2k - r1k) / 1024:.3f} ms/view; fixed ~{r1k - 1024 * (r2k - r1k) / 1024:.1f} ms")
     ctx.set_profiling(True)
-    ks = ("ua_blend", "ua_redo", "preprocess", "select", "item_keys", "sort", "depth_order", "scan",
+    ks = ("ua_blend", "ua_redo", "preprocess", "sort", "depth_order", "scan",
           "emit_keys", "ranges", "score")
     for k in ks:
         ctx.kernel_time(k, reset=True)
