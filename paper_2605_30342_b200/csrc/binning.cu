@@ -121,6 +121,9 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
     pa.item_key_out = ik_a;
     pa.n_items_out = dnum;
     pa.view_bits = std::max(1, bits_for(V));
+    // the UA path reads counts and tile rects only through the appended items;
+    // the VF finalize walks every slot
+    pa.cull_counts = o.vf_mode || o.write_culled;
   }
   c->run("preprocess", [&] { launch_preprocess(pa, c->stream); }, N > 0 ? 1 : 0);
   const auto pairs_fit = [&]() {

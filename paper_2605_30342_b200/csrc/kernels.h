@@ -50,6 +50,8 @@ struct PreprocessArgs {
   // depth-ordered binning: visible (view, particle) items appended (warp-aggregated,
   // any order: the stable key sort + depth_order fix the final order) with their
   // 32-bit keys (view | leading fp32 depth bits); null in the 64-bit key path
+  bool cull_counts = true;             // write count 0 / empty rect for culled slots (false:
+                                       // nothing reads them -- UA renders with appended items)
   uint32_t* item_slot_out = nullptr;   // [V*N] capacity
   uint32_t* item_key_out = nullptr;    // [V*N] capacity
   uint32_t* n_items_out = nullptr;     // [1], zeroed by the caller

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
     bool surv = false;
     if (valid) {
       surv = screen(s_cam[v], px, py, pz, lam, dil2);
-      if (!surv) {
+      if (!surv && a.cull_counts) {
         const int64_t slot = (int64_t)v * N + g;
         a.counts[slot] = 0;
         a.trect[slot] = empty_rect;
