@@ -10,14 +10,32 @@ its own block of --per-gpu candidates. The VF construction (150 training views,
 sharded over ranks + NCCL all-reduce) is timed separately as vf_build_ms.
 Inputs (scene 240 MB + field 72 MB) exceed the 126 MB L2, so no flush is needed.
 
---impl reference times the CPU oracle (the reference's algorithm restated in C,
-the reference itself does not build here) on the host cores, rank 0 only.
+The headline `value` is the fp64 path (`--precision exact`, the reference's own
+arithmetic, common.hpp:14-18); the certified fp32 path (fp32 blend, fp64 redo
+of every pixel whose stop decision fp32 cannot certify, fp64 argmax) is
+measured in the same run as `certified_value` / `certified_e2e`.
+
+Every run checks itself against the CPU oracle on the headline config: the
+oracle's scores of the cpu_baseline sample (rendered with the GPU's field),
+the argmax over that sample, both tracks' per-pixel contributor counts of one
+view, and a two-view field (`parity_gate`), for both device precisions.
+
+`--gpus N` without a torchrun environment re-launches itself as N ranks through
+torch.distributed.run (one process per GPU, NCCL); it fails loudly when fewer
+than N devices are visible.
+
+--impl reference times the CPU oracle (the reference's algorithm restated in C;
+the reference itself does not build here) on the host cores, rank 0 only: the
+field is built by the oracle from the same 150 training views, and each step
+scores the first candidates of the GPU arm's list.
 """
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -32,7 +50,7 @@ METRIC = "UA-render candidate views/s @800²"
 UNIT = "candidate views/s"
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
@@ -41,23 +59,55 @@ def parse():
     p.add_argument("--config", type=int, default=3)
     p.add_argument("--per-gpu", type=int, default=1024, help="candidates per GPU per step")
     p.add_argument("--particles", type=int, default=0, help="override Gaussian count (testing)")
-    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU leg (and the oracle gate)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=0, help="candidates in the CPU sample")
     p.add_argument("--no-extra-vf", action="store_true", help="skip the config-2/4 VF-build timings")
     p.add_argument("--batch", type=int, default=0, help="views per launch batch (0 = library default)")
-    p.add_argument("--sweep5", action="store_true",
-                   help="config-5 active-mapping sweep: 20 incremental rounds x 512..4096 candidates at 400^2")
-    p.add_argument("--precision", default="certified", choices=["certified", "exact"],
-                   help="UA blend arithmetic (certified fp32 + fp64 redo, or fp64 throughout)")
-    return p.parse_args()
+    p.add_argument("--no-sweep5", action="store_true",
+                   help="skip the config-5 active-mapping sweep (20 incremental rounds x 512..4096 @400^2)")
+    p.add_argument("--precision", default="exact", choices=["certified", "exact"],
+                   help="headline blend arithmetic (fp64 throughout, or certified fp32 + fp64 redo)")
+    p.add_argument("--no-certified", action="store_true", help="skip the second (certified) measurement")
+    p.add_argument("--selftest-dist", action="store_true",
+                   help="launcher/collective plumbing only (no device work): prints n_gpus and exits")
+    return p.parse_args(argv)
 
 
-def dist_init(gpus: int):
+# ------------------------------------------------------------------ launcher
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: start N ranks through torch.distributed.run
+    on this node (127.0.0.1) and return their exit code; None = we are a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    backend = os.environ.get("GAVIS_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}\n")
+            return 3
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("MASTER_ADDR", "127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def dist_init():
     """One process per GPU (torchrun env). GAVIS_DIST_BACKEND=gloo runs the same
-    host logic over gloo (code-path smoke test with fewer GPUs than ranks: ranks
-    then share devices round-robin; the collectives are host-side, no kernel of
-    one rank waits on another)."""
+    host logic over gloo (CPU tests of the launcher)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -66,11 +116,12 @@ def dist_init(gpus: int):
         import torch
         import torch.distributed as d
         backend = os.environ.get("GAVIS_DIST_BACKEND", "nccl")
-        if backend != "nccl":
-            local = local % max(1, torch.cuda.device_count())
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
+            if torch.cuda.device_count() <= local:
+                raise RuntimeError(f"rank {rank}: local rank {local} has no CUDA device "
+                                   f"({torch.cuda.device_count()} visible)")
+            torch.cuda.set_device(local)
             d.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             d.init_process_group(backend)
@@ -184,63 +235,114 @@ def cpu_info():
                 break
     except Exception:
         pass
-    return model, os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    return model, cores
 
 
-def oracle_rate(c, gamma, degree, num_views, n_cands, threads):
-    """The reference's algorithm (CPU oracle) on `n_cands` candidates: rasterize (RGB)
-    + render_entropy + image_entropy + argmax, parallel over candidates (planner.hpp:125-131)."""
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
+    return O
+
+
+def oracle_select(c, osc, gamma, degree, num_views, cams, threads):
+    """The reference's algorithm (CPU oracle) on `cams`: rasterize (RGB) +
+    render_entropy + image_entropy + argmax, parallel over candidates
+    (planner.hpp:125-131). Returns (rate, seconds, best, scores)."""
+    O = _oracle()
     from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
-    osc = O.OracleScene(c["scene"])
-    cams = c["candidates"][:n_cands]
     t0 = time.perf_counter()
-    O.select_nbv(osc, gamma, degree, num_views, cams, RasterConfig(), UncertaintyConfig(), threads=threads,
-                 with_rgb=True)
+    best, scores = O.select_nbv(osc, gamma, degree, num_views, cams, RasterConfig(), UncertaintyConfig(),
+                                threads=threads, with_rgb=True)
     dt = time.perf_counter() - t0
-    return n_cands / dt, dt
+    return len(cams) / dt, dt, int(best), np.asarray(scores, np.float64)
 
 
+def oracle_view(osc, gamma, degree, num_views, cam):
+    """Oracle RGB + entropy renders of one view with per-pixel contributor counts
+    (raster.hpp:175-231, uncertainty.hpp:124-260), the two tracks on two threads."""
+    O = _oracle()
+    from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
+    with cf.ThreadPoolExecutor(2) as ex:
+        fr = ex.submit(O.rasterize, osc, cam, RasterConfig(), True)
+        fe = ex.submit(O.render_entropy, osc, gamma, degree, num_views, cam, RasterConfig(),
+                       UncertaintyConfig(), True)
+        rgb, _, _, rcc = fr.result()
+        H, _, _, ecc = fe.result()
+    return rgb, rcc, H, ecc
+
+
+# ------------------------------------------------------------------ reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
+    O = _oracle()
     from paper_2605_30342_b200.model import RasterConfig
-    c = make_config(args.config, 1, max(8, args.cpu_sample or 8), args.particles)
+    c = make_config(args.config, 1, args.per_gpu, args.particles)
     model, cores = cpu_info()
-    # field for the oracle's render: the oracle's own construct_field over a view sample
-    # would take minutes at 1M particles; the candidate-render cost does not depend on
-    # the field's values, so build it from 2 training views.
-    gamma = O.construct_field(O.OracleScene(c["scene"]), c["train"][:2], 1.0, c["degree"], RasterConfig(),
-                              threads=cores)
-    n = args.cpu_sample or max(cores, 8)
+    osc = O.OracleScene(c["scene"])
+    # the field of the stated config: construct_field over all its training views
+    # (parallel_for over views, vfield.hpp:85-87), the reference's own algorithm
+    t0 = time.perf_counter()
+    gamma = O.construct_field(osc, c["train"], 1.0, c["degree"], RasterConfig(), threads=cores)
+    field_s = time.perf_counter() - t0
+    n = args.cpu_sample or cores
+    cams = c["candidates"][:n]  # the first candidates of the GPU arm's list
     rates = []
     for _ in range(args.warmup):
-        oracle_rate(c, gamma, c["degree"], len(c["train"]), min(n, cores), cores)
+        oracle_select(c, osc, gamma, c["degree"], len(c["train"]), cams, cores)
+    best = None
     for _ in range(args.steps):
-        r, dt = oracle_rate(c, gamma, c["degree"], len(c["train"]), n, cores)
+        r, dt, best, _ = oracle_select(c, osc, gamma, c["degree"], len(c["train"]), cams, cores)
         rates.append(r)
     value = float(np.mean(rates))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * n / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"config{args.config}", "candidates_per_step": n},
+            "data": "synthetic (seeded config generator; paper datasets not in the container)",
+            "config": {"workload": f"config{args.config}", "particles": c["scene"].num_particles,
+                       "training_views": len(c["train"]), "field_degree": c["degree"],
+                       "color_degree": c["scene"].color_degree,
+                       "resolution": [cams[0].width, cams[0].height],
+                       "candidates_per_step": n,
+                       "sample": f"candidates 0..{n - 1} of the GPU arm's config-{args.config} list"},
+            "field_build_s": field_s, "best_index_in_sample": best,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{n} candidates/step of config {args.config} at 800x800, "
+                             "sample": f"{n} candidates/step (the GPU arm's first {n}) of config {args.config} "
+                                       f"at 800x800, field from all {len(c['train'])} training views; "
                                        f"oracle select_nbv + rasterize on {cores} threads ({model})"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------ dist selftest
+def run_selftest(args):
+    """Launcher + collective plumbing without device work (CPU tests over gloo)."""
+    rank, local, world, dist = dist_init()
+    from paper_2605_30342_b200 import parallel
+    lo, hi = parallel.shard_range(args.per_gpu * world, rank, world)
+    t = max_over_ranks(float(rank + 1), dist)
+    total = sum_over_ranks(float(hi - lo), dist)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "max_rank_plus_1": t, "candidates": total,
+                          "backend": dist.get_backend() if dist else None}), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
     from paper_2605_30342_b200 import api, parallel
     from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig, VmfParams
-    rank, local, world, dist = dist_init(args.gpus)
+    rank, local, world, dist = dist_init()
     torch.cuda.set_device(local)
     rc, uc = RasterConfig(), UncertaintyConfig()
     c = make_config(args.config, world, args.per_gpu, args.particles)
@@ -256,18 +358,8 @@ def run_ours(args):
 
     # ---------------- VF CONST: sharded views + NCCL all-reduce --------------
     def build_field(views, dscene=None, deg=None):
-        dscene = dscene or ds
-        deg = degree if deg is None else deg
-
-        def partial(lo, hi):
-            f = api.empty_field(ctx, dscene, vmf, deg)
-            if hi > lo:
-                api.accumulate_views(ctx, f, dscene, views[lo:hi], rc)
-            return f
-        f = parallel.construct_field_sharded(partial, len(views), rank, world,
-                                             lambda fld: parallel.allreduce_device_field(fld, dist))
-        f.set_num_views(len(views))
-        return f
+        return parallel.construct_device_field_sharded(ctx, dscene or ds, views, vmf,
+                                                       degree if deg is None else deg, rank, world, dist, rc)
 
     field = build_field(train)  # warm-up + the field used for scoring
     barrier(ctx, dist)
@@ -300,57 +392,50 @@ def run_ours(args):
         return api.select_nbv_sharded(ctx, ds, field, c["candidates"], rank, world, dist, rc, uc,
                                       with_rgb=True)
 
-    for _ in range(args.warmup):
-        res = step()
-    ctx.set_profiling(True)
     KERNELS = ("ua_blend", "ua_redo", "preprocess", "sort", "depth_order", "scan",
                "emit_keys", "ranges", "score")
-    for k in KERNELS:
-        ctx.kernel_time(k, reset=True)
-    redo0, resc0 = ctx.counters()
-    barrier(ctx, dist)
-    clocks = ClockSampler(local)
-    clocks.start()
-    l0 = ctx.launch_count()
-    ctx.timer_start()
-    for _ in range(args.steps):
-        res = step()
-    ms = ctx.timer_stop()
-    launches = ctx.launch_count() - l0
-    barrier(ctx, dist)
-    clk = clocks.stop()
-    ktimes = {k: ctx.kernel_time(k) for k in KERNELS}
-    redo1, resc1 = ctx.counters()
-    certified = {"redo_pixels_per_view": (redo1 - redo0) / float(len(cands) * args.steps),
-                 "redo_fraction": (redo1 - redo0) / float(len(cands) * args.steps * cands[0].width * cands[0].height),
-                 "rescored_candidates_per_step": (resc1 - resc0) / float(args.steps)}
-    ctx.set_profiling(False)
-    ms_max = max_over_ranks(ms, dist)
-    total_cands = sum_over_ranks(float(len(cands) * args.steps), dist)
-    value = total_cands / (ms_max / 1000.0)
 
-    # parity gate of this run: certified scores/argmax against the exact fp64 path on
-    # the first 8 candidates, contributor counts of one view (tests hold the oracle)
-    gate_cams = cands[: min(8, len(cands))]
-    cert = api.render(ctx, ds, field, gate_cams[:1], rc, uc, entropy=True, rgb=True, contributors=True)
-    cert_scores = api.score_views(ctx, ds, field, gate_cams, rc, uc, with_rgb=True)
-    ctx.set_precision("exact")
-    exact = api.render(ctx, ds, field, gate_cams[:1], rc, uc, entropy=True, rgb=True, contributors=True)
-    exact_scores = api.score_views(ctx, ds, field, gate_cams, rc, uc, with_rgb=True)
+    def measure(precision):
+        """K timed select_nbv steps in one precision: device time (CUDA events on the
+        library stream), max over ranks, per-kernel times, clocks, launches."""
+        ctx.set_precision(precision)
+        res = None
+        for _ in range(args.warmup):
+            res = step()
+        ctx.set_profiling(True)
+        for k in KERNELS:
+            ctx.kernel_time(k, reset=True)
+        redo0, resc0 = ctx.counters()
+        barrier(ctx, dist)
+        clocks = ClockSampler(local)
+        clocks.start()
+        l0 = ctx.launch_count()
+        ctx.timer_start()
+        for _ in range(args.steps):
+            res = step()
+        ms = ctx.timer_stop()
+        launches = ctx.launch_count() - l0
+        barrier(ctx, dist)
+        clk = clocks.stop()
+        ktimes = {k: ctx.kernel_time(k) for k in KERNELS}
+        redo1, resc1 = ctx.counters()
+        ctx.set_profiling(False)
+        ms_max = max_over_ranks(ms, dist)
+        total = sum_over_ranks(float(len(cands) * args.steps), dist)
+        out = {"value": total / (ms_max / 1000.0), "ms_per_step": ms_max / args.steps, "ms_local": ms,
+               "ktimes": ktimes, "clocks": clk, "launches": int(launches),
+               "best": int(res.best_index) + (lo if world == 1 else 0)}
+        if precision == "certified":
+            out["certified"] = {
+                "redo_pixels_per_view": (redo1 - redo0) / float(len(cands) * args.steps),
+                "redo_fraction": (redo1 - redo0) / float(len(cands) * args.steps * cands[0].width * cands[0].height),
+                "rescored_candidates_per_step": (resc1 - resc0) / float(args.steps)}
+        return out
+
+    head = measure(args.precision)
+    other_prec = "certified" if args.precision == "exact" else "exact"
+    second = None if args.no_certified else measure(other_prec)
     ctx.set_precision(args.precision)
-    # covered (pixel, list entry) pairs composited per view (SURVEY 8d secondary metric):
-    # the per-pixel contributor counts of both tracks, averaged over the gate views
-    cov_rgb = float(np.sum(exact["rgb_contributors"]))
-    cov_ent = float(np.sum(exact["entropy_contributors"]))
-    parity_gate = {
-        "candidates": len(gate_cams),
-        "scores_max_rel": float(np.max(np.abs(cert_scores - exact_scores) / np.abs(exact_scores))),
-        "argmax_equal": bool(parallel.first_max(cert_scores) == parallel.first_max(exact_scores)),
-        "contributors_equal": bool(np.array_equal(cert["rgb_contributors"], exact["rgb_contributors"]) and
-                                   np.array_equal(cert["entropy_contributors"], exact["entropy_contributors"])),
-        "images_max_abs": float(max(np.max(np.abs(cert["rgb"] - exact["rgb"])),
-                                    np.max(np.abs(cert["entropy"] - exact["entropy"])))),
-        "reference": "exact fp64 device path (pinned to the CPU oracle by tests/test_gpu_parity.py)"}
 
     # secondary: the reference planner's own select_nbv work (entropy + score, no RGB)
     barrier(ctx, dist)
@@ -367,24 +452,43 @@ def run_ours(args):
         keys_per_view.append(len(k))
     K_avg = float(np.mean(keys_per_view))
     P = cands[0].width * cands[0].height
-    blend_ms, blend_n = ktimes["ua_blend"]
-    views_per_launch = len(cands) * args.steps / max(1, blend_n)
-    bytes_per_launch = views_per_launch * (24.0 * K_avg + 16.0 * P)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = bytes_per_launch / (blend_ms / max(1, blend_n) / 1000.0) / 1e9 if blend_n else 0.0
-    step_ms = ms / args.steps
+
+    def roofline(m, precision):
+        blend_ms, blend_n = m["ktimes"]["ua_blend"]
+        vpl = len(cands) * args.steps / max(1, blend_n)
+        bpl = vpl * (24.0 * K_avg + 16.0 * P)
+        achieved = bpl / (blend_ms / max(1, blend_n) / 1000.0) / 1e9 if blend_n else 0.0
+        prof = os.path.join(ROOT, "profiles", "ncu_ua_blend.json" if precision == "certified"
+                            else "ncu_ua_blend_exact.json")
+        traffic, src, compute = None, None, None
+        if os.path.exists(prof):
+            with open(prof) as f:
+                pj = json.load(f)
+            traffic = pj["traffic_bytes_per_launch"] * vpl / pj["views_per_launch"]
+            src = f"{pj['command']} ({pj['views_per_launch']} views/launch, {pj['kernel']})"
+            compute = {"bound": pj.get("compute_bound", "issue/latency"),
+                       "fp64_pipe_active_pct": pj.get("fp64_pipe_active_pct"),
+                       "issue_slots_busy_pct": pj.get("issue_slots_busy_pct"), "source": "same ncu capture"}
+        return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "traffic_source": src, "compute": compute,
+                "kernel": "ua_blend (" + ("ua_blend_fast_kernel, certified" if precision == "certified"
+                                          else "ua_blend_ilp_kernel, fp64") + ")",
+                "bytes_per_launch": bpl, "views_per_launch": vpl,
+                "avg_launch_ms": blend_ms / max(1, blend_n), "launches": blend_n,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+
     N = scene.num_particles
     nb_c = (scene.color_degree + 1) ** 2
     pipe_bytes = N * (45 + 8 * (degree + 1) ** 2 + 12 * nb_c) + len(cands) * (24.0 * K_avg + 16.0 * P)
 
     # ---------------- e2e through the public C-ABI with host buffers ---------
-    e2e = None
-    if not args.no_e2e:
+    def e2e_measure(precision):
         host_field = field.download()
         pinned = {}
         for name in ("positions", "rotations", "scales", "opacities", "colors"):
@@ -401,6 +505,7 @@ def run_ours(args):
         host_field.gamma = gpin
         h2d = sum(v.nbytes for v in pinned.values()) + scene.is_virtual.nbytes + gpin.nbytes + 128 * len(cands)
         d2h = 8 * len(cands) + 4
+        ctx.set_precision(precision)
 
         def e2e_step():
             s2 = ctx.upload(host_scene)
@@ -419,9 +524,13 @@ def run_ours(args):
         barrier(ctx, dist)
         e_ms = max_over_ranks((time.perf_counter() - t0) * 1000.0, dist)
         e_total = sum_over_ranks(float(len(cands) * e_steps), dist)
-        e2e = {"value": e_total / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h),
-               "timing": "host wall clock around upload(scene)+upload(field)+select_nbv, synchronised"}
+        ctx.set_precision(args.precision)
+        return {"value": e_total / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "precision": precision,
+                "timing": "host wall clock around upload(scene)+upload(field)+select_nbv, synchronised"}
+
+    e2e = None if args.no_e2e else e2e_measure(args.precision)
+    e2e_second = None if (args.no_e2e or second is None) else e2e_measure(other_prec)
 
     # ---------------- VF-build ms on configs 2 and 4 (BASELINE metric) ------
     vf_other = {}
@@ -436,123 +545,194 @@ def run_ours(args):
             fld = build_field(cc["train"], dsc, cc["degree"])  # warm-up
             fld.close()
             times = []
-            for _ in range(2):
+            for it in range(2):
                 barrier(ctx, dist)
                 t0 = time.perf_counter()
                 fld = build_field(cc["train"], dsc, cc["degree"])
                 barrier(ctx, dist)
                 times.append((time.perf_counter() - t0) * 1000.0)
-                if _ == 0:
+                if it == 0:
                     fld.close()
-            # UA render + score of this config's candidates (per rank block, device time)
-            clo, chi = parallel.shard_range(len(cc["candidates"]), rank, world)
-            ccands = cc["candidates"][clo:chi]
-            api.select_nbv(ctx, dsc, fld, ccands, rc, uc, with_rgb=True)  # warm-up (buffer sizes)
-            barrier(ctx, dist)
-            ctx.timer_start()
-            api.select_nbv(ctx, dsc, fld, ccands, rc, uc, with_rgb=True)
-            ua_ms = max_over_ranks(ctx.timer_stop(), dist)
+            ccands = cc["candidates"]
+            entry = {"vf_build_ms": min(times), "views": len(cc["train"]), "particles": cc["scene"].num_particles,
+                     "resolution": [cc["train"][0].width, cc["train"][0].height], "field_degree": cc["degree"],
+                     "ua_candidates": len(ccands), "ua_resolution": [ccands[0].width, ccands[0].height]}
+            for prec in ("exact", "certified"):
+                ctx.set_precision(prec)
+                api.select_nbv(ctx, dsc, fld, ccands, rc, uc, with_rgb=True)  # warm-up (buffer sizes)
+                barrier(ctx, dist)
+                ctx.timer_start()
+                api.select_nbv(ctx, dsc, fld, ccands, rc, uc, with_rgb=True)
+                entry["ua_views_per_s" if prec == "exact" else "ua_views_per_s_certified"] = \
+                    len(ccands) / (ctx.timer_stop() / 1000.0)
+            ctx.set_precision(args.precision)
             fld.close()
-            cam = cc["train"][0]
-            vf_other[f"config{cid}"] = {"vf_build_ms": max_over_ranks(min(times), dist),
-                                        "ua_views_per_s": sum_over_ranks(float(len(ccands)), dist) / (ua_ms / 1000.0),
-                                        "ua_candidates": len(cc["candidates"]),
-                                        "ua_resolution": [cc["candidates"][0].width, cc["candidates"][0].height],
-                                        "views": len(cc["train"]), "particles": cc["scene"].num_particles,
-                                        "resolution": [cam.width, cam.height], "field_degree": cc["degree"]}
+            vf_other[f"config{cid}"] = entry
             dsc.close()
             del cc
 
-    # ---------------- config 5: active-mapping iteration sweep (1 GPU) ---------
+    # ---------------- config 5: active-mapping iteration sweep ---------------
     sweep5 = None
-    if args.sweep5 and world == 1:
-        from paper_2605_30342_b200 import synth
-        c5 = synth.config5(0, n_candidates=4096)
-        ds5 = ctx.upload(c5["scene"])
-        sweep5 = {"scene": "config2 (500k Gaussians)", "training_views": len(c5["train"]),
-                  "candidate_resolution": [400, 400], "rounds": c5["rounds"], "per_count": {}}
-        for count in (512, 1024, 2048, 4096):
-            f5 = build_field(c5["train"], ds5, c5["degree"])
-            api.nbv_loop(ctx, ds5, f5, c5["candidates"][:count], 1, rc, uc)  # warm-up round
-            f5.close()
-            f5 = build_field(c5["train"], ds5, c5["degree"])
-            barrier(ctx, dist)
-            ctx.timer_start()
-            chosen, _, _ = api.nbv_loop(ctx, ds5, f5, c5["candidates"][:count], c5["rounds"], rc, uc)
-            ms5 = ctx.timer_stop()
-            sweep5["per_count"][str(count)] = {
-                "ms_per_round": ms5 / c5["rounds"],
-                "candidate_views_per_s": count * c5["rounds"] / (ms5 / 1000.0),
-                "chosen_first_rounds": [int(x) for x in chosen[:5]]}
-            f5.close()
-        ds5.close()
+    if not args.no_sweep5:
+        sweep5 = run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc)
 
-    cpu = None
+    # ---------------- CPU baseline + oracle parity gate ----------------------
+    cpu, parity_gate = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        model, cores = cpu_info()
-        n = args.cpu_sample or max(4, min(16, cores))
-        gamma = field.download().gamma
-        rate, dt = oracle_rate(c, gamma, degree, len(train), n, cores)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{n} of the config-{args.config} candidates (800x800, full scene), oracle "
-                         f"select_nbv + rasterize on {cores} threads, {dt:.1f} s ({model})"}
-
-    # dram bytes per ua_blend launch from the committed ncu --set full capture
-    # (profiles/ncu_ua_blend.json, same launch shape: 16 config-3 views, RGB+entropy)
-    traffic, traffic_src, compute = None, None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_ua_blend.json")
-    if os.path.exists(prof):
-        with open(prof) as f:
-            pj = json.load(f)
-        traffic = pj["traffic_bytes_per_launch"] * views_per_launch / pj["views_per_launch"]
-        traffic_src = f"{pj['command']} ({pj['views_per_launch']} views/launch)"
-        compute = {"bound": pj.get("compute_bound", "issue/latency"),
-                   "fp64_pipe_active_pct": pj["fp64_pipe_active_pct"],
-                   "issue_slots_busy_pct": pj["issue_slots_busy_pct"], "source": "same ncu capture"}
+        parity_gate, cpu = oracle_gate(args, ctx, api, c, ds, field, cands, rc, uc)
 
     if rank == 0:
+        head_prec = args.precision
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if args.precision == "certified" else "f64",
-            "precision": args.precision if args.precision == "exact" else
-            "certified (fp32 blend, fp64 q; fp64 redo of uncertified pixels; exact argmax)",
-            "certified": certified if args.precision == "certified" else None,
+            "dtype": "f64" if head_prec == "exact" else "f32",
+            "precision": "fp64 blend (the reference's arithmetic)" if head_prec == "exact" else
+            "certified (fp32 blend, fp64 q; fp64 redo of uncertified pixels; fp64 argmax)",
             "data": "synthetic (seeded config generator; paper datasets not in the container)",
             "config": {"workload": f"config{args.config}", "particles": N, "resolution": [cands[0].width, cands[0].height],
                        "candidates_per_gpu_per_step": len(cands), "training_views": len(train),
                        "field_degree": degree, "color_degree": scene.color_degree,
                        "parallelism": f"candidates sharded over {world} GPU(s), VF views sharded + NCCL all-reduce",
                        "l2": "inputs (scene+field) exceed the 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "traffic_source": traffic_src, "compute": compute,
-                         "kernel": "ua_blend", "bytes_per_launch": bytes_per_launch,
-                         "avg_launch_ms": blend_ms / max(1, blend_n), "launches": blend_n,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
-            "pipeline": {"bytes_per_step": pipe_bytes, "achieved_gbs": pipe_bytes / (step_ms / 1000.0) / 1e9,
-                         "pairs_per_view": K_avg, "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()}},
+            "roofline": roofline(head, head_prec),
+            "pipeline": {"bytes_per_step": pipe_bytes, "achieved_gbs": pipe_bytes / (head["ms_local"] / args.steps / 1000.0) / 1e9,
+                         "pairs_per_view": K_avg,
+                         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in head["ktimes"].items()}},
             "select_nbv_entropy_only_views_per_s": select_only,
             "vf_build_ms": vf_ms, "vf_build_views": len(train), "vf_build_200_views_ms": vf200_ms,
             "vf_build_other_configs": vf_other,
-            "best_index_last_step": int(res.best_index) + (lo if world == 1 else 0),
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "best_index_last_step": head["best"],
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": head["launches"], "clocks": head["clocks"],
             "parity_gate": parity_gate,
-            "covered_pairs": {"rgb_per_view": cov_rgb, "entropy_per_view": cov_ent,
-                              "per_s": (cov_rgb + cov_ent) * value,
-                              "note": "pixel-entry evaluations until each track terminates, view 0 of the step"},
-            **({"config5_sweep": sweep5} if sweep5 else {}),
         }
-        print(json.dumps(line))
+        if second is not None:
+            key = "certified" if other_prec == "certified" else "exact"
+            line[f"{key}_value"] = second["value"]
+            line[f"{key}_ms_per_step"] = second["ms_per_step"]
+            line[f"{key}_e2e"] = e2e_second
+            line[f"{key}_roofline"] = roofline(second, other_prec)
+            line[f"{key}_kernel_ms_per_step"] = {k: v[0] / args.steps for k, v in second["ktimes"].items()}
+            line[f"{key}_clocks"] = second["clocks"]
+            line[f"{key}_gpu_launches"] = second["launches"]
+            line[f"{key}_best_index_last_step"] = second["best"]
+        cert = head.get("certified") or (second or {}).get("certified")
+        if cert:
+            line["certified"] = cert
+        if sweep5:
+            line["config5_sweep"] = sweep5
+        print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
+def oracle_gate(args, ctx, api, c, ds, field, cands, rc, uc):
+    """CPU leg: time the oracle on a bounded sample of the headline workload (the
+    cpu_baseline), and compare it with the device in BOTH precisions on the same
+    inputs: scores + argmax of the sample (rendered with the device's field),
+    per-pixel contributor counts and images of one view, and a 2-view field."""
+    from paper_2605_30342_b200.model import VmfParams
+    O = _oracle()
+    model, cores = cpu_info()
+    n = args.cpu_sample or max(4, min(16, cores))
+    sample = cands[:n]
+    gamma = field.download().gamma
+    degree, nv = c["degree"], len(c["train"])
+    osc = O.OracleScene(c["scene"])
+    rate, dt, o_best, o_scores = oracle_select(c, osc, gamma, degree, nv, sample, cores)
+    cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"candidates 0..{n - 1} of config {args.config} (800x800, full scene, the device's "
+                     f"{nv}-view field), oracle select_nbv + rasterize on {cores} threads, {dt:.1f} s ({model})"}
+    o_rgb, o_rcc, o_H, o_ecc = oracle_view(osc, gamma, degree, nv, sample[0])
+    # 2-view field: device vs oracle construct_field (vfield.hpp:68-92)
+    two = c["train"][:2]
+    g2 = O.construct_field(osc, two, 1.0, degree, rc, threads=cores)
+    f2 = api.construct_field(ctx, ds, two, VmfParams(1.0), degree, rc)
+    d2 = f2.download().gamma
+    f2.close()
+    scale = np.maximum(np.abs(g2).max(axis=1, keepdims=True), 1e-300)
+    gate = {"reference": "CPU oracle (oracle/gavis_oracle.c, the reference's fp64 algorithm), same seeded inputs",
+            "candidates": n, "oracle_argmax_in_sample": o_best,
+            "field_2views_gamma_max_rel": float((np.abs(d2 - g2) / scale).max()),
+            "field_2views_rows_nonzero": int((np.abs(g2).max(axis=1) > 0).sum())}
+    prev = ctx.precision
+    for prec in ("exact", "certified"):
+        ctx.set_precision(prec)
+        sc = api.score_views(ctx, ds, field, sample, rc, uc, with_rgb=True)
+        sel = api.select_nbv(ctx, ds, field, sample, rc, uc, with_rgb=True)
+        r = api.render(ctx, ds, field, sample[:1], rc, uc, entropy=True, rgb=True, contributors=True)
+        gate[prec] = {
+            "oracle_scores_max_rel": float(np.max(np.abs(sc - o_scores) / np.abs(o_scores))),
+            "oracle_argmax_equal": bool(sel.best_index == o_best),
+            "rgb_contributors_equal": bool(np.array_equal(r["rgb_contributors"], o_rcc)),
+            "entropy_contributors_equal": bool(np.array_equal(r["entropy_contributors"], o_ecc)),
+            "rgb_max_abs": float(np.max(np.abs(r["rgb"] - o_rgb))),
+            "entropy_max_abs": float(np.max(np.abs(r["entropy"] - o_H)))}
+    ctx.set_precision(prev)
+    gate["pass"] = bool(gate["field_2views_gamma_max_rel"] <= 1e-5 and all(
+        gate[p]["oracle_argmax_equal"] and gate[p]["rgb_contributors_equal"] and
+        gate[p]["entropy_contributors_equal"] and gate[p]["rgb_max_abs"] <= 1e-4 and
+        gate[p]["entropy_max_abs"] <= 1e-4 and gate[p]["oracle_scores_max_rel"] <= 1e-6
+        for p in ("exact", "certified")))
+    return gate, cpu
+
+
+def run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc):
+    """Config 5 (BASELINE.json): the config-2 scene, 20 active-mapping rounds, each
+    scoring the candidate pool at 400^2 and appending the chosen view to the field
+    incrementally (linearity, test_vfield.cpp:104-131), at 512..4096 candidates.
+    One GPU: the library's gavis_nbv_loop. N GPUs: candidates sharded per round,
+    scores all-gathered, first-max, every rank appends the chosen view."""
+    from paper_2605_30342_b200 import synth
+    c5 = synth.config5(0, n_candidates=4096)
+    ds5 = ctx.upload(c5["scene"])
+    out = {"scene": "config2 (500k Gaussians, 100 upper-hemisphere views)", "training_views": len(c5["train"]),
+           "candidate_resolution": [400, 400], "rounds": c5["rounds"], "n_gpus": world, "per_count": {}}
+    for count in (512, 1024, 2048, 4096):
+        pool = c5["candidates"][:count]
+
+        def loop(rounds, f):
+            if world == 1:
+                chosen, _, _ = api.nbv_loop(ctx, ds5, f, pool, rounds, rc, uc)
+                return [int(x) for x in chosen]
+            chosen = []
+            for _ in range(rounds):
+                r = api.select_nbv_sharded(ctx, ds5, f, pool, rank, world, dist, rc, uc)
+                chosen.append(int(r.best_index))
+                api.accumulate_views(ctx, f, ds5, [pool[r.best_index]], rc)  # num_views += 1
+            return chosen
+
+        f5 = build_field(c5["train"], ds5, c5["degree"])
+        loop(1, f5)  # warm-up round
+        f5.close()
+        f5 = build_field(c5["train"], ds5, c5["degree"])
+        barrier(ctx, dist)
+        ctx.timer_start()
+        t0 = time.perf_counter()
+        chosen = loop(c5["rounds"], f5)
+        ms_dev = ctx.timer_stop()
+        barrier(ctx, dist)
+        ms = max_over_ranks(ms_dev if world == 1 else (time.perf_counter() - t0) * 1000.0, dist)
+        out["per_count"][str(count)] = {
+            "ms_per_round": ms / c5["rounds"],
+            "candidate_views_per_s": count * c5["rounds"] / (ms / 1000.0),
+            "chosen_first_rounds": chosen[:5],
+            "timing": "device events (library loop)" if world == 1 else "host wall clock, max over ranks"}
+        f5.close()
+    ds5.close()
+    return out
+
+
 def main():
     args = parse()
+    rc = relaunch_if_needed(args)
+    if rc is not None:
+        return rc
+    if args.selftest_dist:
+        return run_selftest(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

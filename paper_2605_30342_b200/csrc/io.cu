@@ -6,6 +6,8 @@
 //   * visibility-field JSON, save_field / load_field (io.hpp:255-295):
 //     {"L", "kappa", "num_views", "gamma": [[...] per particle], "virtual": [...]}.
 // Errors follow the reference: malformed input -> ParameterError (status 2).
+#include <algorithm>
+#include <cctype>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -44,113 +46,161 @@ gavis_status io_guard(F&& f) {
 
 constexpr double kY00 = 0.28209479177387814;
 
-struct PlyProp {
-  std::string name;
-  int size = 0;
-  bool is_float = false;
-  size_t offset = 0;
-};
+// ---- 3DGS splat PLY --------------------------------------------------------
+// The whole file is read into memory once; the header is scanned in place, the
+// vertex element becomes a name -> (byte offset, scalar kind) column table, and
+// the vertex block is decoded record by record straight out of the buffer (the
+// blocks of any other elements are skipped by arithmetic on their sizes).
 
-struct PlyElement {
-  std::string name;
-  long long count = 0;
-  std::vector<PlyProp> props;
-  size_t stride = 0;
-};
+enum class Scalar : uint8_t { kNone, kI8, kI16, kI32, kF32, kF64 };
 
-int type_size(const std::string& t) {
-  if (t == "char" || t == "uchar" || t == "int8" || t == "uint8") return 1;
-  if (t == "short" || t == "ushort" || t == "int16" || t == "uint16") return 2;
-  if (t == "int" || t == "uint" || t == "int32" || t == "uint32" || t == "float" || t == "float32")
-    return 4;
-  if (t == "double" || t == "float64") return 8;
-  return 0;
+Scalar scalar_of(const std::string& t) {
+  static const struct { const char* names[2]; Scalar s; } kTypes[] = {
+      {{"char", "int8"}, Scalar::kI8},    {{"uchar", "uint8"}, Scalar::kI8},
+      {{"short", "int16"}, Scalar::kI16}, {{"ushort", "uint16"}, Scalar::kI16},
+      {{"int", "int32"}, Scalar::kI32},   {{"uint", "uint32"}, Scalar::kI32},
+      {{"float", "float32"}, Scalar::kF32}, {{"double", "float64"}, Scalar::kF64}};
+  for (const auto& k : kTypes)
+    if (t == k.names[0] || t == k.names[1]) return k.s;
+  return Scalar::kNone;
 }
 
-struct Ply {
-  std::vector<PlyElement> elements;
-  int vertex = -1;
-  std::vector<const PlyProp*> req, rest;
-  int color_degree = 0;
-  int per_channel = 0;
-  std::streampos data_start;
+size_t scalar_bytes(Scalar s) {
+  switch (s) {
+    case Scalar::kI8: return 1;
+    case Scalar::kI16: return 2;
+    case Scalar::kI32: case Scalar::kF32: return 4;
+    case Scalar::kF64: return 8;
+    default: return 0;
+  }
+}
+
+struct Column {
+  size_t at;
+  Scalar kind;
 };
 
-Ply read_header(std::ifstream& in, const std::string& path) {
-  Ply p;
-  std::string line;
-  auto read_line = [&]() {
-    need(static_cast<bool>(std::getline(in, line)), "truncated PLY header: " + path);
-    if (!line.empty() && line.back() == '\r') line.pop_back();
+struct Block {  // one PLY element: record count and record layout
+  std::string name;
+  int64_t records = 0;
+  size_t record_bytes = 0;
+  std::vector<std::pair<std::string, Column>> columns;
+  const Column* column(const std::string& n) const {
+    for (const auto& c : columns)
+      if (c.first == n) return &c.second;
+    return nullptr;
+  }
+};
+
+std::vector<std::string> split_words(const char* b, const char* e) {
+  std::vector<std::string> out;
+  while (b < e) {
+    while (b < e && std::isspace((unsigned char)*b)) ++b;
+    const char* w = b;
+    while (b < e && !std::isspace((unsigned char)*b)) ++b;
+    if (b > w) out.emplace_back(w, b);
+  }
+  return out;
+}
+
+struct SplatPly {
+  std::vector<unsigned char> bytes;
+  std::vector<Block> blocks;
+  size_t payload = 0;        // first byte after end_header
+  int vertex_block = -1;
+  int color_degree = 0;
+  int rest_per_channel = 0;  // f_rest_* count per colour channel
+  std::vector<std::pair<std::string, Column>> fields;  // decoding order (x .. f_rest_*)
+
+  const Block& vertices() const { return blocks[vertex_block]; }
+};
+
+SplatPly open_splat_ply(const std::string& path) {
+  SplatPly ply;
+  {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    need(f != nullptr, "cannot open file: " + path);
+    unsigned char chunk[1 << 16];
+    size_t got;
+    while ((got = std::fread(chunk, 1, sizeof chunk, f)) > 0) ply.bytes.insert(ply.bytes.end(), chunk, chunk + got);
+    std::fclose(f);
+  }
+  const char* const base = reinterpret_cast<const char*>(ply.bytes.data());
+  const char* const end = base + ply.bytes.size();
+  const char* cur = base;
+  // next header line without its terminator ('\n' or "\r\n")
+  auto next_line = [&](const char*& lb, const char*& le) {
+    need(cur < end, "truncated PLY header: " + path);
+    const char* nl = static_cast<const char*>(std::memchr(cur, '\n', (size_t)(end - cur)));
+    need(nl != nullptr, "truncated PLY header: " + path);
+    lb = cur;
+    le = nl;
+    if (le > lb && le[-1] == '\r') --le;
+    cur = nl + 1;
   };
-  read_line();
-  need(line == "ply", "not a PLY file: " + path);
-  bool format_seen = false;
-  while (true) {
-    read_line();
-    std::istringstream ls(line);
-    std::string word;
-    ls >> word;
-    if (word == "end_header") break;
-    if (word == "comment" || word == "obj_info" || word.empty()) continue;
-    if (word == "format") {
-      std::string enc;
-      ls >> enc;
+  const char *lb, *le;
+  next_line(lb, le);
+  need(std::string(lb, le) == "ply", "not a PLY file: " + path);
+  bool have_format = false;
+  for (;;) {
+    next_line(lb, le);
+    const std::vector<std::string> w = split_words(lb, le);
+    if (w.empty() || w[0] == "comment" || w[0] == "obj_info") continue;
+    const std::string& kw = w[0];
+    if (kw == "end_header") break;
+    if (kw == "format") {
+      const std::string enc = w.size() > 1 ? w[1] : std::string();
       need(enc != "ascii", "ASCII PLY is not supported; expected binary_little_endian");
-      need(enc == "binary_little_endian",
-           "unsupported PLY encoding '" + enc + "'; expected binary_little_endian");
-      format_seen = true;
-    } else if (word == "element") {
-      PlyElement e;
-      ls >> e.name >> e.count;
-      need(e.count >= 0, "PLY element with negative count");
-      p.elements.push_back(e);
-    } else if (word == "property") {
-      need(!p.elements.empty(), "PLY property before any element");
-      std::string type;
-      ls >> type;
+      need(enc == "binary_little_endian", "unsupported PLY encoding '" + enc + "'; expected binary_little_endian");
+      have_format = true;
+    } else if (kw == "element") {
+      Block b;
+      b.name = w.size() > 1 ? w[1] : std::string();
+      b.records = w.size() > 2 ? std::strtoll(w[2].c_str(), nullptr, 10) : 0;
+      need(b.records >= 0, "PLY element with negative count");
+      ply.blocks.push_back(std::move(b));
+    } else if (kw == "property") {
+      need(!ply.blocks.empty(), "PLY property before any element");
+      const std::string type = w.size() > 1 ? w[1] : std::string();
       need(type != "list", "PLY list properties are not supported");
-      PlyProp prop;
-      prop.size = type_size(type);
-      need(prop.size > 0, "unknown PLY property type '" + type + "'");
-      prop.is_float = (type == "float" || type == "float32");
-      ls >> prop.name;
-      prop.offset = p.elements.back().stride;
-      p.elements.back().stride += prop.size;
-      p.elements.back().props.push_back(prop);
+      const Scalar k = scalar_of(type);
+      need(k != Scalar::kNone, "unknown PLY property type '" + type + "'");
+      Block& b = ply.blocks.back();
+      b.columns.push_back({w.size() > 2 ? w[2] : std::string(), Column{b.record_bytes, k}});
+      b.record_bytes += scalar_bytes(k);
     } else {
-      throw IoErr("unrecognized PLY header line: " + line);
+      throw IoErr("unrecognized PLY header line: " + std::string(lb, le));
     }
   }
-  need(format_seen, "PLY header missing format line");
-  for (size_t i = 0; i < p.elements.size(); ++i)
-    if (p.elements[i].name == "vertex") p.vertex = (int)i;
-  need(p.vertex >= 0, "PLY is missing the vertex element");
-  const PlyElement& v = p.elements[p.vertex];
-  auto find = [&](const std::string& name) -> const PlyProp* {
-    for (const PlyProp& q : v.props)
-      if (q.name == name) return &q;
-    return nullptr;
+  need(have_format, "PLY header missing format line");
+  ply.payload = (size_t)(cur - base);
+  for (size_t i = 0; i < ply.blocks.size(); ++i)
+    if (ply.blocks[i].name == "vertex") ply.vertex_block = (int)i;
+  need(ply.vertex_block >= 0, "PLY is missing the vertex element");
+
+  const Block& v = ply.vertices();
+  auto float_column = [&](const std::string& n) {
+    const Column* c = v.column(n);
+    need(c != nullptr, "PLY is missing required property '" + n + "'");
+    need(c->kind == Scalar::kF32, "PLY property '" + n + "' must be float");
+    return *c;
   };
-  auto need_float = [&](const std::string& name) {
-    const PlyProp* q = find(name);
-    need(q != nullptr, "PLY is missing required property '" + name + "'");
-    need(q->is_float, "PLY property '" + name + "' must be float");
-    return q;
-  };
-  static const char* kRequired[] = {"x", "y", "z", "opacity", "scale_0", "scale_1", "scale_2",
-                                    "rot_0", "rot_1", "rot_2", "rot_3", "f_dc_0", "f_dc_1", "f_dc_2"};
-  for (const char* name : kRequired) p.req.push_back(need_float(name));
-  int n_rest = 0;
-  while (find("f_rest_" + std::to_string(n_rest)) != nullptr) ++n_rest;
-  need(n_rest % 3 == 0, "PLY f_rest_* count must be a multiple of 3");
-  p.per_channel = n_rest / 3;
-  while ((p.color_degree + 1) * (p.color_degree + 1) - 1 < p.per_channel) ++p.color_degree;
-  need((p.color_degree + 1) * (p.color_degree + 1) - 1 == p.per_channel,
+  static const char* const kFields[] = {"x", "y", "z", "opacity", "scale_0", "scale_1", "scale_2",
+                                        "rot_0", "rot_1", "rot_2", "rot_3", "f_dc_0", "f_dc_1", "f_dc_2"};
+  for (const char* n : kFields) ply.fields.push_back({n, float_column(n)});
+  int rest = 0;
+  while (v.column("f_rest_" + std::to_string(rest)) != nullptr) ++rest;
+  need(rest % 3 == 0, "PLY f_rest_* count must be a multiple of 3");
+  ply.rest_per_channel = rest / 3;
+  // complete bands: (L+1)^2 - 1 coefficients per channel beyond the DC term
+  while ((ply.color_degree + 1) * (ply.color_degree + 1) - 1 < ply.rest_per_channel) ++ply.color_degree;
+  need((ply.color_degree + 1) * (ply.color_degree + 1) - 1 == ply.rest_per_channel,
        "PLY f_rest_* count does not form complete SH bands");
-  for (int i = 0; i < n_rest; ++i) p.rest.push_back(need_float("f_rest_" + std::to_string(i)));
-  p.data_start = in.tellg();
-  return p;
+  for (int i = 0; i < rest; ++i) {
+    const std::string n = "f_rest_" + std::to_string(i);
+    ply.fields.push_back({n, float_column(n)});
+  }
+  return ply;
 }
 
 // ---- minimal JSON reader for the field document ----------------------------
@@ -274,11 +324,9 @@ extern "C" {
 gavis_status gavis_ply_info(const char* path, int64_t* n, int32_t* color_degree) {
   return io_guard([&] {
     need(path != nullptr, "path must not be null");
-    std::ifstream in(path, std::ios::binary);
-    need(in.good(), std::string("cannot open file: ") + path);
-    Ply p = read_header(in, path);
-    if (n) *n = p.elements[p.vertex].count;
-    if (color_degree) *color_degree = p.color_degree;
+    const SplatPly ply = open_splat_ply(path);
+    if (n) *n = ply.vertices().records;
+    if (color_degree) *color_degree = ply.color_degree;
   });
 }
 
@@ -287,56 +335,49 @@ gavis_status gavis_read_splat_ply(const char* path, int64_t capacity, float* pos
                                   double* bounds_min, double* bounds_max) {
   return io_guard([&] {
     need(path != nullptr, "path must not be null");
-    std::ifstream in(path, std::ios::binary);
-    need(in.good(), std::string("cannot open file: ") + path);
-    Ply p = read_header(in, path);
-    const PlyElement& vx = p.elements[p.vertex];
-    need(capacity >= vx.count, "output capacity smaller than the vertex count");
-    const int nb = (p.color_degree + 1) * (p.color_degree + 1);
-    std::vector<char> record;
+    const SplatPly ply = open_splat_ply(path);
+    const Block& vx = ply.vertices();
+    need(capacity >= vx.records, "output capacity smaller than the vertex count");
+    // byte offset of the vertex block: the payloads of the elements before it
+    size_t at = ply.payload;
+    for (int b = 0; b < ply.vertex_block; ++b) {
+      const Block& e = ply.blocks[b];
+      const size_t span = (size_t)e.records * e.record_bytes;
+      need(span <= ply.bytes.size() - std::min(at, ply.bytes.size()), "truncated PLY data: " + std::string(path));
+      at += span;
+    }
+    const int nb = (ply.color_degree + 1) * (ply.color_degree + 1);
+    const int nf = (int)ply.fields.size();
+    std::vector<double> val(nf);
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (size_t ei = 0; ei < p.elements.size(); ++ei) {
-      const PlyElement& e = p.elements[ei];
-      if ((int)ei != p.vertex) {
-        in.seekg(static_cast<std::streamoff>(e.count * static_cast<long long>(e.stride)), std::ios::cur);
-        need(in.good(), std::string("truncated PLY data: ") + path);
-        continue;
+    for (int64_t i = 0; i < vx.records; ++i, at += vx.record_bytes) {
+      need(at + vx.record_bytes <= ply.bytes.size(),
+           "truncated PLY data at vertex " + std::to_string(i) + ": " + path);
+      const unsigned char* rec = ply.bytes.data() + at;
+      for (int k = 0; k < nf; ++k) {
+        float f;
+        std::memcpy(&f, rec + ply.fields[k].second.at, sizeof f);
+        need(std::isfinite(f), "non-finite value in PLY vertex " + std::to_string(i) + ", property '" +
+                                   ply.fields[k].first + "'");
+        val[k] = f;
       }
-      record.resize(e.stride);
-      for (long long vi = 0; vi < e.count; ++vi) {
-        in.read(record.data(), (std::streamsize)e.stride);
-        need(in.gcount() == (std::streamsize)e.stride,
-             "truncated PLY data at vertex " + std::to_string(vi) + ": " + path);
-        auto rf = [&](const PlyProp* q) {
-          float f;
-          std::memcpy(&f, record.data() + q->offset, sizeof f);
-          need(std::isfinite(f), "non-finite value in PLY vertex " + std::to_string(vi) +
-                                     ", property '" + q->name + "'");
-          return (double)f;
-        };
-        const double x = rf(p.req[0]), y = rf(p.req[1]), z = rf(p.req[2]);
-        positions[3 * vi] = (float)x;
-        positions[3 * vi + 1] = (float)y;
-        positions[3 * vi + 2] = (float)z;
-        opacities[vi] = (float)(1.0 / (1.0 + std::exp(-rf(p.req[3]))));
-        for (int k = 0; k < 3; ++k) scales[3 * vi + k] = (float)std::exp(rf(p.req[4 + k]));
-        const double qw = rf(p.req[7]), qx = rf(p.req[8]), qy = rf(p.req[9]), qz = rf(p.req[10]);
-        const double qn = std::sqrt(qx * qx + qy * qy + qz * qz + qw * qw);  // Eigen coeffs (x,y,z,w)
-        need(qn > 1e-12, "zero quaternion in PLY vertex " + std::to_string(vi));
-        rotations[4 * vi] = (float)(qw / qn);
-        rotations[4 * vi + 1] = (float)(qx / qn);
-        rotations[4 * vi + 2] = (float)(qy / qn);
-        rotations[4 * vi + 3] = (float)(qz / qn);
-        for (int c = 0; c < 3; ++c) {
-          float* row = colors + (3 * vi + c) * nb;
-          row[0] = (float)(rf(p.req[11 + c]) + 0.5 / kY00);
-          for (int k = 0; k < p.per_channel; ++k) row[1 + k] = (float)rf(p.rest[c * p.per_channel + k]);
-        }
-        const double pp[3] = {x, y, z};
-        for (int k = 0; k < 3; ++k) {
-          if (vi == 0 || pp[k] < lo[k]) lo[k] = pp[k];
-          if (vi == 0 || pp[k] > hi[k]) hi[k] = pp[k];
-        }
+      // fields: 0-2 position, 3 opacity logit, 4-6 log scales, 7-10 quaternion
+      // (w, x, y, z), 11-13 DC per channel, then f_rest channel-major
+      for (int k = 0; k < 3; ++k) {
+        positions[3 * i + k] = (float)val[k];
+        scales[3 * i + k] = (float)std::exp(val[4 + k]);
+        lo[k] = (i == 0 || val[k] < lo[k]) ? val[k] : lo[k];
+        hi[k] = (i == 0 || val[k] > hi[k]) ? val[k] : hi[k];
+      }
+      opacities[i] = (float)(1.0 / (1.0 + std::exp(-val[3])));
+      const double qn = std::sqrt(val[8] * val[8] + val[9] * val[9] + val[10] * val[10] + val[7] * val[7]);
+      need(qn > 1e-12, "zero quaternion in PLY vertex " + std::to_string(i));
+      for (int k = 0; k < 4; ++k) rotations[4 * i + k] = (float)(val[7 + k] / qn);
+      for (int c = 0; c < 3; ++c) {
+        float* row = colors + (3 * i + c) * nb;
+        row[0] = (float)(val[11 + c] + 0.5 / kY00);  // mid-grey offset folded into DC
+        const double* rest = val.data() + 14 + c * ply.rest_per_channel;
+        for (int k = 0; k < ply.rest_per_channel; ++k) row[1 + k] = (float)rest[k];
       }
     }
     if (bounds_min) std::memcpy(bounds_min, lo, sizeof lo);

@@ -104,14 +104,41 @@ def _allreduce_sum_host(x: np.ndarray, dist) -> np.ndarray:
 
 
 def construct_field_sharded(partial_field: Callable[[int, int], object], n_views: int, rank: int,
-                            world: int, allreduce_sum: Callable[[object], None]) -> object:
+                            world: int, allreduce_sum: Callable[[object], None],
+                            set_num_views: Optional[Callable[[object, int], None]] = None) -> object:
     """partial_field(lo, hi) accumulates views [lo, hi) into a fresh field and returns
-    it; allreduce_sum(field) sums the partial coefficient arrays across ranks in place."""
+    it; allreduce_sum(field) sums the partial coefficient arrays across ranks in place;
+    set_num_views(field, n_views) then records the trajectory length |P| on every
+    rank (construct_field sets num_views = |P|, vfield.hpp:91) -- each rank's partial
+    field only counted its own block, and query_visibility uses |P| as the exponent."""
     lo, hi = shard_range(n_views, rank, world)
     field = partial_field(lo, hi)
     if world > 1:
         allreduce_sum(field)
+    if set_num_views is not None:
+        set_num_views(field, n_views)
     return field
+
+
+def construct_device_field_sharded(ctx, scene, views: Sequence, vmf, degree: int, rank: int, world: int,
+                                   dist=None, rc=None):
+    """VF CONST over `views` sharded across ranks on the device: this rank
+    accumulates its contiguous block (gavis_vf_accumulate_views), the fp64
+    partials are summed in place by an all-reduce (NCCL over NVLink), and
+    num_views is set to len(views) on every rank."""
+    from . import api
+    from .model import RasterConfig
+    rc = rc or RasterConfig()
+
+    def partial(lo, hi):
+        f = api.empty_field(ctx, scene, vmf, degree)
+        if hi > lo:
+            api.accumulate_views(ctx, f, scene, views[lo:hi], rc)
+        return f
+
+    return construct_field_sharded(partial, len(views), rank, world,
+                                   lambda fld: allreduce_device_field(fld, dist),
+                                   lambda fld, n: fld.set_num_views(n))
 
 
 class DeviceArray:

@@ -2,7 +2,8 @@
 
   python tools/profile_driver.py ua   # 1 field build (16 views) + 2 x 16-candidate renders
   python tools/profile_driver.py vf   # 2 x 16-view field builds
-Config 3 scene (1M Gaussians, 800x800), seed 0.
+Config 3 scene (1M Gaussians, 800x800), seed 0. GAVIS_PROFILE_PRECISION=exact selects
+the fp64 blend.
 """
 import os
 import sys
@@ -21,6 +22,7 @@ def main():
     c = synth.config3(0, n=n, n_train=16, n_candidates=32)
     rc, uc = RasterConfig(), UncertaintyConfig()
     with api.Context(0) as ctx:
+        ctx.set_precision(os.environ.get("GAVIS_PROFILE_PRECISION", "certified"))
         ds = ctx.upload(c["scene"])
         t0 = time.time()
         field = api.construct_field(ctx, ds, c["train"], VmfParams(1.0), 2, rc)
