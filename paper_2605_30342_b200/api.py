@@ -25,7 +25,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import _native as N
-from .model import (CameraView, EntropyMap, MappingLog, MappingStep, NbvResult, OccluderSet, ParameterError,
+from .model import (CameraView, EntropyMap, InvariantError, MappingLog, MappingStep, NbvResult, OccluderSet, ParameterError,
                     PlannerConfig, RasterConfig, RenderOutput, Scene, UncertaintyConfig, ViewQuery,
                     VisibilityField, VmfParams, require)
 
@@ -255,6 +255,17 @@ def _as_dev(ctx: Context, scene) -> DeviceScene:
     return scene if isinstance(scene, DeviceScene) else ctx.upload(scene)
 
 
+def _splat_vis(vis_by_particle, n: int):
+    """Per-particle visibility for render_entropy_core: one entry per particle
+    (the reference checks splat_vis against its splats, uncertainty.hpp:133-134)."""
+    if vis_by_particle is None:
+        return None
+    v = np.ascontiguousarray(vis_by_particle, np.float64).reshape(-1)
+    if v.size != n:
+        raise InvariantError(f"render_entropy_core: visibility has {v.size} entries, the scene {n} particles")
+    return v if v.size else np.zeros(1)
+
+
 # ----------------------------------------------------------------- VF CONST
 def construct_field(ctx: Context, scene, views: Sequence[CameraView], vmf: VmfParams, degree: int,
                     rc: RasterConfig = RasterConfig()) -> DeviceField:
@@ -283,13 +294,21 @@ def accumulate_views(ctx: Context, field: DeviceField, scene, views: Sequence[Ca
 
 def accumulate_view(ctx: Context, field: DeviceField, scene, view: CameraView, visibility) -> None:
     ds = _as_dev(ctx, scene)
-    v = np.ascontiguousarray(visibility, np.float64)
+    v = np.ascontiguousarray(visibility, np.float64).reshape(-1)
+    require(v.size == ds.n, f"accumulate_view: visibility has {v.size} entries, the scene {ds.n} particles")
+    if v.size == 0:
+        v = np.zeros(1)
     N.check(ctx.lib.gavis_vf_accumulate_visibility(ctx.h, field.h, ds.h, C.byref(camera_c(view)), _ptr(v)))
 
 
 def upload_field(ctx: Context, scene, field: VisibilityField) -> DeviceField:
     ds = _as_dev(ctx, scene)
     g = np.ascontiguousarray(field.gamma, np.float64)
+    nb = (int(field.degree) + 1) ** 2
+    require(g.shape == (ds.n, nb), f"upload_field: gamma has shape {g.shape}, expected ({ds.n}, {nb}) "
+            f"for {ds.n} particles at degree {field.degree}")
+    if g.size == 0:
+        g = np.zeros((1, nb))
     h = C.c_void_p()
     N.check(ctx.lib.gavis_vf_upload(ctx.h, ds.h, C.c_double(field.vmf.kappa), C.c_int32(field.degree),
                                     C.c_int32(field.num_views), _ptr(g), C.byref(h)))
@@ -380,9 +399,7 @@ def render(ctx: Context, scene, field: Optional[DeviceField], cams: Sequence[Cam
     o.entropy_contributors = _ptr(buf("entropy_contributors", contributors and (entropy or scores), P, np.int32))
     o.with_rgb = 1 if with_rgb else 0
     o.with_entropy = 0
-    vis = None if splat_visibility is None else np.ascontiguousarray(splat_visibility, np.float64)
-    if vis is not None and vis.size == 0:
-        vis = np.zeros(1)
+    vis = _splat_vis(splat_visibility, ds.n)
     arr = cameras_c(cams)
     N.check(ctx.lib.gavis_ua_render(ctx.h, ds.h, field.h if field is not None else None, _ptr(vis), arr,
                                     C.c_int32(len(cams)), C.byref(raster_c(rc)), C.byref(unc_c(uc)),
@@ -401,9 +418,7 @@ def render_mixtures(ctx: Context, scene, field: Optional[DeviceField], cam: Came
     P = cam.width * cam.height
     off = np.zeros(P + 1, np.int64)
     prior, resid, H = np.zeros(max(1, P)), np.zeros(max(1, P)), np.zeros(max(1, P))
-    vis = None if splat_visibility is None else np.ascontiguousarray(splat_visibility, np.float64)
-    if vis is not None and vis.size == 0:
-        vis = np.zeros(1)
+    vis = _splat_vis(splat_visibility, ds.n)
     cc = camera_c(cam)
     args = (ctx.h, ds.h, field.h if field is not None else None, _ptr(vis), C.byref(cc),
             C.byref(raster_c(rc)), C.byref(unc_c(uc)))

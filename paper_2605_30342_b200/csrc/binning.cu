@@ -173,6 +173,9 @@ Binned bin_batch(gavis_ctx* c, const gavis_scene* s, const gavis_camera* cams, i
       na.item_count = (int32_t*)c->buf("item_count", sizeof(int32_t) * (n_items + 1));
       int32_t* ioff = (int32_t*)c->buf("item_offset", sizeof(int32_t) * (n_items + 1));
       CK(cudaMemsetAsync(na.item_count + n_items, 0, sizeof(int32_t), c->stream));
+      na.scratch = is_b;  // free after the sort: merge buffer of the long tied runs
+      na.long_runs = (uint2*)c->buf("long_runs", sizeof(uint2) * (n_items / (kShortRun + 1) + 1));
+      na.n_long = (uint32_t*)c->buf("n_long", sizeof(uint32_t));
       c->run("depth_order", [&] { launch_depth_order(na, c->stream); });
       const size_t scb = scan_temp_bytes(n_items + 1);
       void* stmp = c->buf("scan_tmp", scb);

@@ -88,7 +88,14 @@ struct NarrowArgs {
   int32_t* slot_offset = nullptr;      // [V*N] pair offset of each visible slot
   const int64_t* chunk_tile_base = nullptr;  // [V] first tile of the view's sort chunk
   uint32_t* keys32 = nullptr;          // [K] tile ids relative to the chunk's first tile
+  uint32_t* scratch = nullptr;         // [n_items] merge buffer for long tied runs
+  uint2* long_runs = nullptr;          // [n_items / (kShortRun + 1) + 1] (start, length)
+  uint32_t* n_long = nullptr;          // long runs found (zeroed before depth_order)
 };
+
+// Runs of equal 32-bit item keys up to this length are ordered by one thread
+// (insertion sort); longer ones by a CTA each (depth_order_long_kernel).
+constexpr int kShortRun = 32;
 
 struct RangesArgs {
   const DevCam* cams = nullptr;

@@ -6,6 +6,8 @@
 // direction (vfield.hpp:96-112 via uncertainty.hpp:251-257). One thread per
 // Gaussian projects it into all V views of the batch, so the particle record
 // and its SH field row are read from HBM once per batch, not once per view.
+#include <math_constants.h>
+
 #include "kernels.h"
 
 #include <cstdio>
@@ -467,32 +469,129 @@ __global__ void ranges_kernel(RangesArgs a) {
 
 
 
-// K2c: runs of equal fp32 keys ordered by (fp64 depth, index) by the thread at
-// the run's start (the stable sort left them in index order); then every item's
-// tile count, in depth order, for the pair-offset scan.
+// K2c: runs of equal 32-bit item keys ordered by (fp64 depth, index). K1 appends
+// the visible items with warp-aggregated atomics, so a run arrives in scheduling
+// order, not index order: a run of L items can hold O(L^2) inversions (exact
+// depth ties, e.g. an axis-aligned camera facing an axis-aligned wall). Runs of
+// at most kShortRun items are insertion-sorted by the thread at the run's start;
+// longer runs are queued and sorted by depth_order_long_kernel, one CTA per run.
 __global__ void depth_order_kernel(NarrowArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n_items) return;
   const uint32_t key = a.item_key[i];
   const bool run_start = i + 1 < a.n_items && a.item_key[i + 1] == key &&
                          (i == 0 || a.item_key[i - 1] != key);
-  if (run_start) {
-    int64_t j = i;
-    while (j + 1 < a.n_items && a.item_key[j + 1] == key) ++j;
-    uint32_t* sl = a.item_slot_sorted;
-    for (int64_t x = i + 1; x <= j; ++x) {
-      const uint32_t sx = sl[x];
-      const double dx = a.geo[sx].depth;
-      int64_t y = x - 1;
-      while (y >= i) {
-        const uint32_t sy = sl[y];
-        const double dy = a.geo[sy].depth;
-        if (dy < dx || (dy == dx && sy < sx)) break;  // same view: slot order = index order
-        sl[y + 1] = sy;
-        --y;
-      }
-      sl[y + 1] = sx;
+  if (!run_start) return;
+  int64_t j = i;
+  while (j + 1 < a.n_items && a.item_key[j + 1] == key) ++j;
+  if (j - i + 1 > kShortRun) {
+    const uint32_t r = atomicAdd(a.n_long, 1u);
+    a.long_runs[r] = make_uint2((uint32_t)i, (uint32_t)(j - i + 1));
+    return;
+  }
+  uint32_t* sl = a.item_slot_sorted;
+  for (int64_t x = i + 1; x <= j; ++x) {
+    const uint32_t sx = sl[x];
+    const double dx = a.geo[sx].depth;
+    int64_t y = x - 1;
+    while (y >= i) {
+      const uint32_t sy = sl[y];
+      const double dy = a.geo[sy].depth;
+      if (dy < dx || (dy == dx && sy < sx)) break;  // same view: slot order = index order
+      sl[y + 1] = sy;
+      --y;
     }
+    sl[y + 1] = sx;
+  }
+}
+
+namespace {
+constexpr int kLongChunk = 2048;  // elements bitonic-sorted in shared memory per step
+
+// (depth, slot) strict order; slots are distinct inside a run (one view).
+__device__ __forceinline__ bool item_before(double da, uint32_t sa, double db, uint32_t sb) {
+  return da < db || (da == db && sa < sb);
+}
+}  // namespace
+
+// K2c': one CTA per long tied run (grid-stride over the queue, no host read of
+// its length). Chunks of 2048 items are bitonic-sorted in shared memory, then
+// merged pairwise through the scratch buffer: every item's output position is
+// its index in its own half plus the number of items of the other half that
+// precede it (a binary search; the keys are distinct, so no tie rule is needed).
+__global__ void __launch_bounds__(256) depth_order_long_kernel(NarrowArgs a) {
+  __shared__ double s_d[kLongChunk];
+  __shared__ uint32_t s_s[kLongChunk];
+  const int nruns = (int)*a.n_long;
+  for (int r = blockIdx.x; r < nruns; r += gridDim.x) {
+    const uint2 run = a.long_runs[r];
+    uint32_t* const base = a.item_slot_sorted + run.x;
+    uint32_t* const alt = a.scratch + run.x;
+    const int L = (int)run.y;
+    for (int c0 = 0; c0 < L; c0 += kLongChunk) {
+      const int n = min(kLongChunk, L - c0);
+      int pw = 1;
+      while (pw < n) pw <<= 1;
+      for (int k = threadIdx.x; k < pw; k += blockDim.x) {
+        const uint32_t sl = k < n ? base[c0 + k] : 0xFFFFFFFFu;
+        s_s[k] = sl;
+        s_d[k] = k < n ? a.geo[sl].depth : CUDART_INF;
+      }
+      __syncthreads();
+      for (int size = 2; size <= pw; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int k = threadIdx.x; k < pw; k += blockDim.x) {
+            const int m = k ^ stride;
+            if (m > k) {
+              const bool up = (k & size) == 0;
+              const bool swap = up ? item_before(s_d[m], s_s[m], s_d[k], s_s[k])
+                                   : item_before(s_d[k], s_s[k], s_d[m], s_s[m]);
+              if (swap) {
+                const double td = s_d[k];
+                s_d[k] = s_d[m];
+                s_d[m] = td;
+                const uint32_t ts = s_s[k];
+                s_s[k] = s_s[m];
+                s_s[m] = ts;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int k = threadIdx.x; k < n; k += blockDim.x) base[c0 + k] = s_s[k];
+      __syncthreads();
+    }
+    uint32_t* src = base;
+    uint32_t* dst = alt;
+    for (int w = kLongChunk; w < L; w <<= 1) {
+      for (int k = threadIdx.x; k < L; k += blockDim.x) {
+        const int b0 = (k / (2 * w)) * (2 * w);
+        const int mid = min(b0 + w, L), end = min(b0 + 2 * w, L);
+        const uint32_t sk = src[k];
+        const double dk = a.geo[sk].depth;
+        const bool left = k < mid;
+        int lo = left ? mid : b0, hi = left ? end : mid;  // search the other half
+        const int own = left ? k - b0 : k - mid;
+        while (lo < hi) {  // first element of the other half not before (dk, sk)
+          const int h = (lo + hi) >> 1;
+          const uint32_t sh = src[h];
+          if (item_before(a.geo[sh].depth, sh, dk, sk))
+            lo = h + 1;
+          else
+            hi = h;
+        }
+        dst[b0 + own + (lo - (left ? mid : b0))] = sk;
+      }
+      __syncthreads();
+      uint32_t* t = src;
+      src = dst;
+      dst = t;
+    }
+    if (src != base) {
+      for (int k = threadIdx.x; k < L; k += blockDim.x) base[k] = src[k];
+    }
+    __syncthreads();
   }
 }
 
@@ -655,7 +754,9 @@ void launch_emit_keys(const EmitArgs& a, cudaStream_t s) {
 
 void launch_depth_order(const NarrowArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return;
+  cudaMemsetAsync(a.n_long, 0, sizeof(uint32_t), s);
   depth_order_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
+  depth_order_long_kernel<<<148, 256, 0, s>>>(a);
   item_counts_kernel<<<blocks_for(a.n_items, 256), 256, 0, s>>>(a);
 }
 

@@ -215,17 +215,23 @@ gavis_status gavis_vf_upload(gavis_ctx* c, const gavis_scene* s, double kappa, i
                              int32_t num_views, const double* gamma, gavis_field** out) {
   return guard([&] {
     require(c && s && out, "null argument");
+    require(s->dev.n == 0 || gamma != nullptr, "gamma must not be null");
+    require(num_views >= 0, "field: num_views must be non-negative");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
-    gavis_field* f = new_field(c, s, kappa, degree);
-    const int nb = (degree + 1) * (degree + 1);
-    if (f->n > 0) {
-      require(gamma != nullptr, "gamma must not be null");
-      CK(cudaMemcpyAsync(f->gamma, gamma, sizeof(double) * nb * f->n, cudaMemcpyHostToDevice,
-                         c->stream));
+    gavis_field* f = new_field(c, s, kappa, degree);  // validates degree and kappa
+    try {
+      const int nb = (degree + 1) * (degree + 1);
+      if (f->n > 0)
+        CK(cudaMemcpyAsync(f->gamma, gamma, sizeof(double) * nb * f->n, cudaMemcpyHostToDevice,
+                           c->stream));
+      f->num_views = num_views;
+      c->sync();
+    } catch (...) {
+      c->dfree(f->gamma);
+      delete f;
+      throw;
     }
-    f->num_views = num_views;
-    c->sync();
     *out = f;
   });
 }

@@ -120,6 +120,37 @@ def test_depth_ties_follow_index_order(ctx):
     assert list(ids[lo:hi]) == [0, 1, 2]
 
 
+def test_long_exact_depth_ties_across_blocks(ctx):
+    """K1 appends visible items in scheduling order, so a run of exactly
+    tied depths (an axis-aligned camera facing an axis-aligned wall) reaches the
+    depth-order pass unordered. 20 000 splats on the plane z = 5 seen head-on: one
+    tied run spanning many K1 blocks; the composite order must still be the
+    reference's (depth, index) order (raster.hpp:124-128), and the long-run path
+    must not serialise (one thread's insertion sort was O(L^2) here)."""
+    import time
+    rng = np.random.default_rng(7)
+    n = 20000
+    perm = rng.permutation(n)  # index order unrelated to position
+    xs = np.linspace(-2.4, 2.4, 142)
+    grid = np.array([(x, y) for x in xs for y in xs])[perm[:n] % (142 * 142)]
+    parts = [synth.make_particle((float(grid[i, 0]), float(grid[i, 1]), 5.0), float(rng.uniform(0.04, 0.12)),
+                                 float(rng.uniform(0.2, 0.9)), tuple(float(c) for c in rng.uniform(0, 1, 3)))
+             for i in range(n)]
+    sc = Scene.from_particles(parts, 0)
+    cam = make_lookat((0, 0, 0), (0, 0, 1), (0, 1, 0), 256, 256)
+    ds = ctx.upload(sc)
+    api.render(ctx, ds, None, [cam], RC, UC, rgb=True)  # warm-up (buffers)
+    t0 = time.perf_counter()
+    out = api.render(ctx, ds, None, [cam, cam], RC, UC, rgb=True, contributors=True)
+    dt = time.perf_counter() - t0
+    rgb, _, _, cc = O.rasterize(O.OracleScene(sc), cam, RC, contrib=True)
+    P = cam.width * cam.height
+    for k in range(2):
+        assert np.array_equal(out["rgb_contributors"][k * P:(k + 1) * P], cc)
+        assert np.max(np.abs(out["rgb"][3 * k * P:3 * (k + 1) * P] - rgb)) <= 1e-5
+    assert dt < 1.0, f"tied-run ordering took {dt:.2f} s"
+
+
 # ------------------------------------------------------------------ VF CONST
 @pytest.mark.parametrize("tile", [16, 5, 32])
 def test_single_view_visibility_parity(ctx, tile):
@@ -535,3 +566,23 @@ def test_high_degree_fields(ctx, degree):
     H, _, _, cc = O.render_entropy(osc, og, degree, len(views), cam, RC, UC, contrib=True)
     assert np.array_equal(r["entropy_contributors"], cc)
     assert np.max(np.abs(r["entropy"] - H)) <= 2e-5
+
+
+def test_host_array_lengths_are_checked(ctx):
+    """short host arrays are rejected before the C ABI reads them
+    (the reference checks splat_vis against its splats, uncertainty.hpp:133-134)."""
+    c = synth.config1(0)
+    sc = c["scene"]
+    cam = c["train"][0]
+    ds = ctx.upload(sc)
+    f = api.empty_field(ctx, ds, VmfParams(1.0), 2)
+    with pytest.raises(ParameterError):
+        api.accumulate_view(ctx, f, ds, cam, np.ones(sc.num_particles - 1))
+    bad = f.download()
+    bad.gamma = bad.gamma[:-1]
+    with pytest.raises(ParameterError):
+        api.upload_field(ctx, ds, bad)
+    with pytest.raises(InvariantError):
+        api.render_entropy_core(ctx, ds, cam, RC, UC, np.ones(5))
+    with pytest.raises(InvariantError):
+        api.render(ctx, ds, None, [cam], RC, UC, entropy=True, splat_visibility=[])
