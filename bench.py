@@ -672,10 +672,15 @@ def oracle_gate(args, ctx, api, c, ds, field, cands, rc, uc):
             "rgb_max_abs": float(np.max(np.abs(r["rgb"] - o_rgb))),
             "entropy_max_abs": float(np.max(np.abs(r["entropy"] - o_H)))}
     ctx.set_precision(prev)
+    # scores: 1e-6 relative for the fp64 path; the certified path's fp32 transmittance
+    # products carry ~k 2^-24 relative rounding over k ~ 60 composited entries, so
+    # its scores are held to 1e-5 (its argmax is re-certified in fp64)
+    tol = {"exact": 1e-6, "certified": 1e-5}
+    gate["scores_rel_tolerance"] = tol
     gate["pass"] = bool(gate["field_2views_gamma_max_rel"] <= 1e-5 and all(
         gate[p]["oracle_argmax_equal"] and gate[p]["rgb_contributors_equal"] and
         gate[p]["entropy_contributors_equal"] and gate[p]["rgb_max_abs"] <= 1e-4 and
-        gate[p]["entropy_max_abs"] <= 1e-4 and gate[p]["oracle_scores_max_rel"] <= 1e-6
+        gate[p]["entropy_max_abs"] <= 1e-4 and gate[p]["oracle_scores_max_rel"] <= tol[p]
         for p in ("exact", "certified")))
     return gate, cpu
 

@@ -10,8 +10,9 @@ through the C ABI against the CPU oracle on the same seeded fp32 inputs:
     uncertainty.hpp:124-278, planner.hpp:117-137) of 2 candidates (1 at config 4)
     with the device's full field (all training views) handed to the oracle:
     contributor counts of both tracks bit-exact, images within 1e-4 max-abs,
-    scores within 1e-6 relative, the argmax identical -- for both device
-    precisions (fp64 blend, and certified fp32 blend + fp64 redo).
+    scores within 1e-6 relative (fp64 blend) / 1e-5 (certified fp32 blend + fp64
+    redo: its fp32 transmittance products carry ~k 2^-24 relative rounding over
+    k ~ 60 composited entries), the argmax identical -- for both precisions.
 
 These are the scale-only risks the small-config tests cannot see: the table-driven
 exp/log at millions of pairs, pair-budget re-binning, 32-bit pair/pixel indexing,
@@ -115,9 +116,10 @@ def test_candidates_with_full_field(setup, precision):
         assert np.max(np.abs(out["rgb"][3 * off:3 * (off + P)] - o_rgb)) <= 1e-4
         assert np.max(np.abs(out["entropy"][off:off + P] - o_H)) <= 1e-4
         off += P
+    tol = 1e-6 if precision == "exact" else 1e-5
     rel = np.max(np.abs(out["scores"] - o_scores) / np.abs(o_scores))
-    assert rel <= 1e-6, f"config {cfg} {precision}: scores rel {rel}"
-    assert np.max(np.abs(nbv.scores - o_scores) / np.abs(o_scores)) <= 1e-6
+    assert rel <= tol, f"config {cfg} {precision}: scores rel {rel}"
+    assert np.max(np.abs(nbv.scores - o_scores) / np.abs(o_scores)) <= tol
     assert nbv.best_index == o_best
 
 
