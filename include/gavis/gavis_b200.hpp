@@ -20,6 +20,7 @@
 // (device 0, or set_default_device()).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -135,12 +136,24 @@ struct VmfParams {
   }
 };
 
-// uncertainty.hpp:24-52 (constant provider, no correlation hook)
+// uncertainty.hpp:21-22
+enum class VarianceProvider { kConstant, kShPropagation };
+enum class CorrelationMode { kNone, kHook };
+
+// uncertainty.hpp:24-52
 struct UncertaintyConfig {
   double beta = 0.5;
-  double prior_opacity = 0.15;
-  Mat3 prior_cov;
-  double color_sigma = 0.1;
+  double prior_opacity = 0.15;           // o_0
+  Mat3 prior_cov;                        // Q_0 (identity)
+  double color_sigma = 0.1;              // Q_c = sigma^2 I under kConstant
+  VarianceProvider variance_provider = VarianceProvider::kConstant;
+  CorrelationMode correlation = CorrelationMode::kNone;
+  double correlation_lambda = 1.0;
+  // Only mixture dumps read the prior mean (uncertainty.hpp:32-34).
+  Vec3 prior_mean = Vec3(0.5, 0.5, 0.5);
+  // Per-particle per-channel SH coefficient variances for kShPropagation
+  // (uncertainty.hpp:35-37): [N][3][(Lv+1)^2], Lv <= 4 on the device.
+  const std::vector<std::array<std::vector<double>, 3>>* coeff_variances = nullptr;
 };
 
 // vfield.hpp:21-33
@@ -233,7 +246,9 @@ inline gavis_uncertainty_config uc_c(const UncertaintyConfig& u) {
   g.prior_opacity = u.prior_opacity;
   g.color_sigma = u.color_sigma;
   for (int i = 0; i < 9; ++i) g.prior_cov[i] = u.prior_cov.m[i];
-  g.correlation_lambda = 1.0;
+  g.variance_provider = u.variance_provider == VarianceProvider::kShPropagation ? 1 : 0;
+  g.correlation = u.correlation == CorrelationMode::kHook ? 1 : 0;
+  g.correlation_lambda = u.correlation_lambda;
   return g;
 }
 
@@ -277,6 +292,27 @@ inline std::unique_ptr<DeviceScene> upload(const Scene& s) {
   auto ds = std::make_unique<DeviceScene>();
   check(gavis_scene_upload(holder().get(), &d, &ds->h));
   return ds;
+}
+
+// UncertaintyConfig::coeff_variances -> the device scene (kShPropagation).
+inline void attach_variances(const UncertaintyConfig& uc, gavis_scene* s, std::size_t n) {
+  if (uc.variance_provider != VarianceProvider::kShPropagation) return;
+  if (uc.coeff_variances == nullptr)
+    throw ParameterError("variance_provider sh_propagation requires coeff_variances");
+  const auto& cv = *uc.coeff_variances;
+  if (cv.size() != n) throw ParameterError("coeff_variances: one entry per particle");
+  const std::size_t nb = n ? cv[0][0].size() : 1;
+  int deg = 0;
+  while ((std::size_t)((deg + 1) * (deg + 1)) < nb) ++deg;
+  if ((std::size_t)((deg + 1) * (deg + 1)) != nb)
+    throw ParameterError("coeff_variances: channel rows must hold complete SH bands");
+  std::vector<float> flat(n * 3 * nb);
+  for (std::size_t i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) {
+      if (cv[i][c].size() != nb) throw ParameterError("coeff_variances: ragged channel rows");
+      for (std::size_t k = 0; k < nb; ++k) flat[(i * 3 + c) * nb + k] = (float)cv[i][c][k];
+    }
+  check(gavis_scene_set_coeff_variances(holder().get(), s, flat.empty() ? nullptr : flat.data(), deg));
 }
 
 struct DeviceField {
@@ -436,6 +472,7 @@ inline EntropyMap render_entropy(const Scene& scene, const VisibilityField& fiel
   if (field.num_particles != scene.particles.size())
     throw ParameterError("render_entropy: field was built for a different scene");
   auto ds = detail::upload(scene);
+  detail::attach_variances(uc, ds->h, scene.particles.size());
   auto df = detail::upload_field(field, *ds);
   const gavis_camera c = detail::cam_c(cam);
   const gavis_raster_config r = detail::rc_c(rc);
@@ -480,13 +517,22 @@ inline EntropyMap render_entropy(const Scene& scene, const VisibilityField& fiel
   return m;
 }
 
-// uncertainty.hpp:264-272 (correlation none)
+// uncertainty.hpp:264-278: correlation none -> plain sum in pixel order; hook ->
+// sum of H - H exp(-d / lambda) with d the entropy depth (a host fold of the
+// maps the caller already holds; select_nbv folds on the device).
 inline double image_entropy(const EntropyMap& map, const std::vector<double>& depth,
-                            const UncertaintyConfig& /*uc*/) {
+                            const UncertaintyConfig& uc) {
   if (depth.size() != map.entropy.size())
     throw ParameterError("image_entropy: depth map shape differs from the entropy map");
   double sum = 0.0;
-  for (double h : map.entropy) sum += h;
+  if (uc.correlation == CorrelationMode::kNone) {
+    for (double h : map.entropy) sum += h;
+    return sum;
+  }
+  for (std::size_t i = 0; i < map.entropy.size(); ++i) {
+    const double h = map.entropy[i];
+    sum += h - h * std::exp(-depth[i] / uc.correlation_lambda);
+  }
   return sum;
 }
 
@@ -496,6 +542,7 @@ inline NbvResult select_nbv(const Scene& scene_aug, const VisibilityField& field
                             const UncertaintyConfig& uc, int /*threads*/ = 1) {
   if (candidates.empty()) throw ParameterError("select_nbv: candidate list must be nonempty");
   auto ds = detail::upload(scene_aug);
+  detail::attach_variances(uc, ds->h, scene_aug.particles.size());
   auto df = detail::upload_field(field, *ds);
   std::vector<gavis_camera> cams;
   for (const auto& v : candidates) cams.push_back(detail::cam_c(v));
@@ -735,6 +782,7 @@ inline MappingLog run_active_mapping(const Scene& scene, const OccluderSet& occl
                                      const Trajectory& init, const PlannerConfig& pc,
                                      const MappingContext& ctx, int /*threads*/ = 1) {
   auto ds = detail::upload(scene);
+  detail::attach_variances(ctx.uncertainty, ds->h, scene.particles.size());
   const auto rects = detail::rects_c(occluders);
   const gavis_planner_config g = detail::pc_c(pc);
   gavis_mapping_config mc{};
@@ -769,6 +817,199 @@ inline MappingLog run_active_mapping(const Scene& scene, const OccluderSet& occl
     log.steps.push_back(std::move(st));
   }
   return log;
+}
+
+// ---- device-resident handles ------------------------------------------------
+// The reference-signature functions above take host values and upload the scene
+// (and field) per call. A planner loop (planner.hpp:297-301) that scores many
+// candidate sets against one scene keeps them resident instead: upload once,
+// then call the overloads below with the handles (no per-call H2D of the scene
+// or field).
+class ResidentScene {
+ public:
+  explicit ResidentScene(const Scene& s, const UncertaintyConfig* uc = nullptr)
+      : dev_(detail::upload(s)), n_(s.particles.size()), virt_(detail::virtual_mask(s)) {
+    if (uc) detail::attach_variances(*uc, dev_->h, n_);
+  }
+  // attach UncertaintyConfig::coeff_variances (kShPropagation) after the fact
+  void set_variances(const UncertaintyConfig& uc) { detail::attach_variances(uc, dev_->h, n_); }
+  gavis_scene* handle() const { return dev_->h; }
+  std::size_t size() const { return n_; }
+  const std::vector<uint8_t>& virtual_mask() const { return virt_; }
+
+ private:
+  std::unique_ptr<detail::DeviceScene> dev_;
+  std::size_t n_;
+  std::vector<uint8_t> virt_;
+};
+
+class ResidentField {
+ public:
+  ResidentField(const ResidentScene& s, gavis_field* h, int degree, const VmfParams& vmf)
+      : scene_(&s), degree_(degree), vmf_(vmf) {
+    dev_.h = h;
+  }
+  // a host field (e.g. load_field) made resident
+  ResidentField(const ResidentScene& s, const VisibilityField& f)
+      : scene_(&s), degree_(f.degree), vmf_(f.vmf) {
+    if (f.num_particles != s.size()) throw ParameterError("field was built for a different scene");
+    check(gavis_vf_upload(detail::holder().get(), s.handle(), f.vmf.kappa, f.degree, f.num_views,
+                          f.gamma.empty() ? nullptr : f.gamma.data(), &dev_.h));
+  }
+  ResidentField(const ResidentField&) = delete;
+  ResidentField& operator=(const ResidentField&) = delete;
+  ResidentField(ResidentField&& o) noexcept : scene_(o.scene_), degree_(o.degree_), vmf_(o.vmf_) {
+    dev_.h = o.dev_.h;
+    o.dev_.h = nullptr;
+  }
+  gavis_field* handle() const { return dev_.h; }
+  const ResidentScene& scene() const { return *scene_; }
+  int num_views() const {
+    int32_t nv = 0;
+    check(gavis_vf_download(dev_.h, nullptr, &nv, nullptr));
+    return nv;
+  }
+  // appends views (vfield.hpp:38-63 per view, num_views += views)
+  void accumulate(const Trajectory& views, const RasterConfig& rc = {}) {
+    std::vector<gavis_camera> cams;
+    for (const auto& v : views.views) cams.push_back(detail::cam_c(v));
+    const gavis_raster_config r = detail::rc_c(rc);
+    check(gavis_vf_accumulate_views(detail::holder().get(), dev_.h, scene_->handle(), cams.data(),
+                                    (int32_t)cams.size(), &r));
+  }
+  VisibilityField download() const {
+    VisibilityField out;
+    out.degree = degree_;
+    out.vmf = vmf_;
+    out.num_particles = scene_->size();
+    out.gamma.resize(out.num_particles * out.basis_size());
+    int32_t nv = 0;
+    check(gavis_vf_download(dev_.h, out.gamma.empty() ? nullptr : out.gamma.data(), &nv, nullptr));
+    out.num_views = nv;
+    out.virtual_mask = scene_->virtual_mask();
+    return out;
+  }
+
+ private:
+  const ResidentScene* scene_;
+  int degree_;
+  VmfParams vmf_;
+  detail::DeviceField dev_;
+};
+
+// vfield.hpp:68-92 on a resident scene; the field stays on the device.
+inline ResidentField construct_field(const ResidentScene& scene, const Trajectory& trajectory,
+                                     const VmfParams& vmf, int degree, const RasterConfig& rc = {}) {
+  std::vector<gavis_camera> cams;
+  for (const auto& v : trajectory.views) cams.push_back(detail::cam_c(v));
+  const gavis_raster_config r = detail::rc_c(rc);
+  gavis_field* f = nullptr;
+  check(gavis_vf_construct(detail::holder().get(), scene.handle(), cams.data(), (int32_t)cams.size(),
+                           vmf.kappa, degree, &r, &f));
+  return ResidentField(scene, f, degree, vmf);
+}
+
+// uncertainty.hpp:242-260 on resident handles (entropy map + optional entropy depth)
+inline EntropyMap render_entropy(const ResidentScene& scene, const ResidentField& field,
+                                 const CameraView& cam, const RasterConfig& rc,
+                                 const UncertaintyConfig& uc, std::vector<double>* depth_out = nullptr) {
+  const gavis_camera c = detail::cam_c(cam);
+  const gavis_raster_config r = detail::rc_c(rc);
+  const gavis_uncertainty_config u = detail::uc_c(uc);
+  EntropyMap m;
+  m.width = cam.width;
+  m.height = cam.height;
+  const std::size_t P = (std::size_t)cam.width * cam.height;
+  m.entropy.resize(P);
+  m.invisible_mass.resize(P);
+  if (depth_out) depth_out->resize(P);
+  gavis_render_outputs o{};
+  o.entropy = m.entropy.data();
+  o.invisible_mass = m.invisible_mass.data();
+  o.entropy_depth = depth_out ? depth_out->data() : nullptr;
+  check(gavis_ua_render(detail::holder().get(), scene.handle(), field.handle(), nullptr, &c, 1, &r, &u, &o));
+  return m;
+}
+
+// planner.hpp:117-137 on resident handles
+inline NbvResult select_nbv(const ResidentScene& scene, const ResidentField& field,
+                            const std::vector<CameraView>& candidates, const RasterConfig& rc,
+                            const UncertaintyConfig& uc) {
+  if (candidates.empty()) throw ParameterError("select_nbv: candidate list must be nonempty");
+  std::vector<gavis_camera> cams;
+  for (const auto& v : candidates) cams.push_back(detail::cam_c(v));
+  const gavis_raster_config r = detail::rc_c(rc);
+  const gavis_uncertainty_config u = detail::uc_c(uc);
+  NbvResult res;
+  res.scores.resize(candidates.size());
+  int32_t best = -1;
+  check(gavis_select_nbv(detail::holder().get(), scene.handle(), field.handle(), cams.data(),
+                         (int32_t)cams.size(), &r, &u, 0, res.scores.data(), &best));
+  res.best_index = best;
+  return res;
+}
+
+// ---- multi-GPU (one process per GPU) ------------------------------
+// Rank 0 makes the id (Communicator::unique_id), the host ships the bytes to the
+// other ranks (MPI, a file, a socket), every rank builds its Communicator on its
+// own device (set_default_device first).
+class Communicator {
+ public:
+  using Id = std::array<uint8_t, GAVIS_COMM_ID_BYTES>;
+  static Id unique_id() {
+    Id id{};
+    check(gavis_comm_unique_id(id.data()));
+    return id;
+  }
+  Communicator(const Id& id, int nranks, int rank) : nranks_(nranks), rank_(rank) {
+    check(gavis_comm_create(detail::holder().get(), id.data(), nranks, rank, &h_));
+  }
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  ~Communicator() {
+    if (h_) gavis_comm_destroy(h_);
+  }
+  gavis_comm* handle() const { return h_; }
+  int nranks() const { return nranks_; }
+  int rank() const { return rank_; }
+
+ private:
+  gavis_comm* h_ = nullptr;
+  int nranks_, rank_;
+};
+
+// construct_field with the trajectory split in static blocks over the ranks
+// (the reference's parallel_for over views, vfield.hpp:85-90) and the partial
+// fields all-reduced over NCCL. Collective.
+inline ResidentField construct_field_sharded(const Communicator& comm, const ResidentScene& scene,
+                                             const Trajectory& trajectory, const VmfParams& vmf,
+                                             int degree, const RasterConfig& rc = {}) {
+  std::vector<gavis_camera> cams;
+  for (const auto& v : trajectory.views) cams.push_back(detail::cam_c(v));
+  const gavis_raster_config r = detail::rc_c(rc);
+  gavis_field* f = nullptr;
+  check(gavis_vf_construct_sharded(comm.handle(), scene.handle(), cams.data(), (int32_t)cams.size(),
+                                   vmf.kappa, degree, &r, &f));
+  return ResidentField(scene, f, degree, vmf);
+}
+
+// select_nbv with the candidates split in static blocks over the ranks
+// (planner.hpp:125-131); every rank returns all scores and the same index. Collective.
+inline NbvResult select_nbv_sharded(const Communicator& comm, const ResidentScene& scene,
+                                    const ResidentField& field, const std::vector<CameraView>& candidates,
+                                    const RasterConfig& rc, const UncertaintyConfig& uc) {
+  if (candidates.empty()) throw ParameterError("select_nbv: candidate list must be nonempty");
+  std::vector<gavis_camera> cams;
+  for (const auto& v : candidates) cams.push_back(detail::cam_c(v));
+  const gavis_raster_config r = detail::rc_c(rc);
+  const gavis_uncertainty_config u = detail::uc_c(uc);
+  NbvResult res;
+  res.scores.resize(candidates.size());
+  int32_t best = -1;
+  check(gavis_select_nbv_sharded(comm.handle(), scene.handle(), field.handle(), cams.data(),
+                                 (int32_t)cams.size(), &r, &u, 0, res.scores.data(), &best));
+  res.best_index = best;
+  return res;
 }
 
 }  // namespace gavis_b200

@@ -263,6 +263,43 @@ gavis_status gavis_nbv_loop(gavis_ctx* ctx, const gavis_scene* scene, gavis_fiel
                             int32_t with_rgb, int32_t* chosen, double* scores,
                             double* all_scores);
 
+/* ---- multi-GPU: one process per GPU over NCCL -------------- */
+/* The reference parallelises construct_field over views (vfield.hpp:85-90) and
+ * select_nbv over candidates (planner.hpp:125-131) with static blocks
+ * (parallel.hpp:35-60); these entry points apply the same blocks across ranks.
+ * NCCL is loaded at run time (libnccl.so.2; the process's own copy if one is
+ * already loaded). Communicator: rank 0 calls gavis_comm_unique_id, the caller
+ * ships the GAVIS_COMM_ID_BYTES bytes to every rank (MPI, a file, a socket),
+ * and every rank calls gavis_comm_create with its own context; or an existing
+ * ncclComm_t is wrapped with gavis_comm_adopt (not destroyed with the comm). */
+#define GAVIS_COMM_ID_BYTES 128
+typedef struct gavis_comm gavis_comm;
+gavis_status gavis_comm_unique_id(uint8_t* id_out /* [GAVIS_COMM_ID_BYTES] */);
+gavis_status gavis_comm_create(gavis_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank,
+                               gavis_comm** out);
+gavis_status gavis_comm_adopt(gavis_ctx* ctx, void* nccl_comm, int32_t nranks, int32_t rank,
+                              gavis_comm** out);
+gavis_status gavis_comm_destroy(gavis_comm* comm);
+/* In-place sum of a field's fp64 coefficients over the ranks (ncclAllReduce on
+ * the context stream): partial fields of disjoint view blocks -> the full field. */
+gavis_status gavis_vf_allreduce(gavis_comm* comm, gavis_field* field);
+/* construct_field (vfield.hpp:68-92) with the views split in static blocks over
+ * the ranks: each rank renders [n*r/w, n*(r+1)/w), the partials are all-reduced,
+ * num_views = n_views on every rank. Collective: every rank calls it. */
+gavis_status gavis_vf_construct_sharded(gavis_comm* comm, const gavis_scene* scene,
+                                        const gavis_camera* views, int32_t n_views, double kappa,
+                                        int32_t degree, const gavis_raster_config* rc,
+                                        gavis_field** out);
+/* select_nbv (planner.hpp:117-137) over the full candidate list, each rank
+ * scoring its static block; scores [n_cams] (all of them, on every rank) and
+ * the first maximum. Certified mode re-scores the contenders of the maximum in
+ * fp64 on their owning ranks. Collective: every rank calls it. */
+gavis_status gavis_select_nbv_sharded(gavis_comm* comm, const gavis_scene* scene,
+                                      const gavis_field* field, const gavis_camera* cams,
+                                      int32_t n_cams, const gavis_raster_config* rc,
+                                      const gavis_uncertainty_config* uc, int32_t with_rgb,
+                                      double* scores, int32_t* best_index);
+
 /* ---- density control (vfield.hpp:136-199) ------------------------------ */
 /* DensityControlConfig (vfield.hpp:136-147). Defaults rho 100, eta 0.5,
  * eps_v 0.95, seed 0. */

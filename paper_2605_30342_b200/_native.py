@@ -79,11 +79,13 @@ EXPORTS = [
     "gavis_vf_accumulate_views", "gavis_vf_accumulate_visibility", "gavis_vf_upload",
     "gavis_vf_download", "gavis_vf_set_num_views", "gavis_vf_device_gamma", "gavis_vf_destroy",
     "gavis_single_view_visibility", "gavis_vf_query", "gavis_vf_query_view", "gavis_ua_render", "gavis_ua_mixtures",
-    "gavis_select_nbv", "gavis_nbv_loop", "gavis_density_control", "gavis_sample_candidates",
+    "gavis_select_nbv", "gavis_nbv_loop", "gavis_comm_unique_id", "gavis_comm_create", "gavis_comm_adopt",
+    "gavis_comm_destroy", "gavis_vf_allreduce", "gavis_vf_construct_sharded", "gavis_select_nbv_sharded", "gavis_density_control", "gavis_sample_candidates",
     "gavis_vis_coverage", "gavis_active_mapping", "gavis_ply_info",
     "gavis_read_splat_ply", "gavis_field_json_write", "gavis_field_json_read", "gavis_debug_project", "gavis_debug_binning",
 ]
 
+COMM_ID_BYTES = 128
 PRECISION_CERTIFIED = 0
 PRECISION_EXACT = 1
 

@@ -526,6 +526,79 @@ def nbv_loop(ctx: Context, scene, field: DeviceField, candidates: Sequence[Camer
     return chosen[:steps], best[:steps], allsc[:steps]
 
 
+# ------------------------------------------------------------------ multi-GPU
+class Comm:
+    """A communicator of the native library (gavis_comm: NCCL, one process per GPU).
+    Every rank creates it with the same unique id; `Comm.from_dist` ships rank 0's
+    id over an initialised torch.distributed group (any backend)."""
+
+    def __init__(self, ctx: Context, unique_id: bytes, nranks: int, rank: int):
+        require(len(unique_id) == N.COMM_ID_BYTES, "comm: unique id must be 128 bytes")
+        self.ctx, self.nranks, self.rank = ctx, int(nranks), int(rank)
+        buf = (C.c_uint8 * N.COMM_ID_BYTES).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        N.check(ctx.lib.gavis_comm_create(ctx.h, buf, C.c_int32(nranks), C.c_int32(rank), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * N.COMM_ID_BYTES)()
+        N.check(N.load().gavis_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_dist(cls, ctx: Context, dist) -> "Comm":
+        obj = [cls.unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(ctx, obj[0], dist.get_world_size(), dist.get_rank())
+
+    def close(self) -> None:
+        if self.h and self.ctx.h:
+            N.check(self.ctx.lib.gavis_comm_destroy(self.h))
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def vf_allreduce(comm: Comm, field: DeviceField) -> None:
+    """In-place sum of a field's coefficients over the ranks (gavis_vf_allreduce)."""
+    N.check(comm.ctx.lib.gavis_vf_allreduce(comm.h, field.h))
+
+
+def construct_field_sharded(comm: Comm, scene, views: Sequence[CameraView], vmf: VmfParams, degree: int,
+                            rc: RasterConfig = RasterConfig()) -> DeviceField:
+    """construct_field with the views in static blocks over the ranks, partials
+    all-reduced by the library over NCCL (gavis_vf_construct_sharded). Collective."""
+    ctx = comm.ctx
+    ds = _as_dev(ctx, scene)
+    arr = cameras_c(views)
+    h = C.c_void_p()
+    N.check(ctx.lib.gavis_vf_construct_sharded(comm.h, ds.h, arr, C.c_int32(len(views)), C.c_double(vmf.kappa),
+                                               C.c_int32(degree), C.byref(raster_c(rc)), C.byref(h)))
+    return DeviceField(ctx, ds, h, degree, vmf)
+
+
+def select_nbv_comm(comm: Comm, scene, field: DeviceField, candidates: Sequence[CameraView],
+                    rc: RasterConfig = RasterConfig(), uc: UncertaintyConfig = UncertaintyConfig(),
+                    with_rgb: bool = False) -> NbvResult:
+    """select_nbv over the full candidate list, each rank scoring its static block,
+    scores all-gathered by the library over NCCL (gavis_select_nbv_sharded). Collective."""
+    require(len(candidates) > 0, "select_nbv: candidate list must be nonempty")
+    ctx = comm.ctx
+    ds = _as_dev(ctx, scene)
+    scores = np.zeros(len(candidates))
+    best = C.c_int32()
+    arr = cameras_c(candidates)
+    N.check(ctx.lib.gavis_select_nbv_sharded(comm.h, ds.h, field.h, arr, C.c_int32(len(candidates)),
+                                             C.byref(raster_c(rc)), C.byref(unc_c(uc)),
+                                             C.c_int32(1 if with_rgb else 0), _ptr(scores), C.byref(best)))
+    return NbvResult(best.value, scores)
+
+
 # ------------------------------------------------------------------ planner
 def camera_from_c(c: N.Camera) -> CameraView:
     return CameraView(rotation=np.array(list(c.rotation), np.float64).reshape(3, 3),

@@ -442,6 +442,10 @@ inline void copy_out(gavis_ctx* c, double* host, const double* dev, int64_t coun
 void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const double* vis_host,
                const gavis_camera* cams, int n, const gavis_raster_config* rc,
                const gavis_uncertainty_config* uc, gavis_render_outputs* out);
+// Candidates that may be the fp64 argmax given certified scores (empty when the
+// context is not in certified mode); ua_host.cu.
+std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* rc,
+                                      const std::vector<double>& sc);
 // select_nbv argmax over certified scores, contenders re-scored exactly (ua_host.cu).
 int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
                         const gavis_camera* cams, int n, const gavis_raster_config* rc,

@@ -233,6 +233,21 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
 // magnitude inside the window).
 constexpr double kCertScoreRel = 1e-3;
 
+std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* rc,
+                                      const std::vector<double>& sc) {
+  std::vector<int> cont;
+  if (sc.empty() || c->precision != GAVIS_PRECISION_CERTIFIED ||
+      !ua_fast_supported(rc->tile_size, rc->alpha_clamp_max))
+    return cont;
+  int b = 0;
+  for (int i = 1; i < (int)sc.size(); ++i)
+    if (sc[i] > sc[b]) b = i;
+  const double lo = sc[b] - kCertScoreRel * std::fabs(sc[b]);
+  for (int i = 0; i < (int)sc.size(); ++i)
+    if (sc[i] >= lo) cont.push_back(i);
+  return cont;
+}
+
 int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,
                         const gavis_camera* cams, int n, const gavis_raster_config* rc,
                         const gavis_uncertainty_config* uc, std::vector<double>& sc) {
@@ -242,19 +257,10 @@ int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f
       if (sc[i] > sc[b]) b = i;
     return b;
   };
-  int b = first_max();
-  if (c->precision != GAVIS_PRECISION_CERTIFIED ||
-      !ua_fast_supported(rc->tile_size, rc->alpha_clamp_max))
-    return b;
-  const double lo = sc[b] - kCertScoreRel * std::fabs(sc[b]);
-  std::vector<int> cont;
+  const std::vector<int> cont = certified_contenders(c, rc, sc);
+  if (cont.size() < 2) return first_max();
   std::vector<gavis_camera> cc;
-  for (int i = 0; i < n; ++i)
-    if (sc[i] >= lo) {
-      cont.push_back(i);
-      cc.push_back(cams[i]);
-    }
-  if (cont.size() < 2) return b;
+  for (int i : cont) cc.push_back(cams[i]);
   std::vector<double> ex(cont.size());
   gavis_render_outputs o = {};
   o.scores = ex.data();

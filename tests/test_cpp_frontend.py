@@ -63,3 +63,89 @@ def test_cpp_planner_active_mapping_runs(tmp_path):
     r = subprocess.run([_build_planner(tmp_path), "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("step chosen") == 2
+
+
+def _build_modes(tmp_path):
+    from paper_2605_30342_b200 import build
+    build.build()
+    exe = str(tmp_path / "cpp_uncertainty_modes")
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "examples", "cpp_uncertainty_modes.cpp"), "-L",
+           os.path.join(ROOT, "paper_2605_30342_b200"), "-lgavis_b200",
+           "-Wl,-rpath," + os.path.join(ROOT, "paper_2605_30342_b200"), "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def _modes_scene():
+    """The closed-form scene of examples/cpp_uncertainty_modes.cpp, in Python."""
+    import numpy as np
+    from paper_2605_30342_b200.model import K_Y00, Scene, make_lookat
+    parts, k = [], 0
+
+    def colors():
+        nonlocal k
+        c = [[(0.3 + 0.1 * ch) / K_Y00, 0.1 * ((k + ch) % 3 - 1), 0.05 * (k % 4), -0.02 * ch] for ch in range(3)]
+        k += 1
+        return c
+    for i in range(7):
+        for j in range(7):
+            parts.append(dict(pos=(1.0, 0.2 + 0.1 * i, 0.2 + 0.1 * j), scale=(0.05, 0.06, 0.04), opacity=0.85,
+                              color_sh=colors()))
+    for m in range(30):
+        parts.append(dict(pos=(1.2 + 0.05 * (m % 5), 0.2 + 0.07 * (m % 9), 0.25 + 0.06 * (m % 8)),
+                          scale=(0.03, 0.03, 0.03), opacity=0.5 + 0.01 * m, color_sh=colors()))
+    sc = Scene.from_particles(parts, 1)
+    n = sc.num_particles
+    var = np.array([[[0.001 * (1 + (i + c + m) % 5) for m in range(4)] for c in range(3)] for i in range(n)])
+    front = make_lookat((0.3, 0.5, 0.5), (1, 0.5, 0.5), (0, 0, 1), 64, 64)
+    cands = [front, make_lookat((1.9, 0.5, 0.5), (1, 0.5, 0.5), (0, 0, 1), 64, 64),
+             make_lookat((1.1, -0.6, 0.5), (1.1, 0.5, 0.5), (0, 0, 1), 64, 64),
+             make_lookat((0.6, 0.1, 0.9), (1.1, 0.5, 0.5), (0, 0, 1), 64, 64)]
+    return sc, var, front, cands
+
+
+def test_cpp_uncertainty_modes_compiles(tmp_path):
+    assert os.path.exists(_build_modes(tmp_path))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["certified", "exact"])
+def test_cpp_uncertainty_modes_match_oracle(tmp_path, precision):
+    """kShPropagation and kHook from a reference-shaped C++ caller (reference
+    signatures, resident handles, one-rank sharded entry points) against the CPU
+    oracle: uncertainty.hpp:62-83, :149-163, :264-278; planner.hpp:117-137."""
+    import numpy as np
+    import oracle as O
+    from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
+    args = [_build_modes(tmp_path)] + (["exact"] if precision == "exact" else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    out = {}
+    for line in r.stdout.splitlines():
+        w = line.split()
+        out[w[0]] = w[1:]
+    sc, var, front, cands = _modes_scene()
+    rc = RasterConfig()
+    osc = O.OracleScene(sc)
+    og = O.construct_field(osc, [front], 1.0, 2, rc)
+    O.set_coeff_variances(var, 1)
+    try:
+        modes = {"sh": UncertaintyConfig(variance_provider=1),
+                 "hook": UncertaintyConfig(correlation=1, correlation_lambda=0.7),
+                 "both": UncertaintyConfig(variance_provider=1, correlation=1, correlation_lambda=0.7)}
+        tol = 1e-9 if precision == "exact" else 1e-5
+        ref = {}
+        for tag, uc in modes.items():
+            best, scores = O.select_nbv(osc, og, 2, 1, cands, rc, uc)
+            ref[tag] = (best, scores)
+        for tag in ("sh", "hook", "both", "resident_both", "sharded_both"):
+            best, scores = ref[tag.split("_")[-1]]
+            got = np.array([float(x) for x in out[tag][2:]])
+            assert int(out[tag][1]) == best, tag
+            assert np.max(np.abs(got - scores) / np.abs(scores)) <= tol, tag
+        # the host fold of the hook equals the oracle's hook score of candidate 1
+        assert abs(float(out["image_entropy_hook"][0]) - ref["both"][1][1]) <= tol * abs(ref["both"][1][1])
+        assert float(out["sharded_field_max_abs"][0]) == 0.0 and int(out["sharded_field_max_abs"][2]) == 1
+    finally:
+        O.set_coeff_variances(None, 0)

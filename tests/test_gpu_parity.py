@@ -586,3 +586,26 @@ def test_host_array_lengths_are_checked(ctx):
         api.render_entropy_core(ctx, ds, cam, RC, UC, np.ones(5))
     with pytest.raises(InvariantError):
         api.render(ctx, ds, None, [cam], RC, UC, entropy=True, splat_visibility=[])
+
+
+@pytest.mark.parametrize("precision", ["exact", "certified"])
+def test_library_comm_one_rank(precision):
+    """The library's own NCCL path (gavis_comm_*, gavis_vf_construct_sharded,
+    gavis_select_nbv_sharded, gavis_vf_allreduce) on a one-rank communicator:
+    identical to the single-GPU entry points (multi-rank runs use the same code
+    with more ranks; the host logic is covered over gloo in test_parallel_gloo)."""
+    c = synth.config1(0)
+    with api.Context(0) as cx:
+        cx.set_precision(precision)
+        ds = cx.upload(c["scene"])
+        comm = api.Comm(cx, api.Comm.unique_id(), 1, 0)
+        f1 = api.construct_field(cx, ds, c["train"], VmfParams(1.0), 2, RC)
+        f2 = api.construct_field_sharded(comm, ds, c["train"], VmfParams(1.0), 2, RC)
+        g1, g2 = f1.download(), f2.download()
+        assert g2.num_views == len(c["train"]) and np.array_equal(g1.gamma, g2.gamma)
+        api.vf_allreduce(comm, f2)  # one rank: the sum is the field itself
+        assert np.array_equal(f2.download().gamma, g1.gamma)
+        a = api.select_nbv(cx, ds, f1, c["candidates"], RC, UC, with_rgb=True)
+        b = api.select_nbv_comm(comm, ds, f2, c["candidates"], RC, UC, with_rgb=True)
+        assert a.best_index == b.best_index and np.array_equal(a.scores, b.scores)
+        comm.close()
