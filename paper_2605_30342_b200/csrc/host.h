@@ -23,6 +23,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gavis_b200.h"
 #include "kernels.h"
 
@@ -32,6 +34,37 @@ namespace host {
 
 
 inline thread_local std::string g_last_error;
+
+// NVTX ranges (header-only NVTX v3: free without an attached tool) around every
+// kernel family launch, labelled with the DESIGN.md kernel ids (K1-K8), and
+// around the entry points (VF CONST, UA render, select_nbv).
+inline const char* nvtx_label(const char* family) {
+  static const std::map<std::string, const char*> kLabels = {
+      {"preprocess", "K1 preprocess (project + query)"},
+      {"sort", "K2/K4 sort (items by depth / pairs by tile)"},
+      {"depth_order", "K2c depth_order (tied runs)"},
+      {"scan", "K2/K3 scan"},
+      {"emit_keys", "K3 emit tile pairs"},
+      {"wide_keys", "K3w emit 64-bit keys"},
+      {"ranges", "K5 tile ranges"},
+      {"vf_blend", "K6a vf_blend"},
+      {"vf_finalize", "K6b vf_finalize"},
+      {"ua_blend", "K7 ua_blend"},
+      {"ua_redo", "K7r ua_redo (fp64)"},
+      {"score", "K8 image score"},
+      {"query", "query_visibility"},
+      {"mixtures", "mixture dump"},
+      {"density", "density update"}};
+  const auto it = kLabels.find(family);
+  return it == kLabels.end() ? family : it->second;
+}
+
+struct NvtxRange {
+  explicit NvtxRange(const char* family) { nvtxRangePushA(nvtx_label(family)); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct ParamErr : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -287,6 +320,7 @@ struct gavis_ctx {
   template <class F>
   void run(const char* name, F&& launch, int nlaunch = 1, cudaStream_t st = nullptr) {
     if (!st) st = stream;
+    NvtxRange nvtx(name);
     cudaEvent_t a = nullptr, b = nullptr;
     if (profiling) {
       a = event();

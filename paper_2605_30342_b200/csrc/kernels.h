@@ -164,6 +164,7 @@ struct UaBlendArgs {
   int32_t* ent_contrib = nullptr;
   double corr_lambda = 0.0;      // > 0: correlation hook in the image score
   bool do_rgb = true, do_ent = true;
+  bool vis_outside_unit = false;   // caller-given visibility with entries outside [0, 1]
   // Certified fp32 path (kernels_ua_fast.cu): pixels whose early-termination
   // decision the fp32 error bound cannot certify are appended to flag_list
   // (batch pixel index) and recomputed by the fp64 redo kernel.

@@ -36,14 +36,14 @@ __global__ void __launch_bounds__(128) mixture_kernel(MixtureArgs a) {
     const uint32_t g = a.vals[j];
     const GeoRec e = a.geo[g];
     if (!in_rect4(cover_rect4(e.cov_x, e.cov_y), px, py)) continue;
+    // the exact entropy track's operations (ex_* in ua_common.cuh)
     const double al = splat_alpha(e, cxp, cyp, a.amax);
-    const UaRec u = a.ua[g];
-    double as = u.A * al + u.B;  // compensated_alpha (uncertainty.hpp:55-59)
-    as = as < 0.0 ? 0.0 : (a.amax < as ? a.amax : as);
+    const ExUa u = ex_ua(a.ua[g]);
+    const double as = ex_astar<true>(u, al, a.amax);  // compensated_alpha (uncertainty.hpp:55-59)
     const double w = as * T;
     const double s = w * u.v;
-    if (s > 0.0) H += s * (-log_pos(s) + u.hl + kGaussEntropy);
-    w0 += w * (1.0 - u.v);
+    if (s > 0.0) H = fma(s, u.hlc - log_pos(s), H);
+    w0 = fma(w, u.omv, w0);
     if (w > 0.0) {
       if (out) {
         double* m = out + 8 * k;
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128) mixture_kernel(MixtureArgs a) {
       }
       ++k;
     }
-    T *= 1.0 - as;
+    T = fma(-as, T, T);
     if (T < a.cutoff) break;
   }
   if (w0 > 0.0) H += w0 * (-log_pos(w0) + a.hl_q0 + kGaussEntropy);

@@ -30,19 +30,19 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // Any tile size: 256 threads, one pixel each, pixels in rounds of 256.
-template <int LC, bool RGB, bool ENT, bool EXTRA>
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool LO>
 __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
   constexpr int kThreads = 256;
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
-  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(GeoRec));
-  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4)));
-  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(GeoRec) + sizeof(int4) +
-                                                            (ENT ? sizeof(UaRec) : 0)));
+  ExGeo* s_geo = reinterpret_cast<ExGeo*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + kBatch * sizeof(ExGeo));
+  ExUa* s_ua = reinterpret_cast<ExUa*>(s_dyn + kBatch * (sizeof(ExGeo) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + kBatch * (sizeof(ExGeo) + sizeof(int4) +
+                                                            (ENT ? sizeof(ExUa) : 0)));
   load_math_tables();
 
-  const double amax = a.amax, cutoff = a.cutoff, hl_qc = a.hl_qc;
+  const double amax = a.amax, cutoff = a.cutoff;
   const int64_t gt = blockIdx.x;
   const int v = find_view(a.cams, a.V, gt);
   const DevCam& c = a.cams[v];
@@ -73,11 +73,22 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
       if (!live) continue;
       for (int j = 0; j < n; ++j) {
         if (!in_rect4(s_rect[j], px, py)) continue;
-        const GeoRec& e = s_geo[j];
-        const double al = splat_alpha(e, cxp, cyp, amax);
-        if (RGB && !P.rgb_done)
-          rgb_step<LC, EXTRA>(P, al, e.depth, reinterpret_cast<const float2*>(s_col + j * CS), cutoff);
-        if (ENT && !P.ent_done) ent_step<LC, EXTRA>(P, al, e.depth, s_ua[j], amax, cutoff, hl_qc);
+        const ExGeo& e = s_geo[j];
+        const double al = ex_alpha(e, ex_negq(e, cxp, cyp), amax);
+        if (RGB && !P.rgb_done) {
+          float c0, c1, c2;
+          sh_color<LC>(reinterpret_cast<const float2*>(s_col + j * CS), P.bp, c0, c1, c2);
+          if (EXTRA) ++P.n_rgb;
+          ex_rgb<LC, EXTRA>(P, al, e.depth, c0, c1, c2);
+          if (P.T < cutoff) P.rgb_done = true;
+        }
+        if (ENT && !P.ent_done) {
+          const ExUa& u = s_ua[j];
+          if (EXTRA) ++P.n_ent;
+          const double sv = ex_ent<LC, EXTRA>(P, ex_astar<LO>(u, al, amax), u, e.depth);
+          if (sv > 0.0) P.H = fma(sv, u.hlc - log_pos(sv), P.H);
+          if (P.Te < cutoff) P.ent_done = true;
+        }
         if (P.rgb_done && P.ent_done) break;
       }
     }
@@ -94,15 +105,15 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
 // instruction-level parallelism; only T, T*, rgb, H and w0 chain. Masks replace
 // branches: an entry a pixel does not cover, or one past its termination, gets
 // alpha = alpha* = 0, which leaves every accumulator bit-identical.
-template <int LC, bool RGB, bool ENT, bool EXTRA, int BATCH = kBatch>
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool LO, int BATCH = kBatch>
 __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
-  int4* s_rect = reinterpret_cast<int4*>(s_dyn + BATCH * sizeof(GeoRec));
-  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + BATCH * (sizeof(GeoRec) + sizeof(int4)));
-  float* s_col = reinterpret_cast<float*>(s_dyn + BATCH * (sizeof(GeoRec) + sizeof(int4) +
-                                                           (ENT ? sizeof(UaRec) : 0)));
+  ExGeo* s_geo = reinterpret_cast<ExGeo*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + BATCH * sizeof(ExGeo));
+  ExUa* s_ua = reinterpret_cast<ExUa*>(s_dyn + BATCH * (sizeof(ExGeo) + sizeof(int4)));
+  float* s_col = reinterpret_cast<float*>(s_dyn + BATCH * (sizeof(ExGeo) + sizeof(int4) +
+                                                           (ENT ? sizeof(ExUa) : 0)));
   load_math_tables();
 
   const double amax = a.amax, cutoff = a.cutoff;
@@ -146,72 +157,37 @@ __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
         if (has_b) hits &= hits - 1u;
         const bool ca = in_rect4(s_rect[ja], px, py);
         const bool cb = has_b && in_rect4(s_rect[jb], px, py);
-        const GeoRec& ea = s_geo[ja];
-        const GeoRec& eb = s_geo[jb];
+        const ExGeo& ea = s_geo[ja];
+        const ExGeo& eb = s_geo[jb];
         // alphas of both entries (splat_alpha, raster.hpp:101-108), independent chains
-        const double dxa = cxp - ea.mx, dya = cyp - ea.my;
-        const double dxb = cxp - eb.mx, dyb = cyp - eb.my;
-        const double qa = ea.ca * dxa * dxa + ea.cb2 * dxa * dya + ea.cc * dya * dya;
-        const double qb = eb.ca * dxb * dxb + eb.cb2 * dxb * dyb + eb.cc * dyb * dyb;
-        const double exa = exp_neg(fmax(-0.5 * qa, -40.0));
-        const double exb = exp_neg(fmax(-0.5 * qb, -40.0));
-        double ala = (double)ea.opacity * exa, alb = (double)eb.opacity * exb;
-        ala = qa <= kQSkip ? (ala > amax ? amax : ala) : 0.0;
-        alb = qb <= kQSkip ? (alb > amax ? amax : alb) : 0.0;
+        const double ala = ex_alpha(ea, ex_negq(ea, cxp, cyp), amax);
+        const double alb = ex_alpha(eb, ex_negq(eb, cxp, cyp), amax);
         if (RGB) {
-          const bool ra = ca && !P.rgb_done;
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, b0 = 0.f, b1 = 0.f, b2 = 0.f;
+          float a0, a1, a2, b0, b1, b2;
           sh_color<LC>(reinterpret_cast<const float2*>(s_col + ja * CS), P.bp, a0, a1, a2);
           sh_color<LC>(reinterpret_cast<const float2*>(s_col + jb * CS), P.bp, b0, b1, b2);
-          const double aa = ra ? ala : 0.0;
-          const double wa = aa * P.T;
-          P.rgb0 += wa * (double)a0;
-          P.rgb1 += wa * (double)a1;
-          P.rgb2 += wa * (double)a2;
-          if (EXTRA) P.dep += wa * ea.depth;
-          P.T *= 1.0 - aa;
+          const bool ra = ca && !P.rgb_done;
+          ex_rgb<LC, EXTRA>(P, ra ? ala : 0.0, ea.depth, a0, a1, a2);
           const bool rd = P.rgb_done || (ra && P.T < cutoff);
           const bool rb = cb && !rd;
-          const double ab = rb ? alb : 0.0;
-          const double wb = ab * P.T;
-          P.rgb0 += wb * (double)b0;
-          P.rgb1 += wb * (double)b1;
-          P.rgb2 += wb * (double)b2;
-          if (EXTRA) {
-            P.dep += wb * eb.depth;
-            P.n_rgb += (int)ra + (int)rb;
-          }
-          P.T *= 1.0 - ab;
+          ex_rgb<LC, EXTRA>(P, rb ? alb : 0.0, eb.depth, b0, b1, b2);
+          if (EXTRA) P.n_rgb += (int)ra + (int)rb;
           P.rgb_done = rd || (rb && P.T < cutoff);
         }
         if (ENT) {
+          const ExUa& ua = s_ua[ja];
+          const ExUa& ub = s_ua[jb];
+          const double xa = ex_astar<LO>(ua, ala, amax), xb = ex_astar<LO>(ub, alb, amax);
           const bool ea_on = ca && !P.ent_done;
-          const UaRec& ua = s_ua[ja];
-          const UaRec& ub = s_ua[jb];
-          double xa = ua.A * ala + ua.B, xb = ub.A * alb + ub.B;
-          xa = xa < 0.0 ? 0.0 : (amax < xa ? amax : xa);
-          xb = xb < 0.0 ? 0.0 : (amax < xb ? amax : xb);
-          const double asa = ea_on ? xa : 0.0;
-          const double wa = asa * P.Te;
-          const double sa = wa * ua.v;
-          P.w0 += wa * (1.0 - ua.v);
-          if (EXTRA) P.edep += wa * ea.depth;
-          P.Te *= 1.0 - asa;
+          const double sa = ex_ent<LC, EXTRA>(P, ea_on ? xa : 0.0, ua, ea.depth);
           const bool ed = P.ent_done || (ea_on && P.Te < cutoff);
           const bool eb_on = cb && !ed;
-          const double asb = eb_on ? xb : 0.0;
-          const double wb = asb * P.Te;
-          const double sb = wb * ub.v;
+          const double sb = ex_ent<LC, EXTRA>(P, eb_on ? xb : 0.0, ub, eb.depth);
           const double la = log_pos(sa > 0.0 ? sa : 1.0);
           const double lb = log_pos(sb > 0.0 ? sb : 1.0);
-          if (sa > 0.0) P.H += sa * (-la + ua.hl + kGaussEntropy);
-          if (sb > 0.0) P.H += sb * (-lb + ub.hl + kGaussEntropy);
-          P.w0 += wb * (1.0 - ub.v);
-          if (EXTRA) {
-            P.edep += wb * eb.depth;
-            P.n_ent += (int)ea_on + (int)eb_on;
-          }
-          P.Te *= 1.0 - asb;
+          if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
+          if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
+          if (EXTRA) P.n_ent += (int)ea_on + (int)eb_on;
           P.ent_done = ed || (eb_on && P.Te < cutoff);
         }
       }
@@ -225,7 +201,7 @@ void set_smem(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int LC, bool RGB, bool ENT, bool EXTRA>
+template <int LC, bool RGB, bool ENT, bool EXTRA, bool LO>
 void launch_one(const UaBlendArgs& a, cudaStream_t s) {
   const size_t smem = Stage<LC, RGB, ENT>::bytes(kBatch);
   static const int choice = [] {
@@ -239,27 +215,35 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
     constexpr int kIlpBatch = 192;
     const size_t sm = Stage<LC, RGB, ENT>::bytes(kIlpBatch);
     static bool configured = false;
-    if (!configured) set_smem(ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, kIlpBatch>, sm);
+    if (!configured) set_smem(ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, LO, kIlpBatch>, sm);
     configured = true;
-    ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, kIlpBatch><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+    ua_blend_ilp_kernel<LC, RGB, ENT, EXTRA, LO, kIlpBatch><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
     return;
   }
   static bool configured = false;
   if (!configured) {
-    set_smem(ua_blend_kernel<LC, RGB, ENT, EXTRA>, smem);
+    set_smem(ua_blend_kernel<LC, RGB, ENT, EXTRA, LO>, smem);
     configured = true;
   }
-  ua_blend_kernel<LC, RGB, ENT, EXTRA><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
+  ua_blend_kernel<LC, RGB, ENT, EXTRA, LO><<<(unsigned)a.total_tiles, 256, smem, s>>>(a);
 }
 
 template <int LC, bool EXTRA>
 void launch_lc_x(const UaBlendArgs& a, cudaStream_t s) {
-  if (a.do_rgb && a.do_ent)
-    launch_one<LC, true, true, EXTRA>(a, s);
-  else if (a.do_rgb)
-    launch_one<LC, true, false, EXTRA>(a, s);
-  else if (a.do_ent)
-    launch_one<LC, false, true, EXTRA>(a, s);
+  // the lower alpha* clamp only for caller-given visibilities outside [0, 1]
+  if (a.do_rgb && a.do_ent) {
+    if (a.vis_outside_unit)
+      launch_one<LC, true, true, EXTRA, true>(a, s);
+    else
+      launch_one<LC, true, true, EXTRA, false>(a, s);
+  } else if (a.do_rgb) {
+    launch_one<LC, true, false, EXTRA, false>(a, s);
+  } else if (a.do_ent) {
+    if (a.vis_outside_unit)
+      launch_one<LC, false, true, EXTRA, true>(a, s);
+    else
+      launch_one<LC, false, true, EXTRA, false>(a, s);
+  }
 }
 
 template <int LC>

@@ -615,24 +615,26 @@ __global__ void __launch_bounds__(32) ua_redo_kernel(UaBlendArgs a) {
       if (P.rgb_done && P.ent_done) break;
       const uint32_t j = base + lane;
       bool cov = false;
-      double al = 0.0, as = 0.0, dep = 0.0, vv = 0.0, hl = 0.0;
+      double al = 0.0, as = 0.0, dep = 0.0, vv = 0.0, omv = 0.0, hlc = 0.0;
       float c0 = 0.f, c1 = 0.f, c2 = 0.f;
       if (j < rg.y) {
         const uint32_t g = a.vals[j];
-        const GeoRec e = geo[g];
-        cov = in_rect4(cover_rect4(e.cov_x, e.cov_y), px, py);
+        const GeoRec r = geo[g];
+        cov = in_rect4(cover_rect4(r.cov_x, r.cov_y), px, py);
         if (cov) {
-          al = splat_alpha(e, cxp, cyp, amax);
+          // the exact kernels' arithmetic (ua_common.cuh), lane-parallel per entry
+          const ExGeo e = ex_geo(r);
+          al = ex_alpha(e, ex_negq(e, cxp, cyp), amax);
           dep = e.depth;
           if (RGB)
             sh_color<LC>(reinterpret_cast<const float2*>(a.scene.colors + (int64_t)g * CS), P.bp, c0,
                          c1, c2);
           if (ENT) {
-            const UaRec u = uar[g];
-            const double x = u.A * al + u.B;  // compensated_alpha (uncertainty.hpp:55-59)
-            as = x < 0.0 ? 0.0 : (amax < x ? amax : x);
+            const ExUa u = ex_ua(uar[g]);
+            as = ex_astar<true>(u, al, amax);  // the lower clamp is a no-op when A alpha + B >= 0
             vv = u.v;
-            hl = u.hl;
+            omv = u.omv;
+            hlc = u.hlc;
           }
         }
       }
@@ -644,44 +646,37 @@ __global__ void __launch_bounds__(32) ua_redo_kernel(UaBlendArgs a) {
         mm &= mm - 1u;
         const double eal = __shfl_sync(0xffffffffu, al, src);
         const double edep = __shfl_sync(0xffffffffu, dep, src);
-        if (RGB && !P.rgb_done) {  // rgb_step (raster.hpp:209-221)
+        if (RGB && !P.rgb_done) {  // rasterize (raster.hpp:209-221)
           const float e0 = __shfl_sync(0xffffffffu, c0, src);
           const float e1 = __shfl_sync(0xffffffffu, c1, src);
           const float e2 = __shfl_sync(0xffffffffu, c2, src);
           ++P.n_rgb;
-          const double w = eal * P.T;
-          if (w > 0.0) {
-            P.rgb0 += w * (double)e0;
-            P.rgb1 += w * (double)e1;
-            P.rgb2 += w * (double)e2;
-            P.dep += w * edep;
-          }
-          P.T *= 1.0 - eal;
+          ex_rgb<LC, true>(P, eal, edep, e0, e1, e2);
           if (P.T < cutoff) P.rgb_done = true;
         }
-        if (ENT && !P.ent_done) {  // ent_step (uncertainty.hpp:198-222), H deferred
+        if (ENT && !P.ent_done) {  // render_entropy_core (uncertainty.hpp:198-222), H deferred
+          ExUa u;
+          u.v = __shfl_sync(0xffffffffu, vv, src);
+          u.omv = __shfl_sync(0xffffffffu, omv, src);
           const double eas = __shfl_sync(0xffffffffu, as, src);
-          const double ev = __shfl_sync(0xffffffffu, vv, src);
           ++P.n_ent;
-          const double w = eas * P.Te;
-          const double s = w * ev;
-          if (lane == src) my_s = s;
-          P.w0 += w * (1.0 - ev);
-          P.edep += w * edep;
-          P.Te *= 1.0 - eas;
+          const double sv = ex_ent<LC, true>(P, eas, u, edep);
+          if (lane == src) my_s = sv;
           if (P.Te < cutoff) P.ent_done = true;
         }
         if (P.rgb_done && P.ent_done) break;
       }
       if (ENT) {
-        // H += s (-ln s + 1/2 ln|Qc| + C_H) in list order: the logs in parallel
-        // (one per lane), the sum serial; entries not composited add +0.0
-        const double term = my_s > 0.0 ? my_s * (-log_pos(my_s) + hl + kGaussEntropy) : 0.0;
+        // H += s (-ln s + 1/2 ln|Qc| + C_H) in list order as fma(s, hlc - ln s, H):
+        // the logs in parallel (one per lane), the sum serial
+        const double tl = my_s > 0.0 ? hlc - log_pos(my_s) : 0.0;
         mm = m;
         while (mm != 0u) {
           const int src = __ffs(mm) - 1;
           mm &= mm - 1u;
-          P.H += __shfl_sync(0xffffffffu, term, src);
+          const double ss = __shfl_sync(0xffffffffu, my_s, src);
+          const double tt = __shfl_sync(0xffffffffu, tl, src);
+          if (ss > 0.0) P.H = fma(ss, tt, P.H);
         }
       }
     }

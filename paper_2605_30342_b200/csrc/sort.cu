@@ -1,6 +1,10 @@
 // sort.cu -- device scan and radix sort (CUB, header-only part of the CUDA 12.9
-// toolkit) for the tile-key pipeline: K2 exclusive scan of per-(view, particle)
-// tile counts and K4 stable LSD radix sort of (tile << 32 | fp32 depth) keys.
+// toolkit) for the tile-key pipeline: the K2 sort of the visible items by their
+// 32-bit (view | leading fp32 depth bits) keys, the K2/K3 exclusive scans of
+// tile counts, and the K4 stable LSD radix sort of the 32-bit tile-id keys
+// (only the ceil(log2 tiles) low bits: 2 passes), whose stability keeps the
+// depth order inside every tile. The 64-bit (tile << 32 | fp32 depth) key sort
+// remains for the GAVIS_BIN_WIDE=1 path and the debug binning export.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 

@@ -107,52 +107,100 @@ __device__ __forceinline__ void sh_color(const float2* col2, const float2* bp, f
   c2 = __saturatef(a2.x + a2.y);
 }
 
-// alpha of splat e at the pixel (splat_alpha, raster.hpp:101-108).
-__device__ __forceinline__ double splat_alpha(const GeoRec& e, double cxp, double cyp, double amax) {
-  const double dx = cxp - e.mx;
-  const double dy = cyp - e.my;
-  const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-  double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
-  if (q <= kQSkip) {
-    al = (double)e.opacity * exp_neg(-0.5 * q);
-    al = al > amax ? amax : al;
-  }
-  return al;
+// ---------------------------------------------------------------------------
+// fp64 arithmetic of one composited entry, shared by every exact-path kernel
+// (the 16x16 entry-pair kernel, the generic kernel and the certified path's
+// fp64 redo, which must agree bit for bit). The reference's expressions
+// (splat_alpha raster.hpp:101-108, rasterize :209-221, render_entropy_core
+// uncertainty.hpp:198-222) are evaluated in fp64 with FMA contraction where it
+// saves an instruction; results agree with the unfused reference to rounding.
+
+// One list entry as the exact blend stages it: the conic pre-scaled by -1/2
+// (a power of two: exact), so x = -q/2 comes out of two FMAs; opacity widened once.
+struct __align__(16) ExGeo {
+  double mx, my;
+  double na, nb, nc;  // -a/2, -b (= -(2b)/2), -c/2
+  double o, depth, _pad;
+};
+// Entropy-track constants with 1 - v and 1/2 ln|Q_c| + C_H precomputed.
+struct ExUa {
+  double A, B, v, omv, hlc;
+};
+
+__device__ __forceinline__ ExGeo ex_geo(const GeoRec& r) {
+  ExGeo e;
+  e.mx = r.mx;
+  e.my = r.my;
+  e.na = -0.5 * r.ca;
+  e.nb = -0.5 * r.cb2;
+  e.nc = -0.5 * r.cc;
+  e.o = (double)r.opacity;
+  e.depth = r.depth;
+  e._pad = 0.0;
+  return e;
 }
 
-// RGB track update given alpha and (if w > 0) the colour (raster.hpp:209-221).
-// EXTRA: depth and contributor counts (only when an output asks for them).
+__device__ __forceinline__ ExUa ex_ua(const UaRec& u) {
+  ExUa x;
+  x.A = u.A;
+  x.B = u.B;
+  x.v = u.v;
+  x.omv = 1.0 - u.v;
+  x.hlc = u.hl + kGaussEntropy;
+  return x;
+}
+
+// x = -q/2 at the pixel centre, q = a dx^2 + 2b dx dy + c dy^2.
+__device__ __forceinline__ double ex_negq(const ExGeo& e, double cxp, double cyp) {
+  const double dx = cxp - e.mx, dy = cyp - e.my;
+  return fma(dx, fma(e.na, dx, e.nb * dy), e.nc * dy * dy);
+}
+
+// alpha = min(o exp(-q/2), alpha_max); q > kQSkip -> 0 (T bit-identical, fast_math.cuh).
+__device__ __forceinline__ double ex_alpha(const ExGeo& e, double x, double amax) {
+  const double al = e.o * exp_neg(x);
+  return x >= -0.5 * kQSkip ? (al > amax ? amax : al) : 0.0;
+}
+
+// compensated_alpha (uncertainty.hpp:55-59): clamp(A alpha + B, 0, alpha_max).
+// LO: the lower clamp, needed only for caller-given visibilities outside [0, 1]
+// (field queries give v in [0, 1], and beta, o0 in [0, 1] make A, B >= 0).
+template <bool LO>
+__device__ __forceinline__ double ex_astar(const ExUa& u, double al, double amax) {
+  double x = fma(u.A, al, u.B);
+  if (LO) x = x < 0.0 ? 0.0 : x;
+  return x > amax ? amax : x;
+}
+
+// RGB track (raster.hpp:209-221): w = alpha T, rgb += w c, T <- T (1 - alpha).
+// alpha = 0 (masked entry) leaves every accumulator bit-identical.
 template <int LC, bool EXTRA>
-__device__ __forceinline__ void rgb_step(Pixel<LC>& P, double al, double depth, const float2* col2,
-                                         double cutoff) {
-  if (EXTRA) ++P.n_rgb;
+__device__ __forceinline__ void ex_rgb(Pixel<LC>& P, double al, double depth, float c0, float c1,
+                                       float c2) {
   const double w = al * P.T;
-  if (w > 0.0) {
-    float c0, c1, c2;
-    sh_color<LC>(col2, P.bp, c0, c1, c2);
-    P.rgb0 += w * (double)c0;
-    P.rgb1 += w * (double)c1;
-    P.rgb2 += w * (double)c2;
-    if (EXTRA) P.dep += w * depth;
-  }
-  P.T *= 1.0 - al;
-  if (P.T < cutoff) P.rgb_done = true;
+  P.rgb0 = fma(w, (double)c0, P.rgb0);
+  P.rgb1 = fma(w, (double)c1, P.rgb1);
+  P.rgb2 = fma(w, (double)c2, P.rgb2);
+  if (EXTRA) P.dep = fma(w, depth, P.dep);
+  P.T = fma(-al, P.T, P.T);
 }
 
-// Entropy track update (uncertainty.hpp:198-222).
+// Entropy track (uncertainty.hpp:198-222) without the H term: w = a* T*,
+// w0 += w (1 - v), T* <- T* (1 - a*); returns s = w v. H += s (-ln s + hl + C_H)
+// is added by the caller as fma(s, hlc - ln s, H) when s > 0.
 template <int LC, bool EXTRA>
-__device__ __forceinline__ void ent_step(Pixel<LC>& P, double al, double depth, const UaRec& u,
-                                         double amax, double cutoff, double hl_qc) {
-  if (EXTRA) ++P.n_ent;
-  double as = u.A * al + u.B;
-  as = as < 0.0 ? 0.0 : (amax < as ? amax : as);
+__device__ __forceinline__ double ex_ent(Pixel<LC>& P, double as, const ExUa& u, double depth) {
   const double w = as * P.Te;
-  const double s = w * u.v;
-  if (s > 0.0) P.H += s * (-log_pos(s) + u.hl + kGaussEntropy);
-  P.w0 += w * (1.0 - u.v);
-  if (EXTRA) P.edep += w * depth;
-  P.Te *= 1.0 - as;
-  if (P.Te < cutoff) P.ent_done = true;
+  P.w0 = fma(w, u.omv, P.w0);
+  if (EXTRA) P.edep = fma(w, depth, P.edep);
+  P.Te = fma(-as, P.Te, P.Te);
+  return w * u.v;
+}
+
+// alpha of splat e at the pixel from its projection record (mixture dump).
+__device__ __forceinline__ double splat_alpha(const GeoRec& r, double cxp, double cyp, double amax) {
+  const ExGeo e = ex_geo(r);
+  return ex_alpha(e, ex_negq(e, cxp, cyp), amax);
 }
 
 template <int LC, bool RGB, bool ENT, bool EXTRA>
@@ -182,23 +230,24 @@ __device__ __forceinline__ void pixel_finish(Pixel<LC>& P, const UaBlendArgs& a,
 template <int LC, bool RGB, bool ENT>
 struct Stage {
   static constexpr size_t bytes(int batch) {
-    return (size_t)batch * (sizeof(GeoRec) + sizeof(int4) + (ENT ? sizeof(UaRec) : 0) +
+    return (size_t)batch * (sizeof(ExGeo) + sizeof(int4) + (ENT ? sizeof(ExUa) : 0) +
                             (RGB ? sizeof(float) * Col<LC>::STRIDE : 0));
   }
 };
 
-// Stage entries [base, base+n) of the tile list into shared memory.
+// Stage entries [base, base+n) of the tile list into shared memory as exact-path
+// records (ExGeo / coverage rectangle / ExUa) and fp32 colour rows.
 template <int LC, bool RGB, bool ENT>
 __device__ __forceinline__ void stage_batch(const UaBlendArgs& a, const GeoRec* geo, const UaRec* uar,
-                                            uint32_t base, int n, GeoRec* s_geo, int4* s_rect,
-                                            UaRec* s_ua, float* s_col) {
+                                            uint32_t base, int n, ExGeo* s_geo, int4* s_rect,
+                                            ExUa* s_ua, float* s_col) {
   constexpr int V4 = Col<LC>::STRIDE / 4;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const uint32_t g = a.vals[base + j];
     const GeoRec r = geo[g];
-    s_geo[j] = r;
+    s_geo[j] = ex_geo(r);
     s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
-    if (ENT) s_ua[j] = uar[g];
+    if (ENT) s_ua[j] = ex_ua(uar[g]);
   }
   if (RGB) {
     const float4* colors4 = reinterpret_cast<const float4*>(a.scene.colors);

@@ -35,6 +35,7 @@ void cert_window(UaBlendArgs* ua, float max_opacity) {
 void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const double* vis_host,
                const gavis_camera* cams, int n, const gavis_raster_config* rc,
                const gavis_uncertainty_config* uc, gavis_render_outputs* out) {
+  NvtxRange nvtx("UA render (render_entropy + rasterize, uncertainty.hpp:242-260)");
   validate_raster(rc);
   double hl_q0 = 0.0;
   validate_unc(uc, &hl_q0);
@@ -49,6 +50,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
                       out->entropy_contributors || out->with_entropy;
   if (!do_rgb && !do_ent) return;
   const double* vis_dev = nullptr;
+  bool vis_outside_unit = false;  // selects the exact kernels' lower alpha* clamp
   if (!f) {
     require(vis_host != nullptr || N == 0 || !do_ent,
             "render needs a field or per-particle splat visibility");
@@ -56,6 +58,8 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       double* d = (double*)c->buf("vis_given", sizeof(double) * N);
       CK(cudaMemcpyAsync(d, vis_host, sizeof(double) * N, cudaMemcpyHostToDevice, c->stream));
       vis_dev = d;
+      for (int64_t i = 0; i < N && !vis_outside_unit; ++i)
+        vis_outside_unit = !(vis_host[i] >= 0.0 && vis_host[i] <= 1.0);
     }
   }
   const int bv = batch_views(c, N, n);
@@ -151,6 +155,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     ua.vals = b.vals;
     ua.do_rgb = do_rgb;
     ua.do_ent = do_ent;
+    ua.vis_outside_unit = vis_outside_unit;
     // The RGB and entropy images always land in device memory (host copies only
     // when requested; the score folds the entropy image); depth and
     // residual-transmittance maps only on request.
@@ -397,6 +402,7 @@ gavis_status gavis_select_nbv(gavis_ctx* c, const gavis_scene* s, const gavis_fi
     require(n_cams > 0 && cams != nullptr, "select_nbv: candidate list must be nonempty");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
+    NvtxRange nvtx("select_nbv (planner.hpp:117-137)");
     std::vector<double> sc((size_t)n_cams);
     gavis_render_outputs o = {};
     o.scores = sc.data();

@@ -8,6 +8,7 @@ namespace host {
 void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_camera* views,
               int n_views, const gavis_raster_config* rc, double* vis_host, int64_t* touch_host,
               int32_t* contrib_host, const DensityHook* dh) {
+  NvtxRange nvtx("VF CONST (single_view_visibility + accumulate_view)");
   require(s->ctx->device == c->device, "scene was uploaded to another device");
   if (f) require(f->ctx->device == c->device, "field lives on another device");
   const int64_t N = s->dev.n;

@@ -98,6 +98,7 @@ def _modes_scene():
     sc = Scene.from_particles(parts, 1)
     n = sc.num_particles
     var = np.array([[[0.001 * (1 + (i + c + m) % 5) for m in range(4)] for c in range(3)] for i in range(n)])
+    var = var.astype(np.float32).astype(np.float64)  # the device holds coefficient variances in fp32
     front = make_lookat((0.3, 0.5, 0.5), (1, 0.5, 0.5), (0, 0, 1), 64, 64)
     cands = [front, make_lookat((1.9, 0.5, 0.5), (1, 0.5, 0.5), (0, 0, 1), 64, 64),
              make_lookat((1.1, -0.6, 0.5), (1.1, 0.5, 0.5), (0, 0, 1), 64, 64),
