@@ -242,6 +242,9 @@ void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s);
 // Certified fp32 blend (16x16 tiles, alpha_clamp_max <= 0.999) + the fp64 redo
 // of the flagged pixels; same outputs as launch_ua_blend (tile_score unused).
 bool ua_fast_supported(int tile_size, double amax);
+// exact fp64 blend with the tensor-core colour (16x16 tiles, RGB, split colours)
+bool ua_exact_mma_supported(const UaBlendArgs& a);
+void launch_ua_blend_exact_mma(const UaBlendArgs& a, cudaStream_t s);
 void launch_ua_blend_fast(const UaBlendArgs& a, cudaStream_t s);
 void launch_ua_redo(const UaBlendArgs& a, cudaStream_t s);
 // The staged colour form of the tensor-core colour path: its size in bytes, 0

@@ -208,7 +208,7 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
     const char* e = getenv("GAVIS_UA_KERNEL");
     return e ? atoi(e) : 0;
   }();
-  // default for 16x16 tiles: the entry-pair (ILP) kernel; GAVIS_UA_KERNEL=1 selects
+  // 16x16 tiles without the tensor-core colour: the entry-pair (ILP) kernel; GAVIS_UA_KERNEL=1 selects
   // the generic per-pixel kernel (A/B measurements). (batch 192: fewer block
   // barriers per tile list than 128; 3 CTAs of 58 KB fit)
   if (a.tile_size == 16 && choice != 1) {
@@ -259,6 +259,17 @@ void launch_lc(const UaBlendArgs& a, cudaStream_t s) {
 
 void launch_ua_blend(const UaBlendArgs& a, cudaStream_t s) {
   if (a.total_tiles == 0) return;
+  static const int choice = [] {
+    const char* e = getenv("GAVIS_UA_KERNEL");
+    return e ? atoi(e) : 0;
+  }();
+  // RGB renders on 16x16 tiles: the fp64 blend with the tensor-core colour
+  // (kernels_ua_fast.cu); GAVIS_UA_COLOR=ffma / GAVIS_UA_KERNEL=1|2 select the
+  // packed-FFMA colour kernels below (A/B)
+  if (choice == 0 && ua_exact_mma_supported(a)) {
+    launch_ua_blend_exact_mma(a, s);
+    return;
+  }
   switch (a.scene.color_degree) {
     case 0: launch_lc<0>(a, s); break;
     case 1: launch_lc<1>(a, s); break;

@@ -580,6 +580,252 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K7 exact (fp64 blend) with the tensor-core colour: the fp64 arithmetic of
+// ua_blend_ilp_kernel (kernels_ua.cu; the ex_* steps of ua_common.cuh) on K7f's
+// staging and colour machinery -- half the CTA stages the fp64 records, the
+// other half cp.asyncs the pre-split colour records; per group of 8 hit entries
+// the warp's 32 x 24 colour block comes from 18 mma.sync (split fp16, fp32
+// accumulate) instead of 8 x (12 LDS.128 + 24 FFMA2) per lane. Only the SH
+// colour dot product is affected (split-fp16 operands, ~2^-21 relative, as in
+// the certified path); alpha, both transmittances, the stop tests and every
+// accumulation stay fp64. GAVIS_UA_COLOR=ffma selects the packed-FFMA kernel.
+
+template <int LC, bool ENT>
+__device__ __forceinline__ void estage_batch(const UaBlendArgs& a, const GeoRec* geo, const UaRec* uar,
+                                             uint32_t base, int n, ExGeo* s_geo, int4* s_rect,
+                                             ExUa* s_ua, uint32_t* s_col) {
+  constexpr int kHalf = 128;
+  const int t = threadIdx.x;
+  if (t >= kHalf) {
+    uint4* dst = reinterpret_cast<uint4*>(s_col);
+    for (int j = t - kHalf; j < n; j += kHalf) {
+      const uint4* src = a.scene.colors_split + (int64_t)a.vals[base + j] * (kColWords / 4);
+#pragma unroll
+      for (int w = 0; w < kColWords / 4; ++w) cp_async16(dst + j * (kColWords / 4) + w, src + w);
+    }
+    cp_async_wait_all();
+    return;
+  }
+  for (int j = t; j < n; j += kHalf) {
+    const uint32_t g = a.vals[base + j];
+    const GeoRec r = geo[g];
+    s_geo[j] = ex_geo(r);
+    s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
+    if (ENT) s_ua[j] = ex_ua(uar[g]);
+  }
+}
+
+// Two list entries composited in fp64 (the pair step of ua_blend_ilp_kernel).
+template <int LC, bool ENT, bool EXTRA, bool LO>
+__device__ __forceinline__ void exact_pair(Pixel<LC>& P, const ExGeo& ea, const ExGeo& eb, const ExUa& ua,
+                                           const ExUa& ub, bool ca, bool cb, double cxp, double cyp,
+                                           float3 cola, float3 colb, double amax, double cutoff) {
+  const double ala = ex_alpha(ea, ex_negq(ea, cxp, cyp), amax);
+  const double alb = ex_alpha(eb, ex_negq(eb, cxp, cyp), amax);
+  const bool ra = ca && !P.rgb_done;
+  ex_rgb<LC, EXTRA>(P, ra ? ala : 0.0, ea.depth, cola.x, cola.y, cola.z);
+  const bool rd = P.rgb_done || (ra && P.T < cutoff);
+  const bool rb = cb && !rd;
+  ex_rgb<LC, EXTRA>(P, rb ? alb : 0.0, eb.depth, colb.x, colb.y, colb.z);
+  if (EXTRA) P.n_rgb += (int)ra + (int)rb;
+  P.rgb_done = rd || (rb && P.T < cutoff);
+  if (ENT) {
+    const double xa = ex_astar<LO>(ua, ala, amax), xb = ex_astar<LO>(ub, alb, amax);
+    const bool ea_on = ca && !P.ent_done;
+    const double sa = ex_ent<LC, EXTRA>(P, ea_on ? xa : 0.0, ua, ea.depth);
+    const bool ed = P.ent_done || (ea_on && P.Te < cutoff);
+    const bool eb_on = cb && !ed;
+    const double sb = ex_ent<LC, EXTRA>(P, eb_on ? xb : 0.0, ub, eb.depth);
+    const double la = log_pos(sa > 0.0 ? sa : 1.0);
+    const double lb = log_pos(sb > 0.0 ? sb : 1.0);
+    if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
+    if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
+    if (EXTRA) P.n_ent += (int)ea_on + (int)eb_on;
+    P.ent_done = ed || (eb_on && P.Te < cutoff);
+  }
+}
+
+template <bool ENT>
+struct EStage {
+  static constexpr size_t bytes(int batch) {
+    return (size_t)batch * (sizeof(ExGeo) + sizeof(int4) + (ENT ? sizeof(ExUa) : 0) +
+                            sizeof(uint32_t) * kColWords) +
+           8 * 32 * kTrStride * sizeof(float);
+  }
+};
+
+template <int LC, bool ENT, bool EXTRA, bool LO, int B>
+__global__ void __launch_bounds__(256, 3) ua_blend_exact_mma_kernel(UaBlendArgs a) {
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  ExGeo* s_geo = reinterpret_cast<ExGeo*>(s_dyn);
+  int4* s_rect = reinterpret_cast<int4*>(s_dyn + B * sizeof(ExGeo));
+  ExUa* s_ua = reinterpret_cast<ExUa*>(s_dyn + B * (sizeof(ExGeo) + sizeof(int4)));
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_dyn + B * (sizeof(ExGeo) + sizeof(int4) +
+                                                             (ENT ? sizeof(ExUa) : 0)));
+  float* s_tr = reinterpret_cast<float*>(s_col + B * kColWords);
+  load_math_tables();
+
+  const double amax = a.amax, cutoff = a.cutoff;
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tig = lane & 3;  // mma fragment coordinates
+  const int64_t N = a.scene.n;
+  const GeoRec* geo = a.geo + (int64_t)v * N;
+  const UaRec* uar = a.ua + (int64_t)v * N;
+
+  const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 4;
+  const int bx1 = bx0 + 7, by1 = by0 + 3;
+  const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+  const bool inside = px < c.width && py < c.height;
+  const double cxp = px + 0.5, cyp = py + 0.5;
+  float* tr = s_tr + warp * 32 * kTrStride;
+  uint32_t aH[2][4], aL[2][4];  // A fragments of the pixel SH basis (rows = lanes), fp16 hi / lo
+  {
+    constexpr int NB = Col<LC>::NB;
+    double bd[Col<LC>::NBP];
+    pixel_basis_d<LC>(c, px, py, bd);
+    uint32_t* wb = reinterpret_cast<uint32_t*>(tr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float x0 = 2 * i < NB ? (float)bd[2 * i] : 0.f;
+      const float x1 = 2 * i + 1 < NB ? (float)bd[2 * i + 1] : 0.f;
+      uint32_t h, l;
+      split_half2(x0, x1, h, l);
+      wb[lane * 17 + i] = h;
+      wb[lane * 17 + 8 + i] = l;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int r0 = 16 * m + gq, r1 = r0 + 8;
+      aH[m][0] = wb[r0 * 17 + tig];
+      aH[m][1] = wb[r1 * 17 + tig];
+      aH[m][2] = wb[r0 * 17 + tig + 4];
+      aH[m][3] = wb[r1 * 17 + tig + 4];
+      aL[m][0] = wb[r0 * 17 + 8 + tig];
+      aL[m][1] = wb[r1 * 17 + 8 + tig];
+      aL[m][2] = wb[r0 * 17 + 8 + tig + 4];
+      aL[m][3] = wb[r1 * 17 + 8 + tig + 4];
+    }
+    __syncwarp();
+  }
+  Pixel<LC> P;
+  P.T = P.Te = 1.0;
+  P.rgb0 = P.rgb1 = P.rgb2 = P.dep = 0.0;
+  P.H = P.w0 = P.edep = 0.0;
+  P.rgb_done = !inside;
+  P.ent_done = !(ENT && inside);
+  P.n_rgb = P.n_ent = 0;
+  const ColWordsStaged colword;
+
+  for (uint32_t base = rg.x; base < rg.y; base += B) {
+    const bool live = !(P.rgb_done && P.ent_done);
+    if (__syncthreads_count(live) == 0) break;
+    const int n = min((uint32_t)B, rg.y - base);
+    estage_batch<LC, ENT>(a, geo, uar, base, n, s_geo, s_rect, s_ua, s_col);
+    __syncthreads();
+    if (__all_sync(0xffffffffu, !live)) continue;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      if (__all_sync(0xffffffffu, P.rgb_done && P.ent_done)) break;
+      bool hit = false;
+      if (j0 + lane < n) {
+        const int4 r = s_rect[j0 + lane];
+        hit = r.x <= bx1 && r.x + r.y >= bx0 && r.z <= by1 && r.z + r.w >= by0;
+      }
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      while (hits != 0u) {
+        int je[8];
+        int ng = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          je[q] = hits != 0u ? j0 + __ffs(hits) - 1 : -1;
+          ng += hits != 0u ? 1 : 0;
+          hits &= hits - 1u;
+        }
+        if (__any_sync(0xffffffffu, !P.rgb_done)) {
+          int my_e = -1;  // B fragment column gq = entry gq of the group
+#pragma unroll
+          for (int q = 0; q < 8; ++q) my_e = gq == q ? je[q] : my_e;
+          uint32_t bh[3][2], bl[3][2];
+          const int e = max(my_e, 0);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const int w0 = colword(e, ch, tig), w1 = colword(e, ch, tig + 4);
+            bh[ch][0] = my_e >= 0 ? s_col[w0] : 0u;
+            bh[ch][1] = my_e >= 0 ? s_col[w1] : 0u;
+            bl[ch][0] = my_e >= 0 ? s_col[w0 + ColWordsStaged::kLo] : 0u;
+            bl[ch][1] = my_e >= 0 ? s_col[w1 + ColWordsStaged::kLo] : 0u;
+          }
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              float d[4] = {0.f, 0.f, 0.f, 0.f};
+              hmma16816(d, aH[m], bh[ch][0], bh[ch][1]);
+              hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
+              hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
+              const int r0 = 16 * m + gq, r1 = r0 + 8;
+              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
+            }
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          if (q < ng) {
+            const int ja = je[q];
+            const bool has_b = q + 1 < ng;
+            const int jb = has_b ? je[q + 1] : ja;
+            const bool ca = in_rect4(s_rect[ja], px, py);
+            const bool cb = has_b && in_rect4(s_rect[jb], px, py);
+            const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
+            const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
+            const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+            const float3 cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
+            const float3 colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
+            exact_pair<LC, ENT, EXTRA, LO>(P, s_geo[ja], s_geo[jb], s_ua[ENT ? ja : 0], s_ua[ENT ? jb : 0], ca,
+                                           cb, cxp, cyp, cola, colb, amax, cutoff);
+          }
+        }
+        __syncwarp();  // the next group overwrites the colour block
+      }
+    }
+  }
+  pixel_finish<LC, true, ENT, EXTRA>(P, a, c, px, py, inside);
+}
+
+template <int LC, bool ENT, bool EXTRA, bool LO>
+void launch_exact_mma(const UaBlendArgs& a, cudaStream_t s) {
+  constexpr int B = 128;
+  const size_t sm = EStage<ENT>::bytes(B);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ua_blend_exact_mma_kernel<LC, ENT, EXTRA, LO, B>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  ua_blend_exact_mma_kernel<LC, ENT, EXTRA, LO, B><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+}
+
+template <int LC, bool EXTRA>
+void launch_exact_mma_lc(const UaBlendArgs& a, cudaStream_t s) {
+  if (a.do_ent) {
+    if (a.vis_outside_unit)
+      launch_exact_mma<LC, true, EXTRA, true>(a, s);
+    else
+      launch_exact_mma<LC, true, EXTRA, false>(a, s);
+  } else {
+    launch_exact_mma<LC, false, EXTRA, false>(a, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K7r: exact fp64 recomputation of the flagged pixels, one warp per pixel.
 // The lanes walk the pixel's tile list 32 entries at a time: each lane loads
 // its entry, tests coverage and, if covered, evaluates the entry's fp64 alpha,
@@ -809,6 +1055,30 @@ void launch_ua_blend_fast(const UaBlendArgs& a, cudaStream_t s) {
     GAVIS_FAST_LC(2)
     GAVIS_FAST_LC(3)
 #undef GAVIS_FAST_LC
+    default: break;
+  }
+}
+
+bool ua_exact_mma_supported(const UaBlendArgs& a) {
+  return a.tile_size == 16 && a.do_rgb && a.scene.colors_split != nullptr && colour_mma();
+}
+
+void launch_ua_blend_exact_mma(const UaBlendArgs& a, cudaStream_t s) {
+  if (a.total_tiles == 0) return;
+  const bool extra = a.depth || a.edepth || a.rgb_contrib || a.ent_contrib || a.corr_lambda > 0.0;
+  switch (a.scene.color_degree) {
+#define GAVIS_EXACT_LC(L)                 \
+  case L:                                 \
+    if (extra)                            \
+      launch_exact_mma_lc<L, true>(a, s); \
+    else                                  \
+      launch_exact_mma_lc<L, false>(a, s); \
+    break;
+    GAVIS_EXACT_LC(0)
+    GAVIS_EXACT_LC(1)
+    GAVIS_EXACT_LC(2)
+    GAVIS_EXACT_LC(3)
+#undef GAVIS_EXACT_LC
     default: break;
   }
 }
