@@ -356,10 +356,16 @@ def run_ours(args):
     degree = c["degree"]
     train = c["train"]
 
+    # the library's own NCCL communicator (gavis_comm): the VF all-reduce and the
+    # score all-gather of the sharded paths run inside libgavis_b200.so
+    comm = api.Comm.from_dist(ctx, dist) if world > 1 else None
+
     # ---------------- VF CONST: sharded views + NCCL all-reduce --------------
     def build_field(views, dscene=None, deg=None):
-        return parallel.construct_device_field_sharded(ctx, dscene or ds, views, vmf,
-                                                       degree if deg is None else deg, rank, world, dist, rc)
+        deg = degree if deg is None else deg
+        if comm is not None:
+            return api.construct_field_sharded(comm, dscene or ds, views, vmf, deg, rc)
+        return parallel.construct_device_field_sharded(ctx, dscene or ds, views, vmf, deg, rank, world, dist, rc)
 
     field = build_field(train)  # warm-up + the field used for scoring
     barrier(ctx, dist)
@@ -388,9 +394,9 @@ def run_ours(args):
     def step():
         if world == 1:
             return api.select_nbv(ctx, ds, field, cands, rc, uc, with_rgb=True)
-        # global argmax: scores all-gathered, contenders re-scored in fp64 on their ranks
-        return api.select_nbv_sharded(ctx, ds, field, c["candidates"], rank, world, dist, rc, uc,
-                                      with_rgb=True)
+        # global argmax: each rank scores its block, the library all-gathers the
+        # scores over NCCL, contenders are re-scored in fp64 on their ranks
+        return api.select_nbv_comm(comm, ds, field, c["candidates"], rc, uc, with_rgb=True)
 
     KERNELS = ("ua_blend", "ua_redo", "preprocess", "sort", "depth_order", "scan",
                "emit_keys", "ranges", "score")
@@ -574,7 +580,7 @@ def run_ours(args):
     # ---------------- config 5: active-mapping iteration sweep ---------------
     sweep5 = None
     if not args.no_sweep5:
-        sweep5 = run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc)
+        sweep5 = run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc, comm)
 
     # ---------------- CPU baseline + oracle parity gate ----------------------
     cpu, parity_gate = None, None
@@ -594,7 +600,8 @@ def run_ours(args):
             "config": {"workload": f"config{args.config}", "particles": N, "resolution": [cands[0].width, cands[0].height],
                        "candidates_per_gpu_per_step": len(cands), "training_views": len(train),
                        "field_degree": degree, "color_degree": scene.color_degree,
-                       "parallelism": f"candidates sharded over {world} GPU(s), VF views sharded + NCCL all-reduce",
+                       "parallelism": f"candidates sharded over {world} GPU(s), VF views sharded + NCCL all-reduce"
+                                      + (" (libgavis_b200 gavis_comm)" if world > 1 else ""),
                        "l2": "inputs (scene+field) exceed the 126 MB L2; no flush"},
             "roofline": roofline(head, head_prec),
             "pipeline": {"bytes_per_step": pipe_bytes, "achieved_gbs": pipe_bytes / (head["ms_local"] / args.steps / 1000.0) / 1e9,
@@ -623,6 +630,8 @@ def run_ours(args):
         if sweep5:
             line["config5_sweep"] = sweep5
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -685,7 +694,7 @@ def oracle_gate(args, ctx, api, c, ds, field, cands, rc, uc):
     return gate, cpu
 
 
-def run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc):
+def run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc, comm=None):
     """Config 5 (BASELINE.json): the config-2 scene, 20 active-mapping rounds, each
     scoring the candidate pool at 400^2 and appending the chosen view to the field
     incrementally (linearity, test_vfield.cpp:104-131), at 512..4096 candidates.
@@ -705,7 +714,7 @@ def run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc):
                 return [int(x) for x in chosen]
             chosen = []
             for _ in range(rounds):
-                r = api.select_nbv_sharded(ctx, ds5, f, pool, rank, world, dist, rc, uc)
+                r = api.select_nbv_comm(comm, ds5, f, pool, rc, uc)
                 chosen.append(int(r.best_index))
                 api.accumulate_views(ctx, f, ds5, [pool[r.best_index]], rc)  # num_views += 1
             return chosen

@@ -71,7 +71,7 @@ class MappingConfigC(C.Structure):
 EXPORTS = [
     "gavis_abi_version", "gavis_last_error", "gavis_ctx_create", "gavis_ctx_destroy",
     "gavis_ctx_synchronize", "gavis_ctx_set_batch", "gavis_ctx_set_pair_budget", "gavis_ctx_set_precision",
-    "gavis_ctx_get_counters", "gavis_ctx_set_profiling",
+    "gavis_ctx_get_counters", "gavis_ctx_last_score_bounds", "gavis_ctx_set_profiling",
     "gavis_ctx_kernel_time", "gavis_ctx_timer_start", "gavis_ctx_timer_stop",
     "gavis_ctx_launch_count", "gavis_scene_upload", "gavis_scene_destroy",
     "gavis_scene_set_coeff_variances",

@@ -134,6 +134,15 @@ class Context:
         N.check(self.lib.gavis_ctx_get_counters(self.h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def last_score_bounds(self) -> np.ndarray:
+        """Per-candidate bounds on |certified score - fp64 score| of the last scored
+        render (empty unless certified, constant provider, no correlation hook)."""
+        n = C.c_int32()
+        N.check(self.lib.gavis_ctx_last_score_bounds(self.h, None, C.c_int32(0), C.byref(n)))
+        out = np.zeros(max(1, n.value))
+        N.check(self.lib.gavis_ctx_last_score_bounds(self.h, _ptr(out), C.c_int32(out.size), C.byref(n)))
+        return out[: n.value]
+
     def set_profiling(self, on: bool) -> None:
         N.check(self.lib.gavis_ctx_set_profiling(self.h, C.c_int32(1 if on else 0)))
 

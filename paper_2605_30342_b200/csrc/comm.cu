@@ -244,26 +244,42 @@ gavis_status gavis_select_nbv_sharded(gavis_comm* cm, const gavis_scene* s, cons
     }
     // this rank's block, scored into a padded slot of the gather buffer
     std::vector<double> mine((size_t)std::max<int64_t>(1, width), 0.0);
+    c->score_bounds.clear();
     if (hi > lo) {
       gavis_render_outputs o = {};
       o.scores = mine.data();
       o.with_rgb = with_rgb;
       ua_render(c, s, f, nullptr, cams + lo, (int)(hi - lo), rc, uc, &o);
     }
-    double* dsend = (double*)c->buf("nbv_send", sizeof(double) * width);
-    double* drecv = (double*)c->buf("nbv_recv", sizeof(double) * width * W);
-    CK(cudaMemcpyAsync(dsend, mine.data(), sizeof(double) * width, cudaMemcpyHostToDevice, c->stream));
-    nck(nccl().all_gather(dsend, drecv, (size_t)width, ncclFloat64, cm->comm, c->stream),
+    // scores and (certified mode) their error bounds, gathered in one call:
+    // [scores | bounds] per rank, padded to the widest block
+    const bool bounded = hi > lo ? c->score_bounds.size() == (size_t)(hi - lo)
+                                 : c->precision == GAVIS_PRECISION_CERTIFIED;
+    std::vector<double> send((size_t)(2 * width), 0.0);
+    std::copy(mine.begin(), mine.begin() + (hi - lo), send.begin());
+    if (bounded && hi > lo) std::copy(c->score_bounds.begin(), c->score_bounds.end(), send.begin() + width);
+    double* dsend = (double*)c->buf("nbv_send", sizeof(double) * 2 * width);
+    double* drecv = (double*)c->buf("nbv_recv", sizeof(double) * 2 * width * W);
+    CK(cudaMemcpyAsync(dsend, send.data(), sizeof(double) * 2 * width, cudaMemcpyHostToDevice, c->stream));
+    nck(nccl().all_gather(dsend, drecv, (size_t)(2 * width), ncclFloat64, cm->comm, c->stream),
         "ncclAllGather(scores)");
-    std::vector<double> all((size_t)(width * W));
-    CK(cudaMemcpyAsync(all.data(), drecv, sizeof(double) * width * W, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> all((size_t)(2 * width * W));
+    CK(cudaMemcpyAsync(all.data(), drecv, sizeof(double) * 2 * width * W, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
-    std::vector<double> sc((size_t)n_cams);
+    std::vector<double> sc((size_t)n_cams), bd((size_t)n_cams);
     for (int r = 0; r < W; ++r) {
       int64_t a, b;
       block_of(n_cams, r, W, &a, &b);
-      std::copy(all.begin() + (size_t)r * width, all.begin() + (size_t)r * width + (b - a), sc.begin() + a);
+      const size_t o = (size_t)r * 2 * width;
+      std::copy(all.begin() + o, all.begin() + o + (b - a), sc.begin() + a);
+      std::copy(all.begin() + o + width, all.begin() + o + width + (b - a), bd.begin() + a);
     }
+    // every rank holds the same bounds: the contender window is rank-independent
+    // (a rank whose block was empty learns the mode from its context)
+    int any_bounds = 0;
+    for (double x : bd) any_bounds |= x > 0.0;
+    if (any_bounds) c->score_bounds = bd;
+    else c->score_bounds.clear();
     // certified mode: contenders re-scored in fp64 by their owners, summed over ranks
     std::vector<int> cont = certified_contenders(c, rc, sc);
     if (cont.size() >= 2) {

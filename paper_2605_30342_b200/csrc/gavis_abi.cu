@@ -79,6 +79,7 @@ gavis_status gavis_ctx_destroy(gavis_ctx* c) {
     if (c->t1) cudaEventDestroy(c->t1);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pin_scores) cudaFreeHost(c->pin_scores);
+    if (c->pin_bounds) cudaFreeHost(c->pin_bounds);
     for (cudaStream_t st : {c->side, c->front})
       if (st) {
         cudaStreamSynchronize(st);
@@ -126,6 +127,20 @@ gavis_status gavis_ctx_set_precision(gavis_ctx* c, int32_t precision) {
             "precision must be GAVIS_PRECISION_CERTIFIED or GAVIS_PRECISION_EXACT");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->precision = precision;
+  });
+}
+
+gavis_status gavis_ctx_last_score_bounds(gavis_ctx* c, double* bounds, int32_t capacity,
+                                         int32_t* n_out) {
+  return guard([&] {
+    require(c && n_out, "null argument");
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    const int32_t n = (int32_t)c->score_bounds.size();
+    *n_out = n;
+    if (bounds && n > 0) {
+      require(capacity >= n, "score bounds: capacity too small");
+      std::memcpy(bounds, c->score_bounds.data(), sizeof(double) * n);
+    }
   });
 }
 

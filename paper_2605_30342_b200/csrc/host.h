@@ -262,7 +262,11 @@ struct gavis_ctx {
   int64_t launches = 0;
   int32_t* pinned = nullptr;
   double* pin_scores = nullptr;  // pinned staging of per-view scores (async D2H on `side`)
+  double* pin_bounds = nullptr;  // pinned staging of per-view certified score-error bounds
   int64_t pin_scores_cap = 0;
+  // certified score-error bounds of the last ua_render that produced scores
+  // (empty when not certified / not bounded); read by certified_contenders
+  std::vector<double> score_bounds;
   int precision = GAVIS_PRECISION_CERTIFIED;
   int64_t redo_pixels = 0;       // pixels the certified blend handed to the fp64 redo
   double batch_budget = 0.0;     // bytes of per-(view, particle) state one batch may use

@@ -175,6 +175,13 @@ struct UaBlendArgs {
   float cert_sum = 0.f;            // relative window per unit of sum a/(1-a)
   float cert_per_step2 = 0.f;      // second bound (small-alpha steps folded into S)
   float cert_sum2 = 0.f;
+  // Rigorous bound on |H_fp32 - H_fp64| per pixel (certified path, constant
+  // variance provider, no correlation hook): written when non-null; folded per
+  // view like the score (kernels_ua_fast.cu header, "score bound").
+  double* score_bound = nullptr;   // [total_pix]
+  double bound_tail = 0.0;         // per composited entry: 1.7e-3 u o_max (|c| + 89)
+  double w0_tail = 0.0;            // per composited entry: 1.7e-3 u o_max
+  double c0_abs = 0.0;             // |1/2 ln|Q0| + C_H| of the prior term
 };
 
 // Per-pixel mixtures of the entropy track for one view (kernels_mixture.cu).

@@ -13,6 +13,8 @@ namespace host {
 // Opacities above 1 (not excluded by the reference) weaken the alpha-error
 // bounds (q <= 2 ln(o_max / a); A a (1.5 q + 8) <= 8 o_max A): the S coefficient
 // becomes 22 o_max + 6 ln(o_max) (22 for o_max <= 1).
+constexpr double kGaussEntropyHost = 4.256815599614018;  // uncertainty.hpp:19
+
 void cert_window(UaBlendArgs* ua, float max_opacity) {
   const double u = std::ldexp(1.0, -24);
   const double om = std::max(1.0, (double)max_opacity);
@@ -73,11 +75,17 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   if (out->scores && n > c->pin_scores_cap) {
     c->sync_all();
     if (c->pin_scores) CK(cudaFreeHost(c->pin_scores));
-    c->pin_scores = nullptr;
+    if (c->pin_bounds) CK(cudaFreeHost(c->pin_bounds));
+    c->pin_scores = c->pin_bounds = nullptr;
     c->pin_scores_cap = 0;
     CK(cudaMallocHost(&c->pin_scores, sizeof(double) * n));
+    CK(cudaMallocHost(&c->pin_bounds, sizeof(double) * n));
     c->pin_scores_cap = n;
   }
+  // certified scores carry a rigorous error bound (kernels_ua_fast.cu, "score
+  // bound") for the constant variance provider without the correlation hook
+  const bool bounded = fast && out->scores && uc->variance_provider == 0 && uc->correlation == 0;
+  c->score_bounds.clear();
   CK(cudaEventRecord(c->ev_done[0], c->stream));  // side / front work start after this point
   CK(cudaStreamWaitEvent(c->side, c->ev_done[0], 0));
   CK(cudaStreamWaitEvent(c->front, c->ev_done[0], 0));
@@ -181,6 +189,14 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       ua.flag_count = (uint32_t*)c->buf("flag_count", sizeof(uint32_t));
       CK(cudaMemsetAsync(ua.flag_count, 0, sizeof(uint32_t), c->stream));
       cert_window(&ua, s->max_opacity);
+      if (bounded) {
+        ua.score_bound = (double*)c->buf("img_bound", sizeof(double) * P);
+        const double u = std::ldexp(1.0, -24);
+        const double cabs = std::fabs(ua.hl_qc + kGaussEntropyHost);
+        ua.w0_tail = 1.7e-3 * u * std::max(1.0, (double)s->max_opacity);
+        ua.bound_tail = ua.w0_tail * (cabs + 89.0);
+        ua.c0_abs = std::fabs(hl_q0 + kGaussEntropyHost);
+      }
       c->run("ua_blend", [&] { launch_ua_blend_fast(ua, c->stream); });
       CK(cudaEventRecord(c->ev_blend[par], c->stream));
       CK(cudaStreamWaitEvent(side, c->ev_blend[par], 0));
@@ -192,12 +208,20 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       CK(cudaStreamWaitEvent(side, c->ev_blend[par], 0));
     }
     double* dscores = nullptr;
+    double* dbounds = nullptr;
     if (do_ent) {
       dscores = (double*)c->buf("scores", sizeof(double) * V);
       double* part = (double*)c->buf("score_partial", sizeof(double) * V * score_partials_per_view());
       c->run("score", [&] {
         launch_score_image(b.dcams, V, ua.entropy, ua.edepth, ua.corr_lambda, part, dscores, side);
       }, 1, side);
+      if (ua.score_bound) {  // the bound image folds like the score (fixed order)
+        dbounds = (double*)c->buf("score_bounds", sizeof(double) * V);
+        double* bpart = (double*)c->buf("bound_partial", sizeof(double) * V * score_partials_per_view());
+        c->run("score", [&] {
+          launch_score_image(b.dcams, V, ua.score_bound, nullptr, 0.0, bpart, dbounds, side);
+        }, 1, side);
+      }
     }
     copy_out(c, out->rgb ? out->rgb + 3 * pix_done : nullptr, ua.rgb, 3 * P, side);
     copy_out(c, out->depth ? out->depth + pix_done : nullptr, ua.depth, P, side);
@@ -208,6 +232,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
     // scores through pinned staging: a D2H copy into pageable memory would block
     // the host on this batch's side-stream work and serialise the batches
     copy_out(c, out->scores ? c->pin_scores + v0 : nullptr, dscores, V, side);
+    copy_out(c, dbounds ? c->pin_bounds + v0 : nullptr, dbounds, V, side);
     if (out->rgb_contributors)
       CK(cudaMemcpyAsync(out->rgb_contributors + pix_done, ua.rgb_contrib, sizeof(int32_t) * P,
                          cudaMemcpyDeviceToHost, side));
@@ -227,6 +252,11 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   }
   c->sync_all();
   if (out->scores && n > 0) std::memcpy(out->scores, c->pin_scores, sizeof(double) * n);
+  if (bounded && n > 0) {
+    // fp64 folds of non-negative terms: relative rounding far below 1e-12
+    c->score_bounds.assign(c->pin_bounds, c->pin_bounds + n);
+    for (double& bd : c->score_bounds) bd *= 1.0 + 1e-12;
+  }
   if (redo_total) c->redo_pixels += (int64_t)*reinterpret_cast<unsigned long long*>(c->pinned + kPinRedo);
 }
 
@@ -237,6 +267,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
 // the fp64 ones to a few 1e-6 relative -- 3e-6 at config 3 -- over two orders of
 // magnitude inside the window).
 constexpr double kCertScoreRel = 1e-3;
+constexpr double kCertScoreAbs = 1e-9;  // absolute floor: scores near 0 keep a window
 
 std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* rc,
                                       const std::vector<double>& sc) {
@@ -247,9 +278,15 @@ std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* r
   int b = 0;
   for (int i = 1; i < (int)sc.size(); ++i)
     if (sc[i] > sc[b]) b = i;
-  const double lo = sc[b] - kCertScoreRel * std::fabs(sc[b]);
-  for (int i = 0; i < (int)sc.size(); ++i)
-    if (sc[i] >= lo) cont.push_back(i);
+  // candidate i can hold the fp64 maximum only if s_i + e_i >= s_b - e_b, with
+  // e the rigorous per-view bounds of the certified scores (when available);
+  // the window is never narrower than kCertScoreRel |s_b| nor kCertScoreAbs
+  const bool have = c->score_bounds.size() == sc.size();
+  for (int i = 0; i < (int)sc.size(); ++i) {
+    const double bound = have ? c->score_bounds[b] + c->score_bounds[i] : 0.0;
+    const double window = std::max({bound, kCertScoreRel * std::fabs(sc[b]), kCertScoreAbs});
+    if (sc[i] >= sc[b] - window) cont.push_back(i);
+  }
   return cont;
 }
 

@@ -54,15 +54,21 @@ def gather_scores(local: np.ndarray, n_total: int, rank: int, world: int, dist=N
     return np.concatenate(out) if out else np.zeros(0)
 
 
-CERT_SCORE_REL = 1e-3  # same window as the library's single-GPU select (ua_host.cu)
+CERT_SCORE_REL = 1e-3  # same window as the library's select (ua_host.cu kCertScoreRel)
+CERT_SCORE_ABS = 1e-9  # absolute floor (kCertScoreAbs)
 
 
-def contenders(scores: np.ndarray, window: float = CERT_SCORE_REL) -> List[int]:
-    """Candidates whose certified fp32 score lies within `window` (relative) of the
-    best: the only ones that can be the fp64 argmax."""
+def contenders(scores: np.ndarray, window: float = CERT_SCORE_REL, bounds=None) -> List[int]:
+    """Candidates that can hold the fp64 maximum given certified scores: i with
+    s_i >= s_b - max(e_b + e_i, window |s_b|, CERT_SCORE_ABS), e the rigorous
+    per-candidate error bounds when known (Context.last_score_bounds)."""
     b = first_max(scores)
-    lo = scores[b] - window * abs(scores[b])
-    return [i for i in range(len(scores)) if scores[i] >= lo]
+    out = []
+    for i in range(len(scores)):
+        e = (bounds[b] + bounds[i]) if bounds is not None else 0.0
+        if scores[i] >= scores[b] - max(e, window * abs(scores[b]), CERT_SCORE_ABS):
+            out.append(i)
+    return out
 
 
 def select_nbv_sharded(score_block: Callable[[int, int], np.ndarray], n_candidates: int, rank: int,

@@ -424,3 +424,64 @@ def test_pair_budget_splits_batches(ctx, room):
     for k in a:
         assert np.array_equal(a[k], b[k]), k
     assert sel.best_index == api.select_nbv(ctx, ds, f, cams, RC, UC).best_index
+
+
+def _scores_and_bounds(ctx, ctx_exact, scene, f, cams, uc=UC):
+    cert = api.render(ctx, scene, f, cams, RC, uc, scores=True)["scores"]
+    bounds = ctx.last_score_bounds()
+    exact = api.render(ctx_exact, scene, f, cams, RC, uc, scores=True)["scores"]
+    return cert, bounds, exact
+
+
+@pytest.mark.parametrize("which", ["config1", "room", "fuzz"])
+def test_certified_score_bounds_hold(ctx, ctx_exact, room, which):
+    """The per-candidate score bound (kernels_ua_fast.cu, "score bound") is a
+    rigorous bound on |certified - fp64 score|: it must hold on every candidate,
+    and be tight enough to matter (well under the 1e-3 relative floor)."""
+    if which == "config1":
+        c = synth.config1(0)
+    elif which == "room":
+        c = room
+    else:
+        c = synth.config1(7)
+        c["scene"].opacities[:] = np.minimum(c["scene"].opacities * 1.6, 0.999)  # near the clamp
+    scene = c["scene"]
+    f = api.construct_field(ctx_exact, scene, c["train"], VmfParams(1.0), 2, RC)
+    cams = c["candidates"][:6]
+    cert, bounds, exact = _scores_and_bounds(ctx, ctx_exact, scene, f, cams)
+    assert bounds.shape == (len(cams),) and np.all(bounds > 0)
+    assert np.all(np.abs(cert - exact) <= bounds), (np.abs(cert - exact), bounds)
+    assert np.all(bounds <= 1e-3 * np.abs(exact))
+    # the hook and sh_propagation fall back to the relative window: no bounds
+    api.render(ctx, scene, f, cams[:1], RC, UncertaintyConfig(correlation=1, correlation_lambda=2.0),
+               scores=True)
+    assert ctx.last_score_bounds().size == 0
+
+
+def test_certified_argmax_near_ties_around_zero(ctx, ctx_exact):
+    """Scores near 0 (colour_sigma chosen so the fp64 score of the base view is
+    ~0) with candidates a few 1e-9 rad apart: a purely relative window (1e-3
+    |best|) would be empty; the bound-based window re-scores the near-ties in
+    fp64 and the argmax is the fp64 one."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    f = api.construct_field(ctx_exact, scene, c["train"], VmfParams(1.0), 2, RC)
+    base = c["candidates"][3]
+    # score(hl) is affine in hl = 3 ln sigma (d score / d hl = sum of s): solve score = 0
+    s1 = api.render(ctx_exact, scene, f, [base], RC, UncertaintyConfig(color_sigma=0.1), scores=True)["scores"][0]
+    s2 = api.render(ctx_exact, scene, f, [base], RC, UncertaintyConfig(color_sigma=0.2), scores=True)["scores"][0]
+    h1, h2 = 3 * np.log(0.1), 3 * np.log(0.2)
+    hz = h1 - s1 * (h2 - h1) / (s2 - s1)
+    uc = UncertaintyConfig(color_sigma=float(np.exp(hz / 3)))
+    cams = []
+    for k in range(6):
+        eps = 2e-9 * (k - 2.5)
+        cams.append(make_lookat(np.asarray(base.position) + np.array([eps, -eps, eps]),
+                                np.asarray(base.position) + np.asarray(base.rotation)[:, 2], (0, 0, 1),
+                                base.width, base.height, base.fov_h, base.fov_v))
+    exact = api.select_nbv(ctx_exact, scene, f, cams, RC, uc)
+    assert np.max(np.abs(exact.scores)) < 1e-3 * np.max(np.abs(s1)), "scores are not near zero"
+    before = ctx.counters()[1]
+    cert = api.select_nbv(ctx, scene, f, cams, RC, uc)
+    assert cert.best_index == exact.best_index
+    assert ctx.counters()[1] - before >= 2  # near-ties went to the fp64 re-scoring

@@ -134,3 +134,27 @@ def test_first_max_rule():
     assert parallel.first_max([1.0, 3.0, 3.0, 2.0]) == 1
     assert parallel.first_max([5.0]) == 0
     assert parallel.first_max([2.0, 2.0, 2.0]) == 0
+
+
+def test_contenders_window_bounds_and_floor():
+    """The certified argmax window (ua_host.cu certified_contenders): per-candidate
+    error bounds widen it; near score 0 the relative part vanishes and the bound /
+    absolute floor keep the near-ties."""
+    s = np.array([1e-12, -1e-12, 3e-12, -5.0])
+    assert parallel.contenders(s) == [0, 1, 2]               # absolute floor 1e-9
+    assert parallel.contenders(s, bounds=np.full(4, 2.6)) == [0, 1, 2, 3]
+    big = np.array([100.0, 99.95, 99.0])
+    assert parallel.contenders(big) == [0, 1]                  # 1e-3 relative
+    assert parallel.contenders(big, bounds=np.array([0.6, 0.6, 0.6])) == [0, 1, 2]
+
+
+def test_sharded_field_records_trajectory_length():
+    """every rank's field must carry num_views = |P| after the
+    all-reduce (query_visibility uses it as the exponent), not its block size."""
+    class F:
+        num_views = 0
+
+    for rank in range(3):
+        fld = parallel.construct_field_sharded(lambda lo, hi: F(), 10, rank, 3, lambda f: None,
+                                               lambda f, n: setattr(f, "num_views", n))
+        assert fld.num_views == 10
