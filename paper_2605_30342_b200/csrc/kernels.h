@@ -182,6 +182,7 @@ struct UaBlendArgs {
   double bound_tail = 0.0;         // per composited entry: 1.7e-3 u o_max (|c| + 89)
   double w0_tail = 0.0;            // per composited entry: 1.7e-3 u o_max
   double c0_abs = 0.0;             // |1/2 ln|Q0| + C_H| of the prior term
+  double c_ent = 0.0;              // c = 3 ln sigma_c + C_H of every entry
 };
 
 // Per-pixel mixtures of the entropy track for one view (kernels_mixture.cu).

@@ -227,7 +227,6 @@ struct FPix {
   float T, Tp, r0, r1, r2, dp;
   float Te, Tep, h, w0, ed;
   float S, Se;  // sum a/(1-a) over composited entries, per track (error bound)
-  float E1;     // sum s (|c - ln s| + 1) over the entropy track (score bound)
   double R0, R1, R2, DP, H, W0, ED;
   int n_rgb, n_ent;
   bool rd, edn;
@@ -258,29 +257,35 @@ __device__ __forceinline__ float cert_window_of(const UaBlendArgs& a, float k, f
 // Score bound: a rigorous bound on |H_fp32 - H_fp64| of one pixel's entropy
 // (the certified select_nbv widens its fp64 re-scoring window by the folded
 // bounds of the best and of each candidate, so its argmax is the fp64 one).
-// Per composited entry the entropy term is s (c - ln s), s = a* T* v, c =
-// 1/2 ln|Q_c| + C_H (constant provider). With u = 2^-24:
+// Per composited entry the entropy term is s (c - ln s), s = a* T* v, with one
+// c = 3 ln sigma_c + C_H for every entry (constant provider). With u = 2^-24:
 //  * T* is within eps_T = u (22 S + 3.2 k + 16) (relative; the stop-test bound
 //    above, half the certification window) for every k;
 //  * |da*| <= [A a (1.5 q + 8) + 3 a*] u with A a <= a*: <= 41 u a* for
 //    q <= 20, and A a (1.5 q + 8) <= o e^-10 38 <= 1.7e-3 o for q > 20;
 //  * so |ds| <= s (eps_T + 43 u) + 1.7e-3 u o_max T v, and
 //    |d(s (c - ln s))| <= |ds| (|c - ln s| + 1) + s (lg2.approx: 1.65e-7 abs,
-//    the inner fmaf: u |c - ln s|) with |c - ln s| + 1 <= |c| + 89 (s >= 1e-37);
-//  * the fp32 running sum h of a 32-entry chunk rounds <= u |h| <= u E1 per
-//    step (<= 32 steps per chunk), its fp64 folds are exact to 1e-16;
+//    the inner fmaf: u |c - ln s|), |c - ln s| + 1 <= |c| + 89 (s >= 1e-37);
+//  * the fp32 running sum of a 32-entry chunk rounds by <= u E1 per step
+//    (<= 32 steps per chunk); its fp64 folds are exact to 1e-16;
+//  * E1 = sum s (|c - ln s| + 1) needs no per-entry work: sum s <= sum w =
+//    1 - T*_final (telescoping) <= W = 1 - T* + eps_T T*, and
+//    sum s |ln s| = H_e - c sum s <= H_e + max(0, -c) W (H_e the entries' part
+//    of H), so E1 <= (|c| + 1) W + max(0, H_e + max(0, -c) W);
 //  * W0 = sum w (1 - v) is within (eps_T + 75 u) W0 + 1.7e-3 u o_max k, and
 //    H0 = W0 (c0 - ln W0) moves by at most |dW0| max |c0 - ln W - 1| over
 //    [W0 - dW0, W0 + dW0] (or 2 (W0 + dW0)(|c0| + 1 + |ln(W0 + dW0)|) if that
 //    interval reaches 0).
-// E1 = sum s (|t| + 1) is accumulated in fp32 (relative error ~k u, covered by
-// the final 1.01 factor).
-__device__ __forceinline__ double score_bound_px(const UaBlendArgs& a, float E1, double W0, double H,
+// The 1.01 factor covers evaluating the bound from computed (fp32) quantities.
+__device__ __forceinline__ double score_bound_px(const UaBlendArgs& a, double He, double W0, double Te,
                                                  int k, float Se) {
   const double u = 5.9604644775390625e-8;
   const double eps_t = 0.5 * (double)cert_window_of(a, (float)k, Se);
-  const double e1 = (double)E1;
-  double b = (eps_t + 76.0 * u + 1.65e-7) * e1 + a.bound_tail * (double)k;
+  const double W = fmin(1.0, 1.0 - Te + eps_t * Te);
+  const double cneg = fmax(0.0, -a.c_ent);
+  const double e1 = (fabs(a.c_ent) + 1.0) * W + fmax(0.0, 1.001 * He + cneg * W);
+  // (+ 1e-36 per entry: terms of s below fp32's normal range, flushed to zero)
+  double b = (eps_t + 76.0 * u + 1.65e-7) * e1 + (a.bound_tail + 1e-36) * (double)k;
   const double dw = (eps_t + 75.0 * u) * W0 + a.w0_tail * (double)k;
   if (W0 > dw) {
     const double lm = fmax(fabs(log(W0 - dw)), fabs(log(W0 + dw)));
@@ -289,7 +294,7 @@ __device__ __forceinline__ double score_bound_px(const UaBlendArgs& a, float E1,
     const double wt = W0 + dw;
     b += wt > 0.0 ? 2.0 * wt * (a.c0_abs + 1.0 + fabs(log(wt))) : 0.0;
   }
-  return 1.01 * b + 1e-12 * fabs(H);
+  return 1.01 * b + 1e-12 * (fabs(He) + W0);
 }
 
 // Distance of a track's termination tests from the cutoff, relative.
@@ -380,10 +385,6 @@ __device__ __forceinline__ void blend_pair(FPix<LC>& P, const FGeo& ea, const FG
     const float tta = fmaf(-la, kLn2f, ua.w), ttb = fmaf(-lb, kLn2f, ub.w);
     P.h = fmaf(sa, tta, P.h);
     P.h = fmaf(sb, ttb, P.h);
-    // |d/ds s (c - ln s)| = |c - ln s - 1| <= |t| + 1: the weight of each entry's
-    // fp32 error in the score bound
-    P.E1 = fmaf(sa, fabsf(tta) + 1.f, P.E1);
-    P.E1 = fmaf(sb, fabsf(ttb) + 1.f, P.E1);
   }
 }
 
@@ -567,7 +568,6 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   P.R0 = P.R1 = P.R2 = P.DP = P.H = P.W0 = P.ED = 0.0;
   P.n_rgb = P.n_ent = 0;
   P.S = P.Se = 0.f;
-  P.E1 = 0.f;
   P.rd = !(RGB && inside);
   P.edn = !(ENT && inside);
 
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(256, 3) ua_blend_fast_kernel(UaBlendArgs a) {
   if (ENT) {
     double H = P.H;
     if (P.W0 > 0.0) H += P.W0 * (-log(P.W0) + a.hl_q0 + kGaussEntropy);  // :224-225
-    if (a.score_bound) a.score_bound[pix] = score_bound_px(a, P.E1, P.W0, H, P.n_ent, P.Se);
+    if (a.score_bound) a.score_bound[pix] = score_bound_px(a, P.H, P.W0, (double)P.Te, P.n_ent, P.Se);
     if (a.entropy) a.entropy[pix] = H;
     if (a.w0) a.w0[pix] = P.W0;
     if (EXTRA && a.edepth) a.edepth[pix] = P.ED;

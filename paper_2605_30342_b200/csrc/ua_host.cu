@@ -196,6 +196,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
         ua.w0_tail = 1.7e-3 * u * std::max(1.0, (double)s->max_opacity);
         ua.bound_tail = ua.w0_tail * (cabs + 89.0);
         ua.c0_abs = std::fabs(hl_q0 + kGaussEntropyHost);
+        ua.c_ent = ua.hl_qc + kGaussEntropyHost;
       }
       c->run("ua_blend", [&] { launch_ua_blend_fast(ua, c->stream); });
       CK(cudaEventRecord(c->ev_blend[par], c->stream));
