@@ -483,8 +483,8 @@ def run_ours(args):
                        "issue_slots_busy_pct": pj.get("issue_slots_busy_pct"), "source": "same ncu capture"}
         return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": src, "compute": compute,
-                "kernel": "ua_blend (" + ("ua_blend_fast_kernel, certified" if precision == "certified"
-                                          else "ua_blend_ilp_kernel, fp64") + ")",
+                "kernel": "ua_blend (" + ("K7f ua_blend_fast_kernel, certified fp32" if precision == "certified"
+                                          else "K7 exact fp64 blend, tensor-core colour") + ")",
                 "bytes_per_launch": bpl, "views_per_launch": vpl,
                 "avg_launch_ms": blend_ms / max(1, blend_n), "launches": blend_n,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}

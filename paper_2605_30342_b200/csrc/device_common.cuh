@@ -46,8 +46,10 @@ struct __align__(16) GeoRec {
 // alpha* = A*alpha + B with A = v + beta(1-v), B = o0(1-beta)(1-v); hl is the
 // splat's 1/2 log|Q_c| (constant provider: 3 ln sigma_c; sh_propagation:
 // 1/2 sum_c ln q_c(d), uncertainty.hpp:143-163).
+// omv = 1 - v and hlc = hl + C_H are stored too (the blends read them per
+// pixel); 48 bytes: a multiple of 16 for cp.async / bulk copies.
 struct __align__(16) UaRec {
-  double A, B, v, hl;
+  double A, B, v, omv, hlc, hl;
 };
 
 __device__ __forceinline__ int cov_lo(int32_t packed) { return packed & 0xFFFF; }

@@ -346,6 +346,8 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
           if (!(q0 > 0.0 && q1 > 0.0 && q2 > 0.0)) atomicOr(a.err_flag, 1);
           u.hl = 0.5 * (log(q0) + log(q1) + log(q2));
         }
+        u.omv = 1.0 - u.v;
+        u.hlc = u.hl + kGaussEntropy;
         a.ua[slot] = u;
       }
     } else if (a.write_culled) {

@@ -208,7 +208,7 @@ __device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec*
     s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
     if (ENT) {
       const UaRec u = uar[g];
-      s_ua[j] = make_float4((float)u.A, (float)u.B, (float)u.v, (float)(u.hl + kGaussEntropy));
+      s_ua[j] = make_float4((float)u.A, (float)u.B, (float)u.v, (float)u.hlc);
     }
   }
   if (RGB && !MMA) {
@@ -661,8 +661,8 @@ __device__ __forceinline__ void estage_batch(const UaBlendArgs& a, const GeoRec*
 }
 
 // Two list entries composited in fp64 (the pair step of ua_blend_ilp_kernel).
-template <int LC, bool ENT, bool EXTRA, bool LO>
-__device__ __forceinline__ void exact_pair(Pixel<LC>& P, const ExGeo& ea, const ExGeo& eb, const ExUa& ua,
+template <int LC, bool ENT, bool EXTRA, bool LO, class Rec>
+__device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Rec& eb, const ExUa& ua,
                                            const ExUa& ub, bool ca, bool cb, double cxp, double cyp,
                                            float3 cola, float3 colb, double amax, double cutoff) {
   const double ala = ex_alpha(ea, ex_negq(ea, cxp, cyp), amax);
@@ -845,8 +845,316 @@ __global__ void __launch_bounds__(256, 3) ua_blend_exact_mma_kernel(UaBlendArgs 
   pixel_finish<LC, true, ENT, EXTRA>(P, a, c, px, py, inside);
 }
 
+// ---------------------------------------------------------------------------
+// K7 exact, TMA ring (default for RGB renders on 16x16 tiles): the same fp64
+// blend and tensor-core colour as ua_blend_exact_mma_kernel, but the tile list
+// streams through a ring of kRing slots of 32 entries filled by bulk copies
+// (cp.async.bulk, completion on an mbarrier per slot) instead of staged batches
+// between two CTA barriers. The 8 warps are decoupled: a warp waits only for
+// the slot it reads to land, never for the other warps (the block barriers and
+// their per-batch wait for the slowest warp were ~19% of the stall samples).
+// A slot is refilled by the LAST warp to release it (a shared-memory arrival
+// counter), so no producer warp and no extra registers: the 32 lanes of that
+// warp read the next 32 particle ids and issue the record copies (GeoRec 64 B,
+// UaRec 48 B, split colour record 208 B per entry) directly from the K1/scene
+// arrays. The per-slot tag (batch held, or STOP) orders the refill decision
+// before any warp waits on the slot: once every warp's pixels are done the ring
+// stops refilling and each warp leaves at the first STOP, with no copy in
+// flight (every issued slot was waited on before its successor was decided).
+constexpr int kRing = 4;
+constexpr int kRingEntries = 32;
+constexpr int kRingStop = -1;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <bool ENT>
+struct RingLayout {
+  static constexpr size_t geo = (size_t)kRing * kRingEntries * sizeof(GeoRec);
+  static constexpr size_t ua = ENT ? (size_t)kRing * kRingEntries * sizeof(UaRec) : 0;
+  static constexpr size_t col = (size_t)kRing * kRingEntries * kColWords * sizeof(uint32_t);
+  static constexpr size_t tr = 8 * 32 * kTrStride * sizeof(float);
+  static constexpr size_t bytes = geo + ua + col + tr;
+  static constexpr uint32_t entry_bytes =
+      (uint32_t)(sizeof(GeoRec) + (ENT ? sizeof(UaRec) : 0) + kColWords * sizeof(uint32_t));
+};
+
+// Lane j of the calling warp issues the copies of entry j of list batch `bi`
+// into ring slot `slot` (lane 0 first arms the slot's barrier with the bytes).
+template <bool ENT>
+__device__ __forceinline__ void ring_issue(const UaBlendArgs& a, const GeoRec* geo, const UaRec* uar,
+                                           uint2 rg, int bi, int slot, int lane, GeoRec* s_geo, UaRec* s_ua,
+                                           uint32_t* s_col, uint64_t* full) {
+  const uint32_t base = rg.x + (uint32_t)bi * kRingEntries;
+  const int n = (int)min((uint32_t)kRingEntries, rg.y - base);
+  if (lane == 0) mbar_arrive_expect_tx(&full[slot], (uint32_t)n * RingLayout<ENT>::entry_bytes);
+  __syncwarp();
+  if (lane < n) {
+    const uint32_t g = a.vals[base + lane];
+    const int e = slot * kRingEntries + lane;
+    bulk_g2s(s_geo + e, geo + g, sizeof(GeoRec), &full[slot]);
+    if (ENT) bulk_g2s(s_ua + e, uar + g, sizeof(UaRec), &full[slot]);
+    bulk_g2s(s_col + (size_t)e * kColWords, a.scene.colors_split + (int64_t)g * (kColWords / 4),
+             kColWords * sizeof(uint32_t), &full[slot]);
+  }
+}
+
+template <int LC, bool ENT, bool EXTRA, bool LO>
+__global__ void __launch_bounds__(256, 3) ua_blend_exact_tma_kernel(UaBlendArgs a) {
+  using L = RingLayout<ENT>;
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
+  UaRec* s_ua = reinterpret_cast<UaRec*>(s_dyn + L::geo);
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_dyn + L::geo + L::ua);
+  float* s_tr = reinterpret_cast<float*>(s_dyn + L::geo + L::ua + L::col);
+  __shared__ __align__(8) uint64_t full[kRing];
+  __shared__ int s_tag[kRing];
+  __shared__ int s_rel[kRing];
+  __shared__ int s_ndone;
+  load_math_tables();
+
+  const double amax = a.amax, cutoff = a.cutoff;
+  const int64_t gt = blockIdx.x;
+  const int v = find_view(a.cams, a.V, gt);
+  const DevCam& c = a.cams[v];
+  const int64_t t = gt - c.tile_base;
+  const int tx = (int)(t % c.tiles_x), ty = (int)(t / c.tiles_x);
+  const uint2 rg = a.ranges[gt];
+  const int nbatch = (int)((rg.y - rg.x + kRingEntries - 1) / kRingEntries);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tig = lane & 3;
+  const int64_t N = a.scene.n;
+  const GeoRec* geo = a.geo + (int64_t)v * N;
+  const UaRec* uar = a.ua + (int64_t)v * N;
+
+  if (tid == 0) {
+    for (int s = 0; s < kRing; ++s) {
+      mbar_init(&full[s], 1);
+      s_tag[s] = s < nbatch ? s : kRingStop;
+      s_rel[s] = 0;
+    }
+    s_ndone = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int s = 0; s < kRing && s < nbatch; ++s) ring_issue<ENT>(a, geo, uar, rg, s, s, lane, s_geo, s_ua, s_col, full);
+
+  const int bx0 = tx * 16 + (warp & 1) * 8, by0 = ty * 16 + (warp >> 1) * 4;
+  const int bx1 = bx0 + 7, by1 = by0 + 3;
+  const int px = bx0 + (lane & 7), py = by0 + (lane >> 3);
+  const bool inside = px < c.width && py < c.height;
+  const double cxp = px + 0.5, cyp = py + 0.5;
+  float* tr = s_tr + warp * 32 * kTrStride;
+  uint32_t aH[2][4], aL[2][4];
+  {
+    constexpr int NB = Col<LC>::NB;
+    double bd[Col<LC>::NBP];
+    pixel_basis_d<LC>(c, px, py, bd);
+    uint32_t* wb = reinterpret_cast<uint32_t*>(tr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float x0 = 2 * i < NB ? (float)bd[2 * i] : 0.f;
+      const float x1 = 2 * i + 1 < NB ? (float)bd[2 * i + 1] : 0.f;
+      uint32_t h, l;
+      split_half2(x0, x1, h, l);
+      wb[lane * 17 + i] = h;
+      wb[lane * 17 + 8 + i] = l;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int r0 = 16 * m + gq, r1 = r0 + 8;
+      aH[m][0] = wb[r0 * 17 + tig];
+      aH[m][1] = wb[r1 * 17 + tig];
+      aH[m][2] = wb[r0 * 17 + tig + 4];
+      aH[m][3] = wb[r1 * 17 + tig + 4];
+      aL[m][0] = wb[r0 * 17 + 8 + tig];
+      aL[m][1] = wb[r1 * 17 + 8 + tig];
+      aL[m][2] = wb[r0 * 17 + 8 + tig + 4];
+      aL[m][3] = wb[r1 * 17 + 8 + tig + 4];
+    }
+    __syncwarp();
+  }
+  Pixel<LC> P;
+  P.T = P.Te = 1.0;
+  P.rgb0 = P.rgb1 = P.rgb2 = P.dep = 0.0;
+  P.H = P.w0 = P.edep = 0.0;
+  P.rgb_done = !inside;
+  P.ent_done = !(ENT && inside);
+  P.n_rgb = P.n_ent = 0;
+  const ColWordsStaged colword;
+  bool counted = false;  // this warp's pixels are all done and s_ndone knows it
+
+  for (int bi = 0; bi < nbatch; ++bi) {
+    const int slot = bi % kRing;
+    // the slot's refill decision for this batch (made by the last warp to release
+    // batch bi - kRing) precedes any wait on it
+    int tag;
+    volatile int* vtag = s_tag;
+    while ((tag = vtag[slot]) != bi && tag != kRingStop) __nanosleep(20);
+    if (tag == kRingStop) break;
+    mbar_wait(&full[slot], (uint32_t)((bi / kRing) & 1));
+    const bool wdone = __all_sync(0xffffffffu, P.rgb_done && P.ent_done);
+    if (!wdone) {
+      const int n = (int)min((uint32_t)kRingEntries, rg.y - (rg.x + (uint32_t)bi * kRingEntries));
+      const GeoRec* sg = s_geo + slot * kRingEntries;
+      const UaRec* su = s_ua + slot * kRingEntries;
+      const uint32_t* sc = s_col + (size_t)slot * kRingEntries * kColWords;
+      bool hit = false;
+      if (lane < n) {
+        const int4 r = cover_rect4(sg[lane].cov_x, sg[lane].cov_y);
+        hit = r.x <= bx1 && r.x + r.y >= bx0 && r.z <= by1 && r.z + r.w >= by0;
+      }
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      while (hits != 0u) {
+        int je[8];
+        int ng = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          je[q] = hits != 0u ? __ffs(hits) - 1 : -1;
+          ng += hits != 0u ? 1 : 0;
+          hits &= hits - 1u;
+        }
+        if (__any_sync(0xffffffffu, !P.rgb_done)) {
+          int my_e = -1;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) my_e = gq == q ? je[q] : my_e;
+          uint32_t bh[3][2], bl[3][2];
+          const int e = max(my_e, 0);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const int w0 = colword(e, ch, tig), w1 = colword(e, ch, tig + 4);
+            bh[ch][0] = my_e >= 0 ? sc[w0] : 0u;
+            bh[ch][1] = my_e >= 0 ? sc[w1] : 0u;
+            bl[ch][0] = my_e >= 0 ? sc[w0 + ColWordsStaged::kLo] : 0u;
+            bl[ch][1] = my_e >= 0 ? sc[w1 + ColWordsStaged::kLo] : 0u;
+          }
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              float d[4] = {0.f, 0.f, 0.f, 0.f};
+              hmma16816(d, aH[m], bh[ch][0], bh[ch][1]);
+              hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
+              hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
+              const int r0 = 16 * m + gq, r1 = r0 + 8;
+              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
+            }
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          if (q < ng) {
+            const int ja = je[q];
+            const bool has_b = q + 1 < ng;
+            const int jb = has_b ? je[q + 1] : ja;
+            const GeoRec& ga = sg[ja];
+            const GeoRec& gb = sg[jb];
+            const bool ca = in_rect4(cover_rect4(ga.cov_x, ga.cov_y), px, py);
+            const bool cb = has_b && in_rect4(cover_rect4(gb.cov_x, gb.cov_y), px, py);
+            const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
+            const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
+            const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+            const float3 cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
+            const float3 colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
+            exact_pair<LC, ENT, EXTRA, LO>(P, ga, gb, ENT ? ex_ua(su[ja]) : ExUa{},
+                                           ENT ? ex_ua(su[jb]) : ExUa{}, ca, cb, cxp, cyp, cola, colb, amax,
+                                           cutoff);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    // release the slot; the last of the 8 warps decides its refill
+    if (!counted && __all_sync(0xffffffffu, P.rgb_done && P.ent_done)) {
+      counted = true;
+      if (lane == 0) atomicAdd(&s_ndone, 1);
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(&s_rel[slot], 1) == 7;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      const int next = bi + kRing;
+      const bool stop = next >= nbatch || *((volatile int*)&s_ndone) == 8;
+      if (lane == 0) s_rel[slot] = 0;
+      if (stop) {
+        if (lane == 0) {
+          __threadfence_block();
+          ((volatile int*)s_tag)[slot] = kRingStop;
+        }
+      } else {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot reads before the copies' writes
+        ring_issue<ENT>(a, geo, uar, rg, next, slot, lane, s_geo, s_ua, s_col, full);
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          ((volatile int*)s_tag)[slot] = next;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  pixel_finish<LC, true, ENT, EXTRA>(P, a, c, px, py, inside);
+}
+
+template <int LC, bool ENT, bool EXTRA, bool LO>
+void launch_exact_tma(const UaBlendArgs& a, cudaStream_t s) {
+  const size_t sm = RingLayout<ENT>::bytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ua_blend_exact_tma_kernel<LC, ENT, EXTRA, LO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = true;
+  }
+  ua_blend_exact_tma_kernel<LC, ENT, EXTRA, LO><<<(unsigned)a.total_tiles, 256, sm, s>>>(a);
+}
+
+// GAVIS_UA_RING=0 selects the barrier-staged kernel (A/B)
+inline bool exact_ring() {
+  static const bool ring = [] {
+    const char* e = std::getenv("GAVIS_UA_RING");
+    return !(e && e[0] == '0');
+  }();
+  return ring;
+}
+
 template <int LC, bool ENT, bool EXTRA, bool LO>
 void launch_exact_mma(const UaBlendArgs& a, cudaStream_t s) {
+  if (exact_ring()) {
+    launch_exact_tma<LC, ENT, EXTRA, LO>(a, s);
+    return;
+  }
   constexpr int B = 128;
   const size_t sm = EStage<ENT>::bytes(B);
   static bool configured = false;
