@@ -58,7 +58,7 @@ static void print(const char* tag, const NbvResult& r) {
 }
 
 int main(int argc, char** argv) {
-  if (argc > 1 && std::strcmp(argv[1], "exact") == 0) set_exact_precision(true);
+  if (argc > 1) set_exact_precision(std::strcmp(argv[1], "exact") == 0);  // "exact" | "certified"
   try {
     const Scene scene = make_scene();
     const auto variances = make_variances(scene.particles.size());

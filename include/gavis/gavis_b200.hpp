@@ -339,9 +339,9 @@ inline std::vector<uint8_t> virtual_mask(const Scene& s) {
 
 inline void set_default_device(int device) { detail::holder().device = device; }
 
-// Arithmetic of the UA render (gavis_ctx_set_precision): the certified fp32 blend
-// (default; contributor counts and the selected view equal the fp64 reference's,
-// images to ~1e-6) or the exact fp64 blend.
+// Arithmetic of the UA render (gavis_ctx_set_precision): the fp64 blend (default,
+// the reference's arithmetic) or the certified fp32 blend (contributor counts and
+// the selected view equal the fp64 reference's, images to ~1e-6).
 inline void set_exact_precision(bool exact) {
   check(gavis_ctx_set_precision(detail::holder().get(),
                                 exact ? GAVIS_PRECISION_EXACT : GAVIS_PRECISION_CERTIFIED));

@@ -107,14 +107,18 @@ gavis_status gavis_ctx_set_batch(gavis_ctx* ctx, int32_t max_views_per_batch);
  * half the views (down to one view; one view may produce up to 2^31 - 1 pairs). */
 gavis_status gavis_ctx_set_pair_budget(gavis_ctx* ctx, int64_t max_pairs_per_batch);
 /* Arithmetic of the UA render (gavis_ua_render, gavis_select_nbv, loops):
- *  GAVIS_PRECISION_CERTIFIED (default): fp32 blend with a per-pixel error bound
- *    on the early-termination tests; pixels the bound cannot certify are
- *    recomputed in fp64, so contributor counts equal the fp64 reference's;
- *    images agree with it to ~1e-6 (north_star: 1e-4); select_nbv re-scores in
- *    fp64 every candidate within 1e-3 (relative) of the best, so the argmax is
- *    the fp64 one. Used for 16x16 tiles and alpha_clamp_max <= 0.999.
- *  GAVIS_PRECISION_EXACT: every blend in fp64 with the reference's operation
- *    order (images to ~1e-12 of the reference). */
+ *  GAVIS_PRECISION_EXACT (default): every blend in fp64 (alpha, both
+ *    transmittances, stop tests, accumulations; FMA-contracted, to rounding of
+ *    the reference's unfused double code); the SH colour dot product on the
+ *    tensor cores in split fp16 (~2^-21 relative). Images to ~1e-7 of the
+ *    reference, entropy and scores to ~1e-13.
+ *  GAVIS_PRECISION_CERTIFIED: fp32 blend with a per-pixel error bound on the
+ *    early-termination tests; pixels the bound cannot certify are recomputed
+ *    in fp64, so contributor counts equal the fp64 reference's; images agree
+ *    with it to ~1e-6 (north_star: 1e-4); select_nbv re-scores in fp64 every
+ *    candidate whose score interval (rigorous per-candidate error bounds,
+ *    gavis_ctx_last_score_bounds) can reach the best's, so the argmax is the
+ *    fp64 one. Used for 16x16 tiles and alpha_clamp_max <= 0.999. */
 enum { GAVIS_PRECISION_CERTIFIED = 0, GAVIS_PRECISION_EXACT = 1 };
 gavis_status gavis_ctx_set_precision(gavis_ctx* ctx, int32_t precision);
 /* Rigorous per-candidate bounds on |certified score - fp64 score| of the last

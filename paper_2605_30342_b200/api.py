@@ -83,7 +83,7 @@ class Context:
         # device objects of this context, released before it (the C ABI requires
         # scenes and fields to be destroyed before their context)
         self._children = weakref.WeakSet()
-        self.precision = "certified"
+        self.precision = "exact"  # the library default (gavis_ctx_set_precision)
 
     def close(self) -> None:
         if self.h:
@@ -119,8 +119,8 @@ class Context:
         N.check(self.lib.gavis_ctx_set_pair_budget(self.h, C.c_int64(n)))
 
     def set_precision(self, precision: str) -> None:
-        """'certified' (default: fp32 blend, fp64 redo of uncertified pixels,
-        exact argmax) or 'exact' (fp64 throughout)."""
+        """'exact' (default: the fp64 blend, the reference's arithmetic) or
+        'certified' (fp32 blend, fp64 redo of uncertified pixels, fp64 argmax)."""
         modes = {"certified": N.PRECISION_CERTIFIED, "exact": N.PRECISION_EXACT}
         require(precision in modes, "precision must be 'certified' or 'exact'")
         N.check(self.lib.gavis_ctx_set_precision(self.h, C.c_int32(modes[precision])))

@@ -267,7 +267,7 @@ struct gavis_ctx {
   // certified score-error bounds of the last ua_render that produced scores
   // (empty when not certified / not bounded); read by certified_contenders
   std::vector<double> score_bounds;
-  int precision = GAVIS_PRECISION_CERTIFIED;
+  int precision = GAVIS_PRECISION_EXACT;  // the reference's fp64 arithmetic by default
   int64_t redo_pixels = 0;       // pixels the certified blend handed to the fp64 redo
   double batch_budget = 0.0;     // bytes of per-(view, particle) state one batch may use
   int64_t rescored_views = 0;    // candidates re-scored exactly to certify an argmax

@@ -119,7 +119,7 @@ def test_cpp_uncertainty_modes_match_oracle(tmp_path, precision):
     import numpy as np
     import oracle as O
     from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
-    args = [_build_modes(tmp_path)] + (["exact"] if precision == "exact" else [])
+    args = [_build_modes(tmp_path), precision]
     r = subprocess.run(args, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     out = {}
