@@ -183,10 +183,15 @@ __global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
           const bool ed = P.ent_done || (ea_on && P.Te < cutoff);
           const bool eb_on = cb && !ed;
           const double sb = ex_ent<LC, EXTRA>(P, eb_on ? xb : 0.0, ub, eb.depth);
-          const double la = log_pos(sa > 0.0 ? sa : 1.0);
-          const double lb = log_pos(sb > 0.0 ? sb : 1.0);
-          if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
-          if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
+          if (LO) {  // s may be negative (given visibility outside [0, 1]): s > 0 only
+            const double la = log_pos(sa > 0.0 ? sa : 1.0);
+            const double lb = log_pos(sb > 0.0 ? sb : 1.0);
+            if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
+            if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
+          } else {  // s >= 0; s == 0 adds exactly +0 (log_pos(0) is finite)
+            P.H = fma(sa, ua.hlc - log_pos(sa), P.H);
+            P.H = fma(sb, ub.hlc - log_pos(sb), P.H);
+          }
           if (EXTRA) P.n_ent += (int)ea_on + (int)eb_on;
           P.ent_done = ed || (eb_on && P.Te < cutoff);
         }

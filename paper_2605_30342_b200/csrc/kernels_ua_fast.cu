@@ -681,10 +681,15 @@ __device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Re
     const bool ed = P.ent_done || (ea_on && P.Te < cutoff);
     const bool eb_on = cb && !ed;
     const double sb = ex_ent<LC, EXTRA>(P, eb_on ? xb : 0.0, ub, eb.depth);
-    const double la = log_pos(sa > 0.0 ? sa : 1.0);
-    const double lb = log_pos(sb > 0.0 ? sb : 1.0);
-    if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
-    if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
+    if (LO) {  // s may be negative (given visibility outside [0, 1]): s > 0 only
+      const double la = log_pos(sa > 0.0 ? sa : 1.0);
+      const double lb = log_pos(sb > 0.0 ? sb : 1.0);
+      if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
+      if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
+    } else {  // s >= 0; s == 0 adds exactly +0 (log_pos(0) is finite)
+      P.H = fma(sa, ua.hlc - log_pos(sa), P.H);
+      P.H = fma(sb, ub.hlc - log_pos(sb), P.H);
+    }
     if (EXTRA) P.n_ent += (int)ea_on + (int)eb_on;
     P.ent_done = ed || (eb_on && P.Te < cutoff);
   }
@@ -875,6 +880,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -1012,13 +1020,11 @@ __global__ void __launch_bounds__(256, 3) ua_blend_exact_tma_kernel(UaBlendArgs 
 
   for (int bi = 0; bi < nbatch; ++bi) {
     const int slot = bi % kRing;
-    // the slot's refill decision for this batch (made by the last warp to release
-    // batch bi - kRing) precedes any wait on it
-    int tag;
-    volatile int* vtag = s_tag;
-    while ((tag = vtag[slot]) != bi && tag != kRingStop) __nanosleep(20);
-    if (tag == kRingStop) break;
+    // The slot's barrier phase for batch bi completes either when its copies land
+    // or, once the ring stops, by a plain arrival of the deciding warp; the tag
+    // (written before either) says which. The wait sleeps in hardware.
     mbar_wait(&full[slot], (uint32_t)((bi / kRing) & 1));
+    if (((volatile int*)s_tag)[slot] == kRingStop) break;
     const bool wdone = __all_sync(0xffffffffu, P.rgb_done && P.ent_done);
     if (!wdone) {
       const int n = (int)min((uint32_t)kRingEntries, rg.y - (rg.x + (uint32_t)bi * kRingEntries));
@@ -1110,17 +1116,18 @@ __global__ void __launch_bounds__(256, 3) ua_blend_exact_tma_kernel(UaBlendArgs 
       if (lane == 0) s_rel[slot] = 0;
       if (stop) {
         if (lane == 0) {
-          __threadfence_block();
           ((volatile int*)s_tag)[slot] = kRingStop;
+          __threadfence_block();
+          mbar_arrive(&full[slot]);  // completes the phase the other warps wait on
         }
       } else {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot reads before the copies' writes
-        ring_issue<ENT>(a, geo, uar, rg, next, slot, lane, s_geo, s_ua, s_col, full);
-        __syncwarp();
         if (lane == 0) {
-          __threadfence_block();
           ((volatile int*)s_tag)[slot] = next;
+          __threadfence_block();
         }
+        __syncwarp();
+        ring_issue<ENT>(a, geo, uar, rg, next, slot, lane, s_geo, s_ua, s_col, full);
       }
       __syncwarp();
     }
