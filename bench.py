@@ -248,6 +248,14 @@ def _oracle():
     return O
 
 
+def _reference():
+    """oracle/_ref: the reference's unmodified headers compiled against the Eigen
+    shim (`make -C oracle ref`), or None when it was not built."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref as R
+    return R if R.available() else None
+
+
 def oracle_select(c, osc, gamma, degree, num_views, cams, threads):
     """The reference's algorithm (CPU oracle) on `cams`: rasterize (RGB) +
     render_entropy + image_entropy + argmax, parallel over candidates
@@ -281,23 +289,42 @@ def run_reference(args):
     if rank != 0:
         return 0
     O = _oracle()
-    from paper_2605_30342_b200.model import RasterConfig
+    R = _reference()
+    from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
     c = make_config(args.config, 1, args.per_gpu, args.particles)
     model, cores = cpu_info()
     osc = O.OracleScene(c["scene"])
+    rc, uc = RasterConfig(), UncertaintyConfig()
+    n = args.cpu_sample or cores
+    cams = c["candidates"][:n]  # the first candidates of the GPU arm's list
+    nv, deg = len(c["train"]), c["degree"]
     # the field of the stated config: construct_field over all its training views
     # (parallel_for over views, vfield.hpp:85-87), the reference's own algorithm
     t0 = time.perf_counter()
-    gamma = O.construct_field(osc, c["train"], 1.0, c["degree"], RasterConfig(), threads=cores)
+    if R is not None:
+        kind, what = "reference", ("the reference's own code: unmodified R/include/gavis headers compiled "
+                                   "-O3 against the Eigen-subset shim (oracle/_ref)")
+        rs = R.RefScene(osc)
+        gamma = R.construct_field_h(rs, c["train"], 1.0, deg, rc, threads=cores)
+
+        def step():
+            t = time.perf_counter()
+            best, _ = R.select_nbv_rgb_h(rs, gamma, deg, nv, cams, rc, uc, threads=cores)
+            return len(cams) / (time.perf_counter() - t), best
+    else:
+        kind, what = "port", "the C restatement oracle/gavis_oracle.c (oracle/_ref not built)"
+        gamma = O.construct_field(osc, c["train"], 1.0, deg, rc, threads=cores)
+
+        def step():
+            r, _, best, _ = oracle_select(c, osc, gamma, deg, nv, cams, cores)
+            return r, best
     field_s = time.perf_counter() - t0
-    n = args.cpu_sample or cores
-    cams = c["candidates"][:n]  # the first candidates of the GPU arm's list
     rates = []
     for _ in range(args.warmup):
-        oracle_select(c, osc, gamma, c["degree"], len(c["train"]), cams, cores)
+        step()
     best = None
     for _ in range(args.steps):
-        r, dt, best, _ = oracle_select(c, osc, gamma, c["degree"], len(c["train"]), cams, cores)
+        r, best = step()
         rates.append(r)
     value = float(np.mean(rates))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
@@ -305,16 +332,16 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config generator; paper datasets not in the container)",
             "config": {"workload": f"config{args.config}", "particles": c["scene"].num_particles,
-                       "training_views": len(c["train"]), "field_degree": c["degree"],
+                       "training_views": nv, "field_degree": deg,
                        "color_degree": c["scene"].color_degree,
                        "resolution": [cams[0].width, cams[0].height],
                        "candidates_per_step": n,
                        "sample": f"candidates 0..{n - 1} of the GPU arm's config-{args.config} list"},
             "field_build_s": field_s, "best_index_in_sample": best,
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{n} candidates/step (the GPU arm's first {n}) of config {args.config} "
-                                       f"at 800x800, field from all {len(c['train'])} training views; "
-                                       f"oracle select_nbv + rasterize on {cores} threads ({model})"},
+                                       f"at 800x800, field from all {nv} training views; select_nbv + rasterize "
+                                       f"per candidate on {cores} threads ({model}); {what}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -643,18 +670,30 @@ def oracle_gate(args, ctx, api, c, ds, field, cands, rc, uc):
     cpu_baseline), and compare it with the device in BOTH precisions on the same
     inputs: scores + argmax of the sample (rendered with the device's field),
     per-pixel contributor counts and images of one view, and a 2-view field."""
-    from paper_2605_30342_b200.model import VmfParams
+    from paper_2605_30342_b200.model import UncertaintyConfig as UCfg, VmfParams
     O = _oracle()
+    R = _reference()
     model, cores = cpu_info()
     n = args.cpu_sample or max(4, min(16, cores))
     sample = cands[:n]
     gamma = field.download().gamma
     degree, nv = c["degree"], len(c["train"])
     osc = O.OracleScene(c["scene"])
-    rate, dt, o_best, o_scores = oracle_select(c, osc, gamma, degree, nv, sample, cores)
-    cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+    if R is not None:  # the reference's own code (oracle/_ref) times the sample and scores it
+        rs = R.RefScene(osc)
+        t0 = time.perf_counter()
+        o_best, o_scores = R.select_nbv_rgb_h(rs, gamma, degree, nv, sample, rc, UCfg(), threads=cores)
+        dt = time.perf_counter() - t0
+        rate, kind = n / dt, "reference"
+        o_scores = np.asarray(o_scores, np.float64)
+    else:
+        rate, dt, o_best, o_scores = oracle_select(c, osc, gamma, degree, nv, sample, cores)
+        kind = "port"
+    cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
            "sample": f"candidates 0..{n - 1} of config {args.config} (800x800, full scene, the device's "
-                     f"{nv}-view field), oracle select_nbv + rasterize on {cores} threads, {dt:.1f} s ({model})"}
+                     f"{nv}-view field), select_nbv + rasterize per candidate on {cores} threads, {dt:.1f} s "
+                     f"({model}); " + ("the reference's headers compiled against the Eigen shim (oracle/_ref)"
+                                      if R is not None else "the C restatement (oracle/gavis_oracle.c)")}
     o_rgb, o_rcc, o_H, o_ecc = oracle_view(osc, gamma, degree, nv, sample[0])
     # 2-view field: device vs oracle construct_field (vfield.hpp:68-92)
     two = c["train"][:2]
@@ -663,7 +702,10 @@ def oracle_gate(args, ctx, api, c, ds, field, cands, rc, uc):
     d2 = f2.download().gamma
     f2.close()
     scale = np.maximum(np.abs(g2).max(axis=1, keepdims=True), 1e-300)
-    gate = {"reference": "CPU oracle (oracle/gavis_oracle.c, the reference's fp64 algorithm), same seeded inputs",
+    gate = {"reference": ("scores/argmax: the reference's own code (oracle/_ref); " if R is not None else
+                          "scores/argmax: CPU oracle; ") +
+                         "counts/images/field: CPU oracle (oracle/gavis_oracle.c, bit-identical to oracle/_ref "
+                         "on config 1 and config 3, tests/test_ref_oracle.py); same seeded inputs",
             "candidates": n, "oracle_argmax_in_sample": o_best,
             "field_2views_gamma_max_rel": float((np.abs(d2 - g2) / scale).max()),
             "field_2views_rows_nonzero": int((np.abs(g2).max(axis=1) > 0).sum())}

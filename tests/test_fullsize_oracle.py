@@ -124,3 +124,39 @@ def test_candidates_with_full_field(setup, precision):
 
 
 setup_cache = {}
+
+
+def test_device_matches_reference_itself(setup):
+    """The device against the reference's OWN code (oracle/_ref: the unmodified
+    headers compiled against the Eigen-subset shim) at full size: scores and
+    argmax of 2 candidates with the device's full field, one candidate's RGB /
+    transmittance / entropy images, both precisions."""
+    import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    cfg, c, ctx, ds, osc = setup
+    if cfg == 4:
+        pytest.skip("config 4 covered through the restatement (the reference AoS build takes minutes)")
+    f = api.construct_field(ctx, ds, c["train"], VmfParams(1.0), c["degree"], RC)
+    gamma = f.download().gamma
+    cams = c["candidates"][:2]
+    nv = len(c["train"])
+    best, scores = R.select_nbv(osc, gamma, c["degree"], nv, cams, RC, UC, threads=THREADS)
+    rgb, _, T = R.rasterize(osc, cams[0], RC, threads=THREADS)
+    H, w0, _ = R.render_entropy(osc, gamma, c["degree"], nv, cams[0], RC, UC, threads=THREADS)
+    P = cams[0].width * cams[0].height
+    for precision, tol in (("exact", 1e-6), ("certified", 1e-5)):
+        ctx.set_precision(precision)
+        try:
+            nbv = api.select_nbv(ctx, ds, f, cams, RC, UC, with_rgb=True)
+            out = api.render(ctx, ds, f, cams[:1], RC, UC, rgb=True, transmittance=True, entropy=True,
+                             invisible_mass=True)
+        finally:
+            ctx.set_precision("exact")
+        assert nbv.best_index == best
+        assert np.max(np.abs(nbv.scores - scores) / np.abs(scores)) <= tol
+        assert np.max(np.abs(out["rgb"] - rgb)) <= 1e-4
+        assert np.max(np.abs(out["entropy"][:P] - H)) <= 1e-4
+        assert np.max(np.abs(out["invisible_mass"][:P] - w0)) <= 1e-4
+        assert np.max(np.abs(out["transmittance"][:P] - T)) <= (1e-12 if precision == "exact" else 1e-6)
+    f.close()

@@ -1,0 +1,73 @@
+"""The reference ITSELF against the C restatement oracle, on the CPU.
+
+oracle/_ref/libgavis_ref.so is the GAVIS reference's unmodified hot-path headers
+(/root/reference/proj/include/gavis/*.hpp) compiled -O3 -ffp-contract=off
+against a self-written Eigen-subset shim (oracle/eigen_shim: fixed-size
+products summed left to right, Eigen's quaternion-to-matrix formula). Every
+hot-path function of the restatement (oracle/gavis_oracle.c), and so the
+checker the device is held to, must agree with the reference's own code BIT FOR
+BIT: single_view_visibility (raster.hpp:237-290), construct_field
+(vfield.hpp:68-92), rasterize (raster.hpp:175-231), render_entropy
+(uncertainty.hpp:242-260), select_nbv (planner.hpp:117-137).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import ref as R
+from paper_2605_30342_b200 import synth
+from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
+
+pytestmark = pytest.mark.skipif(not R.available(), reason="oracle/_ref not built (no /root/reference here)")
+
+UC = UncertaintyConfig()
+
+
+@pytest.mark.parametrize("tile", [16, 5, 13])
+def test_reference_equals_restatement_config1(tile):
+    c = synth.config1(0)
+    rc = RasterConfig(tile_size=tile)
+    osc = O.OracleScene(c["scene"])
+    for cam in c["train"][:2]:
+        assert np.array_equal(R.single_view_visibility(osc, cam, rc), O.single_view_visibility(osc, cam, rc))
+    g_r = R.construct_field(osc, c["train"], 1.0, 2, rc, threads=4)
+    g_o = O.construct_field(osc, c["train"], 1.0, 2, rc, threads=4)
+    assert np.array_equal(g_r, g_o)
+    for cam in c["candidates"][:2]:
+        for a, b in zip(R.rasterize(osc, cam, rc), O.rasterize(osc, cam, rc)):
+            assert np.array_equal(a, b)
+        H_r, w_r, d_r = R.render_entropy(osc, g_r, 2, 16, cam, rc, UC)
+        H_o, w_o, d_o = O.render_entropy(osc, g_o, 2, 16, cam, rc, UC)
+        assert np.array_equal(H_r, H_o) and np.array_equal(w_r, w_o) and np.array_equal(d_r, d_o)
+    b_r, s_r = R.select_nbv(osc, g_r, 2, 16, c["candidates"], rc, UC, threads=4)
+    b_o, s_o = O.select_nbv(osc, g_o, 2, 16, c["candidates"], rc, UC, threads=4)
+    assert b_r == b_o and np.array_equal(s_r, s_o)
+
+
+def test_reference_equals_restatement_room_and_hook():
+    """Config-3 structure (thin wall slabs: depth ties, flattened conics) and the
+    non-default uncertainty paths: correlation hook, beta/o0/sigma variations."""
+    c = synth.config3(0, n=60_000, n_train=6, n_candidates=4, res=160)
+    rc = RasterConfig()
+    osc = O.OracleScene(c["scene"])
+    g_r = R.construct_field(osc, c["train"], 1.0, 2, rc, threads=4)
+    assert np.array_equal(g_r, O.construct_field(osc, c["train"], 1.0, 2, rc, threads=4))
+    for uc in (UC, UncertaintyConfig(beta=0.2, prior_opacity=0.3, color_sigma=0.05),
+               UncertaintyConfig(correlation=1, correlation_lambda=2.5)):
+        b_r, s_r = R.select_nbv(osc, g_r, 2, 6, c["candidates"], rc, uc, threads=4)
+        b_o, s_o = O.select_nbv(osc, g_r, 2, 6, c["candidates"], rc, uc, threads=4)
+        assert b_r == b_o and np.array_equal(s_r, s_o)
+
+
+def test_reference_bench_step_matches_restatement():
+    """The reference arm's step (select_nbv + rasterize on a prebuilt scene) scores
+    like the restatement."""
+    c = synth.config1(3)
+    rc = RasterConfig()
+    osc = O.OracleScene(c["scene"])
+    rs = R.RefScene(osc)
+    g = R.construct_field_h(rs, c["train"][:6], 1.0, 2, rc, threads=4)
+    b_r, s_r = R.select_nbv_rgb_h(rs, g, 2, 6, c["candidates"][:8], rc, UC, threads=4)
+    b_o, s_o = O.select_nbv(osc, g, 2, 6, c["candidates"][:8], rc, UC, threads=4, with_rgb=True)
+    assert b_r == b_o and np.array_equal(s_r, s_o)
+    rs.close()
