@@ -136,6 +136,7 @@ def test_forced_redo_is_exact(ctx, ctx_exact, monkeypatch, room):
     monkeypatch.setenv("GAVIS_CERT_FORCE_REDO", "1")
     fr = api.render(ctx_exact, scene, f, cams, RC, UC, **kw)  # exact context: knob ignored
     ctx_f = api.Context(0)
+    ctx_f.set_precision("certified")
     try:
         fd = api.upload_field(ctx_f, scene, f.download())
         red0 = ctx_f.counters()[0]
@@ -352,6 +353,7 @@ from paper_2605_30342_b200.model import RasterConfig, UncertaintyConfig
 c = synth.config1(0)
 osc = O.OracleScene(c['scene'])
 with api.Context(0) as ctx:
+    ctx.set_precision('certified')
     for cam in c['candidates'][:2]:
         r = api.render(ctx, c['scene'], None, [cam], RasterConfig(), UncertaintyConfig(), rgb=True,
                        contributors=True)
