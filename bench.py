@@ -543,7 +543,10 @@ def run_ours(args):
         def e2e_step():
             s2 = ctx.upload(host_scene)
             f2 = api.upload_field(ctx, s2, host_field)
-            r = api.select_nbv(ctx, s2, f2, cands, rc, uc, with_rgb=True)
+            if comm is not None:  # the global select: this rank's block, scores gathered by the library
+                r = api.select_nbv_comm(comm, s2, f2, c["candidates"], rc, uc, with_rgb=True)
+            else:
+                r = api.select_nbv(ctx, s2, f2, cands, rc, uc, with_rgb=True)
             f2.close()
             s2.close()
             return r
