@@ -15,6 +15,7 @@
 // (vfield.hpp:38-63): one thread per particle folds its pairs, divides by the
 // touch count and adds v * a_l * Y_lm(d) to its SH row, views in trajectory
 // order.
+#include "alpha.cuh"
 #include "fast_math.cuh"
 #include "kernels.h"
 
@@ -102,15 +103,9 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
           const GeoRec& e = s_geo[j];
           contrib = T;  // v_k += T before the splat (raster.hpp:266)
           ++ncontrib;
-          const double dx = cxp - e.mx;
-          const double dy = cyp - e.my;
-          const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-          double al = 0.0;  // q > kQSkip: alpha < 2^-54, T bit-identical (fast_math.cuh)
-          if (q <= kQSkip) {
-            al = (double)e.opacity * exp_neg(-0.5 * q);
-            al = al > a.amax ? a.amax : al;
-          }
-          T *= 1.0 - al;
+          // alpha (alpha.cuh) and T (1 - alpha) in one rounding
+          const double al = ex_alpha(e, ex_negq(e, cxp, cyp), a.amax);
+          T = fma(-al, T, T);
           if (T < a.cutoff) done = true;
         }
 #pragma unroll
@@ -209,27 +204,15 @@ __global__ void __launch_bounds__(128) vf_blend_tile2_kernel(VfBlendArgs a) {
           if (c0) {
             contrib = T0;  // v_k += T before the splat (raster.hpp:266)
             ++n0;
-            const double dx = cxp - e.mx, dy = cy0 - e.my;
-            const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-            double al = 0.0;
-            if (q <= kQSkip) {
-              al = (double)e.opacity * exp_neg(-0.5 * q);
-              al = al > amax ? amax : al;
-            }
-            T0 *= 1.0 - al;
+            const double al = ex_alpha(e, ex_negq(e, cxp, cy0), amax);
+            T0 = fma(-al, T0, T0);
             d0 = T0 < cutoff;
           }
           if (c1) {
             contrib += T1;
             ++n1;
-            const double dx = cxp - e.mx, dy = cy1 - e.my;
-            const double q = e.ca * dx * dx + e.cb2 * dx * dy + e.cc * dy * dy;
-            double al = 0.0;
-            if (q <= kQSkip) {
-              al = (double)e.opacity * exp_neg(-0.5 * q);
-              al = al > amax ? amax : al;
-            }
-            T1 *= 1.0 - al;
+            const double al = ex_alpha(e, ex_negq(e, cxp, cy1), amax);
+            T1 = fma(-al, T1, T1);
             d1 = T1 < cutoff;
           }
 #pragma unroll

@@ -4,6 +4,7 @@
 // and the shared-memory staging of tile-list batches.
 #pragma once
 
+#include "alpha.cuh"
 #include "fast_math.cuh"
 #include "kernels.h"
 
@@ -154,18 +155,6 @@ __device__ __forceinline__ ExUa ex_ua(const UaRec& u) {
 __device__ __forceinline__ double ex_negq(const ExGeo& e, double cxp, double cyp) {
   const double dx = cxp - e.mx, dy = cyp - e.my;
   return fma(dx, fma(e.na, dx, e.nb * dy), e.nc * dy * dy);
-}
-
-// The same x from the raw projection record: -1/2 times the unscaled form is
-// bit-identical to the pre-scaled one (scaling by a power of two commutes with
-// every rounding), one DMUL instead of the three of ex_geo.
-__device__ __forceinline__ double ex_negq(const GeoRec& r, double cxp, double cyp) {
-  const double dx = cxp - r.mx, dy = cyp - r.my;
-  return -0.5 * fma(dx, fma(r.ca, dx, r.cb2 * dy), r.cc * dy * dy);
-}
-__device__ __forceinline__ double ex_alpha(const GeoRec& r, double x, double amax) {
-  const double al = (double)r.opacity * exp_neg(x);
-  return x >= -0.5 * kQSkip ? (al > amax ? amax : al) : 0.0;
 }
 
 // alpha = min(o exp(-q/2), alpha_max); q > kQSkip -> 0 (T bit-identical, fast_math.cuh).
