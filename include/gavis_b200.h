@@ -122,9 +122,9 @@ gavis_status gavis_ctx_set_pair_budget(gavis_ctx* ctx, int64_t max_pairs_per_bat
 enum { GAVIS_PRECISION_CERTIFIED = 0, GAVIS_PRECISION_EXACT = 1 };
 gavis_status gavis_ctx_set_precision(gavis_ctx* ctx, int32_t precision);
 /* Rigorous per-candidate bounds on |certified score - fp64 score| of the last
- * scored render on this context (certified mode, constant variance provider, no
- * correlation hook; see kernels_ua_fast.cu "score bound"): *n_out = 0 when the
- * last render had none. select_nbv re-scores in fp64 every candidate i with
+ * scored render or select_nbv on this context (certified mode, constant variance
+ * provider, no correlation hook; see kernels_ua_fast.cu "score bound"): *n_out =
+ * 0 when it had none. select_nbv re-scores in fp64 every candidate i with
  * s_i >= s_best - max(e_best + e_i, 1e-3 |s_best|, 1e-9). */
 gavis_status gavis_ctx_last_score_bounds(gavis_ctx* ctx, double* bounds, int32_t capacity,
                                          int32_t* n_out);

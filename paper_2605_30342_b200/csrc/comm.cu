@@ -296,14 +296,17 @@ gavis_status gavis_select_nbv_sharded(gavis_comm* cm, const gavis_scene* s, cons
         gavis_render_outputs o = {};
         o.scores = ex.data();
         const int32_t prec = c->precision;
+        const std::vector<double> keep = c->score_bounds;  // the fp64 re-render must not clear them
         c->precision = GAVIS_PRECISION_EXACT;
         try {
           ua_render(c, s, f, nullptr, cc.data(), (int)cc.size(), rc, uc, &o);
         } catch (...) {
           c->precision = prec;
+          c->score_bounds = keep;
           throw;
         }
         c->precision = prec;
+        c->score_bounds = keep;
         for (size_t k = 0; k < own.size(); ++k) exact[own[k]] = ex[k];
         c->rescored_views += (int64_t)own.size();
       }

@@ -307,14 +307,17 @@ int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f
   std::vector<double> ex(cont.size());
   gavis_render_outputs o = {};
   o.scores = ex.data();
+  const std::vector<double> bounds = c->score_bounds;  // the fp64 re-render must not clear them
   c->precision = GAVIS_PRECISION_EXACT;
   try {
     ua_render(c, s, f, nullptr, cc.data(), (int)cc.size(), rc, uc, &o);
   } catch (...) {
     c->precision = GAVIS_PRECISION_CERTIFIED;
+    c->score_bounds = bounds;
     throw;
   }
   c->precision = GAVIS_PRECISION_CERTIFIED;
+  c->score_bounds = bounds;
   for (size_t k = 0; k < cont.size(); ++k) sc[cont[k]] = ex[k];
   c->rescored_views += (int64_t)cont.size();
   return first_max();

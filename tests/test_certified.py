@@ -487,3 +487,14 @@ def test_certified_argmax_near_ties_around_zero(ctx, ctx_exact):
     cert = api.select_nbv(ctx, scene, f, cams, RC, uc)
     assert cert.best_index == exact.best_index
     assert ctx.counters()[1] - before >= 2  # near-ties went to the fp64 re-scoring
+
+
+def test_select_keeps_score_bounds(ctx):
+    """select_nbv's fp64 re-scoring of its contenders does not clear the bounds of
+    the certified scores it returns (gavis_ctx_last_score_bounds)."""
+    c = synth.config1(0)
+    f = api.construct_field(ctx, c["scene"], c["train"], VmfParams(1.0), 2, RC)
+    cams = [c["candidates"][5]] * 3 + c["candidates"][:3]  # identical triple: contenders
+    api.select_nbv(ctx, c["scene"], f, cams, RC, UC)
+    b = ctx.last_score_bounds()
+    assert b.shape == (len(cams),) and np.all(b > 0)
