@@ -58,3 +58,22 @@ def test_no_cpu_fallback_without_device(lib):
     assert status == 5
     with pytest.raises(DeviceError):
         N.check(status)
+
+
+def test_comm_unique_id_without_device(lib):
+    """The library's NCCL is loaded at run time (dlopen libnccl.so.2); a unique id
+    needs no device (rank 0 makes it, the host ships the 128 bytes)."""
+    from paper_2605_30342_b200 import api
+    a, b = api.Comm.unique_id(), api.Comm.unique_id()
+    assert len(a) == N.COMM_ID_BYTES == 128 and a != b
+
+
+def test_comm_create_fails_loudly_without_device(lib):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a CUDA device is present")
+    except ImportError:
+        pass
+    h = C.c_void_p()
+    assert lib.gavis_ctx_create(0, None, C.byref(h)) == 5  # no context, hence no communicator
