@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
 // branches: an entry a pixel does not cover, or one past its termination, gets
 // alpha = alpha* = 0, which leaves every accumulator bit-identical.
 template <int LC, bool RGB, bool ENT, bool EXTRA, bool LO, int BATCH = kBatch>
-__global__ void __launch_bounds__(256, 3) ua_blend_ilp_kernel(UaBlendArgs a) {
+// (entropy-only renders -- select_nbv without RGB -- fit 4 CTAs per SM in 63
+// registers without spills; the FFMA-colour RGB variants need 80, 3 CTAs)
+__global__ void __launch_bounds__(256, RGB ? 3 : 4) ua_blend_ilp_kernel(UaBlendArgs a) {
   constexpr int CS = Col<LC>::STRIDE;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   ExGeo* s_geo = reinterpret_cast<ExGeo*>(s_dyn);
