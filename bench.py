@@ -124,6 +124,9 @@ def dist_init():
             torch.cuda.set_device(local)
             d.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            # plumbing test: ranks share the visible devices round-robin; every
+            # collective is a host-side gloo call, so no rank's kernel waits on another's
+            local = local % max(1, torch.cuda.device_count())
             d.init_process_group(backend)
         dist = d
     return rank, local, world, dist
@@ -385,7 +388,9 @@ def run_ours(args):
 
     # the library's own NCCL communicator (gavis_comm): the VF all-reduce and the
     # score all-gather of the sharded paths run inside libgavis_b200.so
-    comm = api.Comm.from_dist(ctx, dist) if world > 1 else None
+    # (GAVIS_DIST_BACKEND=gloo, a plumbing test with ranks sharing devices, keeps
+    # the collectives on the host through parallel.py instead)
+    comm = api.Comm.from_dist(ctx, dist) if world > 1 and dist.get_backend() == "nccl" else None
 
     # ---------------- VF CONST: sharded views + NCCL all-reduce --------------
     def build_field(views, dscene=None, deg=None):
@@ -423,7 +428,9 @@ def run_ours(args):
             return api.select_nbv(ctx, ds, field, cands, rc, uc, with_rgb=True)
         # global argmax: each rank scores its block, the library all-gathers the
         # scores over NCCL, contenders are re-scored in fp64 on their ranks
-        return api.select_nbv_comm(comm, ds, field, c["candidates"], rc, uc, with_rgb=True)
+        if comm is not None:
+            return api.select_nbv_comm(comm, ds, field, c["candidates"], rc, uc, with_rgb=True)
+        return api.select_nbv_sharded(ctx, ds, field, c["candidates"], rank, world, dist, rc, uc, with_rgb=True)
 
     KERNELS = ("ua_blend", "ua_redo", "preprocess", "sort", "depth_order", "scan",
                "emit_keys", "ranges", "score")
@@ -545,6 +552,8 @@ def run_ours(args):
             f2 = api.upload_field(ctx, s2, host_field)
             if comm is not None:  # the global select: this rank's block, scores gathered by the library
                 r = api.select_nbv_comm(comm, s2, f2, c["candidates"], rc, uc, with_rgb=True)
+            elif world > 1:
+                r = api.select_nbv_sharded(ctx, s2, f2, c["candidates"], rank, world, dist, rc, uc, with_rgb=True)
             else:
                 r = api.select_nbv(ctx, s2, f2, cands, rc, uc, with_rgb=True)
             f2.close()
@@ -631,7 +640,8 @@ def run_ours(args):
                        "candidates_per_gpu_per_step": len(cands), "training_views": len(train),
                        "field_degree": degree, "color_degree": scene.color_degree,
                        "parallelism": f"candidates sharded over {world} GPU(s), VF views sharded + NCCL all-reduce"
-                                      + (" (libgavis_b200 gavis_comm)" if world > 1 else ""),
+                                      + (" (libgavis_b200 gavis_comm)" if comm is not None else
+                                         " (torch.distributed, gloo plumbing test)" if world > 1 else ""),
                        "l2": "inputs (scene+field) exceed the 126 MB L2; no flush"},
             "roofline": roofline(head, head_prec),
             "pipeline": {"bytes_per_step": pipe_bytes, "achieved_gbs": pipe_bytes / (head["ms_local"] / args.steps / 1000.0) / 1e9,
@@ -759,7 +769,8 @@ def run_sweep5(ctx, api, parallel, rank, world, dist, build_field, rc, uc, comm=
                 return [int(x) for x in chosen]
             chosen = []
             for _ in range(rounds):
-                r = api.select_nbv_comm(comm, ds5, f, pool, rc, uc)
+                r = (api.select_nbv_comm(comm, ds5, f, pool, rc, uc) if comm is not None else
+                     api.select_nbv_sharded(ctx, ds5, f, pool, rank, world, dist, rc, uc))
                 chosen.append(int(r.best_index))
                 api.accumulate_views(ctx, f, ds5, [pool[r.best_index]], rc)  # num_views += 1
             return chosen
