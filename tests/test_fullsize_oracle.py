@@ -160,3 +160,33 @@ def test_device_matches_reference_itself(setup):
         assert np.max(np.abs(out["invisible_mass"][:P] - w0)) <= 1e-4
         assert np.max(np.abs(out["transmittance"][:P] - T)) <= (1e-12 if precision == "exact" else 1e-6)
     f.close()
+
+
+def test_config5_loop_matches_reference_rebuild():
+    """Config 5 (BASELINE.json): the config-2 scene (500k Gaussians, 100 training
+    views at 800^2, field degree 3) and 400^2 candidates. The device's NBV loop
+    appends each chosen view to the field incrementally (gavis_nbv_loop); the
+    reference's own code (oracle/_ref) REBUILDS the field over the grown
+    trajectory every round (construct_field, vfield.hpp:68-92) and selects with
+    select_nbv (planner.hpp:117-137), as run_active_mapping does with density
+    control off (planner.hpp:297-301). Chosen views and their scores must agree."""
+    import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    c = synth.config5(0, n_candidates=48)
+    rounds = 3
+    cams = c["candidates"]
+    with api.Context(0) as ctx:  # fp64 (the default precision)
+        ds = ctx.upload(c["scene"])
+        f = api.construct_field(ctx, ds, c["train"], VmfParams(1.0), c["degree"], RC)
+        chosen, best_scores, all_scores = api.nbv_loop(ctx, ds, f, cams, rounds, RC, UC)
+    osc = O.OracleScene(c["scene"])
+    rs = R.RefScene(osc)
+    traj = list(c["train"])
+    for r in range(rounds):
+        g = R.construct_field_h(rs, traj, 1.0, c["degree"], RC, threads=THREADS)
+        best, scores = R.select_nbv(osc, g, c["degree"], len(traj), cams, RC, UC, threads=THREADS)
+        assert int(chosen[r]) == best, f"round {r}: device {chosen[r]} vs reference {best}"
+        assert np.max(np.abs(all_scores[r] - scores) / np.abs(scores)) <= 1e-9, f"round {r}"
+        traj.append(cams[best])
+    rs.close()
