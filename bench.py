@@ -646,7 +646,11 @@ def run_ours(args):
             "roofline": roofline(head, head_prec),
             "pipeline": {"bytes_per_step": pipe_bytes, "achieved_gbs": pipe_bytes / (head["ms_local"] / args.steps / 1000.0) / 1e9,
                          "pairs_per_view": K_avg,
-                         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in head["ktimes"].items()}},
+                         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in head["ktimes"].items()},
+                         "kernel_ms_note": "CUDA-event spans on each kernel's own stream; the binning kernels and the "
+                                           "side-stream kernels (score, redo) run concurrently with the blend, so "
+                                           "their spans include time queued behind it (fp64 path: the default-"
+                                           "priority side stream's score span covers the next batch's blend)"},
             "select_nbv_entropy_only_views_per_s": select_only,
             "vf_build_ms": vf_ms, "vf_build_views": len(train), "vf_build_200_views_ms": vf200_ms,
             "vf_build_other_configs": vf_other,

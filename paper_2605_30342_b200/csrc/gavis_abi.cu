@@ -39,9 +39,15 @@ gavis_status gavis_ctx_create(int32_t device, void* stream, gavis_ctx** out) {
         c->own_stream = true;
       }
       CK(cudaMallocHost(&c->pinned, sizeof(int32_t) * kPinWords));
-      CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
       int lo_prio = 0, hi_prio = 0;
       CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+      CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      // certified renders' side stream (fp64 redo, scores, copy-outs of batch k):
+      // above the blend's priority, so the redo of batch k is not queued behind
+      // batch k+1's tiles (certified 2032 -> 2042 views/s; the fp64 path keeps
+      // the default-priority side stream: 1481 vs 1472)
+      CK(cudaStreamCreateWithPriority(&c->side_hi, cudaStreamNonBlocking,
+                                      hi_prio < lo_prio ? hi_prio + 1 : hi_prio));
       CK(cudaStreamCreateWithPriority(&c->front, cudaStreamNonBlocking, hi_prio));
       for (int k = 0; k < gavis_ctx::kSets; ++k) {
         CK(cudaEventCreateWithFlags(&c->ev_blend[k], cudaEventDisableTiming));
@@ -80,7 +86,7 @@ gavis_status gavis_ctx_destroy(gavis_ctx* c) {
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->pin_scores) cudaFreeHost(c->pin_scores);
     if (c->pin_bounds) cudaFreeHost(c->pin_bounds);
-    for (cudaStream_t st : {c->side, c->front})
+    for (cudaStream_t st : {c->side, c->side_hi, c->front})
       if (st) {
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);

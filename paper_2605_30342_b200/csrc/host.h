@@ -247,6 +247,7 @@ struct gavis_ctx {
   // `side` overlap batch k+1's binning on `stream`; per-batch buffers alternate
   // between two sets (bufset), events order the reuse.
   cudaStream_t side = nullptr;
+  cudaStream_t side_hi = nullptr;  // the side stream of certified renders (priority above the blend)
   cudaStream_t front = nullptr;  // binning of batch k+1 under batch k's blend (high priority)
   int bufset = 0;
   static constexpr int kSets = 3;  // per-batch buffer sets (UA renders rotate over all three)
@@ -369,6 +370,7 @@ struct gavis_ctx {
   void sync_all() {
     CK(cudaStreamSynchronize(stream));
     if (side) CK(cudaStreamSynchronize(side));
+    if (side_hi) CK(cudaStreamSynchronize(side_hi));
     if (front) CK(cudaStreamSynchronize(front));
     collect(true);
   }

@@ -86,8 +86,9 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   // bound") for the constant variance provider without the correlation hook
   const bool bounded = fast && out->scores && uc->variance_provider == 0 && uc->correlation == 0;
   c->score_bounds.clear();
+  cudaStream_t const side = fast ? c->side_hi : c->side;
   CK(cudaEventRecord(c->ev_done[0], c->stream));  // side / front work start after this point
-  CK(cudaStreamWaitEvent(c->side, c->ev_done[0], 0));
+  CK(cudaStreamWaitEvent(side, c->ev_done[0], 0));
   CK(cudaStreamWaitEvent(c->front, c->ev_done[0], 0));
   cudaStream_t main_stream = c->stream;
   struct BufsetReset {
@@ -182,7 +183,6 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
       if (out->entropy_contributors)
         ua.ent_contrib = (int32_t*)c->buf("img_nent", sizeof(int32_t) * P);
     }
-    cudaStream_t side = c->side;
     if (fast && b.total_tiles > 0) {
       invariant(P < (int64_t(1) << 32), "too many pixels in one batch");
       ua.flag_list = (uint32_t*)c->buf("flag_list", sizeof(uint32_t) * P);
@@ -245,7 +245,7 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
   }
   c->bufset = 0;
   // the main stream continues after the side stream's last batch
-  CK(cudaEventRecord(c->ev_done[0], c->side));
+  CK(cudaEventRecord(c->ev_done[0], side));
   CK(cudaStreamWaitEvent(c->stream, c->ev_done[0], 0));
   if (redo_total) {
     CK(cudaMemcpyAsync(c->pinned + kPinRedo, redo_total, sizeof(unsigned long long),
