@@ -11,7 +11,9 @@ import os
 from .model import DeviceError, InvariantError, OracleError, ParameterError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgavis_b200.so")
+# GAVIS_LIB_PATH: an A/B build of the same sources with other compile-time knobs
+# (python -m paper_2605_30342_b200.build --variant NAME -DKNOB=V)
+LIB_PATH = os.environ.get("GAVIS_LIB_PATH") or os.path.join(_PKG, "libgavis_b200.so")
 
 
 class Camera(C.Structure):

@@ -33,18 +33,22 @@ def _stale(obj: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, ptxas_info: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, ptxas_info: bool = False, defines=(), lib: str = LIB,
+          build_dir: str = BUILD) -> str:
+    """Compile every csrc/*.cu and link `lib`. `defines` (e.g. ["GAVIS_EXACT_BATCH=96"])
+    with a separate `lib`/`build_dir` build an A/B variant of the compile-time knobs
+    (loaded through GAVIS_LIB_PATH)."""
+    os.makedirs(build_dir, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     objs = []
     jobs = []
     for src in sources:
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if _stale(obj, [src] + headers + [__file__]):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
             if ptxas_info:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -58,14 +62,23 @@ def build(verbose: bool = False, ptxas_info: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
         list(ex.map(run, jobs))
-    if jobs or not os.path.exists(LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
+    if jobs or not os.path.exists(lib):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xcompiler", "-fPIC"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, ptxas_info="--ptxas" in sys.argv))
+    # python -m paper_2605_30342_b200.build [-v] [--ptxas] [--variant NAME -DKNOB=V ...]
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        print(build(verbose="-v" in args, ptxas_info="--ptxas" in args, defines=defs,
+                    lib=os.path.join(ROOT, "build", f"libgavis_b200_{name}.so"),
+                    build_dir=os.path.join(ROOT, "build", f"native_{name}")))
+    else:
+        print(build(verbose="-v" in args, ptxas_info="--ptxas" in args, defines=defs))

@@ -323,23 +323,27 @@ gavis_status gavis_debug_project(gavis_ctx* c, const gavis_scene* s, const gavis
                        c->stream));
     c->sync();
     for (int64_t i = 0; i < N; ++i) {
-      const bool ok = g[i].flags & 1u;
+      const bool ok = !std::isnan(g[i].depth);  // K1 marks culled slots with a NaN depth
       if (culled) culled[i] = ok ? 0 : 1;
       if (mean) {
         mean[2 * i] = g[i].mx;
         mean[2 * i + 1] = g[i].my;
       }
       if (conic) {
-        conic[3 * i] = g[i].ca;
-        conic[3 * i + 1] = g[i].cb2 * 0.5;
-        conic[3 * i + 2] = g[i].cc;
+        conic[3 * i] = -2.0 * g[i].na;  // (a, b, c) from the pre-scaled record: exact
+        conic[3 * i + 1] = -g[i].nb;
+        conic[3 * i + 2] = -2.0 * g[i].nc;
       }
       if (depth) depth[i] = g[i].depth;
       if (cover_rect) {
-        cover_rect[4 * i] = g[i].cov_x & 0xFFFF;
-        cover_rect[4 * i + 1] = (g[i].cov_x >> 16) & 0xFFFF;
-        cover_rect[4 * i + 2] = g[i].cov_y & 0xFFFF;
-        cover_rect[4 * i + 3] = (g[i].cov_y >> 16) & 0xFFFF;
+        // (x0, x1, y0, y1); an empty axis as (1, 0)
+        const int32_t cv[2] = {g[i].cov_x, g[i].cov_y};
+        for (int ax = 0; ax < 2; ++ax) {
+          const int lo = cv[ax] & 0xFFFF, w = (int)((uint32_t)cv[ax] >> 16);
+          const bool empty = cv[ax] == kCovEmpty;
+          cover_rect[4 * i + 2 * ax] = empty ? 1 : lo;
+          cover_rect[4 * i + 2 * ax + 1] = empty ? 0 : lo + w;
+        }
       }
       if (tile_rect) {
         tile_rect[4 * i] = tr[i].x & 0xFFFF;

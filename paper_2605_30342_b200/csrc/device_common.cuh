@@ -31,16 +31,19 @@ struct DevCam {
   int64_t pix_base;   // first output pixel of this view
 };
 
-// One projected splat (ImageSpaceSplat, raster.hpp:37-44) in 64 bytes.
+// One projected splat (ImageSpaceSplat, raster.hpp:37-44) in 64 bytes, in the
+// form the blends consume it (no per-use decoding): the conic pre-scaled by -1/2
+// (a power of two: exact), so x = -q/2 comes out of two FMAs; the opacity
+// widened once; the exact coverage interval per axis as (start, width).
 struct __align__(16) GeoRec {
   double mx, my;        // mean
-  double ca, cb2, cc;   // conic a, 2*b, c   (2.0*b is exact)
-  double depth;
-  int32_t cov_x;        // x0 | x1 << 16 : pixels with |x+0.5-mx| <= r
-  int32_t cov_y;        // y0 | y1 << 16
-  float opacity;
-  uint32_t flags;       // bit0: not culled
+  double na, nb, nc;    // -a/2, -b, -c/2 of the conic (a, b, c)
+  double o;             // opacity
+  double depth;         // NaN marks a culled slot (debug dumps only)
+  int32_t cov_x;        // x0 | (x1 - x0) << 16 : pixels with |x+0.5-mx| <= r
+  int32_t cov_y;        // y0 | (y1 - y0) << 16; kCovEmpty when none
 };
+constexpr int32_t kCovEmpty = 0xFFFF;  // start 65535, width 0: never hit (widths < 65535)
 
 // Entropy-track constants of one splat (compensated_alpha, uncertainty.hpp:55-59):
 // alpha* = A*alpha + B with A = v + beta(1-v), B = o0(1-beta)(1-v); hl is the
@@ -53,18 +56,12 @@ struct __align__(16) UaRec {
 };
 
 __device__ __forceinline__ int cov_lo(int32_t packed) { return packed & 0xFFFF; }
-__device__ __forceinline__ int cov_hi(int32_t packed) { return (packed >> 16) & 0xFFFF; }
+__device__ __forceinline__ int cov_width(int32_t packed) { return (int)((uint32_t)packed >> 16); }
 
 // Coverage rectangle as (x0, x1-x0, y0, y1-y0) for a two-compare unsigned test
-// (unsigned)(px - x0) <= x1 - x0; an empty axis becomes (2^30, 0), never hit.
+// (unsigned)(px - x0) <= x1 - x0; an empty axis is (65535, 0), never hit.
 __device__ __forceinline__ int4 cover_rect4(int32_t cov_x, int32_t cov_y) {
-  const int x0 = cov_lo(cov_x), x1 = cov_hi(cov_x), y0 = cov_lo(cov_y), y1 = cov_hi(cov_y);
-  int4 r;
-  r.x = x0 <= x1 ? x0 : (1 << 30);
-  r.y = x0 <= x1 ? x1 - x0 : 0;
-  r.z = y0 <= y1 ? y0 : (1 << 30);
-  r.w = y0 <= y1 ? y1 - y0 : 0;
-  return r;
+  return make_int4(cov_lo(cov_x), cov_width(cov_x), cov_lo(cov_y), cov_width(cov_y));
 }
 
 __device__ __forceinline__ bool in_rect4(int4 r, int px, int py) {
@@ -172,13 +169,13 @@ __device__ __forceinline__ bool covers_1d(int x, double m, double r) {
 // Exact pixel interval of splat_covers along one axis, starting from the
 // binning interval [lo, hi] (never more than a pixel away).
 __device__ __forceinline__ int32_t exact_cover(int lo, int hi, int n, double m, double r) {
-  if (lo > hi) return 1;  // x0 = 1, x1 = 0: empty
+  if (lo > hi) return kCovEmpty;
   while (lo > 0 && covers_1d(lo - 1, m, r)) --lo;
   while (lo <= hi && !covers_1d(lo, m, r)) ++lo;
   while (hi < n - 1 && covers_1d(hi + 1, m, r)) ++hi;
   while (hi >= lo && !covers_1d(hi, m, r)) --hi;
-  if (lo > hi) return 1;
-  return (int32_t)(lo | (hi << 16));
+  if (lo > hi) return kCovEmpty;
+  return (int32_t)(lo | ((hi - lo) << 16));
 }
 
 }  // namespace gavis

@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
         a.trect[slot] = empty_rect;
         if (a.write_culled) {
           GeoRec r = {};
-          r.cov_x = 1;
-          r.cov_y = 1;
+          r.depth = __longlong_as_double(0x7ff8000000000000LL);  // culled
+          r.cov_x = r.cov_y = kCovEmpty;
           a.geo[slot] = r;
         }
       }
@@ -286,14 +286,14 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
       const double inv_det = 1.0 / p.det;
       r.mx = p.mx;
       r.my = p.my;
-      r.ca = p.c11 * inv_det;
-      r.cb2 = 2.0 * (-p.c01 * inv_det);
-      r.cc = p.c00 * inv_det;
+      // conic (a, b, c) = (c11, -c01, c00) / det, scaled by -1/2 (exact)
+      r.na = -0.5 * (p.c11 * inv_det);
+      r.nb = p.c01 * inv_det;
+      r.nc = -0.5 * (p.c00 * inv_det);
+      r.o = (double)po.w;
       r.depth = p.depth;
       r.cov_x = exact_cover(x0, x1, c.width, p.mx, p.radius);
       r.cov_y = exact_cover(y0, y1, c.height, p.my, p.radius);
-      r.opacity = po.w;
-      r.flags = 1u;
       a.geo[slot] = r;
       if (a.ua) {
         double vis = 0.0;
@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
       }
     } else if (a.write_culled) {
       GeoRec r = {};
-      r.cov_x = 1;
-      r.cov_y = 1;
+      r.depth = __longlong_as_double(0x7ff8000000000000LL);  // culled
+      r.cov_x = r.cov_y = kCovEmpty;
       a.geo[slot] = r;
     }
     a.counts[slot] = count;

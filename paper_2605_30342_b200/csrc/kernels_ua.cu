@@ -11,8 +11,10 @@
 // The two tracks share the splat's alpha but terminate independently; a pixel
 // leaves the loop when both are done.
 //
-// Schedules:
-//   * ua_blend_ilp_kernel (16x16 tiles, default): 256 threads, one pixel each,
+// Schedules (the default fp64 kernel for 16x16 tiles with colour degree <= 3 is
+// ua_blend_exact_mma_kernel, kernels_ua_fast.cu, dispatched from launch_ua_blend):
+//   * ua_blend_ilp_kernel (16x16 tiles; colour degree > 3 or GAVIS_UA_COLOR=ffma):
+//     256 threads, one pixel each,
 //     warp pre-filter of the tile list, list entries walked two at a time in
 //     straight-line code (fp64 instruction-level parallelism).
 //   * ua_blend_kernel (any tile size): 256 threads, one pixel each, in rounds.

@@ -206,10 +206,10 @@ __device__ __forceinline__ void fstage_batch(const UaBlendArgs& a, const GeoRec*
     FGeo f;
     f.mx = r.mx;
     f.my = r.my;
-    f.ca = r.ca;
-    f.cb2 = r.cb2;
-    f.cc = r.cc;
-    f.o = r.opacity;
+    f.ca = -2.0 * r.na;  // a, 2b, c: exact rescaling of the K1 record
+    f.cb2 = -2.0 * r.nb;
+    f.cc = -2.0 * r.nc;
+    f.o = (float)r.o;  // widened from the scene's fp32 opacity: exact
     f.depth = (float)r.depth;
     s_geo[j] = f;
     s_rect[j] = cover_rect4(r.cov_x, r.cov_y);
@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(256, kExactMinBlocks) ua_blend_exact_mma_kerne
 }
 
 // ---------------------------------------------------------------------------
-// K7 exact, TMA ring (default for RGB renders on 16x16 tiles): the same fp64
+// K7 exact, TMA ring (opt-in, GAVIS_UA_RING=1; measured slower): the same fp64
 // blend and tensor-core colour as ua_blend_exact_mma_kernel, but the tile list
 // streams through a ring of kRing slots of 32 entries filled by bulk copies
 // (cp.async.bulk, completion on an mbarrier per slot) instead of staged batches
@@ -883,7 +883,12 @@ __global__ void __launch_bounds__(256, kExactMinBlocks) ua_blend_exact_mma_kerne
 // before any warp waits on the slot: once every warp's pixels are done the ring
 // stops refilling and each warp leaves at the first STOP, with no copy in
 // flight (every issued slot was waited on before its successor was decided).
-constexpr int kRing = 4;
+#ifndef GAVIS_RING_SLOTS
+#define GAVIS_RING_SLOTS 4
+#define GAVIS_RING_MIN_BLOCKS 3
+#endif
+constexpr int kRing = GAVIS_RING_SLOTS;
+constexpr int kRingMinBlocks = GAVIS_RING_MIN_BLOCKS;
 constexpr int kRingEntries = 32;
 constexpr int kRingStop = -1;
 
@@ -949,7 +954,7 @@ __device__ __forceinline__ void ring_issue(const UaBlendArgs& a, const GeoRec* g
 }
 
 template <int LC, bool ENT, bool EXTRA, bool LO>
-__global__ void __launch_bounds__(256, 3) ua_blend_exact_tma_kernel(UaBlendArgs a) {
+__global__ void __launch_bounds__(256, kRingMinBlocks) ua_blend_exact_tma_kernel(UaBlendArgs a) {
   using L = RingLayout<ENT>;
   extern __shared__ __align__(128) unsigned char s_dyn[];
   GeoRec* s_geo = reinterpret_cast<GeoRec*>(s_dyn);
@@ -1165,7 +1170,7 @@ void launch_exact_tma(const UaBlendArgs& a, cudaStream_t s) {
 }
 
 // GAVIS_UA_RING=1 selects the TMA-ring kernel (A/B; the barrier-staged kernel
-// is the default: 1411 vs 1300 views/s at config 3)
+// is the default: 720 vs 765 ms of blend per 1024 views at config 3)
 inline bool exact_ring() {
   static const bool ring = [] {
     const char* e = std::getenv("GAVIS_UA_RING");

@@ -116,30 +116,15 @@ __device__ __forceinline__ void sh_color(const float2* col2, const float2* bp, f
 // uncertainty.hpp:198-222) are evaluated in fp64 with FMA contraction where it
 // saves an instruction; results agree with the unfused reference to rounding.
 
-// One list entry as the exact blend stages it: the conic pre-scaled by -1/2
-// (a power of two: exact), so x = -q/2 comes out of two FMAs; opacity widened once.
-struct __align__(16) ExGeo {
-  double mx, my;
-  double na, nb, nc;  // -a/2, -b (= -(2b)/2), -c/2
-  double o, depth, _pad;
-};
+// One list entry as the exact blend stages it: the K1 record itself (conic
+// pre-scaled by -1/2, opacity in fp64: device_common.cuh).
+using ExGeo = GeoRec;
 // Entropy-track constants with 1 - v and 1/2 ln|Q_c| + C_H precomputed.
 struct ExUa {
   double A, B, v, omv, hlc;
 };
 
-__device__ __forceinline__ ExGeo ex_geo(const GeoRec& r) {
-  ExGeo e;
-  e.mx = r.mx;
-  e.my = r.my;
-  e.na = -0.5 * r.ca;
-  e.nb = -0.5 * r.cb2;
-  e.nc = -0.5 * r.cc;
-  e.o = (double)r.opacity;
-  e.depth = r.depth;
-  e._pad = 0.0;
-  return e;
-}
+__device__ __forceinline__ const ExGeo& ex_geo(const GeoRec& r) { return r; }
 
 __device__ __forceinline__ ExUa ex_ua(const UaRec& u) {
   ExUa x;
@@ -149,18 +134,6 @@ __device__ __forceinline__ ExUa ex_ua(const UaRec& u) {
   x.omv = u.omv;  // 1 - v, u.hl + C_H (K1)
   x.hlc = u.hlc;
   return x;
-}
-
-// x = -q/2 at the pixel centre, q = a dx^2 + 2b dx dy + c dy^2.
-__device__ __forceinline__ double ex_negq(const ExGeo& e, double cxp, double cyp) {
-  const double dx = cxp - e.mx, dy = cyp - e.my;
-  return fma(dx, fma(e.na, dx, e.nb * dy), e.nc * dy * dy);
-}
-
-// alpha = min(o exp(-q/2), alpha_max); q > kQSkip -> 0 (T bit-identical, fast_math.cuh).
-__device__ __forceinline__ double ex_alpha(const ExGeo& e, double x, double amax) {
-  const double al = e.o * exp_neg(x);
-  return x >= -0.5 * kQSkip ? (al > amax ? amax : al) : 0.0;
 }
 
 // compensated_alpha (uncertainty.hpp:55-59): clamp(A alpha + B, 0, alpha_max).

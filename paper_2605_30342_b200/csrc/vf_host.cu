@@ -341,16 +341,16 @@ gavis_status gavis_vf_query_view(gavis_ctx* c, const gavis_field* f, const gavis
     o.field = f;
     o.write_culled = true;
     Binned b = bin_batch(c, s, cam, 1, &rc, o);
-    std::vector<uint32_t> flags((size_t)N);
+    std::vector<double> depth((size_t)N);
     std::vector<double> v((size_t)N);
-    CK(cudaMemcpy2DAsync(flags.data(), sizeof(uint32_t), &b.geo[0].flags, sizeof(GeoRec),
-                         sizeof(uint32_t), N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpy2DAsync(depth.data(), sizeof(double), &b.geo[0].depth, sizeof(GeoRec),
+                         sizeof(double), N, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpy2DAsync(v.data(), sizeof(double), &b.ua[0].v, sizeof(UaRec), sizeof(double), N,
                          cudaMemcpyDeviceToHost, c->stream));
     c->sync();
     int64_t k = 0;
     for (int64_t i = 0; i < N; ++i) {
-      if (!(flags[i] & 1u)) continue;
+      if (std::isnan(depth[i])) continue;  // culled (K1 marks it with a NaN depth)
       if (idx) idx[k] = (int32_t)i;
       if (vis) vis[k] = v[i];
       ++k;
