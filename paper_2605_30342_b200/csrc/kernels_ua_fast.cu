@@ -905,15 +905,21 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Sleep until the phase with `parity` completes: try_wait with a suspend-time
+// hint parks the warp in hardware (a bare try_wait returns after a short
+// system-dependent time, and re-issuing it from a C++ loop cost as many issue
+// slots as the blend itself: 5.6 G extra warp instructions per 16 views).
+#ifndef GAVIS_WAIT_HINT_NS
+#define GAVIS_WAIT_HINT_NS 2000
+#endif
+constexpr uint32_t kWaitHintNs = GAVIS_WAIT_HINT_NS;  // ~ one bulk-copy latency
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT;\n}"
+      ::"r"(smem_u32(bar)), "r"(parity), "r"(kWaitHintNs)
+      : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
