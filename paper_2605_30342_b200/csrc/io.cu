@@ -256,6 +256,7 @@ struct FieldDoc {
   int num_views = -1;
   std::vector<double> gamma;
   std::vector<uint8_t> virt;
+  std::vector<long long> row_lengths;
   long long rows = 0;
 };
 
@@ -283,11 +284,13 @@ FieldDoc parse_field(const std::string& path) {
       j.expect('[');
       while (!j.peek(']')) {
         j.expect('[');
+        const size_t row0 = d.gamma.size();
         while (!j.peek(']')) {
           d.gamma.push_back(j.num());
           if (j.peek(',')) j.expect(',');
         }
         j.expect(']');
+        d.row_lengths.push_back((long long)(d.gamma.size() - row0));
         ++d.rows;
         if (j.peek(',')) j.expect(',');
       }
@@ -313,7 +316,8 @@ FieldDoc parse_field(const std::string& path) {
   need(d.kappa >= 0.0 && d.kappa <= 50.0, "vmf kappa must lie in [0, 50]");
   need(d.num_views >= 0, "field: num_views must be non-negative");
   need((long long)d.virt.size() == d.rows, "field: gamma and virtual must be arrays of equal length");
-  need((long long)d.gamma.size() == d.rows * (d.L + 1) * (d.L + 1), "field gamma row: wrong length");
+  for (long long len : d.row_lengths)  // every row (L+1)^2 coefficients (vec_from, io.hpp:290)
+    need(len == (long long)(d.L + 1) * (d.L + 1), "field gamma row: wrong length");
   return d;
 }
 

@@ -95,6 +95,12 @@ def test_field_json_round_trip_and_schema(tmp_path):
     json.dump(bad, open(path, "w"))
     with pytest.raises(ParameterError):
         api.load_field_json(path)
+    # ragged rows with the right total are still rejected row by row (io.hpp:290)
+    bad = dict(doc)
+    bad["gamma"] = [doc["gamma"][0][:8], doc["gamma"][1] + [0.5]] + doc["gamma"][2:]
+    json.dump(bad, open(path, "w"))
+    with pytest.raises(ParameterError, match="row"):
+        api.load_field_json(path)
 
 
 # ---- ports of the reference's io tests (R/tests/test_io.cpp) -----------------
