@@ -79,12 +79,18 @@ __device__ __forceinline__ double exp_neg(double x) {
   return __hiloint2double(__double2hiint(res) + ((k >> 8) << 20), __double2loint(res));
 }
 
-// ln(s) for finite s > 0: s = 2^e * mant, mant in [1,2); mant * inv_j = 1 + r with
+// ln(s) for finite s > 0 (log_pos), and for the per-entry entropy terms
+// s (hl + C_H - ln s) of the blends (log_blend): there s = 0 must give a finite
+// value (s * finite = +0 exactly) and a subnormal s may get a wrong but finite
+// one -- the term is then below 1e-305 either way -- so log_blend skips
+// log_pos's subnormal rescaling (4 instructions per composited entry).
+// s = 2^e * mant, mant in [1,2); mant * inv_j = 1 + r with
 // |r| < 1/512 (inv_j ~ 1/c_j from the top 8 mantissa bits), ln(1+r) by a degree-5
 // Taylor polynomial (remainder < 1e-17), ln(s) = e ln2 - ln(inv_j) + ln(1+r).
-__device__ __forceinline__ double log_pos(double s) {
+template <bool SUBNORMAL>
+__device__ __forceinline__ double log_table(double s) {
   int e = 0;
-  if (__double2hiint(s) < 0x00100000) {  // subnormal: scale by 2^54
+  if (SUBNORMAL && __double2hiint(s) < 0x00100000) {  // subnormal: scale by 2^54
     s *= kMathConst[6];
     e = -54;
   }
@@ -101,5 +107,8 @@ __device__ __forceinline__ double log_pos(double s) {
   const double p = fma(r2, l234, l01) * r;
   return fma((double)e, kMathConst[4], g_log_neg[j] + p);
 }
+
+__device__ __forceinline__ double log_pos(double s) { return log_table<true>(s); }
+__device__ __forceinline__ double log_blend(double s) { return log_table<false>(s); }
 
 }  // namespace gavis

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(128) mixture_kernel(MixtureArgs a) {
     const double as = ex_astar<true>(u, al, a.amax);  // compensated_alpha (uncertainty.hpp:55-59)
     const double w = as * T;
     const double s = w * u.v;
-    if (s > 0.0) H = fma(s, u.hlc - log_pos(s), H);
+    if (s > 0.0) H = fma(s, u.hlc - log_blend(s), H);
     w0 = fma(w, u.omv, w0);
     if (w > 0.0) {
       if (out) {

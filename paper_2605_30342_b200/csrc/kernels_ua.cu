@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
           const ExUa& u = s_ua[j];
           if (EXTRA) ++P.n_ent;
           const double sv = ex_ent<LC, EXTRA>(P, ex_astar<LO>(u, al, amax), u, e.depth);
-          if (sv > 0.0) P.H = fma(sv, u.hlc - log_pos(sv), P.H);
+          if (sv > 0.0) P.H = fma(sv, u.hlc - log_blend(sv), P.H);
           if (P.Te < cutoff) P.ent_done = true;
         }
         if (P.rgb_done && P.ent_done) break;
@@ -188,13 +188,13 @@ __global__ void __launch_bounds__(256, RGB ? 3 : 4) ua_blend_ilp_kernel(UaBlendA
           const bool eb_on = cb && !ed;
           const double sb = ex_ent<LC, EXTRA>(P, eb_on ? xb : 0.0, ub, eb.depth);
           if (LO) {  // s may be negative (given visibility outside [0, 1]): s > 0 only
-            const double la = log_pos(sa > 0.0 ? sa : 1.0);
-            const double lb = log_pos(sb > 0.0 ? sb : 1.0);
+            const double la = log_blend(sa > 0.0 ? sa : 1.0);
+            const double lb = log_blend(sb > 0.0 ? sb : 1.0);
             if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
             if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
-          } else {  // s >= 0; s == 0 adds exactly +0 (log_pos(0) is finite)
-            P.H = fma(sa, ua.hlc - log_pos(sa), P.H);
-            P.H = fma(sb, ub.hlc - log_pos(sb), P.H);
+          } else {  // s >= 0; s == 0 adds exactly +0 (log_blend(0) is finite)
+            P.H = fma(sa, ua.hlc - log_blend(sa), P.H);
+            P.H = fma(sb, ub.hlc - log_blend(sb), P.H);
           }
           if (EXTRA) P.n_ent += (int)ea_on + (int)eb_on;
           P.ent_done = ed || (eb_on && P.Te < cutoff);

@@ -689,13 +689,13 @@ __device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Re
     const bool eb_on = cb && !ed;
     const double sb = ex_ent<LC, EXTRA>(P, eb_on ? xb : 0.0, ub, eb.depth);
     if (LO) {  // s may be negative (given visibility outside [0, 1]): s > 0 only
-      const double la = log_pos(sa > 0.0 ? sa : 1.0);
-      const double lb = log_pos(sb > 0.0 ? sb : 1.0);
+      const double la = log_blend(sa > 0.0 ? sa : 1.0);
+      const double lb = log_blend(sb > 0.0 ? sb : 1.0);
       if (sa > 0.0) P.H = fma(sa, ua.hlc - la, P.H);
       if (sb > 0.0) P.H = fma(sb, ub.hlc - lb, P.H);
-    } else {  // s >= 0; s == 0 adds exactly +0 (log_pos(0) is finite)
-      P.H = fma(sa, ua.hlc - log_pos(sa), P.H);
-      P.H = fma(sb, ub.hlc - log_pos(sb), P.H);
+    } else {  // s >= 0; s == 0 adds exactly +0 (log_blend(0) is finite)
+      P.H = fma(sa, ua.hlc - log_blend(sa), P.H);
+      P.H = fma(sb, ub.hlc - log_blend(sb), P.H);
     }
     if (EXTRA) P.n_ent += (int)ea_on + (int)eb_on;
     P.ent_done = ed || (eb_on && P.Te < cutoff);
@@ -1304,7 +1304,7 @@ __global__ void __launch_bounds__(32) ua_redo_kernel(UaBlendArgs a) {
       if (ENT) {
         // H += s (-ln s + 1/2 ln|Qc| + C_H) in list order as fma(s, hlc - ln s, H):
         // the logs in parallel (one per lane), the sum serial
-        const double tl = my_s > 0.0 ? hlc - log_pos(my_s) : 0.0;
+        const double tl = my_s > 0.0 ? hlc - log_blend(my_s) : 0.0;
         mm = m;
         while (mm != 0u) {
           const int src = __ffs(mm) - 1;
