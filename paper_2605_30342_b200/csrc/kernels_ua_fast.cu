@@ -1290,7 +1290,7 @@ __global__ void __launch_bounds__(32) ua_redo_kernel(UaBlendArgs a) {
           if (P.T < cutoff) P.rgb_done = true;
         }
         if (ENT && !P.ent_done) {  // render_entropy_core (uncertainty.hpp:198-222), H deferred
-          ExUa u;
+          ExUa u = {};
           u.v = __shfl_sync(0xffffffffu, vv, src);
           u.omv = __shfl_sync(0xffffffffu, omv, src);
           const double eas = __shfl_sync(0xffffffffu, as, src);

@@ -119,22 +119,14 @@ __device__ __forceinline__ void sh_color(const float2* col2, const float2* bp, f
 // One list entry as the exact blend stages it: the K1 record itself (conic
 // pre-scaled by -1/2, opacity in fp64: device_common.cuh).
 using ExGeo = GeoRec;
-// Entropy-track constants with 1 - v and 1/2 ln|Q_c| + C_H precomputed.
-struct ExUa {
-  double A, B, v, omv, hlc;
-};
+// Entropy-track constants: the K1 record itself (A, B, v, 1 - v, 1/2 ln|Q_c| + C_H,
+// 1/2 ln|Q_c|; 48 bytes, 16-byte aligned: staged as a pure copy and read with
+// two 128-bit and one 64-bit shared load per entry).
+using ExUa = UaRec;
 
 __device__ __forceinline__ const ExGeo& ex_geo(const GeoRec& r) { return r; }
 
-__device__ __forceinline__ ExUa ex_ua(const UaRec& u) {
-  ExUa x;
-  x.A = u.A;
-  x.B = u.B;
-  x.v = u.v;
-  x.omv = u.omv;  // 1 - v, u.hl + C_H (K1)
-  x.hlc = u.hlc;
-  return x;
-}
+__device__ __forceinline__ const ExUa& ex_ua(const UaRec& u) { return u; }
 
 // compensated_alpha (uncertainty.hpp:55-59): clamp(A alpha + B, 0, alpha_max).
 // LO: the lower clamp, needed only for caller-given visibilities outside [0, 1]
