@@ -42,20 +42,31 @@ __constant__ double kMathConst[8] = {
 
 // Shared-memory copies of the lookup tables (namespace scope: direct shared
 // addressing in the inner loops).
+// The two log tables interleaved as {1/c_j, -ln(1/c_j)} pairs: one 128-bit load
+// per lookup instead of two 64-bit ones (GAVIS_LOG_PAIR=1; A/B).
+#ifndef GAVIS_LOG_PAIR
+#define GAVIS_LOG_PAIR 1
+#endif
 __shared__ double g_exp2_tab[kExpTab];
+#if GAVIS_LOG_PAIR
+__shared__ double2 g_log_tab[kLogTab];
+#else
 __shared__ double g_log_inv[kLogTab];
 __shared__ double g_log_neg[kLogTab];
+#endif
 
 // Cooperative copy of the constant tables into shared memory (indices diverge
 // per lane, which constant memory would serialise). Callers synchronise before use.
 __device__ __forceinline__ void load_math_tables() {
-  for (int i = threadIdx.x; i < kExpTab + 2 * kLogTab; i += blockDim.x) {
+  for (int i = threadIdx.x; i < kExpTab + kLogTab; i += blockDim.x) {
     if (i < kExpTab)
       g_exp2_tab[i] = kExp2Tab[i];
-    else if (i < kExpTab + kLogTab)
-      g_log_inv[i - kExpTab] = kLogInv[i - kExpTab];
     else
-      g_log_neg[i - kExpTab - kLogTab] = kLogNeg[i - kExpTab - kLogTab];
+#if GAVIS_LOG_PAIR
+      g_log_tab[i - kExpTab] = make_double2(kLogInv[i - kExpTab], kLogNeg[i - kExpTab]);
+#else
+      g_log_inv[i - kExpTab] = kLogInv[i - kExpTab], g_log_neg[i - kExpTab] = kLogNeg[i - kExpTab];
+#endif
   }
 }
 
@@ -98,14 +109,19 @@ __device__ __forceinline__ double log_table(double s) {
   e += (hi >> 20) - 1023;
   const int j = (hi >> 12) & (kLogTab - 1);
   const double mant = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, __double2loint(s));
-  const double r = fma(mant, g_log_inv[j], -1.0);
+#if GAVIS_LOG_PAIR
+  const double2 tab = g_log_tab[j];
+#else
+  const double2 tab = make_double2(g_log_inv[j], g_log_neg[j]);
+#endif
+  const double r = fma(mant, tab.x, -1.0);
   // ln(1 + r) = r * (1 - r/2 + r^2/3 - r^3/4 + r^4/5), Estrin's scheme
   const double r2 = r * r;
   const double l01 = fma(r, kLogPoly[3], kLogPoly[4]);   // 1 - r/2
   const double l23 = fma(r, kLogPoly[1], kLogPoly[2]);   // 1/3 - r/4
   const double l234 = fma(r2, kLogPoly[0], l23);         // + r^2/5
   const double p = fma(r2, l234, l01) * r;
-  return fma((double)e, kMathConst[4], g_log_neg[j] + p);
+  return fma((double)e, kMathConst[4], tab.y + p);
 }
 
 __device__ __forceinline__ double log_pos(double s) { return log_table<true>(s); }

@@ -89,10 +89,22 @@ struct __align__(16) FGeo {
 //    own pixel's colours. Coefficients are split once per scene
 //    (SceneDev::colors_split) and staged as-is.
 constexpr int kColWords = 52;  // per staged entry: hi [3][16] f16 (24 words), lo (24), pad (4)
-// floats per pixel row of the warp's colour block, laid out [channel][8 entries]:
-// 26 makes both the fragment stores (STS.64, a (row, entry pair) per lane) and
-// the per-pixel reads (LDS.64, an entry pair per channel) bank-conflict free
+// The warp's colour block: 32 pixel rows of [channel][8 entries] floats. The
+// padded stride 26 keeps the per-pixel reads (LDS.64, lane = row) conflict-free;
+// the mma fragment stores (STS.64) then see 2-way conflicts. An XOR swizzle of
+// the entry pairs (stride 24, GAVIS_TR_SWIZZLE=1) removes those too (store
+// conflicts 198 M -> 33 M per 16 views) but costs an index op per access and was
+// 2 % slower overall: the shared-memory pipe is not the limiter.
+#ifndef GAVIS_TR_SWIZZLE
+#define GAVIS_TR_SWIZZLE 0
+#endif
+#if GAVIS_TR_SWIZZLE
+constexpr int kTrStride = 24;
+__device__ __forceinline__ int tr_idx(int row, int col) { return row * kTrStride + (col ^ (((row >> 2) & 3) << 1)); }
+#else
 constexpr int kTrStride = 26;
+__device__ __forceinline__ int tr_idx(int row, int col) { return row * kTrStride + col; }
+#endif
 
 template <int LC, bool RGB, bool ENT, bool MMA>
 struct FStage {
@@ -461,8 +473,8 @@ __device__ __forceinline__ void blend_batch(FPix<LC>& P, int n, const FGeo* s_ge
               hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
               // C fragment: (row gq | gq+8, cols 2 tig, 2 tig + 1) -> [pixel][channel][entry]
               const int r0 = 16 * m + gq, r1 = r0 + 8;
-              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
-              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
+              *reinterpret_cast<float2*>(tr + tr_idx(r0, ch * 8 + 2 * tig)) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + tr_idx(r1, ch * 8 + 2 * tig)) = make_float2(d[2], d[3]);
             }
           }
           __syncwarp();
@@ -477,9 +489,9 @@ __device__ __forceinline__ void blend_batch(FPix<LC>& P, int n, const FGeo* s_ge
             const bool cb = has_b && in_rect4(s_rect[jb], px, py);
             float3 cola = make_float3(0.f, 0.f, 0.f), colb = cola;
             if (RGB && MMA) {  // entries q, q+1 of the group, own pixel row
-              const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
-              const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
-              const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+              const float2 r = *reinterpret_cast<const float2*>(tr + tr_idx(lane, q));
+              const float2 g = *reinterpret_cast<const float2*>(tr + tr_idx(lane, 8 + q));
+              const float2 b = *reinterpret_cast<const float2*>(tr + tr_idx(lane, 16 + q));
               cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
               colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
             }
@@ -837,8 +849,8 @@ __global__ void __launch_bounds__(256, kExactMinBlocks) ua_blend_exact_mma_kerne
               hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
               hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
               const int r0 = 16 * m + gq, r1 = r0 + 8;
-              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
-              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
+              *reinterpret_cast<float2*>(tr + tr_idx(r0, ch * 8 + 2 * tig)) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + tr_idx(r1, ch * 8 + 2 * tig)) = make_float2(d[2], d[3]);
             }
           }
           __syncwarp();
@@ -851,9 +863,9 @@ __global__ void __launch_bounds__(256, kExactMinBlocks) ua_blend_exact_mma_kerne
             const int jb = has_b ? je[q + 1] : ja;
             const bool ca = in_rect4(s_rect[ja], px, py);
             const bool cb = has_b && in_rect4(s_rect[jb], px, py);
-            const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
-            const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
-            const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+            const float2 r = *reinterpret_cast<const float2*>(tr + tr_idx(lane, q));
+            const float2 g = *reinterpret_cast<const float2*>(tr + tr_idx(lane, 8 + q));
+            const float2 b = *reinterpret_cast<const float2*>(tr + tr_idx(lane, 16 + q));
             const float3 cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
             const float3 colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
             exact_pair<LC, ENT, EXTRA, LO>(P, s_geo[ja], s_geo[jb], s_ua[ENT ? ja : 0], s_ua[ENT ? jb : 0], ca,
@@ -1097,8 +1109,8 @@ __global__ void __launch_bounds__(256, kRingMinBlocks) ua_blend_exact_tma_kernel
               hmma16816(d, aH[m], bl[ch][0], bl[ch][1]);
               hmma16816(d, aL[m], bh[ch][0], bh[ch][1]);
               const int r0 = 16 * m + gq, r1 = r0 + 8;
-              *reinterpret_cast<float2*>(tr + r0 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[0], d[1]);
-              *reinterpret_cast<float2*>(tr + r1 * kTrStride + ch * 8 + 2 * tig) = make_float2(d[2], d[3]);
+              *reinterpret_cast<float2*>(tr + tr_idx(r0, ch * 8 + 2 * tig)) = make_float2(d[0], d[1]);
+              *reinterpret_cast<float2*>(tr + tr_idx(r1, ch * 8 + 2 * tig)) = make_float2(d[2], d[3]);
             }
           }
           __syncwarp();
@@ -1113,9 +1125,9 @@ __global__ void __launch_bounds__(256, kRingMinBlocks) ua_blend_exact_tma_kernel
             const GeoRec& gb = sg[jb];
             const bool ca = in_rect4(cover_rect4(ga.cov_x, ga.cov_y), px, py);
             const bool cb = has_b && in_rect4(cover_rect4(gb.cov_x, gb.cov_y), px, py);
-            const float2 r = *reinterpret_cast<const float2*>(tr + lane * kTrStride + q);
-            const float2 g = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 8 + q);
-            const float2 b = *reinterpret_cast<const float2*>(tr + lane * kTrStride + 16 + q);
+            const float2 r = *reinterpret_cast<const float2*>(tr + tr_idx(lane, q));
+            const float2 g = *reinterpret_cast<const float2*>(tr + tr_idx(lane, 8 + q));
+            const float2 b = *reinterpret_cast<const float2*>(tr + tr_idx(lane, 16 + q));
             const float3 cola = make_float3(__saturatef(r.x), __saturatef(g.x), __saturatef(b.x));
             const float3 colb = make_float3(__saturatef(r.y), __saturatef(g.y), __saturatef(b.y));
             exact_pair<LC, ENT, EXTRA, LO>(P, ga, gb, ENT ? ex_ua(su[ja]) : ExUa{},
