@@ -410,6 +410,12 @@ def run_ours(args):
         vf_times.append((time.perf_counter() - t0) * 1000.0)
         tmp.close()
     vf_ms = max_over_ranks(min(vf_times), dist)
+    # K6a (vf_blend) on its own: CUDA events around each launch in one more build
+    ctx.set_profiling(True)
+    ctx.kernel_time("vf_blend", reset=True)
+    build_field(train).close()
+    vf_blend_ms, vf_blend_n = ctx.kernel_time("vf_blend")
+    ctx.set_profiling(False)
     vf200_ms = None
     if "train200" in c:
         barrier(ctx, dist)
@@ -522,6 +528,36 @@ def run_ours(args):
                 "bytes_per_launch": bpl, "views_per_launch": vpl,
                 "avg_launch_ms": blend_ms / max(1, blend_n), "launches": blend_n,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+
+    def vf_roofline():
+        """K6a vf_blend: algorithmic bytes per training view 36 B per tile pair (the
+        pair's key + id written once and read once, 24 B, plus its fp64 partial sum
+        and count written once, 12 B), K_p from the exact pair counts of 8 views."""
+        kp = []
+        for cam in train[: min(8, len(train))]:
+            k, _, _ = api.debug_binning(ctx, ds, cam, rc)
+            kp.append(len(k))
+        lo_v, hi_v = parallel.shard_range(len(train), rank, world)
+        views_here = hi_v - lo_v
+        vpl = views_here / max(1, vf_blend_n)
+        bpl = vpl * 36.0 * float(np.mean(kp))
+        avg = vf_blend_ms / max(1, vf_blend_n)
+        achieved = bpl / (avg / 1000.0) / 1e9 if vf_blend_n else 0.0
+        out = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+               "kernel": "vf_blend (K6a fp64 VF blend)", "bytes_per_launch": bpl, "views_per_launch": vpl,
+               "pairs_per_view": float(np.mean(kp)), "avg_launch_ms": avg, "launches": vf_blend_n,
+               "share_of_vf_build": vf_blend_ms / max(1e-9, vf_ms) if world == 1 else None,
+               "traffic": None, "compute": None}
+        prof = os.path.join(ROOT, "profiles", "ncu_vf_blend.json")
+        if os.path.exists(prof):
+            with open(prof) as f:
+                pj = json.load(f)
+            out["traffic"] = pj["traffic_bytes_per_launch"] * vpl / pj["views_per_launch"]
+            out["traffic_source"] = f"{pj['command']} ({pj['views_per_launch']} views/launch, {pj['kernel']})"
+            out["compute"] = {"bound": pj.get("compute_bound", "issue/latency"),
+                              "fp64_pipe_active_pct": pj.get("fp64_pipe_active_pct"),
+                              "issue_slots_busy_pct": pj.get("issue_slots_busy_pct"), "source": "same ncu capture"}
+        return out
 
     N = scene.num_particles
     nb_c = (scene.color_degree + 1) ** 2
@@ -653,6 +689,7 @@ def run_ours(args):
                                            "priority side stream's score span covers the next batch's blend)"},
             "select_nbv_entropy_only_views_per_s": select_only,
             "vf_build_ms": vf_ms, "vf_build_views": len(train), "vf_build_200_views_ms": vf200_ms,
+            "vf_roofline": vf_roofline(),
             "vf_build_other_configs": vf_other,
             "best_index_last_step": head["best"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": head["launches"], "clocks": head["clocks"],

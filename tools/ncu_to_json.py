@@ -24,6 +24,7 @@ def main():
     p.add_argument("--command", default="")
     p.add_argument("--workload", default="config3 scene (1M Gaussians), 16 candidate views of 800x800 in one "
                                          "launch, RGB + entropy")
+    p.add_argument("--bound", default="issue/latency (fp64 pipe and block-barrier stalls)")
     a = p.parse_args()
     v, u = raw(a.rep)
 
@@ -44,7 +45,7 @@ def main():
          "executed_ipc": float(v["sm__inst_executed.avg.per_cycle_active"]),
          "achieved_warps_per_sm": float(v["sm__warps_active.avg.per_cycle_active"]),
          "l2_hit_rate_pct": float(v["lts__t_sector_hit_rate.pct"]),
-         "compute_bound": "issue/latency (fp64 pipe and block-barrier stalls)"}
+         "compute_bound": a.bound}
     json.dump(d, open(a.out, "w"), indent=1)
     print(json.dumps(d, indent=1))
 
