@@ -233,6 +233,7 @@ gavis_status gavis_select_nbv_sharded(gavis_comm* cm, const gavis_scene* s, cons
     gavis_ctx* c = cm->ctx;
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
+    ScoringPrecision sp(c, uc);
     const int W = cm->nranks;
     int64_t lo, hi;
     block_of(n_cams, cm->rank, W, &lo, &hi);

@@ -224,6 +224,7 @@ gavis_status gavis_nbv_loop(gavis_ctx* c, const gavis_scene* s, gavis_field* f,
     invariant(f->n == s->dev.n, "accumulate_view: field/scene particle count mismatch");
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
+    ScoringPrecision sp(c, uc);
     std::vector<double> sc((size_t)n_cams);
     for (int step = 0; step < steps; ++step) {
       gavis_render_outputs o = {};

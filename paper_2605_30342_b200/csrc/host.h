@@ -484,6 +484,23 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
                const gavis_uncertainty_config* uc, gavis_render_outputs* out);
 // Candidates that may be the fp64 argmax given certified scores (empty when the
 // context is not in certified mode); ua_host.cu.
+// The certified scores carry a rigorous bound only for the constant variance
+// provider without the correlation hook; for the other two modes a scoring
+// call (select_nbv, the NBV loop) runs the fp64 path instead, so the selected
+// view is the fp64 one by construction in every mode. RAII: restores the
+// context's precision on exit.
+struct ScoringPrecision {
+  gavis_ctx* c;
+  int32_t saved;
+  ScoringPrecision(gavis_ctx* ctx, const gavis_uncertainty_config* uc) : c(ctx), saved(ctx->precision) {
+    if (uc && c->precision == GAVIS_PRECISION_CERTIFIED && (uc->correlation != 0 || uc->variance_provider != 0))
+      c->precision = GAVIS_PRECISION_EXACT;
+  }
+  ~ScoringPrecision() { c->precision = saved; }
+  ScoringPrecision(const ScoringPrecision&) = delete;
+  ScoringPrecision& operator=(const ScoringPrecision&) = delete;
+};
+
 std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* rc,
                                       const std::vector<double>& sc);
 // select_nbv argmax over certified scores, contenders re-scored exactly (ua_host.cu).

@@ -262,11 +262,12 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
 }
 
 // select_nbv's argmax (planner.hpp:132-136: first strictly greater score) over
-// scores from the certified fp32 blend: every candidate within kCertScoreRel
-// (relative) of the best is re-scored with the exact fp64 blend and the argmax
-// is taken again, so it is the exact path's argmax (the fp32 scores agree with
-// the fp64 ones to a few 1e-6 relative -- 3e-6 at config 3 -- over two orders of
-// magnitude inside the window).
+// scores from the certified fp32 blend: every candidate i with
+// s_i >= s_best - max(e_best + e_i, kCertScoreRel |s_best|, kCertScoreAbs), e the
+// rigorous per-candidate score bounds K8 folds from K7f's per-pixel bounds, is
+// re-scored with the exact fp64 blend and the argmax is taken again, so it is the
+// exact path's argmax. (Scoring calls in the modes without a bound -- the
+// correlation hook, sh_propagation -- run the fp64 path: ScoringPrecision, host.h.)
 constexpr double kCertScoreRel = 1e-3;
 constexpr double kCertScoreAbs = 1e-9;  // absolute floor: scores near 0 keep a window
 
@@ -444,6 +445,7 @@ gavis_status gavis_select_nbv(gavis_ctx* c, const gavis_scene* s, const gavis_fi
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
     NvtxRange nvtx("select_nbv (planner.hpp:117-137)");
+    ScoringPrecision sp(c, uc);
     std::vector<double> sc((size_t)n_cams);
     gavis_render_outputs o = {};
     o.scores = sc.data();

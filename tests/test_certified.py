@@ -454,10 +454,36 @@ def test_certified_score_bounds_hold(ctx, ctx_exact, room, which):
     assert bounds.shape == (len(cams),) and np.all(bounds > 0)
     assert np.all(np.abs(cert - exact) <= bounds), (np.abs(cert - exact), bounds)
     assert np.all(bounds <= 1e-3 * np.abs(exact))
-    # the hook and sh_propagation fall back to the relative window: no bounds
+    # the hook and sh_propagation carry no bound (their scoring calls run fp64)
     api.render(ctx, scene, f, cams[:1], RC, UncertaintyConfig(correlation=1, correlation_lambda=2.0),
                scores=True)
     assert ctx.last_score_bounds().size == 0
+
+
+@pytest.mark.parametrize("mode", ["hook", "sh_propagation"])
+def test_unbounded_modes_score_in_fp64(ctx, ctx_exact, mode):
+    """select_nbv in certified mode with the correlation hook or sh_propagation --
+    the modes whose certified scores have no rigorous bound -- runs the fp64 path
+    (ScoringPrecision, host.h): scores bit-identical to the fp64 context's, no
+    contender re-scoring, and the context stays in certified mode afterwards."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    uc = (UncertaintyConfig(correlation=1, correlation_lambda=2.0) if mode == "hook"
+          else UncertaintyConfig(variance_provider=1))
+    ds, de = ctx.upload(scene), ctx_exact.upload(scene)
+    if mode == "sh_propagation":
+        var = np.random.default_rng(3).uniform(0.01, 0.2, size=(scene.num_particles, 3, 9)).astype(np.float32)
+        ds.set_coeff_variances(var, 2)
+        de.set_coeff_variances(var, 2)
+    f = api.construct_field(ctx_exact, de, c["train"], VmfParams(1.0), 2, RC)
+    fc = api.upload_field(ctx, ds, f.download())
+    cams = c["candidates"][:6]
+    r0 = ctx.counters()
+    a = api.select_nbv(ctx, ds, fc, cams, RC, uc)
+    b = api.select_nbv(ctx_exact, de, f, cams, RC, uc)
+    assert np.array_equal(a.scores, b.scores) and a.best_index == b.best_index
+    assert ctx.counters() == r0  # no fp32 pixel redone, no candidate re-scored
+    assert ctx.precision == "certified"
 
 
 def test_certified_argmax_near_ties_around_zero(ctx, ctx_exact):
