@@ -695,14 +695,14 @@ __device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Re
   const double ala = ex_alpha(ea, ex_negq(ea, cxp, cyp), amax);
   const double alb = ex_alpha(eb, ex_negq(eb, cxp, cyp), amax);
   const bool ra = ca && !P.rgb_done;
-#if GAVIS_PRED_TRACKS
+#if GAVIS_PRED_TRACKS >= 1
   if (ra) ex_rgb<LC, EXTRA>(P, ala, ea.depth, cola.x, cola.y, cola.z);
 #else
   ex_rgb<LC, EXTRA>(P, ra ? ala : 0.0, ea.depth, cola.x, cola.y, cola.z);
 #endif
   const bool rd = P.rgb_done || (ra && P.T < cutoff);
   const bool rb = cb && !rd;
-#if GAVIS_PRED_TRACKS
+#if GAVIS_PRED_TRACKS >= 1
   if (rb) ex_rgb<LC, EXTRA>(P, alb, eb.depth, colb.x, colb.y, colb.z);
 #else
   ex_rgb<LC, EXTRA>(P, rb ? alb : 0.0, eb.depth, colb.x, colb.y, colb.z);
@@ -712,7 +712,7 @@ __device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Re
   if (ENT) {
     const double xa = ex_astar<LO>(ua, ala, amax), xb = ex_astar<LO>(ub, alb, amax);
     const bool ea_on = ca && !P.ent_done;
-#if GAVIS_PRED_TRACKS
+#if GAVIS_PRED_TRACKS == 1
     double sa = 0.0;
     if (ea_on) sa = ex_ent<LC, EXTRA>(P, xa, ua, ea.depth);
 #else
@@ -720,7 +720,7 @@ __device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Re
 #endif
     const bool ed = P.ent_done || (ea_on && P.Te < cutoff);
     const bool eb_on = cb && !ed;
-#if GAVIS_PRED_TRACKS
+#if GAVIS_PRED_TRACKS == 1
     double sb = 0.0;
     if (eb_on) sb = ex_ent<LC, EXTRA>(P, xb, ub, eb.depth);
 #else
