@@ -1,7 +1,9 @@
-// kernels_ua_fast.cu -- certified fp32 UA blend (K7f), its fp64 redo (K7r) and
-// the image score (K8).
+// kernels_ua_fast.cu -- the UA blends on 16x16 tiles with the tensor-core colour:
+// the default fp64 blend (K7, ua_blend_exact_mma_kernel, and its opt-in TMA-ring
+// form), the certified fp32 blend (K7f), its fp64 redo (K7r), and the image score
+// (K8).
 //
-// K7f computes the same two tracks as the exact fp64 kernel (kernels_ua.cu;
+// K7f computes the same two tracks as the exact fp64 kernels (ua_common.cuh;
 // rasterize raster.hpp:191-229 and render_entropy_core uncertainty.hpp:177-236)
 // in fp32, except for the quadratic form q, which stays fp64 (a thin splat's
 // conic is ill-conditioned: q cancels in fp32). exp and ln run on the SFU
