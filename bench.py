@@ -15,19 +15,23 @@ arithmetic, common.hpp:14-18); the certified fp32 path (fp32 blend, fp64 redo
 of every pixel whose stop decision fp32 cannot certify, fp64 argmax) is
 measured in the same run as `certified_value` / `certified_e2e`.
 
-Every run checks itself against the CPU oracle on the headline config: the
-oracle's scores of the cpu_baseline sample (rendered with the GPU's field),
-the argmax over that sample, both tracks' per-pixel contributor counts of one
-view, and a two-view field (`parity_gate`), for both device precisions.
+Every run checks itself on the headline config (`parity_gate`), for both device
+precisions: the scores and argmax of the cpu_baseline sample (rendered with the
+GPU's field) against the reference's own code (oracle/_ref; the C restatement
+when it is not built), both tracks' per-pixel contributor counts and images of
+one view and a two-view field against the C restatement.
 
 `--gpus N` without a torchrun environment re-launches itself as N ranks through
 torch.distributed.run (one process per GPU, NCCL); it fails loudly when fewer
 than N devices are visible.
 
---impl reference times the CPU oracle (the reference's algorithm restated in C;
-the reference itself does not build here) on the host cores, rank 0 only: the
-field is built by the oracle from the same 150 training views, and each step
-scores the first candidates of the GPU arm's list.
+--impl reference times the reference's own CPU code (its unmodified headers
+compiled against the Eigen-subset shim, oracle/_ref; the C restatement
+oracle/gavis_oracle.c when that is not built) on all host cores, rank 0 only:
+the field is built by it from the same 150 training views, and each step scores
+the first candidates of the GPU arm's list (select_nbv + the RGB rasterize).
+The line also carries `vf_roofline` (K6a) and, in `roofline.with_records`, the
+per-view record floor beside the SURVEY's algorithmic bytes.
 """
 from __future__ import annotations
 
