@@ -144,30 +144,33 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
 // v >= 1e-4 for every contributing pixel), two 32-bit integer warp reductions
 // (REDUX) add the 26-bit halves, and the 4 warps' integer totals add exactly
 // at the end of the batch -- deterministic in any order, and 6 instructions
-// where the fixed-order fp64 shuffle tree took 15 (GAVIS_VF_FIXED=0 keeps it):
-// K6a 9.42 -> 9.25 ms per 30 views, VF build 56.5 -> 55.6 ms (150 views).
+// where the fixed-order fp64 shuffle tree took 15: K6a 9.42 -> 9.25 ms per 30
+// views, VF build 56.5 -> 55.6 ms (150 views). The fixed point's absolute
+// resolution is relative to T >= cutoff, so it serves cutoffs >= 1e-8 (relative
+// error <= 5e-8 per fold, far inside north_star's 1e-5); smaller cutoffs -- and
+// GAVIS_VF_FIXED=0 -- take the fp64 shuffle tree (FIXED = false).
 #ifndef GAVIS_VF_FIXED
 #define GAVIS_VF_FIXED 1
 #endif
+constexpr double kVfFixedMinCutoff = 1e-8;
 // register budget: the compiler's own choice (54 with the fixed-point sums);
 // capping it (48 / 40) or raising it (62 / 72) measured 2-7 % slower
 #ifndef GAVIS_VF_MIN_BLOCKS
 #define GAVIS_VF_MIN_BLOCKS 0
 #endif
 #if GAVIS_VF_MIN_BLOCKS > 0
+template <bool FIXED>
 __global__ void __launch_bounds__(128, GAVIS_VF_MIN_BLOCKS) vf_blend_tile2_kernel(VfBlendArgs a) {
 #else
+template <bool FIXED>
 __global__ void __launch_bounds__(128) vf_blend_tile2_kernel(VfBlendArgs a) {
 #endif
   constexpr int W = 4;
   __shared__ GeoRec s_geo[kBatch];
   __shared__ int4 s_rect[kBatch];
   __shared__ uint32_t s_pair[kBatch];
-#if GAVIS_VF_FIXED
-  __shared__ unsigned long long s_sum[W][kBatch];  // fixed point, 2^-50
-#else
-  __shared__ double s_sum[W][kBatch];
-#endif
+  // FIXED: fixed point at 2^-50 (bits of the partials); else fp64
+  __shared__ unsigned long long s_sum[W][kBatch];
   __shared__ int32_t s_cnt[W][kBatch];
   load_math_tables();
 
@@ -237,33 +240,28 @@ __global__ void __launch_bounds__(128) vf_blend_tile2_kernel(VfBlendArgs a) {
             T1 = fma(-al, T1, T1);
             d1 = T1 < cutoff;
           }
-#if GAVIS_VF_FIXED
-          const double y = 4.0 + contrib;  // exponent fixed: low 51 mantissa bits = contrib * 2^50
-          const uint32_t ylo = (uint32_t)__double2loint(y), yhi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
-          const uint32_t qlo = __reduce_add_sync(0xffffffffu, ylo & 0x3FFFFFFu);  // < 32 * 2^26
-          const uint32_t qhi = __reduce_add_sync(0xffffffffu, (yhi << 6) | (ylo >> 26));  // < 32 * 2^25
-          if (lane == 0) {
-            s_sum[warp][j] = ((unsigned long long)qhi << 26) + qlo;
-            s_cnt[warp][j] = __popc(m0) + __popc(m1);
-          }
-#else
+          if (FIXED) {
+            const double y = 4.0 + contrib;  // exponent fixed: low 51 mantissa bits = contrib * 2^50
+            const uint32_t ylo = (uint32_t)__double2loint(y), yhi = (uint32_t)__double2hiint(y) & 0xFFFFFu;
+            const uint32_t qlo = __reduce_add_sync(0xffffffffu, ylo & 0x3FFFFFFu);  // < 32 * 2^26
+            const uint32_t qhi = __reduce_add_sync(0xffffffffu, (yhi << 6) | (ylo >> 26));  // < 32 * 2^25
+            if (lane == 0) s_sum[warp][j] = ((unsigned long long)qhi << 26) + qlo;
+          } else {
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
-          if (lane == 0) {
-            s_sum[warp][j] = contrib;
-            s_cnt[warp][j] = __popc(m0) + __popc(m1);
+            for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
+            if (lane == 0) s_sum[warp][j] = (unsigned long long)__double_as_longlong(contrib);
           }
-#endif
+          if (lane == 0) s_cnt[warp][j] = __popc(m0) + __popc(m1);
         }
       }
     }
     __syncthreads();
     for (int j = tid; j < n; j += 128) {
-#if GAVIS_VF_FIXED
-      const double sum = (double)(s_sum[0][j] + s_sum[1][j] + s_sum[2][j] + s_sum[3][j]) * 0x1p-50;
-#else
-      const double sum = ((s_sum[0][j] + s_sum[1][j]) + s_sum[2][j]) + s_sum[3][j];
-#endif
+      const double sum =
+          FIXED ? (double)(s_sum[0][j] + s_sum[1][j] + s_sum[2][j] + s_sum[3][j]) * 0x1p-50
+                : ((__longlong_as_double((long long)s_sum[0][j]) + __longlong_as_double((long long)s_sum[1][j])) +
+                   __longlong_as_double((long long)s_sum[2][j])) +
+                      __longlong_as_double((long long)s_sum[3][j]);
       const int32_t cnt = s_cnt[0][j] + s_cnt[1][j] + s_cnt[2][j] + s_cnt[3][j];
       if (cnt > 0) {
         const uint32_t p = s_pair[j];
@@ -377,10 +375,13 @@ void launch_density_update(double* unseen, const double* vis, int V, int64_t N, 
 void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s) {
   if (a.total_tiles == 0) return;
   static const bool generic = getenv("GAVIS_VF_GENERIC") != nullptr;
-  if (a.tile_size == 16 && !generic)
-    vf_blend_tile2_kernel<<<(unsigned)a.total_tiles, 128, 0, s>>>(a);
-  else
+  if (a.tile_size != 16 || generic) {
     vf_blend_kernel<<<(unsigned)a.total_tiles, kThreads, 0, s>>>(a);
+  } else if (GAVIS_VF_FIXED && a.cutoff >= kVfFixedMinCutoff) {
+    vf_blend_tile2_kernel<true><<<(unsigned)a.total_tiles, 128, 0, s>>>(a);
+  } else {
+    vf_blend_tile2_kernel<false><<<(unsigned)a.total_tiles, 128, 0, s>>>(a);
+  }
 }
 
 void launch_vf_finalize(const VfFinalizeArgs& a, int64_t N, cudaStream_t s) {

@@ -166,6 +166,29 @@ def test_single_view_visibility_parity(ctx, tile):
         assert np.max(np.abs(v - ov)) <= 1e-12
 
 
+@pytest.mark.parametrize("cutoff", [1e-4, 1e-7, 1e-10])
+def test_vf_sums_across_cutoffs(ctx, cutoff):
+    """K6a sums each entry's transmittances in exact 2^-50 fixed point for cutoffs
+    >= 1e-8 and with the fp64 shuffle tree below (kernels_vf.cu): both agree with
+    the oracle, relative to the smallest contributing T, and the field built with
+    them stays within north_star's 1e-5 per row (asserted at 1e-7: a row whose
+    every contribution sits just above a 1e-7 cutoff carries the fixed point's
+    2^-51 per fold at ~4e-9 of its size)."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    osc = O.OracleScene(scene)
+    rc = RasterConfig(transmittance_cutoff=cutoff)
+    for cam in c["train"][:2]:
+        v, touch, cc = api.single_view_visibility(ctx, scene, cam, rc, with_counts=True)
+        ov, otouch, occ = O.single_view_visibility(osc, cam, rc, with_counts=True)
+        assert np.array_equal(touch, otouch) and np.array_equal(cc, occ)
+        seen = ov > 0
+        assert np.all(np.abs(v - ov)[seen] <= 1e-9 * ov[seen] + 1e-15)
+    g = api.construct_field(ctx, scene, c["train"][:4], VmfParams(1.0), 2, rc).download()
+    og = O.construct_field(osc, c["train"][:4], 1.0, 2, rc, threads=8)
+    assert gamma_rel_err(g.gamma, og) <= 1e-7
+
+
 def test_construct_field_config1(ctx):
     c = synth.config1(0)
     scene = c["scene"]
