@@ -45,16 +45,10 @@ def with_degree(s: Scene, d: int) -> Scene:
                  s.is_virtual, d, s.bounds_min, s.bounds_max)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", type=int, default=200)
-    ap.add_argument("--seconds", type=float, default=600.0)
-    ap.add_argument("--seed", type=int, default=11)
-    args = ap.parse_args()
-    if not R.available():
-        print(json.dumps({"ok": False, "skipped": "oracle/_ref not built"}))
-        return
-    rng = np.random.default_rng(args.seed)
+def campaign(cases: int, seconds: float, seed: int, max_particles: int = 60_000) -> dict:
+    """Run up to `cases` random cases (or until `seconds` elapse); returns the stats
+    dict with its `ok` verdict (tests/test_ref_campaign.py runs a short one)."""
+    rng = np.random.default_rng(seed)
     ctx = api.Context(0)
     t0 = time.time()
     st = dict(cases=0, candidates=0, pixels=0, count_mismatch_pixels=0, argmax_mismatch_exact=0,
@@ -63,10 +57,10 @@ def main():
               tile_sizes=[], color_degrees=[], field_degrees=[], hook_cases=0, bounded_candidates=0,
               bound_violations=0, max_error_over_bound=0.0, worst_certified_case=None,
               count_mismatch_pixels_certified=0, max_rgb_abs_certified=0.0, max_entropy_abs_certified=0.0)
-    for case in range(args.cases):
-        if time.time() - t0 > args.seconds:
+    for case in range(cases):
+        if time.time() - t0 > seconds:
             break
-        n = int(rng.choice([5_000, 20_000, 60_000]))
+        n = min(max_particles, int(rng.choice([5_000, 20_000, 60_000])))
         cd = int(rng.integers(0, 4))
         scene = with_degree(scene_for(rng, n), cd)
         w, h = int(rng.integers(48, 300)), int(rng.integers(48, 300))
@@ -168,8 +162,21 @@ def main():
                 st["max_score_rel_exact"] <= 1e-6 and st["bound_violations"] == 0 and
                 st["count_mismatch_pixels_certified"] == 0 and st["max_rgb_abs_certified"] <= 1e-4 and
                 st["max_entropy_abs_certified"] <= 1e-4)
-    st["command"] = " ".join(["python"] + sys.argv)
     ctx.close()
+    return st
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=200)
+    ap.add_argument("--seconds", type=float, default=600.0)
+    ap.add_argument("--seed", type=int, default=11)
+    args = ap.parse_args()
+    if not R.available():
+        print(json.dumps({"ok": False, "skipped": "oracle/_ref not built"}))
+        return
+    st = campaign(args.cases, args.seconds, args.seed)
+    st["command"] = " ".join(["python"] + sys.argv)
     print(json.dumps(st))
 
 
