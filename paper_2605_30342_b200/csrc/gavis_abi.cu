@@ -379,6 +379,7 @@ gavis_status gavis_density_control(gavis_ctx* c, const gavis_scene* scene, const
     for (int64_t k = 0; k < n_virtual; ++k) all[k] = k;
     gavis_scene* probe = alloc_scene(c, n_real + n_virtual, scene->dev.color_degree);
     probe->max_opacity = scene->max_opacity;
+    probe->opacity_nonneg = scene->opacity_nonneg;
     std::vector<double> unseen((size_t)std::max<int64_t>(1, n_virtual), 1.0);
     try {
       copy_particles(c, probe, 0, scene, n_real);
@@ -409,6 +410,7 @@ gavis_status gavis_density_control(gavis_ctx* c, const gavis_scene* scene, const
     }
     gavis_scene* o = alloc_scene(c, n_real + (int64_t)keep.size(), scene->dev.color_degree);
     o->max_opacity = scene->max_opacity;
+    o->opacity_nonneg = scene->opacity_nonneg;
     try {
       copy_particles(c, o, 0, scene, n_real);
       upload_probes(c, o, n_real, p, keep);
@@ -439,7 +441,10 @@ gavis_status gavis_scene_upload(gavis_ctx* c, const gavis_scene_desc* d, gavis_s
     std::lock_guard<std::recursive_mutex> lk(c->mu);
     c->use();
     gavis_scene* s = alloc_scene(c, N, d->color_degree);
-    for (int64_t i = 0; i < N; ++i) s->max_opacity = std::max(s->max_opacity, d->opacities[i]);
+    for (int64_t i = 0; i < N; ++i) {
+      s->max_opacity = std::max(s->max_opacity, d->opacities[i]);
+      if (!(d->opacities[i] >= 0.f)) s->opacity_nonneg = false;  // negative or NaN
+    }
     const int nb = s->dev.nb;
     const int nbp = nb + (nb & 1);
     const int cstride = s->dev.cstride;

@@ -388,6 +388,7 @@ struct gavis_scene {
   float* var = nullptr;  // coefficient variances for the sh_propagation provider
   int var_degree = -1;
   float max_opacity = 1.f;  // enters the certified blend's error bound (q <= 2 ln(o / alpha))
+  bool opacity_nonneg = true;  // every opacity >= 0: T stays in [0, 1] (the VF fixed-point sums)
 };
 
 struct gavis_field {

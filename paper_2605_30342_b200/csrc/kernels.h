@@ -123,6 +123,7 @@ struct VfBlendArgs {
   double* pair_sum = nullptr;          // [K] sum of T (original pair order)
   int32_t* pair_cnt = nullptr;         // [K]
   int32_t* contrib = nullptr;          // [V*W*H] or null
+  bool fixed_sums = false;             // T in [0, 1] guaranteed (opacities >= 0): fixed-point sums allowed
 };
 
 struct VfFinalizeArgs {

@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(kThreads) vf_blend_kernel(VfBlendArgs a) {
 // where the fixed-order fp64 shuffle tree took 15: K6a 9.42 -> 9.25 ms per 30
 // views, VF build 56.5 -> 55.6 ms (150 views). The fixed point's absolute
 // resolution is relative to T >= cutoff, so it serves cutoffs >= 1e-8 (relative
-// error <= 5e-8 per fold, far inside north_star's 1e-5); smaller cutoffs -- and
-// GAVIS_VF_FIXED=0 -- take the fp64 shuffle tree (FIXED = false).
+// error <= 5e-8 per fold, far inside north_star's 1e-5), and its range needs
+// T <= 1 (opacities >= 0, checked at scene upload); smaller cutoffs, scenes with
+// negative or NaN opacities -- and GAVIS_VF_FIXED=0 -- take the fp64 shuffle
+// tree (FIXED = false).
 #ifndef GAVIS_VF_FIXED
 #define GAVIS_VF_FIXED 1
 #endif
@@ -377,7 +379,7 @@ void launch_vf_blend(const VfBlendArgs& a, cudaStream_t s) {
   static const bool generic = getenv("GAVIS_VF_GENERIC") != nullptr;
   if (a.tile_size != 16 || generic) {
     vf_blend_kernel<<<(unsigned)a.total_tiles, kThreads, 0, s>>>(a);
-  } else if (GAVIS_VF_FIXED && a.cutoff >= kVfFixedMinCutoff) {
+  } else if (GAVIS_VF_FIXED && a.fixed_sums && a.cutoff >= kVfFixedMinCutoff) {
     vf_blend_tile2_kernel<true><<<(unsigned)a.total_tiles, 128, 0, s>>>(a);
   } else {
     vf_blend_tile2_kernel<false><<<(unsigned)a.total_tiles, 128, 0, s>>>(a);

@@ -62,6 +62,7 @@ void vf_views(gavis_ctx* c, const gavis_scene* s, gavis_field* f, const gavis_ca
     va.tile_size = rc->tile_size;
     va.cutoff = rc->transmittance_cutoff;
     va.amax = rc->alpha_clamp_max;
+    va.fixed_sums = s->opacity_nonneg;
     va.geo = b.geo;
     va.ranges = b.ranges;
     va.vals = b.vals;

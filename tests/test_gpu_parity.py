@@ -189,6 +189,24 @@ def test_vf_sums_across_cutoffs(ctx, cutoff):
     assert gamma_rel_err(g.gamma, og) <= 1e-7
 
 
+def test_vf_negative_opacities_match_oracle(ctx):
+    """Opacities the reference does not exclude (negative): alpha < 0 lets T
+    exceed 1, outside the fixed-point sums' range, so such scenes take the fp64
+    tree (gavis_scene.opacity_nonneg) and still match the oracle."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    rng = np.random.default_rng(5)
+    flip = rng.uniform(size=scene.num_particles) < 0.05
+    scene.opacities[flip] = -0.3 * scene.opacities[flip]
+    osc = O.OracleScene(scene)
+    for cam in c["train"][:2]:
+        v, touch, cc = api.single_view_visibility(ctx, scene, cam, RC, with_counts=True)
+        ov, otouch, occ = O.single_view_visibility(osc, cam, RC, with_counts=True)
+        assert np.array_equal(touch, otouch) and np.array_equal(cc, occ)
+        assert ov.max() > 1.0  # T above 1 somewhere: the case the fixed point cannot hold
+        assert np.all(np.abs(v - ov) <= 1e-12 * np.maximum(1.0, np.abs(ov)))
+
+
 def test_construct_field_config1(ctx):
     c = synth.config1(0)
     scene = c["scene"]
