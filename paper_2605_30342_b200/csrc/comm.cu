@@ -282,7 +282,7 @@ gavis_status gavis_select_nbv_sharded(gavis_comm* cm, const gavis_scene* s, cons
     if (any_bounds) c->score_bounds = bd;
     else c->score_bounds.clear();
     // certified mode: contenders re-scored in fp64 by their owners, summed over ranks
-    std::vector<int> cont = certified_contenders(c, rc, sc);
+    std::vector<int> cont = certified_contenders(c, s, rc, sc);
     if (cont.size() >= 2) {
       std::vector<double> exact((size_t)n_cams, 0.0);
       std::vector<int> own;

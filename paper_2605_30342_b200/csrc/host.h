@@ -502,7 +502,7 @@ struct ScoringPrecision {
   ScoringPrecision& operator=(const ScoringPrecision&) = delete;
 };
 
-std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* rc,
+std::vector<int> certified_contenders(gavis_ctx* c, const gavis_scene* s, const gavis_raster_config* rc,
                                       const std::vector<double>& sc);
 // select_nbv argmax over certified scores, contenders re-scored exactly (ua_host.cu).
 int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f,

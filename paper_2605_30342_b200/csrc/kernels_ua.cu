@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) ua_blend_kernel(UaBlendArgs a) {
           float c0, c1, c2;
           sh_color<LC>(reinterpret_cast<const float2*>(s_col + j * CS), P.bp, c0, c1, c2);
           if (EXTRA) ++P.n_rgb;
-          ex_rgb<LC, EXTRA>(P, al, e.depth, c0, c1, c2);
+          ex_rgb<LC, EXTRA, LO>(P, al, e.depth, c0, c1, c2);
           if (P.T < cutoff) P.rgb_done = true;
         }
         if (ENT && !P.ent_done) {
@@ -171,10 +171,10 @@ __global__ void __launch_bounds__(256, RGB ? 3 : 4) ua_blend_ilp_kernel(UaBlendA
           sh_color<LC>(reinterpret_cast<const float2*>(s_col + ja * CS), P.bp, a0, a1, a2);
           sh_color<LC>(reinterpret_cast<const float2*>(s_col + jb * CS), P.bp, b0, b1, b2);
           const bool ra = ca && !P.rgb_done;
-          ex_rgb<LC, EXTRA>(P, ra ? ala : 0.0, ea.depth, a0, a1, a2);
+          ex_rgb<LC, EXTRA, LO>(P, ra ? ala : 0.0, ea.depth, a0, a1, a2);
           const bool rd = P.rgb_done || (ra && P.T < cutoff);
           const bool rb = cb && !rd;
-          ex_rgb<LC, EXTRA>(P, rb ? alb : 0.0, eb.depth, b0, b1, b2);
+          ex_rgb<LC, EXTRA, LO>(P, rb ? alb : 0.0, eb.depth, b0, b1, b2);
           if (EXTRA) P.n_rgb += (int)ra + (int)rb;
           P.rgb_done = rd || (rb && P.T < cutoff);
         }
@@ -239,14 +239,18 @@ void launch_one(const UaBlendArgs& a, cudaStream_t s) {
 
 template <int LC, bool EXTRA>
 void launch_lc_x(const UaBlendArgs& a, cudaStream_t s) {
-  // the lower alpha* clamp only for caller-given visibilities outside [0, 1]
+  // LO (the lower alpha* clamp, the RGB w > 0 guard) only for caller-given
+  // visibilities outside [0, 1] or negative opacities (vis_outside_unit)
   if (a.do_rgb && a.do_ent) {
     if (a.vis_outside_unit)
       launch_one<LC, true, true, EXTRA, true>(a, s);
     else
       launch_one<LC, true, true, EXTRA, false>(a, s);
   } else if (a.do_rgb) {
-    launch_one<LC, true, false, EXTRA, false>(a, s);
+    if (a.vis_outside_unit)
+      launch_one<LC, true, false, EXTRA, true>(a, s);
+    else
+      launch_one<LC, true, false, EXTRA, false>(a, s);
   } else if (a.do_ent) {
     if (a.vis_outside_unit)
       launch_one<LC, false, true, EXTRA, true>(a, s);

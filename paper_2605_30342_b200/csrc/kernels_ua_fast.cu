@@ -698,16 +698,16 @@ __device__ __forceinline__ void exact_pair(Pixel<LC>& P, const Rec& ea, const Re
   const double alb = ex_alpha(eb, ex_negq(eb, cxp, cyp), amax);
   const bool ra = ca && !P.rgb_done;
 #if GAVIS_PRED_TRACKS >= 1
-  if (ra) ex_rgb<LC, EXTRA>(P, ala, ea.depth, cola.x, cola.y, cola.z);
+  if (ra) ex_rgb<LC, EXTRA, LO>(P, ala, ea.depth, cola.x, cola.y, cola.z);
 #else
-  ex_rgb<LC, EXTRA>(P, ra ? ala : 0.0, ea.depth, cola.x, cola.y, cola.z);
+  ex_rgb<LC, EXTRA, LO>(P, ra ? ala : 0.0, ea.depth, cola.x, cola.y, cola.z);
 #endif
   const bool rd = P.rgb_done || (ra && P.T < cutoff);
   const bool rb = cb && !rd;
 #if GAVIS_PRED_TRACKS >= 1
-  if (rb) ex_rgb<LC, EXTRA>(P, alb, eb.depth, colb.x, colb.y, colb.z);
+  if (rb) ex_rgb<LC, EXTRA, LO>(P, alb, eb.depth, colb.x, colb.y, colb.z);
 #else
-  ex_rgb<LC, EXTRA>(P, rb ? alb : 0.0, eb.depth, colb.x, colb.y, colb.z);
+  ex_rgb<LC, EXTRA, LO>(P, rb ? alb : 0.0, eb.depth, colb.x, colb.y, colb.z);
 #endif
   if (EXTRA) P.n_rgb += (int)ra + (int)rb;
   P.rgb_done = rd || (rb && P.T < cutoff);
@@ -1249,6 +1249,8 @@ void launch_exact_mma_lc(const UaBlendArgs& a, cudaStream_t s) {
       launch_exact_mma<LC, true, EXTRA, true>(a, s);
     else
       launch_exact_mma<LC, true, EXTRA, false>(a, s);
+  } else if (a.vis_outside_unit) {  // negative opacities: the RGB w > 0 guard
+    launch_exact_mma<LC, false, EXTRA, true>(a, s);
   } else {
     launch_exact_mma<LC, false, EXTRA, false>(a, s);
   }

@@ -138,12 +138,15 @@ __device__ __forceinline__ double ex_astar(const ExUa& u, double al, double amax
   return x > amax ? amax : x;
 }
 
-// RGB track (raster.hpp:209-221): w = alpha T, rgb += w c, T <- T (1 - alpha).
-// alpha = 0 (masked entry) leaves every accumulator bit-identical.
-template <int LC, bool EXTRA>
+// RGB track (raster.hpp:209-221): w = alpha T, rgb += w c if w > 0, T <- T (1 - alpha).
+// alpha = 0 (masked entry) leaves every accumulator bit-identical. LO (inputs with
+// negative opacities, where alpha < 0): the reference's `if (w > 0)` guard --
+// for alpha >= 0 a w of 0 adds +0, so the guard is only needed there.
+template <int LC, bool EXTRA, bool LO = false>
 __device__ __forceinline__ void ex_rgb(Pixel<LC>& P, double al, double depth, float c0, float c1,
                                        float c2) {
-  const double w = al * P.T;
+  double w = al * P.T;
+  if (LO) w = w > 0.0 ? w : 0.0;
   P.rgb0 = fma(w, (double)c0, P.rgb0);
   P.rgb1 = fma(w, (double)c1, P.rgb1);
   P.rgb2 = fma(w, (double)c2, P.rgb2);

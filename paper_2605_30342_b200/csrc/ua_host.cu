@@ -64,8 +64,14 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
         vis_outside_unit = !(vis_host[i] >= 0.0 && vis_host[i] <= 1.0);
     }
   }
+  // negative (or NaN) opacities make alpha, hence A alpha + B, negative: the exact
+  // kernels then need the lower alpha* clamp (LO), as for visibilities outside
+  // [0, 1]; the certified blend assumes neither happens (its bounds and its
+  // clamp-free alpha* rely on alpha, v in [0, 1]) and is not used for such inputs
+  const bool outside = vis_outside_unit || !s->opacity_nonneg;
+  vis_outside_unit = outside;
   const int bv = batch_views(c, N, n);
-  const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED &&
+  const bool fast = c->precision == GAVIS_PRECISION_CERTIFIED && !outside &&
                     ua_fast_supported(rc->tile_size, rc->alpha_clamp_max);
   unsigned long long* redo_total = nullptr;
   if (fast) {
@@ -271,10 +277,12 @@ void ua_render(gavis_ctx* c, const gavis_scene* s, const gavis_field* f, const d
 constexpr double kCertScoreRel = 1e-3;
 constexpr double kCertScoreAbs = 1e-9;  // absolute floor: scores near 0 keep a window
 
-std::vector<int> certified_contenders(gavis_ctx* c, const gavis_raster_config* rc,
+std::vector<int> certified_contenders(gavis_ctx* c, const gavis_scene* s, const gavis_raster_config* rc,
                                       const std::vector<double>& sc) {
   std::vector<int> cont;
-  if (sc.empty() || c->precision != GAVIS_PRECISION_CERTIFIED ||
+  // the same decision as ua_render's `fast` for a field render (identical on every
+  // rank: the sharded select's re-scoring is collective)
+  if (sc.empty() || c->precision != GAVIS_PRECISION_CERTIFIED || !s->opacity_nonneg ||
       !ua_fast_supported(rc->tile_size, rc->alpha_clamp_max))
     return cont;
   int b = 0;
@@ -301,7 +309,7 @@ int certified_first_max(gavis_ctx* c, const gavis_scene* s, const gavis_field* f
       if (sc[i] > sc[b]) b = i;
     return b;
   };
-  const std::vector<int> cont = certified_contenders(c, rc, sc);
+  const std::vector<int> cont = certified_contenders(c, s, rc, sc);
   if (cont.size() < 2) return first_max();
   std::vector<gavis_camera> cc;
   for (int i : cont) cc.push_back(cams[i]);

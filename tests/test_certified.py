@@ -524,3 +524,46 @@ def test_select_keeps_score_bounds(ctx):
     api.select_nbv(ctx, c["scene"], f, cams, RC, UC)
     b = ctx.last_score_bounds()
     assert b.shape == (len(cams),) and np.all(b > 0)
+
+
+@pytest.mark.parametrize("case", ["negative_opacity", "visibility_outside_unit"])
+def test_inputs_outside_the_bounds_assumptions(ctx, ctx_exact, case):
+    """Inputs the reference does not exclude but the certified blend's bounds assume
+    away -- negative opacities (alpha < 0) and caller-given visibilities outside
+    [0, 1] (A alpha + B < 0) -- run the fp64 kernels with the lower alpha* clamp in
+    both precisions (ua_render), and match the oracle: contributor counts
+    bit-exact, images within 1e-9, scores and argmax equal."""
+    c = synth.config1(0)
+    scene = c["scene"]
+    rng = np.random.default_rng(9)
+    vis = rng.uniform(0.0, 1.0, scene.num_particles)
+    if case == "negative_opacity":
+        flip = rng.uniform(size=scene.num_particles) < 0.05
+        scene.opacities[flip] = -0.3 * scene.opacities[flip]
+    else:
+        out = rng.uniform(size=scene.num_particles) < 0.1
+        vis[out] = rng.choice([-0.4, 1.6], int(out.sum()))
+    osc = O.OracleScene(scene)
+    cam = c["candidates"][0]
+    H, w0, _, cc = O.render_entropy_core(osc, cam, RC, UC, vis, contrib=True)
+    rgb, _, T, rc_cc = O.rasterize(osc, cam, RC, contrib=True)
+    for cx in (ctx, ctx_exact):
+        r0 = cx.counters()
+        r = api.render(cx, scene, None, [cam], RC, UC, rgb=True, entropy=True, invisible_mass=True,
+                       contributors=True, splat_visibility=vis)
+        assert cx.counters() == r0  # no certified pixel, no re-score: the fp64 kernels ran
+        assert np.array_equal(r["entropy_contributors"], cc) and np.array_equal(r["rgb_contributors"], rc_cc)
+        assert np.max(np.abs(r["entropy"] - H)) <= 1e-9
+        assert np.max(np.abs(r["invisible_mass"] - w0)) <= 1e-9
+        assert np.max(np.abs(r["rgb"] - rgb)) <= 1e-5
+    if case == "negative_opacity":  # select_nbv with a field: fp64 in both precisions
+        de, dc = ctx_exact.upload(scene), ctx.upload(scene)
+        f = api.construct_field(ctx_exact, de, c["train"][:4], VmfParams(1.0), 2, RC)
+        fc = api.upload_field(ctx, dc, f.download())
+        r0 = ctx.counters()
+        a = api.select_nbv(ctx, dc, fc, c["candidates"][:4], RC, UC)
+        assert ctx.counters() == r0
+        b = api.select_nbv(ctx_exact, de, f, c["candidates"][:4], RC, UC)
+        best, sc = O.select_nbv(osc, f.download().gamma, 2, 4, c["candidates"][:4], RC, UC, threads=8)
+        assert a.best_index == b.best_index == best
+        assert np.max(np.abs(b.scores - sc) / np.abs(sc)) <= 1e-9
