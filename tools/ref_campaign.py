@@ -15,7 +15,8 @@ Per case (both chains independent end to end, each with its own field):
     count output).
 Randomised: particle count, colour degree 0-3, resolution (odd sizes), tile size,
 cutoff, alpha clamp, dilation, beta / prior opacity / colour sigma, the
-correlation hook, field degree 0-4, kappa. Writes one JSON line.
+correlation hook, field degree 0-4, kappa, and (10 % of cases) negative
+opacities. Writes one JSON line.
 
     python tools/ref_campaign.py [--cases 200] [--seconds 600] [--seed 11]
 """
@@ -56,13 +57,18 @@ def campaign(cases: int, seconds: float, seed: int, max_particles: int = 60_000)
               max_entropy_abs=0.0, max_w0_abs=0.0, max_score_rel_exact=0.0, max_score_rel_certified=0.0,
               tile_sizes=[], color_degrees=[], field_degrees=[], hook_cases=0, bounded_candidates=0,
               bound_violations=0, max_error_over_bound=0.0, worst_certified_case=None,
-              count_mismatch_pixels_certified=0, max_rgb_abs_certified=0.0, max_entropy_abs_certified=0.0)
+              count_mismatch_pixels_certified=0, max_rgb_abs_certified=0.0, max_entropy_abs_certified=0.0,
+              negative_opacity_cases=0)
     for case in range(cases):
         if time.time() - t0 > seconds:
             break
         n = min(max_particles, int(rng.choice([5_000, 20_000, 60_000])))
         cd = int(rng.integers(0, 4))
         scene = with_degree(scene_for(rng, n), cd)
+        negative = rng.uniform() < 0.1  # opacities the reference does not exclude: alpha < 0
+        if negative:
+            flip = rng.uniform(size=n) < 0.05
+            scene.opacities[flip] = -0.3 * scene.opacities[flip]
         w, h = int(rng.integers(48, 300)), int(rng.integers(48, 300))
         cams = []
         for _ in range(8):
@@ -151,6 +157,7 @@ def campaign(cases: int, seconds: float, seed: int, max_particles: int = 60_000)
         st["candidates"] += len(cands)
         st["pixels"] += len(cands) * P
         st["hook_cases"] += int(hook)
+        st["negative_opacity_cases"] += int(negative)
         for k, x in (("tile_sizes", rc.tile_size), ("color_degrees", cd), ("field_degrees", L)):
             if x not in st[k]:
                 st[k].append(x)
