@@ -118,7 +118,10 @@ gavis_status gavis_ctx_set_pair_budget(gavis_ctx* ctx, int64_t max_pairs_per_bat
  *    with it to ~1e-6 (north_star: 1e-4); select_nbv re-scores in fp64 every
  *    candidate whose score interval (rigorous per-candidate error bounds,
  *    gavis_ctx_last_score_bounds) can reach the best's, so the argmax is the
- *    fp64 one. Used for 16x16 tiles and alpha_clamp_max <= 0.999. */
+ *    fp64 one. Used for 16x16 tiles and alpha_clamp_max <= 0.999, scenes with
+ *    opacities >= 0 and visibilities in [0, 1] (other inputs, and scoring calls
+ *    with the correlation hook or sh_propagation, which have no score bound,
+ *    run the fp64 path). */
 enum { GAVIS_PRECISION_CERTIFIED = 0, GAVIS_PRECISION_EXACT = 1 };
 gavis_status gavis_ctx_set_precision(gavis_ctx* ctx, int32_t precision);
 /* Rigorous per-candidate bounds on |certified score - fp64 score| of the last
