@@ -15,8 +15,9 @@ Per case (both chains independent end to end, each with its own field):
     count output).
 Randomised: particle count, colour degree 0-3, resolution (odd sizes), tile size,
 cutoff, alpha clamp, dilation, beta / prior opacity / colour sigma, the
-correlation hook, field degree 0-4, kappa, and (10 % of cases) negative
-opacities. Writes one JSON line.
+correlation hook, field degree 0-4, kappa, (10 % of cases) negative opacities,
+(20 %) cameras inside the cloud, (20 %) fields of view up to ~150 degrees, and
+the near plane. Writes one JSON line.
 
     python tools/ref_campaign.py [--cases 200] [--seconds 600] [--seed 11]
 """
@@ -58,7 +59,7 @@ def campaign(cases: int, seconds: float, seed: int, max_particles: int = 60_000)
               tile_sizes=[], color_degrees=[], field_degrees=[], hook_cases=0, bounded_candidates=0,
               bound_violations=0, max_error_over_bound=0.0, worst_certified_case=None,
               count_mismatch_pixels_certified=0, max_rgb_abs_certified=0.0, max_entropy_abs_certified=0.0,
-              negative_opacity_cases=0)
+              negative_opacity_cases=0, inside_cloud_cases=0, wide_fov_cases=0)
     for case in range(cases):
         if time.time() - t0 > seconds:
             break
@@ -71,10 +72,16 @@ def campaign(cases: int, seconds: float, seed: int, max_particles: int = 60_000)
             scene.opacities[flip] = -0.3 * scene.opacities[flip]
         w, h = int(rng.integers(48, 300)), int(rng.integers(48, 300))
         cams = []
+        inside = rng.uniform() < 0.2  # cameras inside the cloud: near-plane culls, clamped Jacobians
+        wide = rng.uniform() < 0.2    # wide fields of view (up to ~150 degrees)
         for _ in range(8):
-            eye = (rng.uniform(-0.6, 0.6), rng.uniform(-0.6, 0.6), rng.uniform(-0.8, 0.8))
-            cams.append(make_lookat(eye, (rng.uniform(-0.4, 0.4), rng.uniform(-0.4, 0.4), 3.6), (0, 1, 0),
-                                    w, h, rng.uniform(0.6, 1.6), rng.uniform(0.6, 1.6)))
+            eye = (rng.uniform(-0.6, 0.6), rng.uniform(-0.6, 0.6),
+                   rng.uniform(2.5, 4.5) if inside else rng.uniform(-0.8, 0.8))
+            fmax = 2.6 if wide else 1.6
+            cam = make_lookat(eye, (rng.uniform(-0.4, 0.4), rng.uniform(-0.4, 0.4), eye[2] + 2.0 if inside else 3.6),
+                              (0, 1, 0), w, h, rng.uniform(0.6, fmax), rng.uniform(0.6, fmax))
+            cam.near = float(rng.choice([0.05, 0.05, 0.2, 1.0]))
+            cams.append(cam)
         train, cands = cams[:4], cams[4:]
         rc = RasterConfig(tile_size=int(rng.choice([16, 16, 16, 8, 13, 32])),
                           transmittance_cutoff=float(rng.choice([1e-4, 1e-4, 1e-3, 1e-5])),
@@ -158,6 +165,8 @@ def campaign(cases: int, seconds: float, seed: int, max_particles: int = 60_000)
         st["pixels"] += len(cands) * P
         st["hook_cases"] += int(hook)
         st["negative_opacity_cases"] += int(negative)
+        st["inside_cloud_cases"] += int(inside)
+        st["wide_fov_cases"] += int(wide)
         for k, x in (("tile_sizes", rc.tile_size), ("color_degrees", cd), ("field_degrees", L)):
             if x not in st[k]:
                 st[k].append(x)
