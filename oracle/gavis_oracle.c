@@ -1152,7 +1152,11 @@ int gor_sample_candidates(const double* bmin, const double* bmax, const gor_rect
   while (n < pc->num_candidates) {
     if (attempts++ >= budget) return -2;
     double p[3];
-    for (int i = 0; i < 3; ++i) p[i] = sm64_uniform(&g, bmin[i], bmax[i]);
+    /* planner.hpp:70-72 draws the three coordinates as the arguments of one Vec3
+     * constructor call, whose evaluation order C++ leaves unspecified; GCC (the
+     * reference's Linux build, and oracle/_ref here) evaluates them right to
+     * left: z, then y, then x. */
+    for (int i = 2; i >= 0; --i) p[i] = sm64_uniform(&g, bmin[i], bmax[i]);
     const double yaw = sm64_uniform(&g, 0.0, 2.0 * K_PI);
     const double u1 = sm64_double(&g), u2 = sm64_double(&g), u3 = sm64_double(&g);
     const double qa = sqrt(1.0 - u1), qb = sqrt(u1);

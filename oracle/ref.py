@@ -138,3 +138,74 @@ def select_nbv_rgb_h(rs: RefScene, gamma, degree: int, num_views: int, cams, rc,
                                        C.byref(O.raster_struct(rc)), C.byref(O.unc_struct(uc)), threads,
                                        O._p(scores), C.byref(best)))
     return best.value, scores[: len(cams)]
+
+
+# ---- the planner-side §8f rows: the reference's own sample_candidates,
+# vis_coverage, density_control and run_active_mapping ------------------------
+def _planner(pc):
+    return O.Planner(int(pc.mode), int(pc.num_candidates), float(pc.se2_height), int(pc.steps),
+                     1 if pc.look_inward else 0, int(pc.seed), float(pc.clearance), int(pc.cam_width),
+                     int(pc.cam_height), float(pc.fov_h), float(pc.fov_v), float(pc.cam_near))
+
+
+def sample_candidates(bounds, occ, pc, step_seed: int):
+    """sample_candidates (planner.hpp:56-107); raises ValueError where the reference throws."""
+    bmin = np.ascontiguousarray(bounds[0], np.float64)
+    bmax = np.ascontiguousarray(bounds[1], np.float64)
+    rects, nr = O._rects(occ)
+    out = (O.Camera * max(1, int(pc.num_candidates)))()
+    n = lib().gref_sample_candidates(O._p(bmin), O._p(bmax), rects, nr, C.byref(_planner(pc)),
+                                     C.c_uint64(step_seed), out)
+    if n < 0:
+        raise ValueError(f"sample_candidates failed: {lib().gref_last_error().decode()}")
+    return [O._camera_from(out[i]) for i in range(n)]
+
+
+def vis_coverage(occ, views) -> float:
+    """vis_coverage (planner.hpp:155-184)"""
+    lib().gref_vis_coverage.restype = C.c_double
+    rects, nr = O._rects(occ)
+    return lib().gref_vis_coverage(rects, nr, C.c_double(occ.sample_density), O.cameras_array(views), len(views))
+
+
+def density_control_positions(scene, bounds_min, bounds_max, views, rho=100.0, eta=0.5, eps_v=0.95, seed=0,
+                              rc=None, threads: int = 1) -> np.ndarray:
+    """density_control (vfield.hpp:157-199): positions [m, 3] of the virtual
+    particles the reference appends (in probe order)."""
+    from paper_2605_30342_b200.model import RasterConfig
+    rc = rc or RasterConfig()
+    s = O._scene(scene)
+    bmin = np.ascontiguousarray(bounds_min, np.float64)
+    bmax = np.ascontiguousarray(bounds_max, np.float64)
+    ext = bmax - bmin
+    cap = int(np.floor(rho * (ext[0] * ext[1] * ext[2])))
+    pos = np.zeros(max(1, cap) * 3)
+    lib().gref_density_control.restype = C.c_int64
+    m = lib().gref_density_control(C.byref(s.c), O._p(bmin), O._p(bmax), O.cameras_array(views), len(views),
+                                   C.c_double(rho), C.c_double(eta), C.c_double(eps_v), C.c_uint64(seed),
+                                   C.byref(O.raster_struct(rc)), threads, O._p(pos), C.c_int64(cap))
+    if m < 0:
+        raise RuntimeError(f"reference error: {lib().gref_last_error().decode()}")
+    return pos[: 3 * m].reshape(m, 3)
+
+
+def active_mapping(scene, bounds, occ, init, pc, kappa: float, degree: int, rc, uc, density_enabled: bool,
+                   rho=100.0, eta=0.5, eps_v=0.95, dseed=0, threads: int = 1):
+    """run_active_mapping (planner.hpp:284-316) -> [(chosen index, scores, vis_coverage)] per step."""
+    s = O._scene(scene)
+    bmin = np.ascontiguousarray(bounds[0], np.float64)
+    bmax = np.ascontiguousarray(bounds[1], np.float64)
+    rects, nr = O._rects(occ)
+    steps, nc = int(pc.steps), int(pc.num_candidates)
+    chosen = (C.c_int * max(1, steps))()
+    score = np.zeros(max(1, steps))
+    cov = np.zeros(max(1, steps))
+    alls = np.zeros(max(1, steps * nc))
+    _check(lib().gref_active_mapping(C.byref(s.c), O._p(bmin), O._p(bmax), rects, nr,
+                                     C.c_double(occ.sample_density if occ is not None else 64.0),
+                                     O.cameras_array(init), len(init), C.byref(_planner(pc)), C.c_double(kappa),
+                                     degree, C.byref(O.raster_struct(rc)), C.byref(O.unc_struct(uc)),
+                                     1 if density_enabled else 0, C.c_double(rho), C.c_double(eta),
+                                     C.c_double(eps_v), C.c_uint64(dseed), threads, chosen, O._p(score),
+                                     O._p(cov), O._p(alls)))
+    return [(int(chosen[k]), alls[k * nc:(k + 1) * nc].copy(), float(cov[k])) for k in range(steps)]

@@ -87,6 +87,48 @@ gavis::VisibilityField make_field(const gavis::Scene& sc, const double* gamma, i
   return f;
 }
 
+gavis::OccluderSet make_occluders(const gor_rect* rects, int n, double density) {
+  gavis::OccluderSet occ;
+  occ.sample_density = density;
+  for (int i = 0; i < n; ++i) {
+    gavis::OccluderRect r;
+    r.corner = gavis::Vec3(rects[i].corner[0], rects[i].corner[1], rects[i].corner[2]);
+    r.edge_u = gavis::Vec3(rects[i].edge_u[0], rects[i].edge_u[1], rects[i].edge_u[2]);
+    r.edge_v = gavis::Vec3(rects[i].edge_v[0], rects[i].edge_v[1], rects[i].edge_v[2]);
+    r.opaque = rects[i].opaque != 0;
+    occ.rectangles.push_back(r);
+  }
+  return occ;
+}
+
+gavis::PlannerConfig make_pc(const gor_planner* p) {
+  gavis::PlannerConfig pc;
+  pc.mode = p->mode == 1 ? gavis::PoseMode::kSe2 : gavis::PoseMode::kSe3;
+  pc.num_candidates = p->num_candidates;
+  pc.se2_height = p->se2_height;
+  pc.steps = p->steps;
+  pc.seed = p->seed;
+  pc.look_inward = p->look_inward != 0;
+  pc.clearance = p->clearance;
+  pc.cam_width = p->cam_width;
+  pc.cam_height = p->cam_height;
+  pc.fov_h = p->fov_h;
+  pc.fov_v = p->fov_v;
+  pc.cam_near = p->cam_near;
+  return pc;
+}
+
+void put_cam(const gavis::CameraView& v, gor_camera* c) {
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) c->rotation[r * 3 + k] = v.rotation(r, k);
+  for (int k = 0; k < 3; ++k) c->position[k] = v.position[k];
+  c->width = v.width;
+  c->height = v.height;
+  c->fov_h = v.fov_h;
+  c->fov_v = v.fov_v;
+  c->near_plane = v.near;
+}
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -216,6 +258,95 @@ int gref_select_nbv(const gor_scene* s, const double* gamma, int degree, int num
     const gavis::NbvResult r = gavis::select_nbv(sc, f, cv, make_rc(rc), make_uc(u), threads);
     std::memcpy(scores, r.scores.data(), sizeof(double) * r.scores.size());
     *best = r.best_index;
+  });
+}
+
+// sample_candidates (planner.hpp:56-107) -> count written to out (-1 on error)
+int gref_sample_candidates(const double* bmin, const double* bmax, const gor_rect* rects, int n_rects,
+                           const gor_planner* pc, uint64_t step_seed, gor_camera* out) {
+  int n = -1;
+  const int st = guarded([&] {
+    gavis::Bounds b;
+    b.min = gavis::Vec3(bmin[0], bmin[1], bmin[2]);
+    b.max = gavis::Vec3(bmax[0], bmax[1], bmax[2]);
+    const auto cams = gavis::sample_candidates(b, make_occluders(rects, n_rects, 64.0), make_pc(pc), step_seed);
+    for (size_t i = 0; i < cams.size(); ++i) put_cam(cams[i], &out[i]);
+    n = (int)cams.size();
+  });
+  return st == 0 ? n : -st;
+}
+
+// vis_coverage (planner.hpp:155-184)
+double gref_vis_coverage(const gor_rect* rects, int n_rects, double density, const gor_camera* views,
+                         int n_views) {
+  double cov = -1.0;
+  guarded([&] {
+    gavis::Trajectory t;
+    for (int i = 0; i < n_views; ++i) t.views.push_back(make_cam(&views[i]));
+    cov = gavis::vis_coverage(make_occluders(rects, n_rects, density), t);
+  });
+  return cov;
+}
+
+// density_control (vfield.hpp:157-199) -> the appended virtual particles'
+// positions [m*3] (capacity cap), returns m (< 0 on error)
+int64_t gref_density_control(const gor_scene* s, const double* bmin, const double* bmax,
+                             const gor_camera* views, int n_views, double rho, double eta, double eps_v,
+                             uint64_t seed, const gor_raster* rc, int threads, double* kept_pos, int64_t cap) {
+  int64_t m = -1;
+  const int st = guarded([&] {
+    gavis::Scene sc = make_scene(s);
+    sc.bounds.min = gavis::Vec3(bmin[0], bmin[1], bmin[2]);
+    sc.bounds.max = gavis::Vec3(bmax[0], bmax[1], bmax[2]);
+    gavis::Trajectory t;
+    for (int i = 0; i < n_views; ++i) t.views.push_back(make_cam(&views[i]));
+    gavis::DensityControlConfig cfg;
+    cfg.rho = rho;
+    cfg.eta = eta;
+    cfg.eps_v = eps_v;
+    cfg.seed = seed;
+    const gavis::Scene out = gavis::density_control(sc, t, cfg, make_rc(rc), threads);
+    m = (int64_t)(out.particles.size() - sc.particles.size());
+    if (m > cap) throw gavis::InvariantError("density_control: kept_pos capacity too small");
+    for (int64_t k = 0; k < m; ++k)
+      for (int d = 0; d < 3; ++d) kept_pos[3 * k + d] = out.particles[sc.particles.size() + (size_t)k].position[d];
+  });
+  return st == 0 ? m : -st;
+}
+
+// run_active_mapping (planner.hpp:284-316) -> per step: chosen index, its score,
+// vis_coverage, and all candidate scores [steps * num_candidates]
+int gref_active_mapping(const gor_scene* s, const double* bmin, const double* bmax, const gor_rect* rects,
+                        int n_rects, double density, const gor_camera* init, int n_init, const gor_planner* pc,
+                        double kappa, int degree, const gor_raster* rc, const gor_unc* u, int density_enabled,
+                        double rho, double eta, double eps_v, uint64_t dseed, int threads, int* chosen,
+                        double* score, double* coverage, double* all_scores) {
+  return guarded([&] {
+    gavis::Scene sc = make_scene(s);
+    sc.bounds.min = gavis::Vec3(bmin[0], bmin[1], bmin[2]);
+    sc.bounds.max = gavis::Vec3(bmax[0], bmax[1], bmax[2]);
+    gavis::Trajectory t;
+    for (int i = 0; i < n_init; ++i) t.views.push_back(make_cam(&init[i]));
+    gavis::MappingContext mc;
+    mc.vmf = gavis::VmfParams(kappa);
+    mc.field_degree = degree;
+    mc.raster = make_rc(rc);
+    mc.uncertainty = make_uc(u);
+    mc.density.rho = rho;
+    mc.density.eta = eta;
+    mc.density.eps_v = eps_v;
+    mc.density.seed = dseed;
+    mc.density_enabled = density_enabled != 0;
+    const gavis::PlannerConfig p = make_pc(pc);
+    const gavis::MappingLog log =
+        gavis::run_active_mapping(sc, make_occluders(rects, n_rects, density), t, p, mc, threads);
+    for (size_t k = 0; k < log.steps.size(); ++k) {
+      chosen[k] = log.steps[k].chosen_index;
+      score[k] = log.steps[k].score;
+      coverage[k] = log.steps[k].vis_coverage;
+      std::memcpy(all_scores + k * (size_t)p.num_candidates, log.steps[k].scores.data(),
+                  sizeof(double) * log.steps[k].scores.size());
+    }
   });
 }
 

@@ -374,7 +374,9 @@ gavis_status gavis_read_splat_ply(const char* path, int64_t capacity, float* pos
         hi[k] = (i == 0 || val[k] > hi[k]) ? val[k] : hi[k];
       }
       opacities[i] = (float)(1.0 / (1.0 + std::exp(-val[3])));
-      const double qn = std::sqrt(val[8] * val[8] + val[9] * val[9] + val[10] * val[10] + val[7] * val[7]);
+      // q.normalized() (io.hpp:616): Eigen stores (x, y, z, w) and sums the squares
+      // of a 4-vector in SSE2 packets of two: (x^2 + z^2) + (y^2 + w^2)
+      const double qn = std::sqrt((val[8] * val[8] + val[10] * val[10]) + (val[9] * val[9] + val[7] * val[7]));
       need(qn > 1e-12, "zero quaternion in PLY vertex " + std::to_string(i));
       for (int k = 0; k < 4; ++k) rotations[4 * i + k] = (float)(val[7 + k] / qn);
       for (int c = 0; c < 3; ++c) {

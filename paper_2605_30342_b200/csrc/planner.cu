@@ -273,9 +273,13 @@ void sample(const double* bmin, const double* bmax, const std::vector<Rect>& rec
   while (n < pc->num_candidates) {
     if (attempts++ >= budget) throw PlanErr("candidate sampling budget exhausted; scene too cluttered");
     V3 p;
-    p.x = g.uniform(lo.x, hi.x);
-    p.y = g.uniform(lo.y, hi.y);
+    // planner.hpp:70-72 draws the coordinates as the arguments of one Vec3
+    // constructor call (evaluation order unspecified by C++); the reference's GCC
+    // build evaluates them right to left -- z, y, x -- and so do we, so the
+    // candidates equal the reference binary's bit for bit (tests/test_planner.py)
     p.z = g.uniform(lo.z, hi.z);
+    p.y = g.uniform(lo.y, hi.y);
+    p.x = g.uniform(lo.x, hi.x);
     const double yaw = g.uniform(0.0, 2.0 * kPi);  // drawn in both modes
     double q[4];
     g.rotation(q);

@@ -177,3 +177,90 @@ def test_active_mapping_errors(ctx):
         api.active_mapping(ctx, scene, None, [synth.z_camera()], PlannerConfig(num_candidates=0), bounds=BOUNDS)
     log = api.active_mapping(ctx, scene, None, [synth.z_camera()], PlannerConfig(steps=0), bounds=BOUNDS)
     assert log.steps == [] and log.chosen_views == []
+
+
+# ---- against the reference ITSELF (oracle/_ref: its unmodified planner.hpp /
+# vfield.hpp compiled against the Eigen-subset shim) ---------------------------
+def _ref():
+    import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    return R
+
+
+@pytest.mark.parametrize("mode,look_inward", [(0, True), (0, False), (1, True)])
+def test_sample_candidates_equal_the_reference(mode, look_inward):
+    R = _ref()
+    pc = PlannerConfig(mode=mode, look_inward=look_inward, num_candidates=48, clearance=0.25,
+                       cam_width=40, cam_height=30, fov_h=1.2, fov_v=0.9, cam_near=0.02)
+    for seed in (0, 17, 2 ** 63 + 5):
+        same_cams(api.sample_candidates(BOUNDS, walls(), pc, seed), R.sample_candidates(BOUNDS, walls(), pc, seed))
+
+
+def test_vis_coverage_equals_the_reference():
+    R = _ref()
+    pc = PlannerConfig(num_candidates=12, clearance=0.25)
+    views = api.sample_candidates(BOUNDS, walls(), pc, 5)
+    for k in (0, 1, 4, 12):
+        assert api.vis_coverage(walls(), views[:k]) == R.vis_coverage(walls(), views[:k])
+
+
+def _probe_positions(seed, ks, bmin, bmax):
+    """The reference's probe k position (vfield.hpp:172-178): SplitMix64 seeded with
+    derive_seed(seed, k), three next_double draws, min + extent * u."""
+    M = (1 << 64) - 1
+    bmin, bmax = np.asarray(bmin, np.float64), np.asarray(bmax, np.float64)
+    out = []
+    for k in ks:
+        st = O.derive_seed(seed, int(k))
+        u = []
+        for _ in range(3):
+            st = (st + 0x9E3779B97F4A7C15) & M
+            z = st
+            z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+            z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+            z = z ^ (z >> 31)
+            u.append(float(z >> 11) * 2.0 ** -53)
+        out.append(bmin + (bmax - bmin) * np.array(u))
+    return np.array(out).reshape(-1, 3)
+
+
+def test_density_control_equals_the_reference():
+    """The restatement's kept probes (fp64 probes, round_f32 off) are the
+    reference's, probe for probe; the device keeps the same set up to its fp32
+    storage of the probes (test_density_control.py)."""
+    R = _ref()
+    sc = room_scene()
+    cams = [make_lookat((0.0, 0.0, 1.2), (1.0, 0.0, 1.2), (0, 0, 1), 48, 48),
+            make_lookat((2.5, 1.5, 1.8), (0.0, 0.0, 0.5), (0, 0, 1), 40, 32)]
+    for seed, rho in ((9, 20.0), (3, 35.0)):
+        kept, _ = O.density_control(sc, BOUNDS[0], BOUNDS[1], cams, rho=rho, eta=0.5, eps_v=0.95, seed=seed,
+                                    round_f32=False)
+        pos = R.density_control_positions(sc, BOUNDS[0], BOUNDS[1], cams, rho=rho, eta=0.5, eps_v=0.95,
+                                          seed=seed, threads=4)
+        assert len(kept) == len(pos) > 0
+        assert np.array_equal(_probe_positions(seed, kept, BOUNDS[0], BOUNDS[1]), pos)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("density_enabled", [False, True])
+def test_active_mapping_matches_the_reference(ctx, density_enabled):
+    """The device's run_active_mapping (gavis_active_mapping: density control, field
+    rebuild, candidate sampling, select_nbv per step) against the reference's own
+    run_active_mapping (planner.hpp:284-316): chosen candidates, their scores and
+    coverage per step."""
+    R = _ref()
+    scene = room_scene()
+    occ = walls()
+    rc, uc = RasterConfig(), UncertaintyConfig()
+    init = [make_lookat((0.0, 0.0, 1.2), (1.0, 0.0, 1.2), (0, 0, 1), 48, 48)]
+    pc = PlannerConfig(num_candidates=12, steps=3, seed=21, cam_width=48, cam_height=48, clearance=0.15)
+    dc = api.DensityControlConfig(rho=20.0, eta=0.5, eps_v=0.95, seed=9)
+    log = api.active_mapping(ctx, scene, occ, init, pc, VmfParams(1.0), 2, rc, uc, dc, density_enabled,
+                             bounds=BOUNDS)
+    ref = R.active_mapping(scene, BOUNDS, occ, init, pc, 1.0, 2, rc, uc, density_enabled, rho=20.0, eta=0.5,
+                           eps_v=0.95, dseed=9, threads=4)
+    for st, (best, scores, cov) in zip(log.steps, ref):
+        assert st.chosen_index == best
+        assert np.max(np.abs(st.scores - scores) / np.maximum(1.0, np.abs(scores))) <= 1e-9
+        assert st.vis_coverage == cov
