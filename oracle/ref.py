@@ -209,3 +209,28 @@ def active_mapping(scene, bounds, occ, init, pc, kappa: float, degree: int, rc, 
                                      C.c_double(eps_v), C.c_uint64(dseed), threads, chosen, O._p(score),
                                      O._p(cov), O._p(alls)))
     return [(int(chosen[k]), alls[k * nc:(k + 1) * nc].copy(), float(cov[k])) for k in range(steps)]
+
+
+def render_entropy_core(scene, cam, rc, uc, vis_by_particle, coeff_var=None, var_degree: int = -1,
+                        mixtures: bool = False, threads: int = 1):
+    """render_entropy_core (uncertainty.hpp:124-238) with per-particle visibility;
+    coeff_var [N, 3, (Lv+1)^2] selects the sh_propagation provider. Returns
+    (H, w0, depth) and, with mixtures, (offsets, components [K, 8], prior, resid, H_mix)."""
+    s = O._scene(scene)
+    P = cam.width * cam.height
+    H, w0, d = np.zeros(P), np.zeros(P), np.zeros(P)
+    v = np.ascontiguousarray(vis_by_particle, np.float64)
+    cv = None if coeff_var is None else np.ascontiguousarray(coeff_var, np.float64).reshape(-1)
+    base = (C.byref(s.c), C.byref(O.camera_struct(cam)), C.byref(O.raster_struct(rc)), C.byref(O.unc_struct(uc)),
+            O._p(v), O._p(cv) if cv is not None else None, var_degree, threads)
+    off = np.zeros(P + 1, np.int64) if mixtures else None
+    _check(lib().gref_render_entropy_core(*base, O._p(H), O._p(w0), O._p(d), O._p(off) if mixtures else None,
+                                          None, C.c_int64(0), None, None, None))
+    if not mixtures:
+        return H, w0, d
+    K = int(off[-1])
+    comps = np.zeros((max(1, K), 8))
+    prior, resid, Hm = np.zeros(P), np.zeros(P), np.zeros(P)
+    _check(lib().gref_render_entropy_core(*base, None, None, None, O._p(off), O._p(comps), C.c_int64(K),
+                                          O._p(prior), O._p(resid), O._p(Hm)))
+    return (H, w0, d), (off, comps[:K], prior, resid, Hm)

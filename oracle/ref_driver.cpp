@@ -350,4 +350,65 @@ int gref_active_mapping(const gor_scene* s, const double* bmin, const double* bm
   });
 }
 
+// render_entropy_core (uncertainty.hpp:124-238) with per-particle visibilities,
+// optional sh_propagation coefficient variances [N][3][(Lv+1)^2] (coeff_var NULL:
+// the constant provider), entropy / w0 / depth per pixel, and the per-pixel
+// mixtures in gor_render_mixtures's layout (offsets[P+1] always; components and
+// the per-pixel prior / residual T / H when comps is non-NULL, capacity cap).
+int gref_render_entropy_core(const gor_scene* s, const gor_camera* cam, const gor_raster* rc, const gor_unc* u,
+                             const double* vis_by_particle, const double* coeff_var, int var_degree, int threads,
+                             double* H, double* w0, double* depth, int64_t* offsets, gor_mixture_component* comps,
+                             int64_t cap, double* prior, double* resid, double* Hm) {
+  return guarded([&] {
+    const gavis::Scene sc = make_scene(s);
+    const gavis::CameraView cv = make_cam(cam);
+    const gavis::RasterConfig r = make_rc(rc);
+    gavis::UncertaintyConfig uc = make_uc(u);
+    std::vector<std::array<std::vector<double>, 3>> var;
+    if (coeff_var) {
+      const size_t nb = (size_t)(var_degree + 1) * (var_degree + 1);
+      var.resize(sc.particles.size());
+      for (size_t i = 0; i < var.size(); ++i)
+        for (int c = 0; c < 3; ++c) var[i][c].assign(coeff_var + (i * 3 + c) * nb, coeff_var + (i * 3 + c + 1) * nb);
+      uc.variance_provider = gavis::VarianceProvider::kShPropagation;
+      uc.coeff_variances = &var;
+    }
+    const gavis::ProjectedView pv = gavis::project_scene(sc, cv, r.dilation);
+    std::vector<double> sv(pv.splats.size());
+    for (size_t k = 0; k < sv.size(); ++k) sv[k] = vis_by_particle[pv.splats[k].particle_index];
+    std::vector<double> d;
+    std::vector<gavis::PixelMixture> mix;
+    const gavis::EntropyMap m = gavis::render_entropy_core(sc, pv, sv, cv, r, uc, threads, &d,
+                                                           offsets ? &mix : nullptr);
+    if (H) std::memcpy(H, m.entropy.data(), sizeof(double) * m.entropy.size());
+    if (w0) std::memcpy(w0, m.invisible_mass.data(), sizeof(double) * m.invisible_mass.size());
+    if (depth) std::memcpy(depth, d.data(), sizeof(double) * d.size());
+    if (offsets) {
+      int64_t k = 0;
+      for (size_t p = 0; p < mix.size(); ++p) {
+        offsets[p] = k;
+        if (comps) {
+          for (const auto& c : mix[p].components) {
+            if (k >= cap) throw gavis::InvariantError("render_entropy_core: component capacity too small");
+            gor_mixture_component& o = comps[k];
+            o.weight = c.weight;
+            o.vis = c.vis;
+            for (int j = 0; j < 3; ++j) {
+              o.mean[j] = c.mean[j];
+              o.var[j] = c.var[j];
+            }
+            ++k;
+          }
+          if (prior) prior[p] = mix[p].prior_weight;
+          if (resid) resid[p] = mix[p].residual_transmittance;
+          if (Hm) Hm[p] = mix[p].entropy;
+        } else {
+          k += (int64_t)mix[p].components.size();
+        }
+      }
+      offsets[mix.size()] = k;
+    }
+  });
+}
+
 }  // extern "C"

@@ -71,3 +71,39 @@ def test_reference_bench_step_matches_restatement():
     b_o, s_o = O.select_nbv(osc, g, 2, 6, c["candidates"][:8], rc, UC, threads=4, with_rgb=True)
     assert b_r == b_o and np.array_equal(s_r, s_o)
     rs.close()
+
+
+def test_reference_mixtures_and_sh_propagation_equal_restatement():
+    """render_entropy_core's optional outputs (uncertainty.hpp:124-238): the
+    per-pixel mixture dump (components w, v, clamped SH colour, diag Q_c; prior
+    weight, residual T, entropy) and the sh_propagation provider (per-splat
+    1/2 sum_c ln q_c(d) from coefficient variances), the reference against the
+    restatement the device is tested on (tests/test_optional_outputs.py)."""
+    c = synth.config1(2)
+    sc = c["scene"]
+    osc = O.OracleScene(sc)
+    rng = np.random.default_rng(4)
+    vis = rng.uniform(0.0, 1.0, sc.num_particles)
+    cam = c["candidates"][1]
+    rc = RasterConfig()
+    for uc in (UC, UncertaintyConfig(beta=0.3, prior_opacity=0.2, color_sigma=0.07)):
+        (H, w0, d), (off, comps, prior, resid, Hm) = R.render_entropy_core(osc, cam, rc, uc, vis, mixtures=True,
+                                                                           threads=4)
+        o_off, o_comps, o_prior, o_resid, o_H = O.render_mixtures(osc, cam, rc, uc, vis)
+        assert np.array_equal(off, o_off) and np.array_equal(comps, o_comps)
+        assert np.array_equal(prior, o_prior) and np.array_equal(resid, o_resid) and np.array_equal(Hm, o_H)
+        oH, ow0, od = O.render_entropy_core(osc, cam, rc, uc, vis)
+        assert np.array_equal(H, oH) and np.array_equal(w0, ow0) and np.array_equal(d, od)
+    var = rng.uniform(0.01, 0.2, size=(sc.num_particles, 3, 9))
+    uc = UncertaintyConfig(variance_provider=1)
+    H, w0, _ = R.render_entropy_core(osc, cam, rc, uc, vis, coeff_var=var, var_degree=2, threads=4)
+    O.set_coeff_variances(var, 2)
+    try:
+        oH, ow0, _ = O.render_entropy_core(osc, cam, rc, uc, vis)
+        (_, _, _), (_, comps, _, _, _) = R.render_entropy_core(osc, cam, rc, uc, vis, coeff_var=var, var_degree=2,
+                                                               mixtures=True, threads=4)
+        _, o_comps, _, _, _ = O.render_mixtures(osc, cam, rc, uc, vis)
+    finally:
+        O.set_coeff_variances(None, -1)
+    assert np.array_equal(H, oH) and np.array_equal(w0, ow0)
+    assert np.array_equal(comps, o_comps)
