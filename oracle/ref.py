@@ -234,3 +234,21 @@ def render_entropy_core(scene, cam, rc, uc, vis_by_particle, coeff_var=None, var
     _check(lib().gref_render_entropy_core(*base, None, None, None, O._p(off), O._p(comps), C.c_int64(K),
                                           O._p(prior), O._p(resid), O._p(Hm)))
     return (H, w0, d), (off, comps[:K], prior, resid, Hm)
+
+
+def project_and_bin(scene, cam, dilation: float = 0.3, tile_size: int = 16):
+    """project_scene (raster.hpp:114-130) + splat_binning (:145-164) of the
+    reference: (splats sorted by (depth, index), tile offsets, entries)."""
+    s = O._scene(scene)
+    buf = (O.Splat * max(1, s.n))()
+    tiles = ((cam.width + tile_size - 1) // tile_size) * ((cam.height + tile_size - 1) // tile_size)
+    off = np.zeros(tiles + 1, np.int64)
+    lib().gref_project_and_bin.restype = C.c_int64
+    n = lib().gref_project_and_bin(C.byref(s.c), C.byref(O.camera_struct(cam)), C.c_double(dilation), tile_size,
+                                   buf, O._p(off), None)
+    if n < 0:
+        raise RuntimeError(f"reference error: {lib().gref_last_error().decode()}")
+    ent = np.zeros(max(1, int(off[-1])), np.int32)
+    lib().gref_project_and_bin(C.byref(s.c), C.byref(O.camera_struct(cam)), C.c_double(dilation), tile_size,
+                               buf, O._p(off), O._p(ent))
+    return [buf[i] for i in range(n)], off, ent[: int(off[-1])]

@@ -411,4 +411,42 @@ int gref_render_entropy_core(const gor_scene* s, const gor_camera* cam, const go
   });
 }
 
+// project_scene (raster.hpp:114-130) -> splats sorted by (depth, index), count;
+// splat_binning (raster.hpp:145-164) of them -> CSR tile lists (entries NULL: size)
+int64_t gref_project_and_bin(const gor_scene* s, const gor_camera* cam, double dilation, int tile_size,
+                             gor_splat* splats, int64_t* tile_offsets, int32_t* entries) {
+  int64_t total = -1;
+  const int st = guarded([&] {
+    const gavis::Scene sc = make_scene(s);
+    const gavis::CameraView cv = make_cam(cam);
+    const gavis::ProjectedView pv = gavis::project_scene(sc, cv, dilation);
+    for (size_t k = 0; k < pv.splats.size(); ++k) {
+      const gavis::ImageSpaceSplat& a = pv.splats[k];
+      gor_splat& o = splats[k];
+      o.particle_index = a.particle_index;
+      o._pad = 0;
+      o.mean_x = a.mean.x();
+      o.mean_y = a.mean.y();
+      o.conic_a = a.conic_a;
+      o.conic_b = a.conic_b;
+      o.conic_c = a.conic_c;
+      o.depth = a.depth;
+      o.radius = a.radius;
+      o.opacity = a.opacity;
+    }
+    const gavis::SplatBinning b = gavis::splat_binning(pv.splats, cv.width, cv.height, tile_size);
+    int64_t k = 0;
+    for (size_t t = 0; t < b.tiles.size(); ++t) {
+      tile_offsets[t] = k;
+      for (int e : b.tiles[t]) {
+        if (entries) entries[k] = e;
+        ++k;
+      }
+    }
+    tile_offsets[b.tiles.size()] = k;
+    total = (int64_t)pv.splats.size();
+  });
+  return st == 0 ? total : -st;
+}
+
 }  // extern "C"

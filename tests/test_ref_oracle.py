@@ -6,9 +6,11 @@ against a self-written Eigen-subset shim (oracle/eigen_shim: fixed-size
 products summed left to right, Eigen's quaternion-to-matrix formula). Every
 hot-path function of the restatement (oracle/gavis_oracle.c), and so the
 checker the device is held to, must agree with the reference's own code BIT FOR
-BIT: single_view_visibility (raster.hpp:237-290), construct_field
-(vfield.hpp:68-92), rasterize (raster.hpp:175-231), render_entropy
-(uncertainty.hpp:242-260), select_nbv (planner.hpp:117-137).
+BIT: project_scene and splat_binning (raster.hpp:114-164), single_view_visibility
+(raster.hpp:237-290), construct_field (vfield.hpp:68-92), rasterize
+(raster.hpp:175-231), render_entropy(_core) incl. mixtures and sh_propagation
+(uncertainty.hpp:124-260), select_nbv (planner.hpp:117-137); the planner and
+density-control rows are pinned in tests/test_planner.py.
 """
 import numpy as np
 import pytest
@@ -107,3 +109,23 @@ def test_reference_mixtures_and_sh_propagation_equal_restatement():
         O.set_coeff_variances(None, -1)
     assert np.array_equal(H, oH) and np.array_equal(w0, ow0)
     assert np.array_equal(comps, o_comps)
+
+
+@pytest.mark.parametrize("tile", [16, 5, 13])
+def test_reference_projection_and_binning_equal_restatement(tile):
+    """project_scene (raster.hpp:114-130: EWA conics, radii, the (depth, index)
+    order) and splat_binning (raster.hpp:145-164: tile lists) of the reference
+    against the restatement, field by field -- the restatement the device's keys,
+    sorted order and conics are held to bit for bit (test_gpu_parity.py)."""
+    for c in (synth.config1(0), synth.config3(0, n=40_000, n_train=2, n_candidates=2, res=128)):
+        osc = O.OracleScene(c["scene"])
+        for cam in (c["train"][:1] + c["candidates"][:1]):
+            sp_r, off_r, ent_r = R.project_and_bin(osc, cam, 0.3, tile)
+            sp_o = O.project_scene(osc, cam, 0.3)
+            off_o, ent_o = O.splat_binning(sp_o, cam.width, cam.height, tile)
+            assert len(sp_r) == len(sp_o) > 0
+            for a, b in zip(sp_r, sp_o):
+                assert (a.particle_index, a.mean_x, a.mean_y, a.conic_a, a.conic_b, a.conic_c, a.depth, a.radius,
+                        a.opacity) == (b.particle_index, b.mean_x, b.mean_y, b.conic_a, b.conic_b, b.conic_c,
+                                       b.depth, b.radius, b.opacity)
+            assert np.array_equal(off_r, off_o) and np.array_equal(ent_r, ent_o)
