@@ -190,3 +190,27 @@ def test_config5_loop_matches_reference_rebuild():
         assert np.max(np.abs(all_scores[r] - scores) / np.abs(scores)) <= 1e-9, f"round {r}"
         traj.append(cams[best])
     rs.close()
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_tile_lists_match_reference_itself_full_size(cfg):
+    """The device's tile lists at full benchmark size (500k / 1M Gaussians,
+    800^2) against the reference's own project_scene + splat_binning
+    (raster.hpp:114-164, oracle/_ref): every tile's particle sequence -- the
+    (depth, index) order the blend composites in -- identical, for one training
+    view and one candidate."""
+    import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    c = GEN[cfg]()
+    osc = O.OracleScene(c["scene"])
+    with api.Context(0) as ctx:
+        ds = ctx.upload(c["scene"])
+        for cam in (c["train"][0], c["candidates"][0]):
+            keys, ids, ranges = api.debug_binning(ctx, ds, cam, RC)
+            sp, off, ent = R.project_and_bin(osc, cam, RC.dilation, RC.tile_size)
+            pid = np.array([s.particle_index for s in sp], np.int64)
+            assert len(ids) == off[-1] > 0
+            for t in range(len(off) - 1):
+                lo, hi = ranges[t]
+                assert np.array_equal(ids[lo:hi], pid[ent[off[t]:off[t + 1]]]), f"config {cfg} tile {t}"
