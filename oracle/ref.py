@@ -252,3 +252,17 @@ def project_and_bin(scene, cam, dilation: float = 0.3, tile_size: int = 16):
     lib().gref_project_and_bin(C.byref(s.c), C.byref(O.camera_struct(cam)), C.c_double(dilation), tile_size,
                                buf, O._p(off), O._p(ent))
     return [buf[i] for i in range(n)], off, ent[: int(off[-1])]
+
+
+def query_view(gamma, degree: int, num_views: int, scene, cam, dilation: float = 0.3):
+    """query_view (vfield.hpp:121-134) -> (particle indices, visibilities)."""
+    s = O._scene(scene)
+    g = np.ascontiguousarray(gamma, np.float64)
+    idx = np.zeros(max(1, s.n), np.int32)
+    vis = np.zeros(max(1, s.n))
+    lib().gref_query_view.restype = C.c_int64
+    n = lib().gref_query_view(C.byref(s.c), O._p(g), degree, num_views, C.byref(O.camera_struct(cam)),
+                              C.c_double(dilation), O._p(idx), O._p(vis))
+    if n < 0:
+        raise RuntimeError(f"reference error: {lib().gref_last_error().decode()}")
+    return idx[:n], vis[:n]

@@ -449,4 +449,22 @@ int64_t gref_project_and_bin(const gor_scene* s, const gor_camera* cam, double d
   return st == 0 ? total : -st;
 }
 
+// query_view (vfield.hpp:121-134) -> the non-culled particle indices and their
+// visibilities; returns the count
+int64_t gref_query_view(const gor_scene* s, const double* gamma, int degree, int num_views, const gor_camera* cam,
+                        double dilation, int32_t* idx, double* vis) {
+  int64_t n = -1;
+  const int st = guarded([&] {
+    const gavis::Scene sc = make_scene(s);
+    const gavis::VisibilityField f = make_field(sc, gamma, degree, num_views);
+    const gavis::ViewQuery q = gavis::query_view(f, sc, make_cam(cam), dilation);
+    for (size_t k = 0; k < q.particle_indices.size(); ++k) {
+      idx[k] = q.particle_indices[k];
+      vis[k] = q.visibilities[k];
+    }
+    n = (int64_t)q.particle_indices.size();
+  });
+  return st == 0 ? n : -st;
+}
+
 }  // extern "C"

@@ -129,3 +129,15 @@ def test_reference_projection_and_binning_equal_restatement(tile):
                         a.opacity) == (b.particle_index, b.mean_x, b.mean_y, b.conic_a, b.conic_b, b.conic_c,
                                        b.depth, b.radius, b.opacity)
             assert np.array_equal(off_r, off_o) and np.array_equal(ent_r, ent_o)
+
+
+def test_reference_query_view_equals_restatement():
+    """query_view (vfield.hpp:121-134), the north_star's VF-QUERY entry point:
+    indices of the non-culled particles and their AM-GM visibilities."""
+    c = synth.config1(0)
+    osc = O.OracleScene(c["scene"])
+    g = R.construct_field(osc, c["train"][:5], 1.0, 3, RasterConfig(), threads=4)
+    for cam in c["candidates"][:3]:
+        i_r, v_r = R.query_view(g, 3, 5, osc, cam)
+        i_o, v_o = O.query_view(g, 3, 5, osc, cam)
+        assert len(i_r) > 0 and np.array_equal(i_r, i_o) and np.array_equal(v_r, v_o)
