@@ -150,3 +150,20 @@ def test_cpp_uncertainty_modes_match_oracle(tmp_path, precision):
         assert float(out["sharded_field_max_abs"][0]) == 0.0 and int(out["sharded_field_max_abs"][2]) == 1
     finally:
         O.set_coeff_variances(None, 0)
+
+
+@pytest.mark.gpu
+def test_dropin_source_compatible_with_reference():
+    """oracle/dropin_check.cpp: ONE templated reference-style caller (Scene of
+    GaussianParticle, Trajectory, make_lookat, construct_field, select_nbv --
+    the planner.hpp:297-301 call shape) compiled against both the reference's
+    own headers (namespace gavis, CPU) and the drop-in front-end (namespace
+    gavis_b200, this library): same chosen view, scores within 1e-9. Built by
+    `make -C oracle ref` where the reference tree exists; the binary travels."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_check not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    f = r.stdout.split()
+    assert f[0] == "reference_best" and f[1] == f[3] and int(f[1]) >= 0, r.stdout
